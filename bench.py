@@ -1,0 +1,417 @@
+#!/usr/bin/env python3
+"""Benchmark of the AHS hot path on B200: features -> select -> sort.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg2] [--impl ours|reference]
+
+One step = one pass of the whole hot path (ahs_features, ahs_select, ahs_sort)
+over the workload's keys, resident in HBM.  The default workload is
+BASELINE.json configs[1] (cfg2: 2^24 uint32 keys uniform over 32 bits,
+GENERAL branch).  L2 is flushed (256 MiB write) before every timed step
+because the 64 MiB input would otherwise stay L2-resident.  Timing: CUDA
+events on the launching stream around each step, barrier + synchronize around
+the timed region, max over ranks.  N > 1 runs independent replicas (one per
+GPU, weak scaling; the method has no cross-GPU exchange: DESIGN.md §7).
+
+Prints ONE JSON line on rank 0.  `--impl reference` times the CPU oracle
+(the only reference this paper has: PAPER.md has no code) on a bounded
+sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "sorted keys/sec (Gkeys/s) per strategy on 1 B200; achieved HBM GB/s vs roofline"
+L2_FLUSH_BYTES = 256 << 20
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,"
+              "utilization.gpu")
+
+    def __init__(self, gpu: int):
+        self.gpu, self.proc, self.lines = gpu, None, []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons, loaded = [], None, set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                c, cm, util = float(parts[0]), float(parts[1]), float(parts[8])
+            except ValueError:
+                continue
+            smax = cm
+            sm.append(c)
+            if util > 0:
+                loaded.append(c)
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        use = loaded or sm
+        return {"sm_mhz": statistics.median(use) if use else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm), "samples_under_load": len(loaded)}
+
+
+# ------------------------------------------------------------ distributed
+def dist_setup(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    pg = None
+    if ws > 1:
+        import torch.distributed as dist
+        backend = "gloo" if args.cpu_dist else "nccl"
+        dist.init_process_group(backend)
+        pg = dist
+    return ws, rank, local, pg
+
+
+def dist_max(pg, x: float, device) -> float:
+    if pg is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    pg.all_reduce(t, op=pg.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(pg):
+    if pg is not None:
+        pg.barrier()
+
+
+# --------------------------------------------------------- oracle (CPU)
+def cpu_oracle_rate(keys, vals, budget_s: float, max_n: int):
+    """Time the oracle pipeline (features -> FSM -> sort) on a bounded prefix."""
+    import oracle
+    n = min(keys.size, max_n)
+    k, v = keys[:n].copy(), (vals[:n].copy() if vals is not None else None)
+    times = []
+    t_end = time.perf_counter() + budget_s
+    while True:
+        t0 = time.perf_counter()
+        oracle.ahs(k, v)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() > t_end or len(times) >= 10:
+            break
+    med = statistics.median(times)
+    return n / med / 1e9, n, len(times), med
+
+
+# ------------------------------------------------------------ GPU timing
+def upload(torch, a: np.ndarray, device):
+    t = torch.from_numpy(a.view(np.int32)).to(device)
+    return t.view(torch.uint32) if a.dtype == np.uint32 else t
+
+
+def time_pipeline(torch, ahs, keys_np, vals_np, steps, warmup, device, flush, profile=False,
+                  pg=None, soak_s=0.0, sampler=None):
+    n = keys_np.size
+    dk = upload(torch, keys_np, device)
+    dv = upload(torch, vals_np, device) if vals_np is not None else None
+    ko = torch.empty_like(dk)
+    vo = torch.empty_like(dv) if dv is not None else None
+    ws = ahs.Workspace(n, dv is not None, device)
+    stream = torch.cuda.current_stream(device)
+
+    def step():
+        f = ahs.ahs_features(dk, ws, stream)
+        s, r = ahs.ahs_select(f)
+        ahs.ahs_sort(dk, dv, ko, vo, s, f, ws, stream)
+        return f, s, r
+
+    for _ in range(warmup):
+        flush.zero_()
+        f, s, r = step()
+    torch.cuda.synchronize(device)
+    if soak_s > 0:  # untimed load so the clock sampler sees the GPU under this workload
+        t_end = time.perf_counter() + soak_s
+        while time.perf_counter() < t_end:
+            flush.zero_()
+            step()
+        torch.cuda.synchronize(device)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    barrier(pg)
+    torch.cuda.synchronize(device)
+    if sampler:
+        sampler.start()
+    launches0 = ahs.ahs_launch_count()
+    if profile:
+        ahs.ahs_profile_begin()
+    for i in range(steps):
+        flush.zero_()
+        ev[i][0].record(stream)
+        f, s, r = step()
+        ev[i][1].record(stream)
+    torch.cuda.synchronize(device)
+    if profile:
+        ahs.ahs_profile_end()
+    launches = ahs.ahs_launch_count() - launches0
+    clocks = sampler.stop() if sampler else None
+    barrier(pg)
+    total_ms = sum(a.elapsed_time(b) for a, b in ev)
+    prof = ahs.ahs_profile_read() if profile else None
+    passes = ahs.ahs_sort_passes(f, s, dv is not None)
+    return dict(total_ms=total_ms, f=f, s=s, r=r, launches=launches, prof=prof, passes=passes,
+                clocks=clocks, step_ms=[a.elapsed_time(b) for a, b in ev])
+
+
+def time_e2e(torch, ahs, keys_np, vals_np, steps, warmup, device):
+    """Same metric through the C-ABI host entry point: pinned host buffers, H2D and D2H
+    inside the timed region every step."""
+    n = keys_np.size
+    hk = torch.from_numpy(keys_np.view(np.int32)).pin_memory()
+    hko = torch.empty_like(hk).pin_memory()
+    hv = torch.from_numpy(vals_np.view(np.int32)).pin_memory() if vals_np is not None else None
+    hvo = torch.empty_like(hv).pin_memory() if hv is not None else None
+    if keys_np.dtype == np.uint32:
+        hk, hko = hk.view(torch.uint32), hko.view(torch.uint32)
+    if hv is not None:
+        hv, hvo = hv.view(torch.uint32), hvo.view(torch.uint32)
+    scratch = torch.empty(ahs.ahs_host_scratch_bytes(n, hv is not None), dtype=torch.uint8, device=device)
+    stream = torch.cuda.current_stream(device)
+    for _ in range(warmup):
+        ahs.ahs_sort_host(hk, hv, hko, hvo, scratch, stream=stream)
+    torch.cuda.synchronize(device)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(steps):
+        ahs.ahs_sort_host(hk, hv, hko, hvo, scratch, stream=stream)
+    b.record(stream)
+    torch.cuda.synchronize(device)
+    ms = a.elapsed_time(b)
+    nb = n * 4 * (2 if hv is not None else 1)
+    return ms, nb, nb
+
+
+def sort_bytes(strategy: int, passes: int, n: int, kv: bool) -> int:
+    """Algorithmic HBM bytes of ahs_sort: radix = histogram read 4n +
+    per pass read+write (8n keys, 16n pairs); counting keys-only = write 4n."""
+    if passes == 0:
+        return 4 * n if strategy == 0 else 0
+    hist = 0 if (strategy == 0 and passes == 1) else 4 * n
+    return hist + passes * (16 if kv else 8) * n
+
+
+def traffic_from_profiles(workload: str):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        d = json.load(open(p))
+        return d.get(workload, {}).get("onesweep_dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def run_ours(args):
+    import torch
+    ws, rank, local, pg = dist_setup(args)
+    device = torch.device("cuda", local)
+    torch.cuda.set_device(device)
+    import paper_2506_20677_b200 as ahs
+    ahs.lib()
+    peak, peak_kind = load_peaks()
+    keys, vals, dt = synth.make(args.workload)
+    n = keys.size
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=device)
+    sampler = ClockSampler(local)
+    res = time_pipeline(torch, ahs, keys, vals, args.steps, args.warmup, device, flush, profile=True,
+                        pg=pg, soak_s=args.soak, sampler=sampler)
+    tmax = dist_max(pg, res["total_ms"], device)
+    value = ws * n * args.steps / (tmax * 1e-3) / 1e9
+    f, s, r, prof = res["f"], res["s"], res["r"], res["prof"]
+    kv = vals is not None
+    # dominant kernel: the onesweep digit pass (read + write of every key (and value))
+    kname = "onesweep_kv" if kv else "onesweep"
+    if prof[kname]["launches"] == 0:
+        kname = max(prof, key=lambda k: prof[k]["ms"])
+    kl = prof[kname]["launches"]
+    kms = prof[kname]["ms"] / max(1, kl)
+    per_launch_bytes = {"onesweep": 8 * n, "onesweep_kv": 16 * n, "count_fill": 4 * n,
+                        "count_scatter_kv": 16 * n, "radix_hist": 4 * n, "feat_reduce": 4 * n,
+                        "feat_hist": 4 * n}.get(kname, 4 * n)
+    achieved = per_launch_bytes / (kms * 1e-3) / 1e9
+    traffic = traffic_from_profiles(args.workload)
+    step_total = sum(v["ms"] for v in prof.values())
+    kernels = {k: {"ms_per_launch": v["ms"] / v["launches"], "launches": v["launches"],
+                   "share_of_kernel_time": v["ms"] / step_total}
+               for k, v in prof.items() if v["launches"]}
+    sb = sort_bytes(s, res["passes"], n, kv)
+    sort_ms = sum(v["ms"] for k, v in prof.items() if not k.startswith("feat")) / args.steps
+    feat_ms = sum(v["ms"] for k, v in prof.items() if k.startswith("feat")) / args.steps
+
+    out = {
+        "metric": METRIC, "value": round(value, 4), "unit": "Gkeys/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": tmax / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dt,
+        "data": "synthetic (SplitMix64 recipe of SURVEY.md §8(d))",
+        "config": {"workload": args.workload, "n": n, "key_dtype": dt, "kv": kv,
+                   "strategy": ahs.STRATEGY_NAMES[s], "rule": ahs.RULE_NAMES[r], "passes": res["passes"],
+                   "l2": "flushed before every timed step (256 MiB write)",
+                   "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU"},
+        "roofline": {"bound": "hbm", "kernel": kname, "achieved": round(achieved, 1), "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                     "traffic": traffic, "algorithmic_bytes_per_launch": per_launch_bytes,
+                     "ms_per_launch": kms},
+        "stages": {"features_ms": feat_ms, "sort_kernels_ms": sort_ms,
+                   "sort_algorithmic_bytes": sb,
+                   "sort_GBps": sb / (sort_ms * 1e-3) / 1e9 if sort_ms > 0 else None,
+                   "step_ms_median": statistics.median(res["step_ms"])},
+        "kernels": kernels,
+        "gpu_launches": res["launches"],
+        "clocks": res["clocks"],
+        "features": {"k": f.k, "nbins": f.nbins, "H": f.entropy, "descents": f.descents},
+    }
+    # end to end through the C ABI with host buffers
+    if not args.no_e2e:
+        e_ms, bi, bo = time_e2e(torch, ahs, keys, vals, max(3, args.steps // 2), 2, device)
+        e_steps = max(3, args.steps // 2)
+        e_max = dist_max(pg, e_ms, device)
+        out["e2e"] = {"value": round(ws * n * e_steps / (e_max * 1e-3) / 1e9, 4), "unit": "Gkeys/s",
+                      "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo,
+                      "ms_per_step": e_max / e_steps, "api": "ahs_sort_host (pinned host buffers)"}
+    # per-strategy table (BASELINE.json metric is per strategy)
+    if args.configs and ws == 1:
+        rows = []
+        for cfg in [c for c in args.configs.split(",") if c]:
+            k2, v2, dt2 = synth.make(cfg)
+            r2 = time_pipeline(torch, ahs, k2, v2, args.table_steps, 2, device, flush, profile=True)
+            p2 = r2["prof"]
+            n2 = k2.size
+            kv2 = v2 is not None
+            sort_ms2 = sum(v["ms"] for k, v in p2.items() if not k.startswith("feat")) / args.table_steps
+            feat_ms2 = sum(v["ms"] for k, v in p2.items() if k.startswith("feat")) / args.table_steps
+            sb2 = sort_bytes(r2["s"], r2["passes"], n2, kv2)
+            rows.append({
+                "workload": cfg, "n": n2, "kv": kv2, "strategy": ahs.STRATEGY_NAMES[r2["s"]],
+                "rule": ahs.RULE_NAMES[r2["r"]], "passes": r2["passes"],
+                "pipeline_Gkeys_s": n2 * args.table_steps / (r2["total_ms"] * 1e-3) / 1e9,
+                "sort_Gkeys_s": n2 / (sort_ms2 * 1e-3) / 1e9 if sort_ms2 > 0 else None,
+                "sort_GBps": sb2 / (sort_ms2 * 1e-3) / 1e9 if sort_ms2 > 0 else None,
+                "sort_frac_of_peak": (sb2 / (sort_ms2 * 1e-3) / 1e9) / peak if sort_ms2 > 0 else None,
+                "features_GBps": 8 * n2 / (feat_ms2 * 1e-3) / 1e9 if feat_ms2 > 0 else None,
+                "kernels_ms": {k: v["ms"] / v["launches"] for k, v in p2.items() if v["launches"]},
+            })
+            del k2, v2
+        out["strategies"] = rows
+    # CPU oracle baseline (rank 0, N = 1 only)
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        rate, ns, reps, med = cpu_oracle_rate(keys, vals, args.cpu_budget, n)
+        out["cpu_baseline"] = {"value": round(rate, 6), "unit": "Gkeys/s", "cores": 1, "kind": "oracle",
+                               "sample": f"full {args.workload} ({ns} keys), oracle features+FSM+sort, "
+                                         f"median of {reps} runs ({med:.2f} s each), one thread"}
+    if rank == 0:
+        print(json.dumps(out))
+    if pg is not None:
+        pg.destroy_process_group()
+
+
+def run_reference(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    oracle.build()
+    keys, vals, dt = synth.make(args.workload)
+    ns = min(keys.size, args.ref_sample)
+    k, v = keys[:ns].copy(), (vals[:ns].copy() if vals is not None else None)
+    for _ in range(args.warmup):
+        oracle.ahs(k, v)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.ahs(k, v)
+    dt_s = time.perf_counter() - t0
+    value = ns * args.steps / dt_s / 1e9
+    sample = (f"first {ns} keys of {args.workload} per step (oracle features+FSM+sort, one thread)")
+    out = {"impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": "Gkeys/s",
+           "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": dt_s * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": dt, "data": "synthetic",
+           "config": {"workload": args.workload, "n": keys.size, "sample_n": ns, "key_dtype": dt,
+                      "kv": vals is not None},
+           "cpu_baseline": {"value": round(value, 6), "unit": "Gkeys/s", "cores": 1, "kind": "oracle",
+                            "sample": sample},
+           "e2e": {"value": round(value, 6), "unit": "Gkeys/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg2", choices=sorted(synth.CONFIGS))
+    ap.add_argument("--configs", default="cfg1,cfg2kv,cfg3,cfg4a,cfg4d,cfg5_r8,cfg5_r32",
+                    help="per-strategy table rows (single GPU only); '' to skip")
+    ap.add_argument("--table-steps", type=int, default=5)
+    ap.add_argument("--soak", type=float, default=1.0, help="untimed seconds of load before timing")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--ref-sample", type=int, default=1 << 22)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-dist", action="store_true", help=argparse.SUPPRESS)
+    args = ap.parse_args()
+    assert args.warmup >= 1
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

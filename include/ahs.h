@@ -1,0 +1,201 @@
+/*
+ * ahs.h — C ABI of libahs.so, the B200-native (sm_100a) hot path of
+ * Adaptive Hybrid Sort (arXiv 2506.20677).
+ *
+ * Three calls make the method (BASELINE.json north_star):
+ *
+ *   ahs_features  feature extraction, §III.A line 96: the state vector
+ *                 v = (n, k, H) with k = max - min + 1 and
+ *                 H = -sum_i p_i log2 p_i, plus min/max and the descent count
+ *                 (presortedness, §I line 25 / north_star).
+ *   ahs_select    the decision FSM, §III.A lines 96-98 (Fig. 2), with
+ *                 Table II thresholds (lines 140-145) and the §III.K shortcuts
+ *                 (line 411), applied on the host to the feature struct.
+ *   ahs_sort      the chosen strategy on the device:
+ *                   COUNTING  Listing 2 (§III.F), reusing the
+ *                             feature histogram (run fill for keys only, stable
+ *                             scatter for key-value pairs);
+ *                   RADIX     §III.G (lines 218-251) base 256 on key - min with
+ *                             d = ceil(log_256 k) passes (Eq. 4);
+ *                   GENERAL   the paper's QuickSort branch (§III.G.1, lines
+ *                             253-288) served by a full-width 4-pass radix sort
+ *                             (identical, stable output).
+ *
+ * All pointers named d_* are DEVICE pointers owned by the caller (the library
+ * never allocates device memory).  `stream` is a cudaStream_t passed as void*
+ * (NULL = legacy default stream).  Keys are 32-bit integers (§III.K
+ * line 409: integer-only input) stored contiguously, 4-byte aligned; values
+ * are uint32 payloads that travel with their keys.  Every call returns an
+ * ahs_status (0 = OK, < 0 = error; no exception crosses the ABI).  Calls are
+ * thread-safe when concurrent calls use distinct ws/tmp buffers; the
+ * profiling switch (ahs_profile_*) is process-global.
+ */
+#ifndef AHS_H
+#define AHS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define AHS_API __attribute__((visibility("default")))
+#else
+#define AHS_API
+#endif
+
+/* ------------------------------------------------------------------ enums */
+typedef enum {
+    AHS_OK = 0,
+    AHS_EINVAL = -1,   /* NULL pointer with n > 0, bad dtype / strategy / thresholds,
+                          misaligned key pointer, vals_out missing when vals_in given */
+    AHS_ENOSPACE = -2, /* ws or tmp smaller than ahs_workspace_bytes / ahs_sort_tmp_bytes */
+    AHS_ERANGE = -3,   /* n > AHS_MAX_N */
+    AHS_EFEAT = -4,    /* feat does not describe these keys (n or dtype mismatch) */
+    AHS_ECUDA = -5,    /* CUDA launch / runtime error (cudaGetLastError) */
+    AHS_ENODEV = -6    /* no CUDA device or not an sm_100 device */
+} ahs_status;
+
+typedef enum { AHS_I32 = 0, AHS_U32 = 1 } ahs_dtype;
+
+/* The GPU's three strategies.  The paper's Insertion (n <= 20) and QuickSort
+ * branches both run as AHS_GENERAL; ahs_rule keeps which rule fired. */
+typedef enum { AHS_COUNTING = 0, AHS_RADIX = 1, AHS_GENERAL = 2 } ahs_strategy;
+
+typedef enum {
+    AHS_RULE_EMPTY = 0,       /* n = 0  -> COUNTING, no-op  */
+    AHS_RULE_CONSTANT = 1,    /* k = 1  -> COUNTING, no-op  */
+    AHS_RULE_SMALL_N = 2,     /* n <= n_insertion   -> GENERAL (Insertion) */
+    AHS_RULE_SMALL_RANGE = 3, /* k <= k_counting   -> COUNTING         */
+    AHS_RULE_LOW_ENTROPY = 4, /* k > k_radix and H < c*log2(norm) -> RADIX */
+    AHS_RULE_DEFAULT = 5      /* otherwise   -> GENERAL (QuickSort) */
+} ahs_rule;
+
+/* Entropy normalisation of the RADIX rule (reading R2):
+ * BUCKETS compares H against c*log2(nbins), RANGE against c*log2(k)
+ * (paper-literal; identical whenever shift = 0). */
+typedef enum { AHS_NORM_BUCKETS = 0, AHS_NORM_RANGE = 1 } ahs_entropy_norm;
+
+/* feature flags (informational; only EMPTY / CONSTANT change ahs_select) */
+#define AHS_FLAG_EMPTY 1u        /* n = 0 */
+#define AHS_FLAG_CONSTANT 2u     /* k = 1 */
+#define AHS_FLAG_BUCKETED 4u     /* shift > 0: H is a 2^16-bucket entropy */
+#define AHS_FLAG_SORTED 8u       /* descents = 0 */
+#define AHS_FLAG_STRICT_DESC 16u /* descents = n - 1 (n >= 2) */
+#define AHS_FLAG_SIGNED 32u      /* dtype = AHS_I32 */
+
+#define AHS_ENTROPY_BITS 16u     /* at most 2^16 histogram bins (reading R1) */
+#define AHS_MAX_N ((1ull << 30) - 1) /* look-back counts are 30-bit */
+
+/* ------------------------------------------------------------------ types */
+/* The state vector v = (n, k, H) of PAPER.md §III.A (line 96) and friends.
+ *   min, max   in the key's own signedness (sign-extended for AHS_I32)
+ *   k          max - min + 1 (up to 2^32, hence 64-bit)
+ *   bits       bitlen(k - 1); shift = max(0, bits - 16);
+ *   nbins      ((k - 1) >> shift) + 1  — histogram bins of (key - min) >> shift
+ *   entropy    H = -sum_b p_b log2 p_b over those bins, fp64, clamped to
+ *              [0, log2 nbins]  (equals the per-value entropy when shift = 0)
+ *   descents   #{ i < n-1 : key[i] > key[i+1] } */
+typedef struct {
+    uint64_t n;
+    int64_t min, max;
+    uint64_t k;
+    uint32_t bits, shift, nbins, dtype;
+    double entropy;
+    uint64_t descents;
+    uint32_t flags;
+    uint32_t entropy_bits;
+} ahs_features_t;
+
+/* Decision thresholds (Table II; R3-R5).
+ * Valid iff all > 0, k_counting < k_radix, 0 < entropy_coeff <= 1
+ * and entropy_norm is an ahs_entropy_norm. */
+typedef struct {
+    uint64_t n_insertion;   /* 20        : n <= n_insertion -> Insertion (GENERAL) */
+    uint64_t k_counting;    /* 1024      : k <= k_counting  -> COUNTING            */
+    uint64_t k_radix;       /* 1000000   : k >  k_radix and H < coeff*log2(norm)    */
+    double entropy_coeff;   /* 0.7                                                   */
+    uint32_t entropy_norm;  /* AHS_NORM_BUCKETS                                      */
+    uint32_t reserved;      /* must be 0                                             */
+} ahs_thresholds_t;
+
+/* ------------------------------------------------------------ utilities */
+AHS_API const char *ahs_version(void);
+AHS_API const char *ahs_status_string(int status);
+AHS_API void ahs_thresholds_default(ahs_thresholds_t *th);
+
+/* Device workspace for ahs_features (histogram, scan, reduction partials).
+ * Independent of n in this version (~600 KiB); pass n anyway. */
+AHS_API size_t ahs_workspace_bytes(uint64_t n);
+
+/* Device scratch for ahs_sort: a second key buffer (and value buffer when
+ * has_vals) plus per-tile look-back status.  Sufficient for every strategy. */
+AHS_API size_t ahs_sort_tmp_bytes(uint64_t n, int has_vals);
+
+/* Number of 8-bit digit passes ahs_sort will run for this strategy
+ * (RADIX: ceil(bits/8) per Eq. 4; GENERAL: 4; COUNTING: 0 keys-only or 1 KV). */
+AHS_API int ahs_sort_passes(const ahs_features_t *feat, int32_t strategy, int has_vals);
+
+/* ---------------------------------------------------------- the hot path */
+
+/* Feature extraction.  Reads d_keys[0..n) twice (min/max/descents, then the
+ * histogram of (key - min) >> shift), computes H in fp64 on the device, then
+ * copies the ~72-byte result to *feat and SYNCHRONIZES `stream` (the one host
+ * sync of the pipeline: the FSM runs on the host).  d_ws (>= ahs_workspace_bytes)
+ * keeps the histogram and its exclusive scan for a following ahs_sort(COUNTING).
+ * n = 0 returns AHS_OK with feat->flags = EMPTY and launches nothing. */
+AHS_API int ahs_features(const void *d_keys, uint64_t n, int32_t dtype, void *d_ws, size_t ws_bytes,
+                 ahs_features_t *feat, void *stream);
+
+/* The FSM, host only, O(1).  th = NULL uses ahs_thresholds_default.  Rules in
+ * order: EMPTY, CONSTANT, SMALL_N, SMALL_RANGE, LOW_ENTROPY, DEFAULT (see
+ * ahs_rule).  rule may be NULL.  AHS_EINVAL for invalid thresholds. */
+AHS_API int ahs_select(const ahs_features_t *feat, const ahs_thresholds_t *th, int32_t *strategy,
+               int32_t *rule);
+
+/* Sort n keys (and their values) with `strategy`, asynchronously on `stream`.
+ *   d_keys_in / d_vals_in     input (d_vals_in NULL = keys only)
+ *   d_keys_out / d_vals_out   output, ascending, stable (ties keep input order);
+ *                             may alias the inputs (in place: odd pass counts
+ *                             then cost one extra device copy)
+ *   feat                      from ahs_features on the same keys (n, dtype, min,
+ *                             bits, shift must match; AHS_EFEAT otherwise)
+ *   d_ws                      the ahs_features workspace (read for COUNTING)
+ *   d_tmp                     >= ahs_sort_tmp_bytes(n, d_vals_in != NULL)
+ * COUNTING with shift > 0 (only reachable with k_counting > 65536) runs as
+ * radix passes on key - min; the output is identical.  Empty and constant
+ * inputs are copies.  The keys must not change between the two calls. */
+AHS_API int ahs_sort(const void *d_keys_in, const uint32_t *d_vals_in, void *d_keys_out,
+             uint32_t *d_vals_out, uint64_t n, int32_t strategy, const ahs_features_t *feat,
+             const void *d_ws, size_t ws_bytes, void *d_tmp, size_t tmp_bytes, void *stream);
+
+/* End to end from HOST buffers: H2D copy, ahs_features, ahs_select, ahs_sort,
+ * D2H copy, stream sync.  h_* are host pointers (pinned for full speed);
+ * d_scratch (>= ahs_host_scratch_bytes) is carved into the device buffers.
+ * feat / strategy / rule may be NULL. */
+AHS_API size_t ahs_host_scratch_bytes(uint64_t n, int has_vals);
+AHS_API int ahs_sort_host(const void *h_keys_in, const uint32_t *h_vals_in, void *h_keys_out,
+                  uint32_t *h_vals_out, uint64_t n, int32_t dtype, const ahs_thresholds_t *th,
+                  void *d_scratch, size_t scratch_bytes, ahs_features_t *feat,
+                  int32_t *strategy, int32_t *rule, void *stream);
+
+/* -------------------------------------------------------- instrumentation */
+/* Kernels launched by this library since load (all streams, all threads). */
+AHS_API uint64_t ahs_launch_count(void);
+
+/* Per-kernel timing: while enabled, every launch is bracketed by CUDA events
+ * on its own stream.  ahs_profile_read synchronizes those events and returns,
+ * per kernel id (0 .. ahs_kernel_count()-1), the summed milliseconds and the
+ * launch count since ahs_profile_begin. */
+AHS_API int ahs_kernel_count(void);
+AHS_API const char *ahs_kernel_name(int id);
+AHS_API int ahs_profile_begin(void);
+AHS_API int ahs_profile_end(void);
+AHS_API int ahs_profile_read(double *ms, uint64_t *launches, int n_ids);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AHS_H */

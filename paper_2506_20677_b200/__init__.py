@@ -1,0 +1,17 @@
+"""paper_2506_20677_b200 — B200-native hot path of Adaptive Hybrid Sort (arXiv 2506.20677).
+
+A thin Python binding over the C ABI of ``lib/libahs.so`` (include/ahs.h).  The
+functions carry the C names (``ahs_features``, ``ahs_select``, ``ahs_sort``,
+``ahs_sort_host``); they only marshal torch tensors / numpy arrays into
+pointers and sizes.  Every step of the path runs in the library's CUDA kernels;
+there is no CPU fallback: if the extension is missing or no sm_100 device is
+present, calls raise.
+"""
+from ._lib import (  # noqa: F401
+    AHS_COUNTING, AHS_RADIX, AHS_GENERAL, AHS_I32, AHS_U32,
+    STRATEGY_NAMES, RULE_NAMES, FLAG_NAMES, Features, Thresholds, AhsError,
+    lib, lib_path, ahs_version, ahs_thresholds_default, ahs_workspace_bytes, ahs_sort_tmp_bytes,
+    ahs_sort_passes, ahs_features, ahs_select, ahs_sort, ahs_sort_host, ahs_host_scratch_bytes,
+    ahs_launch_count, ahs_kernel_names, ahs_profile_begin, ahs_profile_end, ahs_profile_read,
+    Workspace, sort,
+)

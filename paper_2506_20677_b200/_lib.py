@@ -1,0 +1,261 @@
+"""ctypes marshalling for libahs.so.  Argument meaning: include/ahs.h."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "lib", "libahs.so")
+
+AHS_I32, AHS_U32 = 0, 1
+AHS_COUNTING, AHS_RADIX, AHS_GENERAL = 0, 1, 2
+STRATEGY_NAMES = {AHS_COUNTING: "COUNTING", AHS_RADIX: "RADIX", AHS_GENERAL: "GENERAL"}
+RULE_NAMES = {0: "EMPTY", 1: "CONSTANT", 2: "SMALL_N", 3: "SMALL_RANGE", 4: "LOW_ENTROPY", 5: "DEFAULT"}
+FLAG_NAMES = {1: "EMPTY", 2: "CONSTANT", 4: "BUCKETED", 8: "SORTED", 16: "STRICT_DESC", 32: "SIGNED"}
+
+
+class AhsError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        msg = lib().ahs_status_string(status).decode() if _lib is not None else str(status)
+        super().__init__(f"{where}: {msg} (status {status})")
+
+
+class Features(C.Structure):
+    _fields_ = [("n", C.c_uint64), ("min", C.c_int64), ("max", C.c_int64), ("k", C.c_uint64),
+                ("bits", C.c_uint32), ("shift", C.c_uint32), ("nbins", C.c_uint32), ("dtype", C.c_uint32),
+                ("entropy", C.c_double), ("descents", C.c_uint64), ("flags", C.c_uint32),
+                ("entropy_bits", C.c_uint32)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class Thresholds(C.Structure):
+    _fields_ = [("n_insertion", C.c_uint64), ("k_counting", C.c_uint64), ("k_radix", C.c_uint64),
+                ("entropy_coeff", C.c_double), ("entropy_norm", C.c_uint32), ("reserved", C.c_uint32)]
+
+
+_lib = None
+
+
+def lib_path() -> str:
+    return _LIB_PATH
+
+
+def lib():
+    """Load libahs.so; raise loudly if it was not built (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH):
+            raise ImportError(f"{_LIB_PATH} is missing: run `python -m paper_2506_20677_b200.build` "
+                              "(nvcc, sm_100a); there is no CPU fallback")
+        L = C.CDLL(_LIB_PATH)
+        vp, u64, i32, sz, p_i32 = C.c_void_p, C.c_uint64, C.c_int32, C.c_size_t, C.POINTER(C.c_int32)
+        sig = {
+            "ahs_version": ([], C.c_char_p),
+            "ahs_status_string": ([C.c_int], C.c_char_p),
+            "ahs_thresholds_default": ([C.POINTER(Thresholds)], None),
+            "ahs_workspace_bytes": ([u64], sz),
+            "ahs_sort_tmp_bytes": ([u64, C.c_int], sz),
+            "ahs_sort_passes": ([C.POINTER(Features), i32, C.c_int], C.c_int),
+            "ahs_features": ([vp, u64, i32, vp, sz, C.POINTER(Features), vp], C.c_int),
+            "ahs_select": ([C.POINTER(Features), C.POINTER(Thresholds), p_i32, p_i32], C.c_int),
+            "ahs_sort": ([vp, vp, vp, vp, u64, i32, C.POINTER(Features), vp, sz, vp, sz, vp], C.c_int),
+            "ahs_host_scratch_bytes": ([u64, C.c_int], sz),
+            "ahs_sort_host": ([vp, vp, vp, vp, u64, i32, C.POINTER(Thresholds), vp, sz,
+                               C.POINTER(Features), p_i32, p_i32, vp], C.c_int),
+            "ahs_launch_count": ([], C.c_uint64),
+            "ahs_kernel_count": ([], C.c_int),
+            "ahs_kernel_name": ([C.c_int], C.c_char_p),
+            "ahs_profile_begin": ([], C.c_int),
+            "ahs_profile_end": ([], C.c_int),
+            "ahs_profile_read": ([C.POINTER(C.c_double), C.POINTER(C.c_uint64), C.c_int], C.c_int),
+        }
+        for name, (args, res) in sig.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = L
+    return _lib
+
+
+def _check(rc: int, where: str):
+    if rc != 0:
+        raise AhsError(rc, where)
+
+
+# ------------------------------------------------------------- utilities
+def ahs_version() -> str:
+    return lib().ahs_version().decode()
+
+
+def ahs_thresholds_default(**overrides) -> Thresholds:
+    th = Thresholds()
+    lib().ahs_thresholds_default(C.byref(th))
+    for k, v in overrides.items():
+        setattr(th, k, v)
+    return th
+
+
+def ahs_workspace_bytes(n: int) -> int:
+    return lib().ahs_workspace_bytes(n)
+
+
+def ahs_sort_tmp_bytes(n: int, has_vals: bool) -> int:
+    return lib().ahs_sort_tmp_bytes(n, int(bool(has_vals)))
+
+
+def ahs_host_scratch_bytes(n: int, has_vals: bool) -> int:
+    return lib().ahs_host_scratch_bytes(n, int(bool(has_vals)))
+
+
+def ahs_sort_passes(feat: Features, strategy: int, has_vals: bool) -> int:
+    return lib().ahs_sort_passes(C.byref(feat), strategy, int(bool(has_vals)))
+
+
+def ahs_launch_count() -> int:
+    return lib().ahs_launch_count()
+
+
+def ahs_kernel_names() -> list[str]:
+    L = lib()
+    return [L.ahs_kernel_name(i).decode() for i in range(L.ahs_kernel_count())]
+
+
+def ahs_profile_begin():
+    _check(lib().ahs_profile_begin(), "ahs_profile_begin")
+
+
+def ahs_profile_end():
+    _check(lib().ahs_profile_end(), "ahs_profile_end")
+
+
+def ahs_profile_read() -> dict:
+    L = lib()
+    k = L.ahs_kernel_count()
+    ms = (C.c_double * k)()
+    cnt = (C.c_uint64 * k)()
+    _check(L.ahs_profile_read(ms, cnt, k), "ahs_profile_read")
+    names = ahs_kernel_names()
+    return {names[i]: {"ms": ms[i], "launches": cnt[i]} for i in range(k)}
+
+
+# ------------------------------------------------------ torch marshalling
+def _torch():
+    import torch
+    return torch
+
+
+def _dtype_code(t) -> int:
+    torch = _torch()
+    if t.dtype == torch.int32:
+        return AHS_I32
+    if t.dtype == torch.uint32:
+        return AHS_U32
+    raise TypeError(f"keys must be int32 or uint32 (PAPER.md P:409 integer-only), got {t.dtype}")
+
+
+def _dev_ptr(t):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("expected a CUDA tensor (device pointer)")
+    if not t.is_contiguous():
+        raise ValueError("expected a contiguous tensor")
+    return C.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    torch = _torch()
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return C.c_void_p(stream.cuda_stream)
+
+
+class Workspace:
+    """Device buffers for one n: ws (features) and tmp (sort), owned by torch."""
+
+    def __init__(self, n: int, has_vals: bool, device=None):
+        torch = _torch()
+        device = device or torch.device("cuda", torch.cuda.current_device())
+        self.n, self.has_vals = n, has_vals
+        self.ws_bytes = ahs_workspace_bytes(n)
+        self.tmp_bytes = ahs_sort_tmp_bytes(n, has_vals)
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=device)
+        self.tmp = torch.empty(self.tmp_bytes, dtype=torch.uint8, device=device)
+
+
+def ahs_features(keys, ws: Workspace, stream=None) -> Features:
+    """Run K1-K3 on device keys (int32/uint32 CUDA tensor); synchronizes the stream."""
+    f = Features()
+    rc = lib().ahs_features(_dev_ptr(keys), keys.numel(), _dtype_code(keys), _dev_ptr(ws.ws), ws.ws_bytes,
+                            C.byref(f), _stream(stream))
+    _check(rc, "ahs_features")
+    return f
+
+
+def ahs_select(feat: Features, th: Thresholds | None = None) -> tuple[int, int]:
+    s, r = C.c_int32(), C.c_int32()
+    rc = lib().ahs_select(C.byref(feat), None if th is None else C.byref(th), C.byref(s), C.byref(r))
+    _check(rc, "ahs_select")
+    return s.value, r.value
+
+
+def ahs_sort(keys_in, vals_in, keys_out, vals_out, strategy: int, feat: Features, ws: Workspace,
+             stream=None):
+    rc = lib().ahs_sort(_dev_ptr(keys_in), _dev_ptr(vals_in), _dev_ptr(keys_out), _dev_ptr(vals_out),
+                        keys_in.numel(), strategy, C.byref(feat), _dev_ptr(ws.ws), ws.ws_bytes,
+                        _dev_ptr(ws.tmp), ws.tmp_bytes, _stream(stream))
+    _check(rc, "ahs_sort")
+
+
+def sort(keys, vals=None, th: Thresholds | None = None, ws: Workspace | None = None, out=None,
+         stream=None):
+    """Full pipeline on device tensors: features -> select -> sort.
+
+    Returns (keys_out, vals_out, features, strategy, rule)."""
+    torch = _torch()
+    n = keys.numel()
+    if ws is None:
+        ws = Workspace(n, vals is not None, keys.device)
+    feat = ahs_features(keys, ws, stream)
+    strategy, rule = ahs_select(feat, th)
+    if out is None:
+        ko = torch.empty_like(keys)
+        vo = torch.empty_like(vals) if vals is not None else None
+    else:
+        ko, vo = out
+    ahs_sort(keys, vals, ko, vo, strategy, feat, ws, stream)
+    return ko, vo, feat, strategy, rule
+
+
+def ahs_sort_host(keys: np.ndarray, vals: np.ndarray | None, keys_out: np.ndarray,
+                  vals_out: np.ndarray | None, scratch, th: Thresholds | None = None, stream=None):
+    """End to end from host arrays (numpy or pinned torch CPU tensors) through the C ABI."""
+    def hptr(a):
+        if a is None:
+            return None
+        if isinstance(a, np.ndarray):
+            return a.ctypes.data_as(C.c_void_p)
+        return C.c_void_p(a.data_ptr())
+
+    def code(a):
+        dt = str(a.dtype)
+        if "uint32" in dt:
+            return AHS_U32
+        if "int32" in dt:
+            return AHS_I32
+        raise TypeError(f"keys must be int32 or uint32, got {dt}")
+
+    n = keys.size if isinstance(keys, np.ndarray) else keys.numel()
+    f = Features()
+    s, r = C.c_int32(), C.c_int32()
+    nbytes = scratch.numel() * scratch.element_size()
+    rc = lib().ahs_sort_host(hptr(keys), hptr(vals), hptr(keys_out), hptr(vals_out), n, code(keys),
+                             None if th is None else C.byref(th), _dev_ptr(scratch), nbytes, C.byref(f),
+                             C.byref(s), C.byref(r), _stream(stream))
+    _check(rc, "ahs_sort_host")
+    return f, s.value, r.value

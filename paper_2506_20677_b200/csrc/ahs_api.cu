@@ -1,0 +1,601 @@
+// ahs_api.cu — host side of libahs.so: argument validation, workspace
+// carving, the FSM, pass planning and the kernel launch sequence.
+// Declarations, argument meaning, ownership and error behaviour: include/ahs.h.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "../../include/ahs.h"
+#include "features.cuh"
+#include "sort.cuh"
+
+using namespace ahs;
+
+namespace {
+
+// ------------------------------------------------------------ device info
+struct DevInfo {
+    bool ok = false;
+    bool init = false;
+    int sms = 0;
+};
+std::mutex g_dev_mu;
+DevInfo g_dev[64];
+
+int device_info(int *sms)
+{
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
+        cudaGetLastError();
+        return AHS_ENODEV;
+    }
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    DevInfo &d = g_dev[dev];
+    if (!d.init) {
+        d.init = true;
+        int major = 0;
+        if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+            cudaGetLastError();
+            return AHS_ENODEV;
+        }
+        d.ok = (major == 10);
+        if (d.ok) {
+            // opt-in shared memory sizes (once per device)
+            bool good = true;
+            good &= cudaFuncSetAttribute(k_feat_hist<kHistBlock, kHistUnroll>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kHistSmemBytes) == cudaSuccess;
+            good &= cudaFuncSetAttribute(k_onesweep<false, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)OnesweepCfg<false, 8>::kSmem) == cudaSuccess;
+            good &= cudaFuncSetAttribute(k_onesweep<true, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)OnesweepCfg<true, 8>::kSmem) == cudaSuccess;
+            good &= cudaFuncSetAttribute(k_onesweep<true, 10>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)OnesweepCfg<true, 10>::kSmem) == cudaSuccess;
+            if (!good) {
+                cudaGetLastError();
+                d.ok = false;
+            }
+        }
+    }
+    if (!d.ok) return AHS_ENODEV;
+    *sms = d.sms;
+    return AHS_OK;
+}
+
+// -------------------------------------------------- launch accounting / profiling
+enum KernelId {
+    KID_FEAT_REDUCE = 0,
+    KID_FEAT_HIST,
+    KID_FEAT_FINALIZE,
+    KID_RADIX_HIST,
+    KID_ONESWEEP,
+    KID_ONESWEEP_KV,
+    KID_COUNT_FILL,
+    KID_COUNT_SCATTER_KV,
+    KID_COUNT
+};
+const char *kKernelNames[KID_COUNT] = {"feat_reduce", "feat_hist",   "feat_finalize",
+                                       "radix_hist",  "onesweep",    "onesweep_kv",
+                                       "count_fill",  "count_scatter_kv"};
+
+std::atomic<uint64_t> g_launches{0};
+std::atomic<bool> g_prof{false};
+std::mutex g_prof_mu;
+struct ProfRec {
+    int kid;
+    cudaEvent_t a, b;
+};
+std::vector<ProfRec> g_prof_recs;
+
+template <typename F>
+cudaError_t launch(int kid, cudaStream_t s, F &&f)
+{
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    if (!g_prof.load(std::memory_order_relaxed)) {
+        f();
+        return cudaGetLastError();
+    }
+    ProfRec r{kid, nullptr, nullptr};
+    cudaEventCreate(&r.a);
+    cudaEventCreate(&r.b);
+    cudaEventRecord(r.a, s);
+    f();
+    cudaError_t e = cudaGetLastError();
+    cudaEventRecord(r.b, s);
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_prof_recs.push_back(r);
+    return e;
+}
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// ------------------------------------------------------------ ws layout
+constexpr int kMaxReduceBlocks = 2048;
+struct WsLayout {
+    size_t feat, partials, hist, scan, total;
+};
+WsLayout ws_layout()
+{
+    WsLayout L;
+    size_t o = 0;
+    L.feat = o;
+    o += align_up(sizeof(DevFeatures), 256);
+    L.partials = o;
+    o += align_up(sizeof(Partial) * kMaxReduceBlocks, 256);
+    L.hist = o;  // hist[65536] then scan[65537] contiguous: K1 zeroes both
+    o += (size_t)kMaxBins * 4;
+    L.scan = o;
+    o += align_up((size_t)(kMaxBins + 1) * 4, 256);
+    L.total = o;
+    return L;
+}
+
+// ------------------------------------------------------------ tmp layout
+struct TmpLayout {
+    size_t keys, vals, ctrl, dhist, bucket, ticket, status, status_bytes, total;
+};
+constexpr int kStatusWordsPerTile = 1024;  // 4 passes x 256, or 1 pass x 1024
+TmpLayout tmp_layout(uint64_t n, int has_vals)
+{
+    TmpLayout L;
+    size_t o = 0;
+    L.keys = o;
+    o += align_up(n * 4, 256);
+    L.vals = o;
+    if (has_vals) o += align_up(n * 4, 256);
+    L.ctrl = o;
+    L.dhist = o;
+    L.bucket = o + 4 * 256 * 4;
+    L.ticket = o + 2 * 4 * 256 * 4;  // 8 tickets
+    o += 2 * 4 * 256 * 4 + 256;
+    L.status = o;
+    const uint64_t tiles = (n + kMinTile - 1) / kMinTile;
+    L.status_bytes = (size_t)tiles * kStatusWordsPerTile * 4;
+    o += align_up(L.status_bytes, 256);
+    L.total = o;
+    return L;
+}
+
+inline uint32_t flip_of(int32_t dtype) { return dtype == AHS_I32 ? 0x80000000u : 0u; }
+inline uint32_t umin_of(const ahs_features_t *f) { return (uint32_t)f->min ^ flip_of((int32_t)f->dtype); }
+
+bool thresholds_valid(const ahs_thresholds_t *th)
+{
+    return th->n_insertion > 0 && th->k_counting > 0 && th->k_radix > 0 &&
+           th->k_counting < th->k_radix && th->entropy_coeff > 0.0 && th->entropy_coeff <= 1.0 &&
+           (th->entropy_norm == AHS_NORM_BUCKETS || th->entropy_norm == AHS_NORM_RANGE) &&
+           th->reserved == 0;
+}
+
+int radix_passes(uint32_t bits) { return (int)((bits + 7u) / 8u); }
+
+}  // namespace
+
+// ====================================================================== API
+extern "C" {
+
+const char *ahs_version(void) { return "ahs-b200 0.1 (sm_100a)"; }
+
+const char *ahs_status_string(int s)
+{
+    switch (s) {
+    case AHS_OK: return "ok";
+    case AHS_EINVAL: return "invalid argument";
+    case AHS_ENOSPACE: return "workspace or tmp buffer too small";
+    case AHS_ERANGE: return "n exceeds AHS_MAX_N";
+    case AHS_EFEAT: return "features do not match the keys (n or dtype)";
+    case AHS_ECUDA: return "CUDA error";
+    case AHS_ENODEV: return "no sm_100 CUDA device";
+    default: return "unknown status";
+    }
+}
+
+void ahs_thresholds_default(ahs_thresholds_t *th)
+{
+    if (!th) return;
+    th->n_insertion = 20;      // Table II
+    th->k_counting = 1024;     // Table II
+    th->k_radix = 1000000;     // Table II
+    th->entropy_coeff = 0.7;
+    th->entropy_norm = AHS_NORM_BUCKETS;
+    th->reserved = 0;
+}
+
+size_t ahs_workspace_bytes(uint64_t) { return ws_layout().total; }
+
+size_t ahs_sort_tmp_bytes(uint64_t n, int has_vals) { return tmp_layout(n, has_vals).total; }
+
+int ahs_sort_passes(const ahs_features_t *f, int32_t strategy, int has_vals)
+{
+    if (!f) return AHS_EINVAL;
+    if (f->n == 0 || f->k <= 1) return 0;
+    switch (strategy) {
+    case AHS_GENERAL: return 4;
+    case AHS_RADIX: return radix_passes(f->bits);
+    case AHS_COUNTING:
+        if (f->shift > 0) return radix_passes(f->bits);
+        if (!has_vals) return 0;
+        return f->bits <= 10 ? 1 : radix_passes(f->bits);
+    default: return AHS_EINVAL;
+    }
+}
+
+uint64_t ahs_launch_count(void) { return g_launches.load(); }
+int ahs_kernel_count(void) { return KID_COUNT; }
+const char *ahs_kernel_name(int id) { return (id >= 0 && id < KID_COUNT) ? kKernelNames[id] : ""; }
+
+int ahs_profile_begin(void)
+{
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    for (auto &r : g_prof_recs) {
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    g_prof_recs.clear();
+    g_prof.store(true);
+    return AHS_OK;
+}
+
+int ahs_profile_end(void)
+{
+    g_prof.store(false);
+    return AHS_OK;
+}
+
+int ahs_profile_read(double *ms, uint64_t *launches, int n_ids)
+{
+    if (!ms || !launches || n_ids < KID_COUNT) return AHS_EINVAL;
+    for (int i = 0; i < n_ids; i++) {
+        ms[i] = 0.0;
+        launches[i] = 0;
+    }
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    for (auto &r : g_prof_recs) {
+        if (cudaEventSynchronize(r.b) != cudaSuccess) return AHS_ECUDA;
+        float t = 0.f;
+        if (cudaEventElapsedTime(&t, r.a, r.b) != cudaSuccess) return AHS_ECUDA;
+        ms[r.kid] += t;
+        launches[r.kid] += 1;
+    }
+    return AHS_OK;
+}
+
+// --------------------------------------------------------------- features
+int ahs_features(const void *d_keys, uint64_t n, int32_t dtype, void *d_ws, size_t ws_bytes,
+                 ahs_features_t *feat, void *stream)
+{
+    if (!feat || (dtype != AHS_I32 && dtype != AHS_U32)) return AHS_EINVAL;
+    std::memset(feat, 0, sizeof(*feat));
+    feat->n = n;
+    feat->dtype = (uint32_t)dtype;
+    feat->entropy_bits = AHS_ENTROPY_BITS;
+    if (dtype == AHS_I32) feat->flags |= AHS_FLAG_SIGNED;
+    if (n == 0) {  // empty input exits in O(1)
+        feat->flags |= AHS_FLAG_EMPTY | AHS_FLAG_SORTED;
+        return AHS_OK;
+    }
+    if (n > AHS_MAX_N) return AHS_ERANGE;
+    if (!d_keys || !d_ws || ((uintptr_t)d_keys & 3u) || ((uintptr_t)d_ws & 15u)) return AHS_EINVAL;
+    const WsLayout L = ws_layout();
+    if (ws_bytes < L.total) return AHS_ENOSPACE;
+    int sms = 0;
+    int rc = device_info(&sms);
+    if (rc) return rc;
+
+    cudaStream_t s = (cudaStream_t)stream;
+    char *ws = (char *)d_ws;
+    const uint32_t *keys = (const uint32_t *)d_keys;
+    const uint32_t flip = flip_of(dtype);
+    Partial *partials = (Partial *)(ws + L.partials);
+    uint32_t *hist = (uint32_t *)(ws + L.hist);
+    uint32_t *scan = (uint32_t *)(ws + L.scan);
+    DevFeatures *dfeat = (DevFeatures *)(ws + L.feat);
+
+    const uint64_t nvec = n / 4;
+    uint64_t g1 = (nvec + (uint64_t)kReduceBlock * kReduceUnroll - 1) / ((uint64_t)kReduceBlock * kReduceUnroll);
+    const uint64_t g1max = std::min<uint64_t>(kMaxReduceBlocks, (uint64_t)sms * 8);
+    g1 = std::max<uint64_t>(1, std::min(g1, g1max));
+    const uint32_t nzero = kMaxBins + kMaxBins + 1;  // hist + scan (contiguous)
+
+    cudaError_t e = launch(KID_FEAT_REDUCE, s, [&] {
+        k_feat_reduce<kReduceBlock, kReduceUnroll><<<(unsigned)g1, kReduceBlock, 0, s>>>(
+            keys, n, flip, partials, hist, nzero);
+    });
+    if (e != cudaSuccess) return AHS_ECUDA;
+    uint64_t g2 = (nvec + (uint64_t)kHistBlock * kHistUnroll - 1) / ((uint64_t)kHistBlock * kHistUnroll);
+    g2 = std::max<uint64_t>(1, std::min<uint64_t>(g2, (uint64_t)sms));
+    e = launch(KID_FEAT_HIST, s, [&] {
+        k_feat_hist<kHistBlock, kHistUnroll><<<(unsigned)g2, kHistBlock, kHistSmemBytes, s>>>(
+            keys, n, flip, partials, (int)g1, hist);
+    });
+    if (e != cudaSuccess) return AHS_ECUDA;
+    e = launch(KID_FEAT_FINALIZE, s, [&] {
+        k_feat_finalize<kFinalBlock><<<1, kFinalBlock, 0, s>>>(n, partials, (int)g1, hist, scan, dfeat);
+    });
+    if (e != cudaSuccess) return AHS_ECUDA;
+
+    DevFeatures hf;
+    if (cudaMemcpyAsync(&hf, dfeat, sizeof(hf), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess) {
+        cudaGetLastError();
+        return AHS_ECUDA;
+    }
+    if (dtype == AHS_I32) {
+        feat->min = (int64_t)(int32_t)(hf.umin ^ 0x80000000u);
+        feat->max = (int64_t)(int32_t)(hf.umax ^ 0x80000000u);
+    } else {
+        feat->min = (int64_t)hf.umin;
+        feat->max = (int64_t)hf.umax;
+    }
+    feat->k = hf.k;
+    feat->bits = hf.bits;
+    feat->shift = hf.shift;
+    feat->nbins = hf.nb;
+    feat->entropy = hf.entropy;
+    feat->descents = hf.descents;
+    if (hf.k == 1) feat->flags |= AHS_FLAG_CONSTANT;
+    if (hf.shift > 0) feat->flags |= AHS_FLAG_BUCKETED;
+    if (hf.descents == 0) feat->flags |= AHS_FLAG_SORTED;
+    if (n >= 2 && hf.descents == n - 1) feat->flags |= AHS_FLAG_STRICT_DESC;
+    return AHS_OK;
+}
+
+// ----------------------------------------------------------------- select
+int ahs_select(const ahs_features_t *f, const ahs_thresholds_t *th, int32_t *strategy, int32_t *rule)
+{
+    ahs_thresholds_t def;
+    if (!th) {
+        ahs_thresholds_default(&def);
+        th = &def;
+    }
+    if (!f || !strategy || !thresholds_valid(th)) return AHS_EINVAL;
+    int32_t st, ru;
+    if (f->n == 0) {                       // P:411 empty
+        st = AHS_COUNTING;
+        ru = AHS_RULE_EMPTY;
+    } else if (f->k == 1) {                // P:411 constant (k = 1)
+        st = AHS_COUNTING;
+        ru = AHS_RULE_CONSTANT;
+    } else if (f->n <= th->n_insertion) {  // P:96 n <= 20 -> Insertion
+        st = AHS_GENERAL;
+        ru = AHS_RULE_SMALL_N;
+    } else if (f->k <= th->k_counting) {   // P:96 k <= 1000 (Table II: 1,024) -> Counting
+        st = AHS_COUNTING;
+        ru = AHS_RULE_SMALL_RANGE;
+    } else if (f->k > th->k_radix &&       // P:98 k > 10^6 and H < 0.7 log2 k -> Radix
+               f->entropy < th->entropy_coeff *
+                                std::log2(th->entropy_norm == AHS_NORM_RANGE ? (double)f->k
+                                                                              : (double)f->nbins)) {
+        st = AHS_RADIX;
+        ru = AHS_RULE_LOW_ENTROPY;
+    } else {                               // P:98 otherwise QuickSort
+        st = AHS_GENERAL;
+        ru = AHS_RULE_DEFAULT;
+    }
+    *strategy = st;
+    if (rule) *rule = ru;
+    return AHS_OK;
+}
+
+// ------------------------------------------------------------------- sort
+int ahs_sort(const void *d_keys_in, const uint32_t *d_vals_in, void *d_keys_out, uint32_t *d_vals_out,
+             uint64_t n, int32_t strategy, const ahs_features_t *feat, const void *d_ws, size_t ws_bytes,
+             void *d_tmp, size_t tmp_bytes, void *stream)
+{
+    if (!feat) return AHS_EINVAL;
+    if (strategy != AHS_COUNTING && strategy != AHS_RADIX && strategy != AHS_GENERAL) return AHS_EINVAL;
+    if (feat->n != n) return AHS_EFEAT;
+    if (n == 0) return AHS_OK;
+    if (n > AHS_MAX_N) return AHS_ERANGE;
+    const int32_t dtype = (int32_t)feat->dtype;
+    if (dtype != AHS_I32 && dtype != AHS_U32) return AHS_EFEAT;
+    const bool kv = d_vals_in != nullptr;
+    if (!d_keys_in || !d_keys_out || (kv && !d_vals_out) || ((uintptr_t)d_keys_in & 3u) ||
+        ((uintptr_t)d_keys_out & 3u) || (kv && (((uintptr_t)d_vals_in & 3u) || ((uintptr_t)d_vals_out & 3u))))
+        return AHS_EINVAL;
+    if (feat->k == 0 || feat->k > (1ull << 32) || feat->nbins == 0) return AHS_EFEAT;
+    int sms = 0;
+    int rc = device_info(&sms);
+    if (rc) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    const uint32_t *kin = (const uint32_t *)d_keys_in;
+    uint32_t *kout = (uint32_t *)d_keys_out;
+    const uint32_t flip = flip_of(dtype);
+    const uint32_t umin = umin_of(feat);
+    const uint32_t n32 = (uint32_t)n;
+
+    // constant input: stable identity
+    if (feat->k == 1) {
+        if (kout != kin && cudaMemcpyAsync(kout, kin, n * 4, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+            return AHS_ECUDA;
+        if (kv && d_vals_out != d_vals_in &&
+            cudaMemcpyAsync(d_vals_out, d_vals_in, n * 4, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+            return AHS_ECUDA;
+        return AHS_OK;
+    }
+
+    const WsLayout WL = ws_layout();
+    const bool exact_hist = feat->shift == 0 && feat->nbins == feat->k;
+    // ---- keys-only COUNTING from the feature histogram (Listing 2)
+    if (strategy == AHS_COUNTING && exact_hist && !kv) {
+        if (!d_ws || ws_bytes < WL.total) return AHS_ENOSPACE;
+        const uint32_t *scan = (const uint32_t *)((const char *)d_ws + WL.scan);
+        const uint64_t nvec = n / 4;
+        uint64_t g = (4 * nvec + kFillChunk - 1) / kFillChunk;
+        g = std::max<uint64_t>(1, g);
+        cudaError_t e = launch(KID_COUNT_FILL, s, [&] {
+            k_count_fill<<<(unsigned)g, kFillBlock, 0, s>>>(kout, n32, scan, feat->nbins, flip, umin);
+        });
+        return e == cudaSuccess ? AHS_OK : AHS_ECUDA;
+    }
+
+    // ---- digit passes: plan
+    const TmpLayout TL = tmp_layout(n, kv);
+    if (!d_tmp || tmp_bytes < TL.total || ((uintptr_t)d_tmp & 255u)) return AHS_ENOSPACE;
+    char *tmp = (char *)d_tmp;
+    uint32_t *tkeys = (uint32_t *)(tmp + TL.keys);
+    uint32_t *tvals = kv ? (uint32_t *)(tmp + TL.vals) : nullptr;
+    uint32_t *dhist = (uint32_t *)(tmp + TL.dhist);
+    uint32_t *bucket = (uint32_t *)(tmp + TL.bucket);
+    uint32_t *tickets = (uint32_t *)(tmp + TL.ticket);
+    uint32_t *status = (uint32_t *)(tmp + TL.status);
+
+    const bool count_kv = strategy == AHS_COUNTING && exact_hist && kv && feat->bits <= 10;
+    int passes;
+    uint32_t sub;
+    if (count_kv) {
+        passes = 1;
+        sub = umin;
+    } else if (strategy == AHS_GENERAL) {
+        passes = 4;
+        sub = 0;
+    } else {  // RADIX, or COUNTING that cannot use the histogram directly
+        passes = radix_passes(feat->bits);
+        sub = umin;
+    }
+
+    // zero control words + the status of every pass (one memset)
+    const uint64_t tile = kv ? (uint64_t)OnesweepCfg<true, 8>::kTile : (uint64_t)OnesweepCfg<false, 8>::kTile;
+    const uint64_t tiles = (n + tile - 1) / tile;
+    const int bins_per_pass = count_kv && feat->bits > 8 ? 1024 : 256;
+    const size_t status_words_per_pass = (size_t)tiles * bins_per_pass;
+    const size_t zero_bytes = (TL.status - TL.ctrl) + status_words_per_pass * 4 * passes;
+    if (cudaMemsetAsync(tmp + TL.ctrl, 0, zero_bytes, s) != cudaSuccess) return AHS_ECUDA;
+
+    // in place with an odd pass count: stream the input to tmp first
+    const uint32_t *src_k = kin;
+    const uint32_t *src_v = d_vals_in;
+    const bool inplace = (const void *)kout == d_keys_in || (kv && (const void *)d_vals_out == d_vals_in);
+    if (inplace && (passes & 1)) {
+        if (cudaMemcpyAsync(tkeys, kin, n * 4, cudaMemcpyDeviceToDevice, s) != cudaSuccess) return AHS_ECUDA;
+        if (kv && cudaMemcpyAsync(tvals, d_vals_in, n * 4, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+            return AHS_ECUDA;
+        src_k = tkeys;
+        src_v = tvals;
+    }
+
+    const uint32_t *bases;
+    if (count_kv) {
+        bases = (const uint32_t *)((const char *)d_ws + WL.scan);
+        if (!d_ws || ws_bytes < WL.total) return AHS_ENOSPACE;
+    } else {
+        uint64_t g5 = (n / 4 + (uint64_t)kRHBlock * kRHUnroll - 1) / ((uint64_t)kRHBlock * kRHUnroll);
+        g5 = std::max<uint64_t>(1, std::min<uint64_t>(g5, (uint64_t)sms * 4));
+        // the input transform is applied inside K5; when src is tmp it holds raw keys too
+        cudaError_t e = launch(KID_RADIX_HIST, s, [&] {
+            k_radix_hist<kRHBlock, kRHUnroll><<<(unsigned)g5, kRHBlock, 0, s>>>(
+                src_k, n, flip, sub, passes, dhist, bucket, tickets + 7);
+        });
+        if (e != cudaSuccess) return AHS_ECUDA;
+        bases = bucket;
+    }
+
+    for (int p = 0; p < passes; p++) {
+        const bool first = p == 0, last = p == passes - 1;
+        // destination parity: the last pass always lands in out
+        const bool to_out = ((passes - 1 - p) & 1) == 0;
+        uint32_t *dk = to_out ? kout : tkeys;
+        uint32_t *dv = kv ? (to_out ? d_vals_out : tvals) : nullptr;
+        const uint32_t *sk = first ? src_k : (to_out ? tkeys : kout);
+        const uint32_t *sv = kv ? (first ? src_v : (to_out ? tvals : d_vals_out)) : nullptr;
+        const uint32_t in_flip = first ? flip : 0u, in_sub = first ? sub : 0u;
+        const uint32_t out_flip = last ? flip : 0u, out_add = last ? sub : 0u;
+        const uint32_t shift = count_kv ? 0u : 8u * (uint32_t)p;
+        uint32_t *st = status + (size_t)p * status_words_per_pass;
+        uint32_t *tk = tickets + p;
+        const uint32_t *bb = count_kv ? bases : bases + 256 * p;
+        cudaError_t e;
+        if (!kv) {
+            using C = OnesweepCfg<false, 8>;
+            e = launch(KID_ONESWEEP, s, [&] {
+                k_onesweep<false, 8><<<(unsigned)tiles, kSortBlock, C::kSmem, s>>>(
+                    sk, nullptr, dk, nullptr, n32, shift, in_flip, in_sub, out_flip, out_add, bb, st, tk);
+            });
+        } else if (count_kv && feat->bits > 8) {
+            using C = OnesweepCfg<true, 10>;
+            e = launch(KID_COUNT_SCATTER_KV, s, [&] {
+                k_onesweep<true, 10><<<(unsigned)tiles, kSortBlock, C::kSmem, s>>>(
+                    sk, sv, dk, dv, n32, shift, in_flip, in_sub, out_flip, out_add, bb, st, tk);
+            });
+        } else {
+            using C = OnesweepCfg<true, 8>;
+            e = launch(count_kv ? KID_COUNT_SCATTER_KV : KID_ONESWEEP_KV, s, [&] {
+                k_onesweep<true, 8><<<(unsigned)tiles, kSortBlock, C::kSmem, s>>>(
+                    sk, sv, dk, dv, n32, shift, in_flip, in_sub, out_flip, out_add, bb, st, tk);
+            });
+        }
+        if (e != cudaSuccess) return AHS_ECUDA;
+    }
+    return AHS_OK;
+}
+
+// -------------------------------------------------------------- host e2e
+size_t ahs_host_scratch_bytes(uint64_t n, int has_vals)
+{
+    const size_t kb = align_up(n * 4, 256);
+    return kb * (has_vals ? 4 : 2) + ws_layout().total + tmp_layout(n, has_vals).total;
+}
+
+int ahs_sort_host(const void *h_keys_in, const uint32_t *h_vals_in, void *h_keys_out, uint32_t *h_vals_out,
+                  uint64_t n, int32_t dtype, const ahs_thresholds_t *th, void *d_scratch, size_t scratch_bytes,
+                  ahs_features_t *feat, int32_t *strategy, int32_t *rule, void *stream)
+{
+    if (dtype != AHS_I32 && dtype != AHS_U32) return AHS_EINVAL;
+    const bool kv = h_vals_in != nullptr;
+    if (n > 0 && (!h_keys_in || !h_keys_out || (kv && !h_vals_out) || !d_scratch)) return AHS_EINVAL;
+    if (n > AHS_MAX_N) return AHS_ERANGE;
+    if (n > 0 && scratch_bytes < ahs_host_scratch_bytes(n, kv)) return AHS_ENOSPACE;
+    if ((uintptr_t)d_scratch & 255u) return AHS_EINVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    ahs_features_t f;
+    int32_t st = AHS_COUNTING, ru = AHS_RULE_EMPTY;
+    if (n == 0) {
+        int rc = ahs_features(nullptr, 0, dtype, nullptr, 0, &f, stream);
+        if (rc) return rc;
+        rc = ahs_select(&f, th, &st, &ru);
+        if (rc) return rc;
+    } else {
+        const size_t kb = align_up(n * 4, 256);
+        char *p = (char *)d_scratch;
+        void *dk_in = p;
+        p += kb;
+        void *dk_out = p;
+        p += kb;
+        uint32_t *dv_in = nullptr, *dv_out = nullptr;
+        if (kv) {
+            dv_in = (uint32_t *)p;
+            p += kb;
+            dv_out = (uint32_t *)p;
+            p += kb;
+        }
+        void *ws = p;
+        p += ws_layout().total;
+        void *tmp = p;
+        const size_t tmpb = tmp_layout(n, kv).total;
+        if (cudaMemcpyAsync(dk_in, h_keys_in, n * 4, cudaMemcpyHostToDevice, s) != cudaSuccess) return AHS_ECUDA;
+        if (kv && cudaMemcpyAsync(dv_in, h_vals_in, n * 4, cudaMemcpyHostToDevice, s) != cudaSuccess)
+            return AHS_ECUDA;
+        int rc = ahs_features(dk_in, n, dtype, ws, ws_layout().total, &f, stream);
+        if (rc) return rc;
+        rc = ahs_select(&f, th, &st, &ru);
+        if (rc) return rc;
+        rc = ahs_sort(dk_in, dv_in, dk_out, dv_out, n, st, &f, ws, ws_layout().total, tmp, tmpb, stream);
+        if (rc) return rc;
+        if (cudaMemcpyAsync(h_keys_out, dk_out, n * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+            return AHS_ECUDA;
+        if (kv && cudaMemcpyAsync(h_vals_out, dv_out, n * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+            return AHS_ECUDA;
+        if (cudaStreamSynchronize(s) != cudaSuccess) return AHS_ECUDA;
+    }
+    if (feat) *feat = f;
+    if (strategy) *strategy = st;
+    if (rule) *rule = ru;
+    return AHS_OK;
+}
+
+}  // extern "C"

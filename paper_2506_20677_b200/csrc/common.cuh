@@ -1,0 +1,153 @@
+// common.cuh — device-side helpers shared by the libahs kernels (sm_100a only).
+//
+// Key space: every kernel works on the ORDERED image u = key ^ flip of a key
+// (flip = 0x80000000 for int32, 0 for uint32), so unsigned comparison of u is
+// the key's own order and u - u_min = key - min (mod 2^32).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ahs {
+
+constexpr uint32_t kFull = 0xffffffffu;
+
+// Per-block result of K1 feat_reduce (ws); reduced again by K2 and K3.
+struct Partial {
+    uint32_t mn, mx;   // ordered space
+    uint64_t desc;
+};
+
+// Device-side feature record, written by K3 into ws and copied to the host.
+struct DevFeatures {
+    uint32_t umin, umax;
+    uint64_t descents;
+    uint64_t k;
+    uint32_t bits, shift, nb, pad0;
+    double entropy;
+    uint64_t pad1[2];
+};
+static_assert(sizeof(DevFeatures) == 64, "DevFeatures is 64 bytes");
+
+// Derived range quantities (§III.A line 96 k = max - min + 1;
+// DESIGN.md R1: shift = max(0, bitlen(k-1) - 16), nb = ((k-1) >> shift) + 1).
+struct Range {
+    uint64_t k;
+    uint32_t bits, shift, nb;
+};
+
+__host__ __device__ __forceinline__ Range derive_range(uint32_t umin, uint32_t umax, uint32_t entropy_bits)
+{
+    Range r;
+    r.k = (uint64_t)(umax - umin) + 1ull;
+    uint64_t km1 = r.k - 1ull;
+#ifdef __CUDA_ARCH__
+    r.bits = km1 ? 64u - (uint32_t)__clzll((long long)km1) : 0u;
+#else
+    r.bits = 0;
+    while (km1 >> r.bits) r.bits++;
+#endif
+    r.shift = r.bits > entropy_bits ? r.bits - entropy_bits : 0u;
+    r.nb = (uint32_t)(((r.k - 1ull) >> r.shift) + 1ull);
+    return r;
+}
+
+// ---------------------------------------------------------------- memory ops
+__device__ __forceinline__ uint4 ld_nc_v4(const uint4 *p)
+{
+    uint4 r;
+    asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+        : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+        : "l"(p));
+    return r;
+}
+
+__device__ __forceinline__ uint32_t ld_nc(const uint32_t *p)
+{
+    uint32_t r;
+    asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
+    return r;
+}
+
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t *p)
+{
+    uint32_t r;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(p) : "memory");
+    return r;
+}
+
+__device__ __forceinline__ void st_relaxed(uint32_t *p, uint32_t v)
+{
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void st_cs_v4(uint4 *p, uint4 v)
+{
+    asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+                 "r"(v.w)
+                 : "memory");
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt()
+{
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// Split of a 4-byte-aligned key array into an unaligned head (< 4 keys), a
+// 16-byte-aligned body of uint4 vectors, and a tail (< 4 keys).
+struct VecSplit {
+    uint64_t head, nvec, tail0;
+};
+
+__device__ __forceinline__ VecSplit vec_split(const uint32_t *p, uint64_t n)
+{
+    VecSplit s;
+    uint64_t mis = ((16u - ((uintptr_t)p & 15u)) & 15u) >> 2;
+    s.head = mis < n ? mis : n;
+    s.nvec = (n - s.head) >> 2;
+    s.tail0 = s.head + 4ull * s.nvec;
+    return s;
+}
+
+// Visit every key once with warp-uniform calls op(u, active) where
+// u = key ^ flip.  All 32 lanes of a warp call op together (so op may use
+// warp collectives); inactive lanes pass active = false.  Body: uint4
+// streaming loads, UNROLL vectors in flight per thread, grid-stride.
+// Head/tail (<= 6 keys): warp 0 of block 0.
+template <int UNROLL, typename Op>
+__device__ __forceinline__ void for_each_key(const uint32_t *__restrict__ keys, uint64_t n,
+                                             uint32_t flip, Op &op)
+{
+    const VecSplit sp = vec_split(keys, n);
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint4 *vp = reinterpret_cast<const uint4 *>(keys + sp.head);
+    for (uint64_t vb = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); vb < sp.nvec;
+         vb += stride * UNROLL) {
+        uint4 x[UNROLL];
+#pragma unroll
+        for (int u = 0; u < UNROLL; u++) {
+            uint64_t v = vb + (uint64_t)u * stride + lane;
+            x[u] = v < sp.nvec ? ld_nc_v4(vp + v) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < UNROLL; u++) {
+            uint64_t v = vb + (uint64_t)u * stride + lane;
+            bool act = v < sp.nvec;
+            op(x[u].x ^ flip, act);
+            op(x[u].y ^ flip, act);
+            op(x[u].z ^ flip, act);
+            op(x[u].w ^ flip, act);
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x < 32) {
+        uint64_t i = lane < 3 ? lane : sp.tail0 + (lane - 3);
+        bool act = lane < 3 ? i < sp.head : (lane < 6 && i < n);
+        uint32_t u = act ? (keys[i] ^ flip) : 0u;
+        op(u, act);
+    }
+}
+
+}  // namespace ahs

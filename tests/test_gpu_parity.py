@@ -1,0 +1,277 @@
+"""T4/T5: the CUDA path through the C ABI against the CPU oracle.
+
+Bar: features n/min/max/k/bits/shift/nbins/descents bit-exact, |dH| <= 1e-9
+(BASELINE.json north_star), strategy + rule identical, keys and values
+bit-exact (the unique stable order).  Sizes span several tiles (8192 keys /
+4096 pairs) with ragged tails; full BASELINE.json configs at the end.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+import paper_2506_20677_b200 as ahs  # noqa: E402
+
+H_TOL = 1e-9
+
+
+@pytest.fixture(scope="module", autouse=True)
+def cuda_ready():
+    assert torch.cuda.is_available(), "gpu tests need a CUDA device"
+    ahs.lib()
+
+
+def to_dev(a: np.ndarray, misalign: int = 0):
+    """Upload; with misalign > 0 the tensor starts `misalign` elements into a buffer."""
+    t = torch.from_numpy(a.view(np.int32) if a.dtype == np.uint32 else a)
+    if a.dtype == np.uint32:
+        base = torch.empty(a.size + misalign, dtype=torch.int32, device="cuda")
+        base[misalign:].copy_(t)
+        return base.view(torch.uint32)[misalign:]
+    base = torch.empty(a.size + misalign, dtype=torch.int32, device="cuda")
+    base[misalign:].copy_(t)
+    return base[misalign:]
+
+
+def to_host(t) -> np.ndarray:
+    if t.dtype == torch.uint32:
+        return t.view(torch.int32).cpu().numpy().view(np.uint32)
+    return t.cpu().numpy()
+
+
+def check_features(f, of):
+    assert f.n == of.n
+    if of.n == 0:
+        return
+    assert (f.min, f.max, f.k, f.bits, f.shift, f.nbins, f.descents) == \
+        (of.min, of.max, of.k, of.bits, of.shift, of.nb, of.descents)
+    assert abs(f.entropy - of.entropy) <= H_TOL
+    assert f.flags == of.flags
+
+
+def run_gpu(keys, vals=None, strategy=None, misalign=0, inplace=False, th=None, stream=None):
+    n = keys.size
+    dk = to_dev(keys, misalign)
+    dv = to_dev(vals, misalign) if vals is not None else None
+    ws = ahs.Workspace(n, vals is not None)
+    f = ahs.ahs_features(dk, ws, stream)
+    s, r = ahs.ahs_select(f, th)
+    if strategy is not None:
+        s = strategy
+    if inplace:
+        ko, vo = dk, dv
+    else:
+        ko = to_dev(np.zeros_like(keys), misalign)
+        vo = to_dev(np.zeros_like(vals), misalign) if vals is not None else None
+    ahs.ahs_sort(dk, dv, ko, vo, s, f, ws, stream)
+    torch.cuda.synchronize()
+    return f, s, r, to_host(ko), (to_host(vo) if vo is not None else None)
+
+
+def expected(keys, vals):
+    order = np.argsort(keys, kind="stable")  # only used to cross-check the oracle below
+    r = oracle.ahs(keys, vals)
+    assert np.array_equal(r["keys"], keys[order])
+    return r
+
+
+def check_pipeline(keys, vals=None, **kw):
+    f, s, r, ko, vo = run_gpu(keys, vals, **kw)
+    ref = oracle.ahs(keys, vals)
+    check_features(f, ref["features"])
+    assert ahs.STRATEGY_NAMES[s] == oracle.gpu_strategy(ref["strategy4"])
+    assert ahs.RULE_NAMES[r] == oracle.RULE_NAMES[ref["rule"]]
+    assert np.array_equal(ko, ref["keys"])
+    if vals is not None:
+        assert np.array_equal(vo, ref["vals"])
+    return f, s, r
+
+
+def check_forced(keys, vals, strategy, **kw):
+    f, s, r, ko, vo = run_gpu(keys, vals, strategy=strategy, **kw)
+    ok, ov = oracle.sort(keys, vals, oracle.QUICK)   # the unique stable order
+    assert np.array_equal(ko, ok), ahs.STRATEGY_NAMES[strategy]
+    if vals is not None:
+        assert np.array_equal(vo, ov), ahs.STRATEGY_NAMES[strategy]
+
+
+# --------------------------------------------------------------- T4 small
+
+SIZES = [1, 2, 3, 4, 5, 7, 8, 15, 16, 17, 21, 33, 1000, 4095, 4096, 4097, 8191, 8192, 8193,
+         3 * 8192 + 77, 65537, 250_001]
+
+FAMILIES = {
+    "u1000": lambda n, s: synth.uniform_range(s, n, 0, 999),
+    "neg16": lambda n, s: synth.uniform_range(s, n, -8, 7),
+    "full32": lambda n, s: synth.uniform_range(s, n, -(2 ** 31), 2 ** 31 - 1),
+    "range3M": lambda n, s: synth.uniform_range(s, n, -1_500_000, 1_500_000),
+    "zipf_wide": lambda n, s: synth.cfg3(n, seed=s),
+    "sawtooth": lambda n, s: synth.sawtooth(n, period=97),
+    "desc": lambda n, s: synth.cfg4b(n),
+    "alt_extremes": lambda n, s: synth.alternating(n, -(2 ** 31), 2 ** 31 - 1),
+    "const": lambda n, s: synth.cfg4c(n),
+}
+
+
+@pytest.mark.parametrize("family", list(FAMILIES))
+def test_pipeline_small_sizes(family):
+    for i, n in enumerate(SIZES):
+        keys = FAMILIES[family](n, 100 + i)
+        check_pipeline(keys)
+        check_pipeline(keys, np.arange(n, dtype=np.uint32))
+
+
+def test_pipeline_empty():
+    for vals in (None, np.zeros(0, np.uint32)):
+        f, s, r, ko, vo = run_gpu(np.zeros(0, np.int32), vals)
+        assert f.n == 0 and ahs.RULE_NAMES[r] == "EMPTY" and ko.size == 0
+
+
+@pytest.mark.parametrize("dtype", ["i32", "u32"])
+@pytest.mark.parametrize("strategy", [0, 1, 2])
+def test_forced_strategies(dtype, strategy):
+    rng = np.random.default_rng(strategy)
+    for i, n in enumerate([1, 2, 17, 4097, 8193, 40_000]):
+        for lo, hi in ((0, 999), (-5, 5), (-(2 ** 31), 2 ** 31 - 1), (3, 70_000), (0, 2 ** 24)):
+            if dtype == "u32":
+                lo, hi = lo + 2 ** 31, hi + 2 ** 31
+            keys = synth.uniform_range(i * 7 + strategy, n, lo, hi, dtype=np.int64)
+            keys = keys.astype(np.int32 if dtype == "i32" else np.uint32)
+            vals = rng.integers(0, 2 ** 32, n, dtype=np.uint64).astype(np.uint32)
+            check_forced(keys, None, strategy)
+            check_forced(keys, vals, strategy)
+
+
+@pytest.mark.parametrize("misalign", [1, 2, 3])
+def test_misaligned_pointers(misalign):
+    for n in (5, 4099, 20_003):
+        for fam in ("u1000", "full32", "range3M"):
+            keys = FAMILIES[fam](n, misalign)
+            check_pipeline(keys, misalign=misalign)
+            check_pipeline(keys, np.arange(n, dtype=np.uint32), misalign=misalign)
+
+
+@pytest.mark.parametrize("strategy", [0, 1, 2])
+def test_in_place(strategy):
+    # RADIX on k ~ 2^17 has 3 passes (odd): exercises the extra copy
+    for lo, hi in ((0, 999), (0, 130_000), (-(2 ** 31), 2 ** 31 - 1), (0, 200)):
+        keys = synth.uniform_range(5, 30_011, lo, hi)
+        vals = np.arange(keys.size, dtype=np.uint32)
+        check_forced(keys, None, strategy, inplace=True)
+        check_forced(keys, vals, strategy, inplace=True)
+
+
+def test_unsigned_full_range_and_extremes():
+    keys = np.array([0, 2 ** 32 - 1, 2 ** 31, 2 ** 31 - 1, 1, 2 ** 32 - 1, 0] * 3001, dtype=np.uint32)
+    check_pipeline(keys)
+    check_pipeline(keys, np.arange(keys.size, dtype=np.uint32))
+
+
+def test_side_stream():
+    s = torch.cuda.Stream()
+    keys = synth.cfg2(100_003)
+    with torch.cuda.stream(s):
+        f, st, r, ko, vo = run_gpu(keys, None, stream=s)
+    assert np.array_equal(ko, np.sort(keys))
+
+
+def test_thresholds_custom():
+    keys = synth.uniform_range(3, 50_000, 0, 4999)
+    th = ahs.ahs_thresholds_default(k_counting=8192)
+    f, s, r, ko, vo = run_gpu(keys, np.arange(keys.size, dtype=np.uint32), th=th)
+    assert ahs.STRATEGY_NAMES[s] == "COUNTING"  # 13 bits: counting via 2 radix passes on key - min
+    ok, ov = oracle.sort(keys, np.arange(keys.size, dtype=np.uint32), oracle.COUNTING)
+    assert np.array_equal(ko, ok) and np.array_equal(vo, ov)
+    th = ahs.ahs_thresholds_default(k_counting=1 << 20)
+    keys = synth.uniform_range(4, 50_000, 0, 200_000)  # shift > 0: histogram bucketed
+    f, s, r, ko, vo = run_gpu(keys, None, th=th)
+    assert ahs.STRATEGY_NAMES[s] == "COUNTING" and f.shift > 0
+    assert np.array_equal(ko, np.sort(keys))
+
+
+def test_host_entry_point():
+    keys = synth.cfg1(1 << 18)
+    vals = np.arange(keys.size, dtype=np.uint32)
+    ko, vo = np.empty_like(keys), np.empty_like(vals)
+    scratch = torch.empty(ahs.ahs_host_scratch_bytes(keys.size, True), dtype=torch.uint8, device="cuda")
+    f, s, r = ahs.ahs_sort_host(keys, vals, ko, vo, scratch)
+    ref = oracle.ahs(keys, vals)
+    check_features(f, ref["features"])
+    assert np.array_equal(ko, ref["keys"]) and np.array_equal(vo, ref["vals"])
+
+
+def test_launch_count_and_profile():
+    keys = synth.cfg2(1 << 16)
+    c0 = ahs.ahs_launch_count()
+    ahs.ahs_profile_begin()
+    run_gpu(keys, None)
+    ahs.ahs_profile_end()
+    prof = ahs.ahs_profile_read()
+    assert ahs.ahs_launch_count() - c0 == 3 + 1 + 4
+    assert prof["onesweep"]["launches"] == 4 and prof["onesweep"]["ms"] > 0
+
+
+def test_repeat_deterministic():
+    keys = synth.cfg3(300_000)
+    a = run_gpu(keys, None)
+    b = run_gpu(keys, None)
+    assert a[0].entropy == b[0].entropy and np.array_equal(a[3], b[3])
+
+
+def test_hist_overflow_guard_bits():
+    # > 32768 copies of a few values in a 2^16-bucket histogram within one CTA: exercises the
+    # 15-bit counters' overflow path (mode B)
+    n = 3_000_000
+    keys = np.full(n, 5, np.int32)
+    keys[::2] = 2 ** 30
+    keys[1::1000] = -(2 ** 31)
+    keys[7::777] = 123456789
+    check_pipeline(keys)
+
+
+# ------------------------------------------------------ T5 full configs
+
+FULL = ["cfg1", "cfg2", "cfg2kv", "cfg3", "cfg4a", "cfg4b", "cfg4c", "cfg4d"]
+
+
+@pytest.mark.parametrize("cfg", FULL)
+def test_config_full_size(cfg):
+    keys, vals, _ = synth.make(cfg)
+    f, s, r = check_pipeline(keys, vals)
+    expect = {"cfg1": "COUNTING", "cfg2": "GENERAL", "cfg2kv": "GENERAL", "cfg3": "RADIX",
+              "cfg4a": "GENERAL", "cfg4b": "GENERAL", "cfg4c": "COUNTING", "cfg4d": "COUNTING"}[cfg]
+    assert ahs.STRATEGY_NAMES[s] == expect
+
+
+@pytest.mark.parametrize("r", synth.CFG5_R)
+def test_cfg5_full_size(r):
+    """2^28 pairs: features vs the oracle; the sort by the properties that
+    define the unique stable order (sorted, payload permutation consistent
+    with the keys, ties in index order) plus oracle-computed samples."""
+    keys, vals = synth.cfg5(r)
+    n = keys.size
+    f, s, rule, ko, vo = run_gpu(keys, vals)
+    of, hist = oracle.features(keys, with_hist=True)
+    check_features(f, of)
+    s4, r4 = oracle.select(of)
+    assert ahs.STRATEGY_NAMES[s] == oracle.gpu_strategy(s4)
+    assert ahs.RULE_NAMES[rule] == oracle.RULE_NAMES[r4]
+    assert np.all(ko[1:] >= ko[:-1])
+    seen = np.zeros(n, dtype=bool)
+    seen[vo] = True
+    assert seen.all()
+    assert np.array_equal(ko, keys[vo])
+    tie = ko[1:] == ko[:-1]
+    assert np.all(vo[1:][tie] > vo[:-1][tie])
+    if of.shift == 0:
+        # sampled slots: out[i] = min + the bin holding rank i (oracle histogram)
+        cum = np.cumsum(hist.astype(np.int64))
+        idx = synth.uniform_below(synth.stream(99, 4096), n).astype(np.int64)
+        b = np.searchsorted(cum, idx, side="right")
+        assert np.array_equal(ko[idx].astype(np.int64), b + of.min)
