@@ -5,6 +5,7 @@
 
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -22,11 +23,13 @@ struct DevInfo {
     bool ok = false;
     bool init = false;
     int sms = 0;
+    int hist_clusters = 0;  // co-resident K2 clusters
 };
 std::mutex g_dev_mu;
 DevInfo g_dev[64];
 
-int device_info(int *sms)
+#define K2_KERNEL k_feat_hist<kHistBlock, kHistUnroll, kHistCluster>
+int device_info(int *sms, int *hist_clusters = nullptr)
 {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
@@ -47,15 +50,35 @@ int device_info(int *sms)
         if (d.ok) {
             // opt-in shared memory sizes (once per device)
             bool good = true;
-            good &= cudaFuncSetAttribute(k_feat_hist<kHistBlock, kHistUnroll>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+            good &= cudaFuncSetAttribute(K2_KERNEL, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          kHistSmemBytes) == cudaSuccess;
-            good &= cudaFuncSetAttribute(k_onesweep<false, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)OnesweepCfg<false, 8>::kSmem) == cudaSuccess;
-            good &= cudaFuncSetAttribute(k_onesweep<true, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)OnesweepCfg<true, 8>::kSmem) == cudaSuccess;
-            good &= cudaFuncSetAttribute(k_onesweep<true, 10>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)OnesweepCfg<true, 10>::kSmem) == cudaSuccess;
+            if (good) {
+                cudaLaunchConfig_t cfg = {};
+                cfg.gridDim = dim3(kHistCluster * 64);
+                cfg.blockDim = dim3(kHistBlock);
+                cfg.dynamicSmemBytes = kHistSmemBytes;
+                cudaLaunchAttribute attr;
+                attr.id = cudaLaunchAttributeClusterDimension;
+                attr.val.clusterDim.x = kHistCluster;
+                attr.val.clusterDim.y = 1;
+                attr.val.clusterDim.z = 1;
+                cfg.attrs = &attr;
+                cfg.numAttrs = 1;
+                int nc = 0;
+                if (cudaOccupancyMaxActiveClusters(&nc, (void *)K2_KERNEL, &cfg) != cudaSuccess || nc < 1) {
+                    cudaGetLastError();
+                    nc = d.sms / kHistCluster;
+                }
+                d.hist_clusters = nc;
+            }
+good &= cudaFuncSetAttribute(k_onesweep<false, kRankAtomic>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)OnesweepCfg<false>::kSmem) == cudaSuccess;
+            good &= cudaFuncSetAttribute(k_onesweep<true, kRankAtomic>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)OnesweepCfg<true>::kSmem) == cudaSuccess;
+            good &= cudaFuncSetAttribute(k_onesweep<false, kRankBallot>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)OnesweepCfg<false>::kSmem) == cudaSuccess;
+            good &= cudaFuncSetAttribute(k_onesweep<true, kRankBallot>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)OnesweepCfg<true>::kSmem) == cudaSuccess;
             if (!good) {
                 cudaGetLastError();
                 d.ok = false;
@@ -64,6 +87,7 @@ int device_info(int *sms)
     }
     if (!d.ok) return AHS_ENODEV;
     *sms = d.sms;
+    if (hist_clusters) *hist_clusters = d.hist_clusters;
     return AHS_OK;
 }
 
@@ -116,8 +140,9 @@ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 // ------------------------------------------------------------ ws layout
 constexpr int kMaxReduceBlocks = 2048;
+constexpr int kMaxHistRows = 64;  // K2 clusters (rows of partial histograms)
 struct WsLayout {
-    size_t feat, partials, hist, scan, total;
+    size_t feat, partials, fctrl, ovf, hist, scan, parts, total;
 };
 WsLayout ws_layout()
 {
@@ -127,10 +152,16 @@ WsLayout ws_layout()
     o += align_up(sizeof(DevFeatures), 256);
     L.partials = o;
     o += align_up(sizeof(Partial) * kMaxReduceBlocks, 256);
-    L.hist = o;  // hist[65536] then scan[65537] contiguous: K1 zeroes both
+    L.fctrl = o;
+    o += align_up(sizeof(FinalCtrl), 256);
+    L.ovf = o;
+    o += (size_t)kMaxBins * 4;
+    L.hist = o;
     o += (size_t)kMaxBins * 4;
     L.scan = o;
     o += align_up((size_t)(kMaxBins + 1) * 4, 256);
+    L.parts = o;
+    o += (size_t)kMaxHistRows * kMaxBins * 4;
     L.total = o;
     return L;
 }
@@ -139,7 +170,7 @@ WsLayout ws_layout()
 struct TmpLayout {
     size_t keys, vals, ctrl, dhist, bucket, ticket, status, status_bytes, total;
 };
-constexpr int kStatusWordsPerTile = 1024;  // 4 passes x 256, or 1 pass x 1024
+constexpr int kStatusWordsPerTile = 4 * kBins;  // up to 4 passes
 TmpLayout tmp_layout(uint64_t n, int has_vals)
 {
     TmpLayout L;
@@ -173,6 +204,18 @@ bool thresholds_valid(const ahs_thresholds_t *th)
 }
 
 int radix_passes(uint32_t bits) { return (int)((bits + 7u) / 8u); }
+
+// Warp-ranking variant of the onesweep pass (env AHS_RANK=atomic|ballot, for measurement).
+int rank_variant()
+{
+    static int v = [] {
+        const char *e = getenv("AHS_RANK");
+        return (e && e[0] == 'b') ? kRankBallot : kRankAtomic;
+    }();
+    return v;
+}
+
+
 
 }  // namespace
 
@@ -220,7 +263,7 @@ int ahs_sort_passes(const ahs_features_t *f, int32_t strategy, int has_vals)
     case AHS_COUNTING:
         if (f->shift > 0) return radix_passes(f->bits);
         if (!has_vals) return 0;
-        return f->bits <= 10 ? 1 : radix_passes(f->bits);
+        return f->bits <= 8 ? 1 : radix_passes(f->bits);
     default: return AHS_EINVAL;
     }
 }
@@ -283,8 +326,8 @@ int ahs_features(const void *d_keys, uint64_t n, int32_t dtype, void *d_ws, size
     if (!d_keys || !d_ws || ((uintptr_t)d_keys & 3u) || ((uintptr_t)d_ws & 15u)) return AHS_EINVAL;
     const WsLayout L = ws_layout();
     if (ws_bytes < L.total) return AHS_ENOSPACE;
-    int sms = 0;
-    int rc = device_info(&sms);
+    int sms = 0, hclusters = 0;
+    int rc = device_info(&sms, &hclusters);
     if (rc) return rc;
 
     cudaStream_t s = (cudaStream_t)stream;
@@ -292,30 +335,38 @@ int ahs_features(const void *d_keys, uint64_t n, int32_t dtype, void *d_ws, size
     const uint32_t *keys = (const uint32_t *)d_keys;
     const uint32_t flip = flip_of(dtype);
     Partial *partials = (Partial *)(ws + L.partials);
+    FinalCtrl *fctrl = (FinalCtrl *)(ws + L.fctrl);
+    uint32_t *ovf = (uint32_t *)(ws + L.ovf);
     uint32_t *hist = (uint32_t *)(ws + L.hist);
     uint32_t *scan = (uint32_t *)(ws + L.scan);
+    uint32_t *parts = (uint32_t *)(ws + L.parts);
     DevFeatures *dfeat = (DevFeatures *)(ws + L.feat);
 
     const uint64_t nvec = n / 4;
     uint64_t g1 = (nvec + (uint64_t)kReduceBlock * kReduceUnroll - 1) / ((uint64_t)kReduceBlock * kReduceUnroll);
     const uint64_t g1max = std::min<uint64_t>(kMaxReduceBlocks, (uint64_t)sms * 8);
     g1 = std::max<uint64_t>(1, std::min(g1, g1max));
-    const uint32_t nzero = kMaxBins + kMaxBins + 1;  // hist + scan (contiguous)
 
     cudaError_t e = launch(KID_FEAT_REDUCE, s, [&] {
         k_feat_reduce<kReduceBlock, kReduceUnroll><<<(unsigned)g1, kReduceBlock, 0, s>>>(
-            keys, n, flip, partials, hist, nzero);
+            keys, n, flip, partials, ovf, kMaxBins, fctrl);
     });
     if (e != cudaSuccess) return AHS_ECUDA;
-    uint64_t g2 = (nvec + (uint64_t)kHistBlock * kHistUnroll - 1) / ((uint64_t)kHistBlock * kHistUnroll);
-    g2 = std::max<uint64_t>(1, std::min<uint64_t>(g2, (uint64_t)sms));
+    // K2: clusters of kHistCluster CTAs, one partial-histogram row per cluster
+    const uint64_t per_cluster = (uint64_t)kHistBlock * kHistUnroll * kHistCluster;
+    uint64_t rows = (nvec + per_cluster - 1) / per_cluster;
+    rows = std::max<uint64_t>(1, std::min<uint64_t>(rows, (uint64_t)std::min(hclusters, kMaxHistRows)));
     e = launch(KID_FEAT_HIST, s, [&] {
-        k_feat_hist<kHistBlock, kHistUnroll><<<(unsigned)g2, kHistBlock, kHistSmemBytes, s>>>(
-            keys, n, flip, partials, (int)g1, hist);
+        K2_KERNEL<<<(unsigned)(rows * kHistCluster), kHistBlock, kHistSmemBytes, s>>>(
+            keys, n, flip, partials, (int)g1, ovf, parts);
     });
     if (e != cudaSuccess) return AHS_ECUDA;
     e = launch(KID_FEAT_FINALIZE, s, [&] {
-        k_feat_finalize<kFinalBlock><<<1, kFinalBlock, 0, s>>>(n, partials, (int)g1, hist, scan, dfeat);
+        int np = (int)g1, nr = (int)rows;
+        uint64_t nn = n;
+        void *args[] = {&nn, &partials, &np, &parts, &nr, &ovf, &hist, &scan, &fctrl, &dfeat};
+        cudaLaunchCooperativeKernel((void *)k_feat_finalize<kFinalBlock>, dim3(kFinalGrid),
+                                    dim3(kFinalBlock), args, 0, s);
     });
     if (e != cudaSuccess) return AHS_ECUDA;
 
@@ -445,7 +496,7 @@ int ahs_sort(const void *d_keys_in, const uint32_t *d_vals_in, void *d_keys_out,
     uint32_t *tickets = (uint32_t *)(tmp + TL.ticket);
     uint32_t *status = (uint32_t *)(tmp + TL.status);
 
-    const bool count_kv = strategy == AHS_COUNTING && exact_hist && kv && feat->bits <= 10;
+    const bool count_kv = strategy == AHS_COUNTING && exact_hist && kv && feat->bits <= 8;
     int passes;
     uint32_t sub;
     if (count_kv) {
@@ -460,10 +511,9 @@ int ahs_sort(const void *d_keys_in, const uint32_t *d_vals_in, void *d_keys_out,
     }
 
     // zero control words + the status of every pass (one memset)
-    const uint64_t tile = kv ? (uint64_t)OnesweepCfg<true, 8>::kTile : (uint64_t)OnesweepCfg<false, 8>::kTile;
+    const uint64_t tile = kv ? (uint64_t)OnesweepCfg<true>::kTile : (uint64_t)OnesweepCfg<false>::kTile;
     const uint64_t tiles = (n + tile - 1) / tile;
-    const int bins_per_pass = count_kv && feat->bits > 8 ? 1024 : 256;
-    const size_t status_words_per_pass = (size_t)tiles * bins_per_pass;
+    const size_t status_words_per_pass = (size_t)tiles * kBins;
     const size_t zero_bytes = (TL.status - TL.ctrl) + status_words_per_pass * 4 * passes;
     if (cudaMemsetAsync(tmp + TL.ctrl, 0, zero_bytes, s) != cudaSuccess) return AHS_ECUDA;
 
@@ -509,24 +559,26 @@ int ahs_sort(const void *d_keys_in, const uint32_t *d_vals_in, void *d_keys_out,
         uint32_t *st = status + (size_t)p * status_words_per_pass;
         uint32_t *tk = tickets + p;
         const uint32_t *bb = count_kv ? bases : bases + 256 * p;
+        const uint32_t tma_ok = (((uintptr_t)sk & 15u) == 0) && (!kv || ((uintptr_t)sv & 15u) == 0);
         cudaError_t e;
+        const bool ballot = rank_variant() == kRankBallot;
         if (!kv) {
-            using C = OnesweepCfg<false, 8>;
             e = launch(KID_ONESWEEP, s, [&] {
-                k_onesweep<false, 8><<<(unsigned)tiles, kSortBlock, C::kSmem, s>>>(
-                    sk, nullptr, dk, nullptr, n32, shift, in_flip, in_sub, out_flip, out_add, bb, st, tk);
-            });
-        } else if (count_kv && feat->bits > 8) {
-            using C = OnesweepCfg<true, 10>;
-            e = launch(KID_COUNT_SCATTER_KV, s, [&] {
-                k_onesweep<true, 10><<<(unsigned)tiles, kSortBlock, C::kSmem, s>>>(
-                    sk, sv, dk, dv, n32, shift, in_flip, in_sub, out_flip, out_add, bb, st, tk);
+                if (ballot)
+                    k_onesweep<false, kRankBallot><<<(unsigned)tiles, kSortBlock, OnesweepCfg<false>::kSmem, s>>>(
+                        sk, nullptr, dk, nullptr, n32, shift, in_flip, in_sub, out_flip, out_add, bb, st, tk, tma_ok);
+                else
+                    k_onesweep<false, kRankAtomic><<<(unsigned)tiles, kSortBlock, OnesweepCfg<false>::kSmem, s>>>(
+                        sk, nullptr, dk, nullptr, n32, shift, in_flip, in_sub, out_flip, out_add, bb, st, tk, tma_ok);
             });
         } else {
-            using C = OnesweepCfg<true, 8>;
             e = launch(count_kv ? KID_COUNT_SCATTER_KV : KID_ONESWEEP_KV, s, [&] {
-                k_onesweep<true, 8><<<(unsigned)tiles, kSortBlock, C::kSmem, s>>>(
-                    sk, sv, dk, dv, n32, shift, in_flip, in_sub, out_flip, out_add, bb, st, tk);
+                if (ballot)
+                    k_onesweep<true, kRankBallot><<<(unsigned)tiles, kSortBlock, OnesweepCfg<true>::kSmem, s>>>(
+                        sk, sv, dk, dv, n32, shift, in_flip, in_sub, out_flip, out_add, bb, st, tk, tma_ok);
+                else
+                    k_onesweep<true, kRankAtomic><<<(unsigned)tiles, kSortBlock, OnesweepCfg<true>::kSmem, s>>>(
+                        sk, sv, dk, dv, n32, shift, in_flip, in_sub, out_flip, out_add, bb, st, tk, tma_ok);
             });
         }
         if (e != cudaSuccess) return AHS_ECUDA;

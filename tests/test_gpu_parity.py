@@ -188,7 +188,7 @@ def test_thresholds_custom():
     assert ahs.STRATEGY_NAMES[s] == "COUNTING"  # 13 bits: counting via 2 radix passes on key - min
     ok, ov = oracle.sort(keys, np.arange(keys.size, dtype=np.uint32), oracle.COUNTING)
     assert np.array_equal(ko, ok) and np.array_equal(vo, ov)
-    th = ahs.ahs_thresholds_default(k_counting=1 << 20)
+    th = ahs.ahs_thresholds_default(k_counting=1 << 20, k_radix=1 << 24)
     keys = synth.uniform_range(4, 50_000, 0, 200_000)  # shift > 0: histogram bucketed
     f, s, r, ko, vo = run_gpu(keys, None, th=th)
     assert ahs.STRATEGY_NAMES[s] == "COUNTING" and f.shift > 0
