@@ -28,7 +28,7 @@ struct DevInfo {
 std::mutex g_dev_mu;
 DevInfo g_dev[64];
 
-#define K2_KERNEL k_feat_hist<kHistBlock, kHistUnroll, kHistCluster>
+#define K2_KERNEL k_feat_hist<kHistBlock, kHistCluster>
 int device_info(int *sms, int *hist_clusters = nullptr)
 {
     int dev = 0;
@@ -52,9 +52,13 @@ int device_info(int *sms, int *hist_clusters = nullptr)
             bool good = true;
             good &= cudaFuncSetAttribute(K2_KERNEL, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          kHistSmemBytes) == cudaSuccess;
+            good &= cudaFuncSetAttribute(k_feat_reduce<kReduceBlock>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kReduceSmem) == cudaSuccess;
+            good &= cudaFuncSetAttribute(k_radix_hist<kRHBlock>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kRHSmem) == cudaSuccess;
             if (good) {
                 cudaLaunchConfig_t cfg = {};
-                cfg.gridDim = dim3(kHistCluster * 64);
+                cfg.gridDim = dim3(kHistCluster * 128);
                 cfg.blockDim = dim3(kHistBlock);
                 cfg.dynamicSmemBytes = kHistSmemBytes;
                 cudaLaunchAttribute attr;
@@ -140,7 +144,7 @@ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 // ------------------------------------------------------------ ws layout
 constexpr int kMaxReduceBlocks = 2048;
-constexpr int kMaxHistRows = 64;  // K2 clusters (rows of partial histograms)
+constexpr int kMaxHistRows = 80;  // K2 clusters (rows of partial histograms)
 struct WsLayout {
     size_t feat, partials, fctrl, ovf, hist, scan, parts, total;
 };
@@ -343,22 +347,21 @@ int ahs_features(const void *d_keys, uint64_t n, int32_t dtype, void *d_ws, size
     DevFeatures *dfeat = (DevFeatures *)(ws + L.feat);
 
     const uint64_t nvec = n / 4;
-    uint64_t g1 = (nvec + (uint64_t)kReduceBlock * kReduceUnroll - 1) / ((uint64_t)kReduceBlock * kReduceUnroll);
-    const uint64_t g1max = std::min<uint64_t>(kMaxReduceBlocks, (uint64_t)sms * 8);
-    g1 = std::max<uint64_t>(1, std::min(g1, g1max));
+    const uint64_t nch1 = (nvec + kReduceChunk / 16 - 1) / (kReduceChunk / 16);
+    const uint64_t g1 = std::max<uint64_t>(1, std::min<uint64_t>(nch1, (uint64_t)sms * 2));
 
     cudaError_t e = launch(KID_FEAT_REDUCE, s, [&] {
-        k_feat_reduce<kReduceBlock, kReduceUnroll><<<(unsigned)g1, kReduceBlock, 0, s>>>(
-            keys, n, flip, partials, ovf, kMaxBins, fctrl);
+        k_feat_reduce<kReduceBlock><<<(unsigned)g1, kReduceBlock, kReduceSmem, s>>>(keys, n, flip, partials, ovf,
+                                                                                     kMaxBins, fctrl);
     });
     if (e != cudaSuccess) return AHS_ECUDA;
     // K2: clusters of kHistCluster CTAs, one partial-histogram row per cluster
-    const uint64_t per_cluster = (uint64_t)kHistBlock * kHistUnroll * kHistCluster;
-    uint64_t rows = (nvec + per_cluster - 1) / per_cluster;
+    const uint64_t nch2 = (nvec + kHistChunk / 16 - 1) / (kHistChunk / 16);
+    uint64_t rows = (nch2 + kHistCluster - 1) / kHistCluster;
     rows = std::max<uint64_t>(1, std::min<uint64_t>(rows, (uint64_t)std::min(hclusters, kMaxHistRows)));
     e = launch(KID_FEAT_HIST, s, [&] {
-        K2_KERNEL<<<(unsigned)(rows * kHistCluster), kHistBlock, kHistSmemBytes, s>>>(
-            keys, n, flip, partials, (int)g1, ovf, parts);
+        K2_KERNEL<<<(unsigned)(rows * kHistCluster), kHistBlock, kHistSmemBytes, s>>>(keys, n, flip, partials,
+                                                                                       (int)g1, ovf, parts);
     });
     if (e != cudaSuccess) return AHS_ECUDA;
     e = launch(KID_FEAT_FINALIZE, s, [&] {
@@ -503,8 +506,8 @@ int ahs_sort(const void *d_keys_in, const uint32_t *d_vals_in, void *d_keys_out,
         passes = 1;
         sub = umin;
     } else if (strategy == AHS_GENERAL) {
-        passes = 4;
-        sub = 0;
+        passes = 4;  // full width; on key - min (same order, lets K5 reuse the feature histogram)
+        sub = umin;
     } else {  // RADIX, or COUNTING that cannot use the histogram directly
         passes = radix_passes(feat->bits);
         sub = umin;
@@ -529,17 +532,22 @@ int ahs_sort(const void *d_keys_in, const uint32_t *d_vals_in, void *d_keys_out,
         src_v = tvals;
     }
 
+    if (!d_ws || ws_bytes < WL.total) return AHS_ENOSPACE;
     const uint32_t *bases;
     if (count_kv) {
         bases = (const uint32_t *)((const char *)d_ws + WL.scan);
-        if (!d_ws || ws_bytes < WL.total) return AHS_ENOSPACE;
     } else {
-        uint64_t g5 = (n / 4 + (uint64_t)kRHBlock * kRHUnroll - 1) / ((uint64_t)kRHBlock * kRHUnroll);
-        g5 = std::max<uint64_t>(1, std::min<uint64_t>(g5, (uint64_t)sms * 4));
-        // the input transform is applied inside K5; when src is tmp it holds raw keys too
+        const uint32_t *fhist = (const uint32_t *)((const char *)d_ws + WL.hist);
+        uint64_t g5;
+        if (feat->shift > 0) {
+            const uint64_t nch = (n / 4 + kRHChunk / 16 - 1) / (kRHChunk / 16);
+            g5 = std::max<uint64_t>(1, std::min<uint64_t>(nch, (uint64_t)sms));
+        } else {
+            g5 = std::max<uint64_t>(1, ((uint64_t)feat->nbins + kRHBlock - 1) / kRHBlock);
+        }
         cudaError_t e = launch(KID_RADIX_HIST, s, [&] {
-            k_radix_hist<kRHBlock, kRHUnroll><<<(unsigned)g5, kRHBlock, 0, s>>>(
-                src_k, n, flip, sub, passes, dhist, bucket, tickets + 7);
+            k_radix_hist<kRHBlock><<<(unsigned)g5, kRHBlock, kRHSmem, s>>>(
+                src_k, n, flip, sub, passes, fhist, feat->nbins, feat->shift, dhist, bucket, tickets + 7);
         });
         if (e != cudaSuccess) return AHS_ECUDA;
         bases = bucket;

@@ -128,6 +128,13 @@ __device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t
         : "memory");
 }
 
+// order this thread's earlier generic-proxy shared-memory accesses (made
+// visible to it by a barrier) before later async-proxy (TMA) writes
+__device__ __forceinline__ void fence_proxy_async()
+{
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase)
 {
     asm volatile(
@@ -139,6 +146,54 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase)
         "}\n" ::"r"(smem_u32(bar)),
         "r"(phase)
         : "memory");
+}
+
+// Streaming reader: the 16-byte-aligned body of the key array (nvec uint4
+// vectors) in chunks of CHUNK bytes; CTA b consumes chunks b, b + G, ...
+// Thread 0 keeps STAGES chunks in flight with TMA bulk copies (each chunk
+// buffer also receives the 16 bytes after the chunk when they exist, so a
+// consumer can see the successor of the chunk's last key); all threads wait
+// on the chunk's mbarrier, call consume(chunk_smem, nv, v0) and meet at a
+// barrier before the buffer is refilled.  Memory-level parallelism is
+// STAGES * CHUNK bytes per CTA independent of register pressure.
+template <int STAGES, int CHUNK, typename F>
+__device__ __forceinline__ void stream_chunks(const uint4 *__restrict__ body, uint64_t nvec, uint8_t *buf,
+                                              uint64_t *bars, F &&consume)
+{
+    constexpr uint32_t VPC = CHUNK / 16;
+    constexpr uint32_t STRIDE = CHUNK + 16;
+    const uint32_t nchunks = (uint32_t)((nvec + VPC - 1) / VPC);
+    const uint32_t mine = blockIdx.x < nchunks ? (nchunks - blockIdx.x + gridDim.x - 1) / gridDim.x : 0u;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; s++) mbar_init(&bars[s], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    auto issue = [&](uint32_t i, uint32_t s) {
+        const uint64_t v0 = (uint64_t)(blockIdx.x + i * gridDim.x) * VPC;
+        const uint64_t nv = min((uint64_t)VPC, nvec - v0);
+        const uint64_t ncopy = min(nv + 1, nvec - v0);  // + successor vector when it exists
+        mbar_expect_tx(&bars[s], (uint32_t)(ncopy * 16));
+        tma_load_1d(buf + s * STRIDE, body + v0, (uint32_t)(ncopy * 16), &bars[s]);
+    };
+    if (threadIdx.x == 0)
+        for (uint32_t i = 0; i < (uint32_t)STAGES && i < mine; i++) issue(i, i);
+    uint32_t s = 0, phase = 0;
+    for (uint32_t i = 0; i < mine; i++) {
+        mbar_wait(&bars[s], phase);
+        const uint64_t v0 = (uint64_t)(blockIdx.x + i * gridDim.x) * VPC;
+        const uint32_t nv = (uint32_t)min((uint64_t)VPC, nvec - v0);
+        consume(reinterpret_cast<const uint4 *>(buf + s * STRIDE), nv, v0);
+        __syncthreads();
+        if (threadIdx.x == 0 && i + STAGES < mine) {
+            fence_proxy_async();
+            issue(i + STAGES, s);
+        }
+        if (++s == (uint32_t)STAGES) {
+            s = 0;
+            phase ^= 1u;
+        }
+    }
 }
 
 // Split of a 4-byte-aligned key array into an unaligned head (< 4 keys), a

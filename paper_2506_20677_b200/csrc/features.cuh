@@ -28,15 +28,19 @@ namespace ahs {
 namespace cg = cooperative_groups;
 
 constexpr int kReduceBlock = 256;
-constexpr int kReduceUnroll = 4;
-constexpr int kHistBlock = 1024;
-constexpr int kHistUnroll = 2;
-constexpr int kHistCluster = 4;
-constexpr int kHistSmemBytes = 128 * 1024;           // 2^16 packed 16-bit counters
-constexpr uint32_t kHistWords = kHistSmemBytes / 4;  // 32768
-constexpr int kFinalBlock = 1024;
+constexpr int kReduceChunk = 32 * 1024;  // bytes per TMA chunk: 8 vectors per thread
+constexpr int kReduceStages = 3;
+constexpr int kReduceSmem = kReduceStages * (kReduceChunk + 16);
+constexpr int kHistBlock = 512;
+constexpr int kHistChunk = 40 * 1024;  // 5 vectors per thread
+constexpr int kHistStages = 2;
+constexpr int kHistCluster = 2;
+constexpr int kHistBins = 128 * 1024;                // bytes: 2^16 packed 16-bit counters
+constexpr uint32_t kHistWords = kHistBins / 4;       // 32768
+constexpr int kHistSmemBytes = kHistBins + kHistStages * (kHistChunk + 16);
+constexpr int kFinalBlock = 256;
 constexpr uint32_t kMaxBins = 1u << 16;
-constexpr int kFinalGrid = (int)(kMaxBins / kFinalBlock);  // 64
+constexpr int kFinalGrid = (int)(kMaxBins / kFinalBlock);  // 256
 
 // K3 control block in ws (zeroed by K1 where noted)
 struct FinalCtrl {
@@ -47,50 +51,45 @@ struct FinalCtrl {
 };
 
 // ------------------------------------------------------------------ K1 ----
-template <int BLOCK, int UNROLL>
+// Streams the aligned body through shared memory (TMA, kReduceStages chunks in
+// flight per CTA); each thread folds whole uint4 vectors: min, max, and the
+// descents inside the vector plus the one into the next key (next vector of
+// the chunk, the chunk's extra successor vector, or the first tail key).
+template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK)
     k_feat_reduce(const uint32_t *__restrict__ keys, uint64_t n, uint32_t flip,
                   Partial *__restrict__ partials, uint32_t *__restrict__ zero_words, uint32_t nzero,
                   FinalCtrl *__restrict__ fctrl)
 {
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    __shared__ __align__(8) uint64_t bars[kReduceStages];
     for (uint32_t i = blockIdx.x * BLOCK + threadIdx.x; i < nzero; i += gridDim.x * BLOCK)
         zero_words[i] = 0u;
     if (blockIdx.x == 0 && threadIdx.x == 0) fctrl->barrier = 0u;
 
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     const VecSplit sp = vec_split(keys, n);
-    const uint64_t stride = (uint64_t)gridDim.x * BLOCK;
-    const uint4 *vp = reinterpret_cast<const uint4 *>(keys + sp.head);
-
+    const uint4 *body = reinterpret_cast<const uint4 *>(keys + sp.head);
     uint32_t mn = 0xffffffffu, mx = 0u, desc = 0u;
-    for (uint64_t vb = (uint64_t)blockIdx.x * BLOCK + warp * 32u; vb < sp.nvec; vb += stride * UNROLL) {
-        uint4 x[UNROLL];
-#pragma unroll
-        for (int u = 0; u < UNROLL; u++) {
-            uint64_t v = vb + (uint64_t)u * stride + lane;
-            x[u] = v < sp.nvec ? ld_nc_v4(vp + v) : make_uint4(0, 0, 0, 0);
-        }
-#pragma unroll
-        for (int u = 0; u < UNROLL; u++) {
-            const uint64_t v = vb + (uint64_t)u * stride + lane;
-            const bool act = v < sp.nvec;
-            const uint32_t a0 = x[u].x ^ flip, a1 = x[u].y ^ flip, a2 = x[u].z ^ flip, a3 = x[u].w ^ flip;
-            // the first key of the next vector lives in lane + 1 (same slot)
-            uint32_t nxt = __shfl_down_sync(kFull, a0, 1);
-            bool has_next = act;
-            if (act && (lane == 31u || v + 1 >= sp.nvec)) {
-                const uint64_t j = sp.head + 4ull * v + 4ull;
-                has_next = j < n;
-                if (has_next) nxt = keys[j] ^ flip;
-            }
-            if (act) {
+    stream_chunks<kReduceStages, kReduceChunk>(
+        body, sp.nvec, smem_raw, bars, [&](const uint4 *c, uint32_t nv, uint64_t v0) {
+            for (uint32_t j = threadIdx.x; j < nv; j += BLOCK) {
+                const uint4 x = c[j];
+                const uint32_t a0 = x.x ^ flip, a1 = x.y ^ flip, a2 = x.z ^ flip, a3 = x.w ^ flip;
+                bool has_next = true;
+                uint32_t nxt;
+                if (v0 + j + 1 < sp.nvec) {
+                    nxt = c[j + 1].x ^ flip;  // in-chunk or the chunk's successor vector
+                } else {
+                    has_next = sp.tail0 < n;
+                    nxt = has_next ? (keys[sp.tail0] ^ flip) : 0u;
+                }
                 mn = min(mn, min(min(a0, a1), min(a2, a3)));
                 mx = max(mx, max(max(a0, a1), max(a2, a3)));
                 desc += (uint32_t)(a0 > a1) + (uint32_t)(a1 > a2) + (uint32_t)(a2 > a3) +
                         (uint32_t)(has_next && a3 > nxt);
             }
-        }
-    }
+        });
     // unaligned head and tail (< 4 keys each): block 0, one thread each
     if (blockIdx.x == 0 && threadIdx.x < 8) {
         const uint64_t i = threadIdx.x < 4 ? threadIdx.x : sp.tail0 + (threadIdx.x - 4);
@@ -164,9 +163,10 @@ __device__ __forceinline__ Partial reduce_partials(const Partial *__restrict__ p
 }
 
 // ------------------------------------------------------------------ K2 ----
-// Mode A (nb <= 32768): R = min(#warps, 32768 / nb) private 32-bit copies;
-//   warp w increments copy w % R; nb <= 64 additionally warp-aggregates with
-//   match.any.
+// Mode C (nb <= 64): private per-thread counters, layout [bin][thread]
+//   (conflict-free, no atomics).
+// Mode A (64 < nb <= 32768): R = min(#warps, 32768 / nb) private 32-bit
+//   copies; warp w increments copy w % R.
 // Mode B (nb > 32768): 2^16 packed counters, two per 32-bit word, each a
 //   15-bit count plus a guard bit.  The thread whose atomicAdd carries a half
 //   across 0x8000 owns the overflow: it subtracts 0x8000 from that half and
@@ -200,25 +200,24 @@ struct HistAdd {
     }
 };
 
-__device__ __forceinline__ void hist_vec(const HistAdd &add, uint4 x, bool act, uint32_t umin,
-                                         uint32_t shift, bool aggregate)
+// x holds 4 keys already mapped to v = key - min (mod 2^32); bins v >> shift.
+template <typename Add>
+__device__ __forceinline__ void hist_vec(const Add &add, uint4 x, bool act, uint32_t shift)
 {
     const uint32_t lane = threadIdx.x & 31u;
-    const uint32_t b0 = (x.x - umin) >> shift, b1 = (x.y - umin) >> shift;
-    const uint32_t b2 = (x.z - umin) >> shift, b3 = (x.w - umin) >> shift;
-    if (aggregate) {  // few bins: match.any per key slot, one atomic per distinct bin
-        const uint32_t bb[4] = {b0, b1, b2, b3};
-#pragma unroll
-        for (int j = 0; j < 4; j++) {
-            const uint32_t key = act ? bb[j] : 0xffffffffu;
-            const uint32_t peers = __match_any_sync(kFull, key);
-            if (act && lane == (uint32_t)(__ffs(peers) - 1)) add(bb[j], (uint32_t)__popc(peers));
+    const uint32_t b0 = x.x >> shift, b1 = x.y >> shift, b2 = x.z >> shift, b3 = x.w >> shift;
+    const bool single = act && b0 == b1 && b1 == b2 && b2 == b3;
+    const uint32_t smask = __ballot_sync(kFull, single);
+    if (smask == 0u) {  // no lane with a one-bin vector: plain per-key adds (random data)
+        if (act) {
+            add(b0, 1u);
+            add(b1, 1u);
+            add(b2, 1u);
+            add(b3, 1u);
         }
         return;
     }
-    const bool single = act && b0 == b1 && b1 == b2 && b2 == b3;
     const uint32_t pb = __shfl_up_sync(kFull, b0, 1);
-    const uint32_t smask = __ballot_sync(kFull, single);
     const bool prev_single = lane > 0 && ((smask >> (lane - 1)) & 1u);
     const bool head = single && !(prev_single && pb == b0);
     const uint32_t hmask = __ballot_sync(kFull, head);
@@ -236,59 +235,78 @@ __device__ __forceinline__ void hist_vec(const HistAdd &add, uint4 x, bool act, 
     }
 }
 
-template <int BLOCK, int UNROLL, int CL>
+// nb <= 64: per-thread private counters, layout [bin][thread] (conflict-free,
+// no atomics; the same thread's updates are ordered)
+template <int BLOCK>
+struct ThreadCols {
+    uint32_t *sh;
+    __device__ __forceinline__ void operator()(uint32_t b, uint32_t c) const
+    {
+        sh[b * BLOCK + threadIdx.x] += c;
+    }
+};
+
+template <int BLOCK, int CL>
 __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(BLOCK, 1)
     k_feat_hist(const uint32_t *__restrict__ keys, uint64_t n, uint32_t flip,
                 const Partial *__restrict__ partials, int nparts, uint32_t *__restrict__ ovf,
                 uint32_t *__restrict__ parts)
 {
-    extern __shared__ __align__(16) uint32_t sh[];
+    extern __shared__ __align__(128) uint32_t sh[];
+    __shared__ __align__(8) uint64_t bars[kHistStages];
     cg::cluster_group cluster = cg::this_cluster();
     const Partial p = reduce_partials<BLOCK>(partials, nparts);
     const Range rg = derive_range(p.mn, p.mx, 16u);
     if (rg.nb <= 1u) return;  // k = 1 (uniform for the whole grid): no histogram
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
     const bool packed = rg.nb > kHistWords;
+    const bool cols = rg.nb <= 64u;  // per-thread columns
     uint32_t R = 1;
-    if (!packed) {
+    if (!packed && !cols) {
         R = kHistWords / rg.nb;
         if (R > BLOCK / 32) R = BLOCK / 32;
     }
-    const uint32_t words = packed ? (rg.nb + 1u) >> 1 : R * rg.nb;
+    const uint32_t words = packed ? (rg.nb + 1u) >> 1 : (cols ? rg.nb * BLOCK : R * rg.nb);
     for (uint32_t i = threadIdx.x; i < words; i += BLOCK) sh[i] = 0u;
     __syncthreads();
 
-    const HistAdd add{sh, ovf, packed ? 0u : (warp % R) * rg.nb, packed};
-    const bool aggregate = !packed && rg.nb <= 64u;
     const uint32_t umin = p.mn, shift = rg.shift;
-
+    const uint32_t c0 = umin - flip;  // (key ^ flip) - umin == key - (umin - flip)  (mod 2^32)
     const VecSplit sp = vec_split(keys, n);
-    const uint64_t stride = (uint64_t)gridDim.x * BLOCK;
-    const uint4 *vp = reinterpret_cast<const uint4 *>(keys + sp.head);
-    for (uint64_t vb = (uint64_t)blockIdx.x * BLOCK + warp * 32u; vb < sp.nvec; vb += stride * UNROLL) {
-        uint4 x[UNROLL];
-#pragma unroll
-        for (int u = 0; u < UNROLL; u++) {
-            const uint64_t v = vb + (uint64_t)u * stride + lane;
-            x[u] = v < sp.nvec ? ld_nc_v4(vp + v) : make_uint4(0, 0, 0, 0);
+    const uint4 *body = reinterpret_cast<const uint4 *>(keys + sp.head);
+    uint8_t *stage = reinterpret_cast<uint8_t *>(sh) + kHistBins;
+    auto run = [&](const auto &add) {
+        stream_chunks<kHistStages, kHistChunk>(body, sp.nvec, stage, bars,
+                                               [&](const uint4 *c, uint32_t nv, uint64_t) {
+            for (uint32_t j0 = 0; j0 < nv; j0 += BLOCK) {  // block-uniform trip count
+                const uint32_t j = j0 + threadIdx.x;
+                const bool act = j < nv;
+                const uint4 x = act ? c[j] : make_uint4(c0, c0, c0, c0);
+                hist_vec(add, make_uint4(x.x - c0, x.y - c0, x.z - c0, x.w - c0), act, shift);
+            }
+        });
+        if (blockIdx.x == 0 && warp == 0) {  // head / tail keys, one per lane
+            const uint64_t i = lane < 3 ? lane : sp.tail0 + (lane - 3);
+            if (lane < 3 ? i < sp.head : (lane < 6 && i < n)) add((keys[i] - c0) >> shift, 1u);
         }
-#pragma unroll
-        for (int u = 0; u < UNROLL; u++) {
-            const uint64_t v = vb + (uint64_t)u * stride + lane;
-            const uint4 y = make_uint4(x[u].x ^ flip, x[u].y ^ flip, x[u].z ^ flip, x[u].w ^ flip);
-            hist_vec(add, y, v < sp.nvec, umin, shift, aggregate);
-        }
-    }
-    if (blockIdx.x == 0 && warp == 0) {  // head / tail keys, one per lane
-        const uint64_t i = lane < 3 ? lane : sp.tail0 + (lane - 3);
-        const bool act = lane < 3 ? i < sp.head : (lane < 6 && i < n);
-        const uint32_t u = act ? (keys[i] ^ flip) : umin;
-        const uint32_t key = act ? (u - umin) >> shift : 0xffffffffu;
-        const uint32_t peers = __match_any_sync(kFull, key);
-        if (act && lane == (uint32_t)(__ffs(peers) - 1)) add(key, (uint32_t)__popc(peers));
+    };
+    if (cols) {
+        run(ThreadCols<BLOCK>{sh});
+    } else {
+        run(HistAdd{sh, ovf, (warp % R) * rg.nb, packed});
     }
     __syncthreads();
-    if (!packed && R > 1) {  // fold the private copies into copy 0
+    if (cols) {  // fold the per-thread columns: warp w sums bins w, w + 16, ...
+        for (uint32_t b = warp; b < rg.nb; b += BLOCK / 32) {
+            uint32_t s = 0;
+            for (uint32_t t = lane; t < BLOCK; t += 32) s += sh[b * BLOCK + t];
+            s = __reduce_add_sync(kFull, s);
+            if (lane == 0) sh[rg.nb * BLOCK + b] = s;  // scratch past the columns (stage area is idle)
+        }
+        __syncthreads();
+        for (uint32_t b = threadIdx.x; b < rg.nb; b += BLOCK) sh[b] = sh[rg.nb * BLOCK + b];
+        __syncthreads();
+    } else if (!packed && R > 1) {  // fold the private copies into copy 0
         for (uint32_t b = threadIdx.x; b < rg.nb; b += BLOCK) {
             uint32_t s = 0;
             for (uint32_t r = 0; r < R; r++) s += sh[r * rg.nb + b];
@@ -331,16 +349,43 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(BLOCK, 1)
 }
 
 // ------------------------------------------------------------------ K3 ----
-// Cooperative launch of kFinalGrid CTAs x 1024 threads (co-resident by
-// construction, 1 CTA per SM): CTA j owns bins [1024 j, 1024 j + 1024).
-//   phase 1: c_b = sum of the cluster rows + overflow; hist[b] = c_b;
+// Cooperative launch of kFinalGrid CTAs x kFinalBlock threads (co-resident by
+// construction); thread b owns bin b.
+//   phase 1: c_b = sum of the cluster rows + overflow; hist[b] = c_b; per-CTA
 //            chunk total and chunk sum of c_b log2 c_b (fixed tree).
-//   barrier (atomic counter zeroed by K1; kFinalGrid CTAs are resident)
-//   phase 2: scan[b] = exclusive prefix (chunk offsets + local), scan[nb] = n;
+//   barrier (atomic counter zeroed by K1; all CTAs are resident)
+//   phase 2: scan[b] = exclusive prefix (chunk offset + local), scan[nb] = n;
 //            CTA 0: H = log2 n - (1/n) sum_j S_j (fixed order), clamped to
 //            [0, log2 nb] (R11), written with the other features.
 template <int BLOCK>
-__global__ void __launch_bounds__(BLOCK, 1)
+__device__ __forceinline__ uint32_t block_sum_u32(uint32_t x, uint32_t *s_tmp)
+{
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    x = __reduce_add_sync(kFull, x);
+    if (lane == 0) s_tmp[warp] = x;
+    __syncthreads();
+    uint32_t t = 0;
+    for (int w = 0; w < BLOCK / 32; w++) t += s_tmp[w];
+    __syncthreads();
+    return t;
+}
+
+template <int BLOCK>
+__device__ __forceinline__ double block_sum_f64_fixed(double x, double *s_tmp)
+{
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(kFull, x, o);
+    if (lane == 0) s_tmp[warp] = x;
+    __syncthreads();
+    double t = 0.0;
+    for (int w = 0; w < BLOCK / 32; w++) t += s_tmp[w];
+    __syncthreads();
+    return t;
+}
+
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK)
     k_feat_finalize(uint64_t n, const Partial *__restrict__ partials, int nparts,
                     const uint32_t *__restrict__ parts, int nrows, const uint32_t *__restrict__ ovf,
                     uint32_t *__restrict__ hist, uint32_t *__restrict__ scan, FinalCtrl *__restrict__ fctrl,
@@ -348,9 +393,8 @@ __global__ void __launch_bounds__(BLOCK, 1)
 {
     const Partial p = reduce_partials<BLOCK>(partials, nparts);
     const Range rg = derive_range(p.mn, p.mx, 16u);
-    __shared__ uint32_t s_cnt[BLOCK / 32];
-    __shared__ double s_sum[BLOCK / 32];
-    __shared__ uint32_t s_off;
+    __shared__ uint32_t s_u[BLOCK / 32];
+    __shared__ double s_d[BLOCK / 32];
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     const uint32_t b = blockIdx.x * BLOCK + threadIdx.x;
 
@@ -365,65 +409,61 @@ __global__ void __launch_bounds__(BLOCK, 1)
         }
         hist[b] = c;
     }
-    double S = c > 1u ? (double)c * log2((double)c) : 0.0;
     uint32_t incl = c;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const uint32_t t = __shfl_up_sync(kFull, incl, o);
         if (lane >= (uint32_t)o) incl += t;
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) S += __shfl_down_sync(kFull, S, o);
-    if (lane == 31) s_cnt[warp] = incl;
-    if (lane == 0) s_sum[warp] = S;
+    if (lane == 31) s_u[warp] = incl;
     __syncthreads();
-    uint32_t wofs = 0;
-    for (uint32_t w = 0; w < warp; w++) wofs += s_cnt[w];
+    uint32_t wofs = 0, tot = 0;
+    for (uint32_t w = 0; w < BLOCK / 32; w++) {
+        wofs += w < warp ? s_u[w] : 0u;
+        tot += s_u[w];
+    }
     const uint32_t local_excl = wofs + incl - c;
+    __syncthreads();
+    const double S = block_sum_f64_fixed<BLOCK>(c > 1u ? (double)c * log2((double)c) : 0.0, s_d);
     if (threadIdx.x == 0) {
-        uint32_t tot = 0;
-        double cs = 0.0;
-        for (int w = 0; w < BLOCK / 32; w++) {
-            tot += s_cnt[w];
-            cs += s_sum[w];
-        }
         fctrl->chunk_tot[blockIdx.x] = tot;
-        fctrl->chunk_S[blockIdx.x] = cs;
+        fctrl->chunk_S[blockIdx.x] = S;
         __threadfence();
         atomicAdd(&fctrl->barrier, 1u);
         uint32_t spins = 0;
         while (ld_relaxed(&fctrl->barrier) < gridDim.x)
             if (++spins > (1u << 28)) __trap();
         __threadfence();
-        uint32_t off = 0;
-        for (uint32_t j = 0; j < blockIdx.x; j++) off += __ldcg(&fctrl->chunk_tot[j]);
-        s_off = off;
     }
     __syncthreads();
     // ---- phase 2
-    if (b < rg.nb) scan[b] = s_off + local_excl;
+    const uint32_t mine = threadIdx.x < blockIdx.x ? __ldcg(&fctrl->chunk_tot[threadIdx.x]) : 0u;
+    const uint32_t off = block_sum_u32<BLOCK>(mine, s_u);
+    if (b < rg.nb) scan[b] = off + local_excl;
     if (b == rg.nb - 1u) scan[rg.nb] = (uint32_t)n;
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        double tot = 0.0;
-        for (int j = 0; j < (int)gridDim.x; j++) tot += __ldcg(&fctrl->chunk_S[j]);
-        double H = 0.0;
-        if (rg.nb > 1u) {
-            const double dn = (double)n;
-            H = log2(dn) - tot / dn;
-            const double hmax = log2((double)rg.nb);
-            if (H < 0.0) H = 0.0;
-            if (H > hmax) H = hmax;
+    if (blockIdx.x == 0) {
+        const double cs = threadIdx.x < gridDim.x ? __ldcg(&fctrl->chunk_S[threadIdx.x]) : 0.0;
+        const double tot_S = block_sum_f64_fixed<BLOCK>(cs, s_d);
+        if (threadIdx.x == 0) {
+            double H = 0.0;
+            if (rg.nb > 1u) {
+                const double dn = (double)n;
+                H = log2(dn) - tot_S / dn;
+                const double hmax = log2((double)rg.nb);
+                if (H < 0.0) H = 0.0;
+                if (H > hmax) H = hmax;
+            }
+            DevFeatures f{};
+            f.umin = p.mn;
+            f.umax = p.mx;
+            f.descents = p.desc;
+            f.k = rg.k;
+            f.bits = rg.bits;
+            f.shift = rg.shift;
+            f.nb = rg.nb;
+            f.entropy = H;
+            *out = f;
         }
-        DevFeatures f{};
-        f.umin = p.mn;
-        f.umax = p.mx;
-        f.descents = p.desc;
-        f.k = rg.k;
-        f.bits = rg.bits;
-        f.shift = rg.shift;
-        f.nb = rg.nb;
-        f.entropy = H;
-        *out = f;
     }
 }
 

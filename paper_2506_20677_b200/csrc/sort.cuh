@@ -20,6 +20,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "features.cuh"
 
 namespace ahs {
 
@@ -54,47 +55,110 @@ struct OnesweepCfg {
 };
 
 // ------------------------------------------------------------------ K5 ----
-// One read of the keys: the `passes` digit histograms of v = (u ^ flip) - sub,
-// smem-privatised (8 copies), flushed with global atomics into dhist (zeroed by
-// the host's memset); the last CTA (atomic ticket) turns them into exclusive
-// bucket bases, one warp per digit position.
+// Digit histograms of v = (key ^ flip) - min for the `passes` 8-bit digits.
+// Digits whose bits lie inside [fshift, 32) are read off the feature
+// histogram (ws, exact counts of v >> fshift): a bucket's keys share those
+// bits.  Only when fshift > 0 (k > 2^16) are the keys read again, for the
+// joint histogram of their low 16 bits (digits 0 and 1) in 2^16 packed
+// guard-bit counters: ONE shared atomic per key instead of one per digit
+// (the kernel is shared-atomic bound otherwise), with the same run merging
+// as feat_hist.  Marginals are flushed with global atomics into dhist (zeroed
+// by the host's memset); the last CTA turns them into exclusive bucket bases.
 constexpr int kRHBlock = 512;
-constexpr int kRHUnroll = 4;
-constexpr int kRHCopies = 8;
+constexpr int kRHChunk = 40 * 1024;  // 5 vectors per thread
+constexpr int kRHStages = 2;
+constexpr int kRHSmem = kHistBins + kRHStages * (kRHChunk + 16);
 
-struct RadixHistOp {
-    uint32_t *sh;  // [kRHCopies][4][256], this warp's copy
-    uint32_t sub;
-    int passes;
-    __device__ __forceinline__ void operator()(uint32_t u, bool act)
+struct JointAdd {  // packed joint counter; overflow goes straight to the marginals
+    uint32_t *sh, *dig0, *dig1;
+    __device__ __forceinline__ void operator()(uint32_t b, uint32_t c) const
     {
-        if (!act) return;
-        const uint32_t v = u - sub;
-#pragma unroll
-        for (int p = 0; p < 4; p++)
-            if (p < passes) atomicAdd(&sh[p * 256 + ((v >> (8 * p)) & 255u)], 1u);
+        const uint32_t sft = (b & 1u) << 4;
+        const uint32_t old = atomicAdd(&sh[b >> 1], c << sft);
+        const uint32_t h = (old >> sft) & 0xffffu;
+        if (h < 0x8000u && h + c >= 0x8000u) {
+            atomicSub(&sh[b >> 1], 0x8000u << sft);
+            atomicAdd(&dig0[b & 255u], 0x8000u);
+            atomicAdd(&dig1[b >> 8], 0x8000u);
+        }
     }
 };
 
-template <int BLOCK, int UNROLL>
-__global__ void __launch_bounds__(BLOCK)
-    k_radix_hist(const uint32_t *__restrict__ keys, uint64_t n, uint32_t flip, uint32_t sub,
-                 int passes, uint32_t *__restrict__ dhist, uint32_t *__restrict__ bucket_base,
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK, 1)
+    k_radix_hist(const uint32_t *__restrict__ keys, uint64_t n, uint32_t flip, uint32_t sub, int passes,
+                 const uint32_t *__restrict__ fhist, uint32_t nb, uint32_t fshift,
+                 uint32_t *__restrict__ dhist, uint32_t *__restrict__ bucket_base,
                  uint32_t *__restrict__ ticket)
 {
-    __shared__ uint32_t sh[kRHCopies * 4 * 256];
+    extern __shared__ __align__(128) uint32_t sh[];
+    __shared__ uint32_t s_dig[4][256];
+    __shared__ __align__(8) uint64_t bars[kRHStages];
     __shared__ bool s_last;
-    for (int i = threadIdx.x; i < kRHCopies * 4 * 256; i += BLOCK) sh[i] = 0u;
-    __syncthreads();
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
-    RadixHistOp op{sh + (warp % kRHCopies) * 1024, sub, passes};
-    for_each_key<UNROLL>(keys, n, flip, op);
+    const bool from_keys = fshift > 0u;  // digits 0 and 1 need the keys
+    for (int i = threadIdx.x; i < 4 * 256; i += BLOCK) (&s_dig[0][0])[i] = 0u;
+    if (from_keys)
+        for (int i = threadIdx.x; i < (int)kHistWords; i += BLOCK) sh[i] = 0u;
+    __syncthreads();
+
+    if (from_keys) {
+        const JointAdd add{sh, s_dig[0], s_dig[1]};
+        const uint32_t c0 = sub - flip;
+        const VecSplit sp = vec_split(keys, n);
+        const uint4 *body = reinterpret_cast<const uint4 *>(keys + sp.head);
+        uint8_t *stage = reinterpret_cast<uint8_t *>(sh) + kHistBins;
+        stream_chunks<kRHStages, kRHChunk>(body, sp.nvec, stage, bars, [&](const uint4 *c, uint32_t nv, uint64_t) {
+            for (uint32_t j0 = 0; j0 < nv; j0 += BLOCK) {
+                const uint32_t j = j0 + threadIdx.x;
+                const bool act = j < nv;
+                const uint4 x = act ? c[j] : make_uint4(0u, 0u, 0u, 0u);
+                // bins = low 16 bits of v = key - (sub - flip)  (mod 2^32)
+                hist_vec(add,
+                         make_uint4((x.x - c0) & 0xffffu, (x.y - c0) & 0xffffu, (x.z - c0) & 0xffffu,
+                                    (x.w - c0) & 0xffffu),
+                         act, 0u);
+            }
+        });
+        if (blockIdx.x == 0 && warp == 0) {  // head / tail keys, one per lane
+            const uint64_t i = lane < 3 ? lane : sp.tail0 + (lane - 3);
+            const bool act = lane < 3 ? i < sp.head : (lane < 6 && i < n);
+            if (act) add((keys[i] - c0) & 0xffffu, 1u);
+        }
+        __syncthreads();
+        // marginals: threads 0..255 own digit-0 value t, 256..511 digit-1 value t - 256
+        if (threadIdx.x < 512) {
+            const uint32_t t = threadIdx.x & 255u;
+            uint32_t sum = 0;
+            if (threadIdx.x < 256) {
+                for (uint32_t d1 = 0; d1 < 256; d1++) {
+                    const uint32_t b = (d1 << 8) | t;
+                    sum += (sh[b >> 1] >> ((b & 1u) << 4)) & 0xffffu;
+                }
+                atomicAdd(&s_dig[0][t], sum);
+            } else {
+                for (uint32_t w = t << 7; w < (t << 7) + 128u; w++) {
+                    const uint32_t x = sh[w];
+                    sum += (x & 0xffffu) + (x >> 16);
+                }
+                atomicAdd(&s_dig[1][t], sum);
+            }
+        }
+    }
+    // digits inside the feature buckets: this CTA's slice of the bins
+    for (uint32_t b = blockIdx.x * BLOCK + threadIdx.x; b < nb; b += gridDim.x * BLOCK) {
+        const uint32_t c = __ldg(&fhist[b]);
+        if (!c) continue;
+        const uint32_t base = b << fshift;
+#pragma unroll
+        for (int p = 0; p < 4; p++)
+            if (p < passes && (uint32_t)(8 * p) >= fshift && !(from_keys && p < 2))
+                atomicAdd(&s_dig[p][(base >> (8 * p)) & 255u], c);
+    }
     __syncthreads();
     for (int i = threadIdx.x; i < passes * 256; i += BLOCK) {
-        uint32_t s = 0;
-#pragma unroll
-        for (int c = 0; c < kRHCopies; c++) s += sh[c * 1024 + i];
-        if (s) atomicAdd(&dhist[i], s);
+        const uint32_t v = (&s_dig[0][0])[i];
+        if (v) atomicAdd(&dhist[i], v);
     }
     __threadfence();
     __syncthreads();
