@@ -63,8 +63,8 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "50"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except Exception:
@@ -101,8 +101,12 @@ class ClockSampler:
                 if v.lower().startswith("active"):
                     reasons.add(nm)
         use = loaded or sm
-        return {"sm_mhz": statistics.median(use) if use else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm), "samples_under_load": len(loaded)}
+        out = {"sm_mhz": statistics.median(use) if use else None, "sm_max_mhz": smax,
+               "reasons": sorted(reasons), "samples": len(sm), "samples_under_load": len(loaded),
+               "window": "soak + timed steps"}
+        if not sm:
+            out["raw"] = self.lines[:3]
+        return out
 
 
 # ------------------------------------------------------------ distributed
@@ -177,6 +181,9 @@ def time_pipeline(torch, ahs, keys_np, vals_np, steps, warmup, device, flush, pr
         flush.zero_()
         f, s, r = step()
     torch.cuda.synchronize(device)
+    if sampler:
+        sampler.start()
+        time.sleep(0.5)  # nvidia-smi start-up
     if soak_s > 0:  # untimed load so the clock sampler sees the GPU under this workload
         t_end = time.perf_counter() + soak_s
         while time.perf_counter() < t_end:
@@ -186,8 +193,6 @@ def time_pipeline(torch, ahs, keys_np, vals_np, steps, warmup, device, flush, pr
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     barrier(pg)
     torch.cuda.synchronize(device)
-    if sampler:
-        sampler.start()
     launches0 = ahs.ahs_launch_count()
     if profile:
         ahs.ahs_profile_begin()
@@ -399,7 +404,7 @@ def main():
     ap.add_argument("--configs", default="cfg1,cfg2kv,cfg3,cfg4a,cfg4d,cfg5_r8,cfg5_r32",
                     help="per-strategy table rows (single GPU only); '' to skip")
     ap.add_argument("--table-steps", type=int, default=5)
-    ap.add_argument("--soak", type=float, default=1.0, help="untimed seconds of load before timing")
+    ap.add_argument("--soak", type=float, default=2.0, help="untimed seconds of load before timing")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-sample", type=int, default=1 << 22)
     ap.add_argument("--no-cpu", action="store_true")
