@@ -75,13 +75,9 @@ int device_info(int *sms, int *hist_clusters = nullptr)
                 }
                 d.hist_clusters = nc;
             }
-good &= cudaFuncSetAttribute(k_onesweep<false, kRankAtomic>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+good &= cudaFuncSetAttribute(k_onesweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)OnesweepCfg<false>::kSmem) == cudaSuccess;
-            good &= cudaFuncSetAttribute(k_onesweep<true, kRankAtomic>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)OnesweepCfg<true>::kSmem) == cudaSuccess;
-            good &= cudaFuncSetAttribute(k_onesweep<false, kRankBallot>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)OnesweepCfg<false>::kSmem) == cudaSuccess;
-            good &= cudaFuncSetAttribute(k_onesweep<true, kRankBallot>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            good &= cudaFuncSetAttribute(k_onesweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)OnesweepCfg<true>::kSmem) == cudaSuccess;
             if (!good) {
                 cudaGetLastError();
@@ -209,15 +205,7 @@ bool thresholds_valid(const ahs_thresholds_t *th)
 
 int radix_passes(uint32_t bits) { return (int)((bits + 7u) / 8u); }
 
-// Warp-ranking variant of the onesweep pass (env AHS_RANK=atomic|ballot, for measurement).
-int rank_variant()
-{
-    static int v = [] {
-        const char *e = getenv("AHS_RANK");
-        return (e && e[0] == 'b') ? kRankBallot : kRankAtomic;
-    }();
-    return v;
-}
+
 
 
 
@@ -569,24 +557,15 @@ int ahs_sort(const void *d_keys_in, const uint32_t *d_vals_in, void *d_keys_out,
         const uint32_t *bb = count_kv ? bases : bases + 256 * p;
         const uint32_t tma_ok = (((uintptr_t)sk & 15u) == 0) && (!kv || ((uintptr_t)sv & 15u) == 0);
         cudaError_t e;
-        const bool ballot = rank_variant() == kRankBallot;
         if (!kv) {
             e = launch(KID_ONESWEEP, s, [&] {
-                if (ballot)
-                    k_onesweep<false, kRankBallot><<<(unsigned)tiles, kSortBlock, OnesweepCfg<false>::kSmem, s>>>(
-                        sk, nullptr, dk, nullptr, n32, shift, in_flip, in_sub, out_flip, out_add, bb, st, tk, tma_ok);
-                else
-                    k_onesweep<false, kRankAtomic><<<(unsigned)tiles, kSortBlock, OnesweepCfg<false>::kSmem, s>>>(
-                        sk, nullptr, dk, nullptr, n32, shift, in_flip, in_sub, out_flip, out_add, bb, st, tk, tma_ok);
+                k_onesweep<false><<<(unsigned)tiles, kSortBlock, OnesweepCfg<false>::kSmem, s>>>(
+                    sk, nullptr, dk, nullptr, n32, shift, in_flip, in_sub, out_flip, out_add, bb, st, tk, tma_ok);
             });
         } else {
             e = launch(count_kv ? KID_COUNT_SCATTER_KV : KID_ONESWEEP_KV, s, [&] {
-                if (ballot)
-                    k_onesweep<true, kRankBallot><<<(unsigned)tiles, kSortBlock, OnesweepCfg<true>::kSmem, s>>>(
-                        sk, sv, dk, dv, n32, shift, in_flip, in_sub, out_flip, out_add, bb, st, tk, tma_ok);
-                else
-                    k_onesweep<true, kRankAtomic><<<(unsigned)tiles, kSortBlock, OnesweepCfg<true>::kSmem, s>>>(
-                        sk, sv, dk, dv, n32, shift, in_flip, in_sub, out_flip, out_add, bb, st, tk, tma_ok);
+                k_onesweep<true><<<(unsigned)tiles, kSortBlock, OnesweepCfg<true>::kSmem, s>>>(
+                    sk, sv, dk, dv, n32, shift, in_flip, in_sub, out_flip, out_add, bb, st, tk, tma_ok);
             });
         }
         if (e != cudaSuccess) return AHS_ECUDA;

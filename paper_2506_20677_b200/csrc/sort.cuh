@@ -206,10 +206,7 @@ __device__ __forceinline__ uint32_t digit8(uint32_t v, uint32_t shift)
     return __byte_perm(v, 0u, 0x4440u | (shift >> 3));
 }
 
-constexpr int kRankAtomic = 0;  // shared atomicOr {mask, count} words (smem-pipe heavy)
-constexpr int kRankBallot = 1;  // 8 ballots + nibble-mask lookup (ALU heavy)
-
-template <bool KV, int RANK>
+template <bool KV>
 __global__ void __launch_bounds__(kSortBlock, 2)
     k_onesweep(const uint32_t *__restrict__ keys_in, const uint32_t *__restrict__ vals_in,
                uint32_t *__restrict__ keys_out, uint32_t *__restrict__ vals_out, uint32_t n,
@@ -266,8 +263,6 @@ __global__ void __launch_bounds__(kSortBlock, 2)
     uint2 *wc = s_wc + warp * kBins;
     const uint32_t lt = lanemask_lt();
     const uint32_t wbase = warp * 32u * ITEMS;
-    const uint32_t mk0 = (lane & 1u) ? 0u : kFull, mk1 = (lane & 2u) ? 0u : kFull;
-    const uint32_t mk2 = (lane & 4u) ? 0u : kFull, mk3 = (lane & 8u) ? 0u : kFull;
 #pragma unroll
     for (int it = 0; it < ITEMS; it++) {
         const uint32_t idx = wbase + it * 32u + lane;
@@ -275,26 +270,6 @@ __global__ void __launch_bounds__(kSortBlock, 2)
         v[it] = valid ? ((s_k[idx] ^ in_flip) - in_sub) : 0u;
         const uint32_t d = digit8(v[it], shift);
         uint32_t r;
-        if constexpr (RANK == kRankBallot) {
-            // peers from 8 ballots: lanes 0..15 build the mask of high-nibble value
-            // `lane`, every lane the mask of low-nibble value lane & 15; two
-            // shuffles fetch the masks of this lane's nibbles
-            uint32_t b[8];
-#pragma unroll
-            for (int j = 0; j < 8; j++) b[j] = __ballot_sync(kFull, (d >> j) & 1u);
-            const uint32_t mh = (b[4] ^ mk0) & (b[5] ^ mk1) & (b[6] ^ mk2) & (b[7] ^ mk3);
-            const uint32_t ml = (b[0] ^ mk0) & (b[1] ^ mk1) & (b[2] ^ mk2) & (b[3] ^ mk3);
-            const uint32_t vm = __ballot_sync(kFull, valid);
-            const uint32_t peers = __shfl_sync(kFull, mh, d >> 4) & __shfl_sync(kFull, ml, d & 15u) & vm;
-            const uint32_t leader = 31u - __clz(peers | 1u);
-            uint32_t base = 0;
-            if (valid && lane == leader) {
-                base = wc[d].y;
-                wc[d].y = base + __popc(peers);
-            }
-            base = __shfl_sync(kFull, base, leader);
-            r = base + __popc(peers & lt);
-        } else {
         // one digit across the warp (constant digits, sorted runs): no atomics
         // (same-address shared atomics serialise)
         const uint32_t d0 = __shfl_sync(kFull, d, 0);
@@ -311,7 +286,6 @@ __global__ void __launch_bounds__(kSortBlock, 2)
             __syncwarp();
             if (valid && lane == 31u - __clz(e.x)) wc[d] = make_uint2(0u, e.y + __popc(e.x));
             r = e.y + __popc(e.x & lt);
-        }
         }
         if (it & 1) rank2[it / 2] |= r << 16;
         else rank2[it / 2] = r;
