@@ -3,6 +3,7 @@
 // Declarations, argument meaning, ownership and error behaviour: include/ahs.h.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdlib>
@@ -24,12 +25,13 @@ struct DevInfo {
     bool init = false;
     int sms = 0;
     int hist_clusters = 0;  // co-resident K2 clusters
+    int os_keys_per_sm = 0, os_pairs_per_sm = 0;  // co-resident K6 CTAs
 };
 std::mutex g_dev_mu;
 DevInfo g_dev[64];
 
 #define K2_KERNEL k_feat_hist<kHistBlock, kHistCluster>
-int device_info(int *sms, int *hist_clusters = nullptr)
+int device_info(int *sms, int *hist_clusters = nullptr, int *os_keys = nullptr, int *os_pairs = nullptr)
 {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
@@ -75,10 +77,18 @@ int device_info(int *sms, int *hist_clusters = nullptr)
                 }
                 d.hist_clusters = nc;
             }
-good &= cudaFuncSetAttribute(k_onesweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)OnesweepCfg<false>::kSmem) == cudaSuccess;
-            good &= cudaFuncSetAttribute(k_onesweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)OnesweepCfg<true>::kSmem) == cudaSuccess;
+            good &= cudaFuncSetAttribute(K6_KEYS, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)OsKeys::kSmem) == cudaSuccess;
+            good &= cudaFuncSetAttribute(K6_PAIRS, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)OsPairs::kSmem) == cudaSuccess;
+            // persistent K6 grids: co-resident CTAs per SM
+            if (good) {
+                good &= cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.os_keys_per_sm, K6_KEYS, kSortBlock,
+                                                                      OsKeys::kSmem) == cudaSuccess;
+                good &= cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.os_pairs_per_sm, K6_PAIRS, kSortBlock,
+                                                                      OsPairs::kSmem) == cudaSuccess;
+                good &= d.os_keys_per_sm > 0 && d.os_pairs_per_sm > 0;
+            }
             if (!good) {
                 cudaGetLastError();
                 d.ok = false;
@@ -88,6 +98,8 @@ good &= cudaFuncSetAttribute(k_onesweep<false>, cudaFuncAttributeMaxDynamicShare
     if (!d.ok) return AHS_ENODEV;
     *sms = d.sms;
     if (hist_clusters) *hist_clusters = d.hist_clusters;
+    if (os_keys) *os_keys = d.os_keys_per_sm;
+    if (os_pairs) *os_pairs = d.os_pairs_per_sm;
     return AHS_OK;
 }
 
@@ -441,8 +453,8 @@ int ahs_sort(const void *d_keys_in, const uint32_t *d_vals_in, void *d_keys_out,
         ((uintptr_t)d_keys_out & 3u) || (kv && (((uintptr_t)d_vals_in & 3u) || ((uintptr_t)d_vals_out & 3u))))
         return AHS_EINVAL;
     if (feat->k == 0 || feat->k > (1ull << 32) || feat->nbins == 0) return AHS_EFEAT;
-    int sms = 0;
-    int rc = device_info(&sms);
+    int sms = 0, os_keys = 0, os_pairs = 0;
+    int rc = device_info(&sms, nullptr, &os_keys, &os_pairs);
     if (rc) return rc;
     cudaStream_t s = (cudaStream_t)stream;
     const uint32_t *kin = (const uint32_t *)d_keys_in;
@@ -502,8 +514,9 @@ int ahs_sort(const void *d_keys_in, const uint32_t *d_vals_in, void *d_keys_out,
     }
 
     // zero control words + the status of every pass (one memset)
-    const uint64_t tile = kv ? (uint64_t)OnesweepCfg<true>::kTile : (uint64_t)OnesweepCfg<false>::kTile;
+    const uint64_t tile = kv ? (uint64_t)OsPairs::kTile : (uint64_t)OsKeys::kTile;
     const uint64_t tiles = (n + tile - 1) / tile;
+    const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)sms * (kv ? os_pairs : os_keys));
     const size_t status_words_per_pass = (size_t)tiles * kBins;
     const size_t zero_bytes = (TL.status - TL.ctrl) + status_words_per_pass * 4 * passes;
     if (cudaMemsetAsync(tmp + TL.ctrl, 0, zero_bytes, s) != cudaSuccess) return AHS_ECUDA;
@@ -559,12 +572,12 @@ int ahs_sort(const void *d_keys_in, const uint32_t *d_vals_in, void *d_keys_out,
         cudaError_t e;
         if (!kv) {
             e = launch(KID_ONESWEEP, s, [&] {
-                k_onesweep<false><<<(unsigned)tiles, kSortBlock, OnesweepCfg<false>::kSmem, s>>>(
+                K6_KEYS<<<grid, kSortBlock, OsKeys::kSmem, s>>>(
                     sk, nullptr, dk, nullptr, n32, shift, in_flip, in_sub, out_flip, out_add, bb, st, tk, tma_ok);
             });
         } else {
             e = launch(count_kv ? KID_COUNT_SCATTER_KV : KID_ONESWEEP_KV, s, [&] {
-                k_onesweep<true><<<(unsigned)tiles, kSortBlock, OnesweepCfg<true>::kSmem, s>>>(
+                K6_PAIRS<<<grid, kSortBlock, OsPairs::kSmem, s>>>(
                     sk, sv, dk, dv, n32, shift, in_flip, in_sub, out_flip, out_add, bb, st, tk, tma_ok);
             });
         }

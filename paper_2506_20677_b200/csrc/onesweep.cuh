@@ -1,0 +1,344 @@
+// onesweep.cuh — K6: one stable 8-bit LSD digit pass, onesweep style
+// (one read + one write of the keys per pass; §III.G,
+// each pass a stable counting sort by one base-256 digit, Eq. 4).
+//
+// Persistent CTAs.  A CTA takes tiles from an atomic ticket in increasing
+// order and, while it works on tile t, its next tile is already arriving in
+// the second shared-memory buffer (TMA bulk copy), so HBM latency is hidden
+// behind the work on t.  Per tile:
+//
+//   rank      each half-warp (a "sub-warp" of 16 lanes) owns a contiguous
+//             segment of 16 x ITEMS keys and a 256-word digit table in shared
+//             memory; word = {bit 16+j: lane j has this digit in the current
+//             item | low 16 bits: running count}.  Per item every lane adds
+//             (1 << (16 + j)) + 1 to its digit's word, reads the word back
+//             (peers = the mask, count after the item) and clears the mask
+//             half: rank = count - popc(peers at or above me).  Stable (items
+//             in order, lanes in order) with three shared-memory operations
+//             per key and no match.any (which costs ~60 cycles per warp
+//             instruction on sm_100).  An item whose 32 keys share one digit
+//             (constant digits, sorted runs) skips the atomics.
+//   publish   per digit: tile count -> status word (aggregate) for look-back.
+//   prefix    per digit: exclusive prefix over the sub-warps, plus the tile's
+//             digit start (scan over the 256 tile counts).
+//   look-back decoupled look-back over predecessor tiles (kLookback statuses
+//             per round), inclusive status published.
+//   scatter   keys (and values) into shared memory in digit order.
+//   write     consecutive tile slots of one digit -> consecutive global slots
+//             (coalesced), output transform fused.
+//
+// The two half-warps of one warp read segments 16 * ITEMS apart (ITEMS odd),
+// i.e. disjoint bank halves: key loads from shared memory are conflict-free.
+#pragma once
+
+#include <type_traits>
+
+#include "common.cuh"
+
+namespace ahs {
+
+// status[tile][digit] = flag << 30 | count (count < 2^30 > AHS_MAX_N)
+constexpr uint32_t kFlagAgg = 1u << 30;
+constexpr uint32_t kFlagIncl = 2u << 30;
+constexpr uint32_t kCountMask = (1u << 30) - 1u;
+constexpr int kBins = 256;     // 8-bit digits
+constexpr int kLookback = 16;  // predecessor statuses loaded per look-back round
+
+__device__ __forceinline__ uint32_t digit8(uint32_t v, uint32_t shift)
+{
+    return __byte_perm(v, 0u, 0x4440u | (shift >> 3));
+}
+
+template <bool KV, int BLOCK, int ITEMS>
+struct Onesweep {
+    static constexpr int kWarps = BLOCK / 32;
+    static constexpr int kSub = kWarps * 2;  // half-warp sub-warps
+    static constexpr int kTile = BLOCK * ITEMS;
+    static constexpr int kSeg = 16 * ITEMS;  // keys per sub-warp
+    static constexpr int kTPD = BLOCK / kBins;  // threads per digit in the per-tile scans
+    static_assert(ITEMS % 2 == 1, "odd ITEMS: the half-warps of a warp read disjoint bank halves");
+    static_assert(BLOCK * ITEMS < 65536, "16-bit slot field");
+    static_assert(BLOCK == 256 || BLOCK == 512, "one or two threads per digit");
+    static_assert((kTile * 4) % 16 == 0, "TMA tile size");
+    static constexpr size_t kBuf = (size_t)kTile * 4;
+    static constexpr size_t kOffK = 0;                                   // keys   [2][TILE]
+    static constexpr size_t kOffV = kOffK + 2 * kBuf;                    // values [2][TILE]
+    static constexpr size_t kOffCnt = kOffV + (KV ? 2 * kBuf : 0);       // digit tables [SUB][256]
+    static constexpr size_t kOffAux = kOffCnt + (size_t)kSub * kBins * 4;
+    // aux: part[2][256], start[256], gofs[256], wsum[8]
+    static constexpr size_t kSmem = kOffAux + (size_t)(4 * kBins + 8) * 4;
+};
+
+template <bool KV, int BLOCK, int ITEMS, int MINB>
+__global__ void __launch_bounds__(BLOCK, MINB)
+    k_onesweep(const uint32_t *__restrict__ keys_in, const uint32_t *__restrict__ vals_in,
+               uint32_t *__restrict__ keys_out, uint32_t *__restrict__ vals_out, uint32_t n,
+               uint32_t shift, uint32_t in_flip, uint32_t in_sub, uint32_t out_flip, uint32_t out_add,
+               const uint32_t *__restrict__ bucket_base, uint32_t *__restrict__ status,
+               uint32_t *__restrict__ tile_ticket, uint32_t tma_ok)
+{
+    using C = Onesweep<KV, BLOCK, ITEMS>;
+    constexpr int TILE = C::kTile, SEG = C::kSeg;
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint32_t *s_kb = reinterpret_cast<uint32_t *>(smem + C::kOffK);
+    uint32_t *s_vb = reinterpret_cast<uint32_t *>(smem + C::kOffV);
+    uint32_t *s_cnt = reinterpret_cast<uint32_t *>(smem + C::kOffCnt);
+    uint32_t *s_part = reinterpret_cast<uint32_t *>(smem + C::kOffAux);
+    uint32_t *s_start = s_part + 2 * kBins;
+    uint32_t *s_gofs = s_start + kBins;
+    uint32_t *s_wsum = s_gofs + kBins;
+    __shared__ __align__(8) uint64_t s_bar[2];
+    __shared__ uint32_t s_ticket[2];
+
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    const uint32_t h = lane >> 4, j = lane & 15u;
+    const uint32_t sub = warp * 2u + h;
+    const uint32_t ntiles = (n + TILE - 1) / TILE;
+    const uint32_t lt16 = (1u << j) - 1u;
+
+    auto tile_full = [&](uint32_t t) { return (uint64_t)(t + 1) * TILE <= n; };
+    auto issue = [&](uint32_t t, uint32_t b) {  // thread 0
+        const uint32_t bytes = (uint32_t)TILE * 4u;
+        mbar_expect_tx(&s_bar[b], bytes * (KV ? 2u : 1u));
+        tma_load_1d(s_kb + b * TILE, keys_in + (size_t)t * TILE, bytes, &s_bar[b]);
+        if constexpr (KV) tma_load_1d(s_vb + b * TILE, vals_in + (size_t)t * TILE, bytes, &s_bar[b]);
+    };
+
+    // skewed digit distribution (a digit holds > 1/16 of the keys): enable the
+    // warp-uniform fast path (same-address shared atomics serialise)
+    __shared__ uint32_t s_skew;
+    if (tid == 0) s_skew = 0u;
+    __syncthreads();
+    if (tid < kBins) {
+        const uint32_t hi = tid == kBins - 1 ? n : __ldg(&bucket_base[tid + 1]);
+        if (hi - __ldg(&bucket_base[tid]) > n / 16u) s_skew = 1u;
+    }
+    for (int i = tid; i < C::kSub * kBins / 4; i += BLOCK)
+        reinterpret_cast<uint4 *>(s_cnt)[i] = make_uint4(0u, 0u, 0u, 0u);
+    if (tid == 0) {
+        mbar_init(&s_bar[0], 1);
+        mbar_init(&s_bar[1], 1);
+        mbar_fence_init();
+        const uint32_t t0 = atomicAdd(tile_ticket, 1u);
+        s_ticket[0] = t0;
+        if (t0 < ntiles && tma_ok && tile_full(t0)) issue(t0, 0);
+    }
+    __syncthreads();
+
+    const bool skew = s_skew != 0u;
+    uint32_t phase = 0;  // bit b: parity of buffer b's next completion
+    for (uint32_t iter = 0;; iter++) {
+        const uint32_t b = iter & 1u;
+        const uint32_t tile = s_ticket[b];
+        if (tile >= ntiles) break;
+        const uint32_t tile_base = tile * (uint32_t)TILE;
+        const uint32_t tile_n = min((uint32_t)TILE, n - tile_base);
+        const bool full = tile_n == (uint32_t)TILE;
+        uint32_t *sk = s_kb + b * TILE;
+        uint32_t *sv = s_vb + b * TILE;
+        if (tma_ok && full) {
+            mbar_wait(&s_bar[b], (phase >> b) & 1u);
+            phase ^= 1u << b;
+        } else {
+            for (uint32_t i = tid; i < tile_n; i += BLOCK) {
+                sk[i] = ld_nc(keys_in + tile_base + i);
+                if constexpr (KV) sv[i] = ld_nc(vals_in + tile_base + i);
+            }
+            __syncthreads();
+        }
+
+        auto tile_work = [&](auto full_c) {
+            constexpr bool FULL = decltype(full_c)::value;
+            // --------------------------------------------- early counts
+            // keys (and values) into registers; per sub-warp digit counts
+            uint32_t v[ITEMS];
+            [[maybe_unused]] uint32_t pv[KV ? ITEMS : 1];
+            uint32_t *cw = s_cnt + sub * kBins;
+            const uint32_t sbase = sub * SEG + j;
+    #pragma unroll
+            for (int it = 0; it < ITEMS; it++) {
+                const uint32_t idx = sbase + it * 16;
+                const bool valid = FULL || idx < tile_n;
+                v[it] = ((valid ? sk[idx] : 0u) ^ in_flip) - in_sub;
+                if constexpr (KV) pv[it] = valid ? sv[idx] : 0u;
+                const uint32_t d = digit8(v[it], shift);
+                if (skew) {
+                    const uint32_t d0 = __shfl_sync(kFull, d, 0);
+                    if (__all_sync(kFull, !valid || d == d0)) {
+                        // one digit across the warp: same-address atomics would serialise
+                        const uint32_t vm = FULL ? kFull : __ballot_sync(kFull, valid);
+                        if (j == 0) cw[d0] += __popc((vm >> (h * 16u)) & 0xffffu);
+                        __syncwarp();
+                        continue;
+                    }
+                }
+                if (valid) atomicAdd(&cw[d], 1u);
+            }
+            __syncthreads();
+
+            // ------------------ per-digit totals, publish aggregate, tile scan
+            const uint32_t d = tid & (kBins - 1), part = tid / kBins;
+            constexpr int SPP = C::kSub / C::kTPD;  // sub-warps per thread
+            uint32_t psum = 0;
+    #pragma unroll 8
+            for (int s = 0; s < SPP; s++) psum += s_cnt[(part * SPP + s) * kBins + d];
+            if constexpr (C::kTPD == 2) {
+                s_part[part * kBins + d] = psum;
+                __syncthreads();
+            }
+            uint32_t total = 0;
+            if (tid < kBins) {
+                total = C::kTPD == 2 ? s_part[d] + s_part[kBins + d] : psum;
+                st_relaxed(&status[(size_t)tile * kBins + d], (tile == 0 ? kFlagIncl : kFlagAgg) | total);
+                uint32_t incl = total;
+    #pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t t = __shfl_up_sync(kFull, incl, o);
+                    if (lane >= (uint32_t)o) incl += t;
+                }
+                if (lane == 31) s_wsum[warp] = incl;
+                asm volatile("bar.sync 1, %0;" ::"n"(kBins) : "memory");
+                uint32_t before = 0;
+    #pragma unroll
+                for (int w = 0; w < kBins / 32; w++)
+                    if (w < (int)warp) before += s_wsum[w];
+                s_start[d] = before + incl - total;
+            }
+            __syncthreads();
+            // sub-warp digit offsets in the tile (digit start + earlier sub-warps)
+            {
+                uint32_t run = s_start[d] + (part ? s_part[d] : 0u);
+    #pragma unroll 8
+                for (int s = 0; s < SPP; s++) {
+                    uint32_t *p = &s_cnt[(part * SPP + s) * kBins + d];
+                    const uint32_t c = *p;
+                    *p = run;
+                    run += c;
+                }
+            }
+            __syncthreads();
+
+            // ------------------------------------- rank + scatter in digit order
+            // word = {bit 16+j: lane j has this digit in this item | low 16: next slot}
+    #pragma unroll
+            for (int it = 0; it < ITEMS; it++) {
+                const uint32_t idx = sbase + it * 16;
+                const bool valid = FULL || idx < tile_n;
+                const uint32_t dd = digit8(v[it], shift);
+                uint32_t pos;
+                bool done = false;
+                if (skew) {
+                    const uint32_t d0 = __shfl_sync(kFull, dd, 0);
+                    if (__all_sync(kFull, !valid || dd == d0)) {
+                        const uint32_t vm = FULL ? kFull : __ballot_sync(kFull, valid);
+                        const uint32_t mh = (vm >> (h * 16u)) & 0xffffu;
+                        const uint32_t c = cw[d0];
+                        pos = c + __popc(mh & lt16);
+                        __syncwarp();
+                        if (j == 0) cw[d0] = c + __popc(mh);
+                        done = true;
+                    }
+                }
+                if (!done) {
+                    if (valid) atomicAdd(&cw[dd], (1u << (16u + j)) + 1u);
+                    __syncwarp();
+                    const uint32_t w = cw[dd];
+                    __syncwarp();
+                    if (valid) reinterpret_cast<uint16_t *>(cw + dd)[1] = 0;
+                    pos = (w & 0xffffu) - __popc(w >> (16u + j));
+                }
+                if (valid) {
+                    sk[pos] = v[it];
+                    if constexpr (KV) sv[pos] = pv[it];
+                }
+                __syncwarp();
+            }
+            // this warp's two digit tables are no longer needed: clear for the next tile
+            {
+                uint4 *t4 = reinterpret_cast<uint4 *>(s_cnt + warp * 2 * kBins);
+    #pragma unroll
+                for (int q = 0; q < 2 * kBins / 4 / 32; q++) t4[q * 32 + lane] = make_uint4(0u, 0u, 0u, 0u);
+            }
+
+            // ------------------------------------------- decoupled look-back
+            // kLookback predecessor statuses per round, consumed newest-first: AGG
+            // counts accumulate, the first INCL ends the walk, an unpublished one is
+            // re-read next round.  Tile -1 is INCL 0.
+            if (tid < kBins) {
+                uint32_t excl = 0;
+                if (tile > 0) {
+                    int jt = (int)tile - 1;
+                    uint32_t spins = 0;
+                    while (true) {
+                        uint32_t st[kLookback];
+    #pragma unroll
+                        for (int q = 0; q < kLookback; q++)
+                            st[q] = (jt - q >= 0) ? ld_relaxed(&status[(size_t)(jt - q) * kBins + d]) : kFlagIncl;
+                        int used = 0;
+                        bool fin = false, stop = false;
+    #pragma unroll
+                        for (int q = 0; q < kLookback; q++) {
+                            if (!stop) {
+                                const uint32_t flag = st[q] & ~kCountMask;
+                                if (flag == 0u) {
+                                    stop = true;
+                                } else {
+                                    excl += st[q] & kCountMask;
+                                    used++;
+                                    if (flag == kFlagIncl) fin = stop = true;
+                                }
+                            }
+                        }
+                        if (fin) break;
+                        jt -= used;
+                        if (used == 0) {
+                            // predecessors hold earlier tickets and publish before they wait
+                            if (++spins > (1u << 24)) __trap();
+                            __nanosleep(64);
+                        }
+                    }
+                    st_relaxed(&status[(size_t)tile * kBins + d], kFlagIncl | (excl + total));
+                }
+                s_gofs[d] = __ldg(&bucket_base[d]) + excl - s_start[d];
+            }
+            __syncthreads();
+            // Next tile: its ticket is taken only now, after this tile's inclusive
+            // prefix is published, so a tile whose ticket is held but not yet
+            // started never waits on anything but this CTA's write-out (taking it
+            // earlier chains the look-backs of different CTAs into convoys).  Its
+            // keys arrive in the other buffer (free: the last tile ended with a
+            // barrier) during the write-out below.
+            if (tid == 0) {
+                const uint32_t nt = atomicAdd(tile_ticket, 1u);
+                s_ticket[b ^ 1u] = nt;
+                if (nt < ntiles && tma_ok && tile_full(nt)) {
+                    fence_proxy_async();
+                    issue(nt, b ^ 1u);
+                }
+            }
+
+            // ------------------------------------------------------- write out
+            if constexpr (FULL) {
+    #pragma unroll 5
+                for (int i = tid; i < TILE; i += BLOCK) {
+                    const uint32_t x = sk[i];
+                    const uint32_t o = s_gofs[digit8(x, shift)] + i;
+                    keys_out[o] = (x + out_add) ^ out_flip;
+                    if constexpr (KV) vals_out[o] = sv[i];
+                }
+            } else {
+                for (uint32_t i = tid; i < tile_n; i += BLOCK) {
+                    const uint32_t x = sk[i];
+                    const uint32_t o = s_gofs[digit8(x, shift)] + i;
+                    keys_out[o] = (x + out_add) ^ out_flip;
+                    if constexpr (KV) vals_out[o] = sv[i];
+                }
+            }
+        };
+        if (full) tile_work(std::true_type{});
+        else tile_work(std::false_type{});
+        __syncthreads();
+    }
+}
+
+}  // namespace ahs

@@ -1,4 +1,4 @@
-// sort.cuh — K4 count_fill, K5 radix_hist, K6 onesweep pass.
+// sort.cuh — K4 count_fill, K5 radix_hist (K6, the onesweep pass, is in onesweep.cuh).
 //
 // COUNTING  PAPER.md §III.F Listing 2 (lines 187-214): the histogram of
 //           key - min (already built by ahs_features when shift = 0) and its
@@ -11,48 +11,27 @@
 //           the full 32-bit ordered key (4 passes).  LSD with stable passes
 //           yields the unique stable sorted order, identical to the oracle.
 //
-// K6 is a onesweep digit pass (one read + one write of the keys per pass):
-// each CTA takes the next tile from an atomic ticket, ranks its keys with
-// warp-private digit counters + match.any (stable: warp-striped order), publishes
-// per-digit tile counts, resolves its exclusive prefix by decoupled look-back
-// over predecessor tiles, reorders the tile in shared memory and writes runs
-// of equal digits to consecutive global addresses.
+// K6 (onesweep.cuh) is a onesweep digit pass: one read + one write of the
+// keys per pass, persistent CTAs, stable shared-memory ranking, decoupled
+// look-back over tile statuses.
 #pragma once
 
 #include "common.cuh"
 #include "features.cuh"
+#include "onesweep.cuh"
 
 namespace ahs {
 
-// ----------------------------------------------------------- status words
-// status[tile][digit] = flag << 30 | count (count < 2^30 = AHS_MAX_N + 1)
-constexpr uint32_t kFlagAgg = 1u << 30;
-constexpr uint32_t kFlagIncl = 2u << 30;
-constexpr uint32_t kCountMask = (1u << 30) - 1u;
-
+// K6 launch configurations (see onesweep.cuh): keys 512 x 15 (tile 7680,
+// two CTAs per SM), pairs 512 x 9 (tile 4608, two CTAs per SM).
 constexpr int kSortBlock = 512;
-constexpr int kSortWarps = kSortBlock / 32;
-constexpr int kItemsKeys = 16;  // tile 8192 keys
-constexpr int kItemsPairs = 8;  // tile 4096 pairs
-constexpr int kMinTile = kSortBlock * kItemsPairs;
-constexpr int kLookback = 8;    // predecessor statuses loaded per look-back round
-constexpr int kBins = 256;      // 8-bit digits
-
-template <bool KV>
-struct OnesweepCfg {
-    static constexpr int kItems = KV ? kItemsPairs : kItemsKeys;
-    static constexpr int kTile = kSortBlock * kItems;
-    // dynamic shared memory:
-    //   s_k    [TILE]          tile keys (TMA / loads), reused for the reordered keys
-    //   s_vin  [TILE]    (KV)  tile values
-    //   s_vout [TILE]    (KV)  reordered values
-    //   s_wc   [WARPS][256]    uint2 {peer mask, running count} per warp and digit
-    //   s_off  [WARPS][256]    combined scatter offset per warp and digit
-    //   s_count, s_start, s_gofs [256]
-    static constexpr size_t kKeyBytes = (size_t)kTile * 4 * (KV ? 3 : 1);
-    static constexpr size_t kSmem = kKeyBytes + (size_t)kSortWarps * kBins * 8 + (size_t)kSortWarps * kBins * 4 +
-                                    (size_t)3 * kBins * 4;
-};
+constexpr int kItemsKeys = 15;
+constexpr int kItemsPairs = 9;
+using OsKeys = Onesweep<false, kSortBlock, kItemsKeys>;
+using OsPairs = Onesweep<true, kSortBlock, kItemsPairs>;
+#define K6_KEYS k_onesweep<false, kSortBlock, kItemsKeys, 2>
+#define K6_PAIRS k_onesweep<true, kSortBlock, kItemsPairs, 2>
+constexpr int kMinTile = OsPairs::kTile < OsKeys::kTile ? OsPairs::kTile : OsKeys::kTile;
 
 // ------------------------------------------------------------------ K5 ----
 // Digit histograms of v = (key ^ flip) - min for the `passes` 8-bit digits.
@@ -186,216 +165,6 @@ __global__ void __launch_bounds__(BLOCK, 1)
             bucket_base[warp * 256 + lane * 8 + j] = run;
             run += c[j];
         }
-    }
-}
-
-// ------------------------------------------------------------------ K6 ----
-// One stable 8-bit digit pass.  Input transform on load: v = (key ^ in_flip) -
-// in_sub; output transform on store: key = (v + out_add) ^ out_flip; digit =
-// byte (shift / 8) of v.  bucket_base[d] = first global slot of digit d.
-//
-// Tile load: one TMA bulk copy (keys, and values for KV) when the input is
-// 16-byte aligned and the tile full, else coalesced loads.  Ranking (stable,
-// warp-striped order): per item, every lane sets its bit in the warp's
-// {mask, count} word of its digit with a shared atomicOr, reads the word back
-// (peers = lanes with the same digit, count = earlier items' total), and the
-// highest peer lane writes {0, count + popc(peers)}.  On sm_100 this is ~2x
-// the throughput of ballot-based ranking and ~4x match.any (tools/rankbench.cu).
-__device__ __forceinline__ uint32_t digit8(uint32_t v, uint32_t shift)
-{
-    return __byte_perm(v, 0u, 0x4440u | (shift >> 3));
-}
-
-template <bool KV>
-__global__ void __launch_bounds__(kSortBlock, 2)
-    k_onesweep(const uint32_t *__restrict__ keys_in, const uint32_t *__restrict__ vals_in,
-               uint32_t *__restrict__ keys_out, uint32_t *__restrict__ vals_out, uint32_t n,
-               uint32_t shift, uint32_t in_flip, uint32_t in_sub, uint32_t out_flip,
-               uint32_t out_add, const uint32_t *__restrict__ bucket_base,
-               uint32_t *__restrict__ status, uint32_t *__restrict__ tile_ticket, uint32_t tma_ok)
-{
-    using Cfg = OnesweepCfg<KV>;
-    constexpr int TILE = Cfg::kTile, ITEMS = Cfg::kItems, WARPS = kSortWarps;
-    extern __shared__ __align__(128) uint8_t smem_raw[];
-    uint32_t *s_k = reinterpret_cast<uint32_t *>(smem_raw);
-    uint32_t *s_vin = s_k + TILE;
-    uint32_t *s_vout = s_vin + TILE;
-    uint2 *s_wc = reinterpret_cast<uint2 *>(smem_raw + Cfg::kKeyBytes);
-    uint32_t *s_off = reinterpret_cast<uint32_t *>(s_wc + WARPS * kBins);
-    uint32_t *s_count = s_off + WARPS * kBins;
-    uint32_t *s_start = s_count + kBins;
-    uint32_t *s_gofs = s_start + kBins;
-    __shared__ uint32_t s_tile;
-    __shared__ __align__(8) uint64_t s_bar;
-
-    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-    if (tid == 0) {
-        s_tile = atomicAdd(tile_ticket, 1u);
-        mbar_init(&s_bar, 1);
-        mbar_fence_init();
-    }
-    for (int i = tid; i < WARPS * kBins / 2; i += kSortBlock)
-        reinterpret_cast<uint4 *>(s_wc)[i] = make_uint4(0u, 0u, 0u, 0u);
-    __syncthreads();
-    const uint32_t tile = s_tile;
-    if (tile >= gridDim.x) __trap();  // ticket not zeroed: refuse instead of waiting forever
-    const uint32_t tile_base = tile * (uint32_t)TILE;
-    const uint32_t tile_n = min((uint32_t)TILE, n - tile_base);
-
-    // ---- tile load
-    if (tma_ok && tile_n == (uint32_t)TILE) {
-        if (tid == 0) {
-            mbar_expect_tx(&s_bar, (uint32_t)TILE * 4u * (KV ? 2u : 1u));
-            tma_load_1d(s_k, keys_in + tile_base, (uint32_t)TILE * 4u, &s_bar);
-            if constexpr (KV) tma_load_1d(s_vin, vals_in + tile_base, (uint32_t)TILE * 4u, &s_bar);
-        }
-        mbar_wait(&s_bar, 0);
-    } else {
-        for (uint32_t i = tid; i < tile_n; i += kSortBlock) {
-            s_k[i] = ld_nc(keys_in + tile_base + i);
-            if constexpr (KV) s_vin[i] = ld_nc(vals_in + tile_base + i);
-        }
-        __syncthreads();
-    }
-
-    // ---- rank within the warp (stable: items in order, lanes in order)
-    uint32_t v[ITEMS], rank2[ITEMS / 2];  // ranks < TILE <= 2^13, packed two per register
-    uint2 *wc = s_wc + warp * kBins;
-    const uint32_t lt = lanemask_lt();
-    const uint32_t wbase = warp * 32u * ITEMS;
-#pragma unroll
-    for (int it = 0; it < ITEMS; it++) {
-        const uint32_t idx = wbase + it * 32u + lane;
-        const bool valid = idx < tile_n;
-        v[it] = valid ? ((s_k[idx] ^ in_flip) - in_sub) : 0u;
-        const uint32_t d = digit8(v[it], shift);
-        uint32_t r;
-        // one digit across the warp (constant digits, sorted runs): no atomics
-        // (same-address shared atomics serialise)
-        const uint32_t d0 = __shfl_sync(kFull, d, 0);
-        if (__all_sync(kFull, !valid || d == d0)) {
-            const uint32_t vm = __ballot_sync(kFull, valid);
-            const uint32_t base = wc[d0].y;
-            __syncwarp();
-            if (lane == 0) wc[d0].y = base + __popc(vm);
-            r = base + __popc(vm & lt);
-        } else {
-            if (valid) atomicOr(&wc[d].x, 1u << lane);
-            __syncwarp();
-            const uint2 e = valid ? wc[d] : make_uint2(0u, 0u);
-            __syncwarp();
-            if (valid && lane == 31u - __clz(e.x)) wc[d] = make_uint2(0u, e.y + __popc(e.x));
-            r = e.y + __popc(e.x & lt);
-        }
-        if (it & 1) rank2[it / 2] |= r << 16;
-        else rank2[it / 2] = r;
-        __syncwarp();
-    }
-    __syncthreads();
-
-    // ---- per digit: warp-exclusive offsets, tile count, publish aggregate
-    if (tid < kBins) {
-        const uint32_t d = tid;
-        uint32_t sum = 0;
-#pragma unroll
-        for (int w = 0; w < WARPS; w++) {
-            const uint32_t t = s_wc[w * kBins + d].y;
-            s_off[w * kBins + d] = sum;
-            sum += t;
-        }
-        s_count[d] = sum;
-        st_relaxed(&status[(size_t)tile * kBins + d], (tile == 0 ? kFlagIncl : kFlagAgg) | sum);
-    }
-    __syncthreads();
-
-    // ---- decoupled look-back (threads 0..255, one digit each) || local digit scan (warp 8).
-    // Each round loads the statuses of kLookback predecessor tiles at once and
-    // consumes them newest-first: AGG counts accumulate, the first INCL ends
-    // the walk, an unpublished one is re-read next round.  Tile -1 is INCL 0.
-    if (tid < kBins) {
-        const uint32_t d = tid;
-        uint32_t excl = 0;
-        if (tile > 0) {
-            int j = (int)tile - 1;
-            uint32_t spins = 0;
-            while (true) {
-                uint32_t st[kLookback];
-#pragma unroll
-                for (int q = 0; q < kLookback; q++)
-                    st[q] = (j - q >= 0) ? ld_relaxed(&status[(size_t)(j - q) * kBins + d]) : kFlagIncl;
-                int used = 0;
-                bool done = false, stop = false;
-#pragma unroll
-                for (int q = 0; q < kLookback; q++) {
-                    if (!stop) {
-                        const uint32_t flag = st[q] & ~kCountMask;
-                        if (flag == 0u) {
-                            stop = true;  // not published yet: retry from here
-                        } else {
-                            excl += st[q] & kCountMask;
-                            used++;
-                            if (flag == kFlagIncl) done = stop = true;
-                        }
-                    }
-                }
-                if (done) break;
-                j -= used;
-                // predecessors always publish (they took their tickets earlier and
-                // never wait before publishing); never hang the GPU on a bug
-                if (used == 0 && ++spins > (1u << 26)) __trap();
-            }
-            st_relaxed(&status[(size_t)tile * kBins + d], kFlagIncl | (excl + s_count[d]));
-        }
-        s_gofs[d] = __ldg(&bucket_base[d]) + excl;
-    } else if (warp == kBins / 32) {
-        constexpr int PER = kBins / 32;
-        uint32_t c[PER], sum = 0;
-#pragma unroll
-        for (int j = 0; j < PER; j++) {
-            c[j] = s_count[lane * PER + j];
-            sum += c[j];
-        }
-        uint32_t incl = sum;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t t = __shfl_up_sync(kFull, incl, o);
-            if (lane >= (uint32_t)o) incl += t;
-        }
-        uint32_t run = incl - sum;
-#pragma unroll
-        for (int j = 0; j < PER; j++) {
-            s_start[lane * PER + j] = run;
-            run += c[j];
-        }
-    }
-    __syncthreads();
-    // global slot of tile position i with digit d = s_gofs[d] + i; warp scatter
-    // offset = tile start of d + earlier warps' count of d
-    if (tid < kBins) s_gofs[tid] -= s_start[tid];
-    for (int i = tid; i < WARPS * kBins; i += kSortBlock) s_off[i] += s_start[i & (kBins - 1)];
-    __syncthreads();
-
-    // ---- scatter into shared memory in digit order
-    const uint32_t *off = s_off + warp * kBins;
-#pragma unroll
-    for (int it = 0; it < ITEMS; it++) {
-        const uint32_t idx = wbase + it * 32u + lane;
-        if (idx < tile_n) {
-            const uint32_t r = (it & 1) ? (rank2[it / 2] >> 16) : (rank2[it / 2] & 0xffffu);
-            const uint32_t pos = off[digit8(v[it], shift)] + r;
-            s_k[pos] = v[it];
-            if constexpr (KV) s_vout[pos] = s_vin[idx];
-        }
-    }
-    __syncthreads();
-
-    // ---- write out: consecutive tile slots of one digit -> consecutive global slots
-#pragma unroll 4
-    for (uint32_t i = tid; i < tile_n; i += kSortBlock) {
-        const uint32_t x = s_k[i];
-        const uint32_t o = s_gofs[digit8(x, shift)] + i;
-        keys_out[o] = (x + out_add) ^ out_flip;
-        if constexpr (KV) vals_out[o] = s_vout[i];
     }
 }
 

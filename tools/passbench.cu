@@ -1,0 +1,220 @@
+// passbench.cu — development tool: one onesweep digit pass (K6) in isolation,
+// several launch configurations, checked against a host counting sort, plus
+// CUB's DeviceRadixSort on the same data as an outside reference point.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -o tools/pb tools/passbench.cu
+#include <cub/device/device_radix_sort.cuh>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "../paper_2506_20677_b200/csrc/onesweep.cuh"
+
+using namespace ahs;
+
+#define CK(x)                                                                                  \
+    do {                                                                                       \
+        cudaError_t e_ = (x);                                                                  \
+        if (e_ != cudaSuccess) {                                                               \
+            printf("CUDA error %s at %s:%d\n", cudaGetErrorString(e_), __FILE__, __LINE__);   \
+            exit(1);                                                                           \
+        }                                                                                      \
+    } while (0)
+
+__host__ __device__ inline uint32_t hash32(uint32_t x)
+{
+    x ^= x >> 16;
+    x *= 0x7feb352du;
+    x ^= x >> 15;
+    x *= 0x846ca68bu;
+    x ^= x >> 16;
+    return x;
+}
+
+// dist 0: uniform 32-bit; 1: 64 distinct values Zipf-ish (low-entropy digit); 2: constant digit
+__global__ void k_gen(uint32_t *k, uint32_t *v, uint32_t n, int dist, uint32_t seed)
+{
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        uint32_t x = hash32(i * 2654435761u + seed);
+        if (dist == 1) {
+            uint32_t u = hash32(x) & 0xffffu;
+            uint32_t r = 0;
+            while (r < 63 && u < (65536u >> (r / 4 + 1))) r++;  // skewed
+            x = (r << 2) | (x & 0xffffff00u);
+        } else if (dist == 2) {
+            x = (x & 0xffffff00u) | 42u;
+        }
+        k[i] = x;
+        v[i] = i;
+    }
+}
+
+__global__ void k_dhist(const uint32_t *k, uint32_t n, uint32_t shift, uint32_t *hist)
+{
+    __shared__ uint32_t sh[256];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        atomicAdd(&sh[(k[i] >> shift) & 255u], 1u);
+    __syncthreads();
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) atomicAdd(&hist[i], sh[i]);
+}
+
+__global__ void k_flush(uint32_t *p, size_t n)
+{
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        p[i] = (uint32_t)i;
+}
+
+struct Bufs {
+    uint32_t *k, *v, *ko, *vo, *bb, *status, *ticket, *flush;
+    size_t flush_n;
+};
+
+static int g_only = -1, g_idx = 0;
+
+template <bool KV, int BLOCK, int ITEMS, int MINB>
+float run_cfg(const Bufs &B, uint32_t n, uint32_t shift, int sms, int reps, bool check,
+              const std::vector<uint32_t> &hk, const std::vector<uint32_t> &hbase)
+{
+    if (g_only >= 0 && g_idx++ != g_only) return 0.f;
+    using C = Onesweep<KV, BLOCK, ITEMS>;
+    auto kern = k_onesweep<KV, BLOCK, ITEMS, MINB>;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmem));
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, BLOCK, C::kSmem));
+    const uint32_t tiles = (n + C::kTile - 1) / C::kTile;
+    const uint32_t grid = std::min<uint32_t>(tiles, (uint32_t)(occ * sms));
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    std::vector<float> ts;
+    for (int r = 0; r < reps + 2; r++) {
+        k_flush<<<sms * 4, 512>>>(B.flush, B.flush_n);
+        CK(cudaMemsetAsync(B.status, 0, (size_t)tiles * 256 * 4));
+        CK(cudaMemsetAsync(B.ticket, 0, 4));
+        CK(cudaEventRecord(a));
+        kern<<<grid, BLOCK, C::kSmem>>>(B.k, B.v, B.ko, B.vo, n, shift, 0u, 0u, 0u, 0u, B.bb, B.status, B.ticket,
+                                        1u);
+        CK(cudaEventRecord(b));
+        CK(cudaEventSynchronize(b));
+        CK(cudaGetLastError());
+        float ms;
+        CK(cudaEventElapsedTime(&ms, a, b));
+        if (r >= 2) ts.push_back(ms);
+    }
+    std::sort(ts.begin(), ts.end());
+    const float med = ts[ts.size() / 2];
+    bool ok = true;
+    if (check) {
+        std::vector<uint32_t> got(n), gotv(n), pos(hbase);
+        CK(cudaMemcpy(got.data(), B.ko, n * 4ull, cudaMemcpyDeviceToHost));
+        if (KV) CK(cudaMemcpy(gotv.data(), B.vo, n * 4ull, cudaMemcpyDeviceToHost));
+        for (uint32_t i = 0; i < n && ok; i++) {
+            const uint32_t p = pos[(hk[i] >> shift) & 255u]++;
+            if (got[p] != hk[i] || (KV && gotv[p] != i)) {
+                printf("  MISMATCH at out %u (in %u): got %08x want %08x\n", p, i, got[p], hk[i]);
+                ok = false;
+            }
+        }
+    }
+    const double bytes = (KV ? 16.0 : 8.0) * n;
+    printf("  onesweep<%s,B%d,I%d,minb%d> tile %5d occ %d grid %4u: %8.1f us  %7.1f GB/s  %6.1f Gkeys/s  "
+           "%.2f keys/clk/SM@1.9 max %.1f us %s\n",
+           KV ? "kv" : "k", BLOCK, ITEMS, MINB, C::kTile, occ, grid, med * 1e3, bytes / med / 1e6,
+           n / med / 1e6, n / med / 1e6 / sms / 1.9, ts.back() * 1e3, check ? (ok ? "ok" : "FAIL") : "");
+    return med;
+}
+
+template <bool KV>
+void run_cub(const Bufs &B, uint32_t n, int begin_bit, int end_bit, int sms, int reps)
+{
+    size_t tb = 0;
+    if (KV)
+        cub::DeviceRadixSort::SortPairs(nullptr, tb, B.k, B.ko, B.v, B.vo, (int)n, begin_bit, end_bit);
+    else
+        cub::DeviceRadixSort::SortKeys(nullptr, tb, B.k, B.ko, (int)n, begin_bit, end_bit);
+    void *tmp;
+    CK(cudaMalloc(&tmp, tb));
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    std::vector<float> ts;
+    for (int r = 0; r < reps + 2; r++) {
+        k_flush<<<sms * 4, 512>>>(B.flush, B.flush_n);
+        CK(cudaEventRecord(a));
+        if (KV)
+            cub::DeviceRadixSort::SortPairs(tmp, tb, B.k, B.ko, B.v, B.vo, (int)n, begin_bit, end_bit);
+        else
+            cub::DeviceRadixSort::SortKeys(tmp, tb, B.k, B.ko, (int)n, begin_bit, end_bit);
+        CK(cudaEventRecord(b));
+        CK(cudaEventSynchronize(b));
+        float ms;
+        CK(cudaEventElapsedTime(&ms, a, b));
+        if (r >= 2) ts.push_back(ms);
+    }
+    std::sort(ts.begin(), ts.end());
+    const float med = ts[ts.size() / 2];
+    const int passes = (end_bit - begin_bit + 7) / 8;
+    const double bytes = (KV ? 4.0 + 16.0 * passes : 4.0 + 8.0 * passes) * n;
+    printf("  CUB %s bits [%d,%d): %8.1f us  %6.1f Gkeys/s  (%.0f GB/s at (%s) bytes)\n", KV ? "pairs" : "keys",
+           begin_bit, end_bit, med * 1e3, n / med / 1e6, bytes / med / 1e6, KV ? "4+16p" : "4+8p");
+    CK(cudaFree(tmp));
+}
+
+int main(int argc, char **argv)
+{
+    const uint32_t n = argc > 1 ? (uint32_t)atol(argv[1]) : (1u << 26);
+    const int dist = argc > 2 ? atoi(argv[2]) : 0;
+    const int reps = argc > 3 ? atoi(argv[3]) : 10;
+    const bool cub = argc > 4 ? atoi(argv[4]) != 0 : true;
+    g_only = argc > 5 ? atoi(argv[5]) : -1;
+    int sms;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+    Bufs B;
+    CK(cudaMalloc(&B.k, n * 4ull));
+    CK(cudaMalloc(&B.v, n * 4ull));
+    CK(cudaMalloc(&B.ko, n * 4ull));
+    CK(cudaMalloc(&B.vo, n * 4ull));
+    CK(cudaMalloc(&B.bb, 256 * 4));
+    CK(cudaMalloc(&B.status, ((size_t)n / 1024 + 16) * 256 * 4));
+    CK(cudaMalloc(&B.ticket, 64));
+    B.flush_n = 64u << 20;  // 256 MiB
+    CK(cudaMalloc(&B.flush, B.flush_n * 4));
+    k_gen<<<sms * 8, 256>>>(B.k, B.v, n, dist, 12345u);
+    CK(cudaDeviceSynchronize());
+    std::vector<uint32_t> hk(n);
+    CK(cudaMemcpy(hk.data(), B.k, n * 4ull, cudaMemcpyDeviceToHost));
+    printf("n = %u, dist %d, %d SMs\n", n, dist, sms);
+    for (uint32_t shift : {0u, 24u})
+        if (g_only < 0 || shift == 0) {
+        std::vector<uint32_t> hist(256, 0), base(256);
+        for (uint32_t i = 0; i < n; i++) hist[(hk[i] >> shift) & 255u]++;
+        uint32_t run = 0, mx = 0;
+        for (int d = 0; d < 256; d++) {
+            base[d] = run;
+            run += hist[d];
+            mx = std::max(mx, hist[d]);
+        }
+        CK(cudaMemcpy(B.bb, base.data(), 1024, cudaMemcpyHostToDevice));
+        printf("digit shift %u (max digit share %.3f)\n", shift, (double)mx / n);
+        g_idx = 0;
+        run_cfg<false, 512, 15, 2>(B, n, shift, sms, reps, true, hk, base);
+        run_cfg<false, 512, 13, 2>(B, n, shift, sms, reps, true, hk, base);
+        run_cfg<false, 512, 21, 2>(B, n, shift, sms, reps, true, hk, base);
+        run_cfg<false, 256, 15, 4>(B, n, shift, sms, reps, true, hk, base);
+        run_cfg<false, 512, 15, 1>(B, n, shift, sms, reps, false, hk, base);
+        run_cfg<true, 512, 9, 2>(B, n, shift, sms, reps, true, hk, base);
+        run_cfg<true, 512, 15, 1>(B, n, shift, sms, reps, true, hk, base);
+        run_cfg<true, 256, 15, 2>(B, n, shift, sms, reps, false, hk, base);
+        run_cfg<true, 512, 11, 1>(B, n, shift, sms, reps, true, hk, base);
+    }
+    if (cub) {
+        run_cub<false>(B, n, 0, 32, sms, reps);
+        run_cub<false>(B, n, 0, 8, sms, reps);
+        run_cub<true>(B, n, 0, 32, sms, reps);
+    }
+    return 0;
+}
