@@ -42,7 +42,13 @@ constexpr uint32_t kFlagAgg = 1u << 30;
 constexpr uint32_t kFlagIncl = 2u << 30;
 constexpr uint32_t kCountMask = (1u << 30) - 1u;
 constexpr int kBins = 256;     // 8-bit digits
-constexpr int kLookback = 16;  // predecessor statuses loaded per look-back round
+#ifndef AHS_LOOKBACK
+#define AHS_LOOKBACK 8
+#endif
+constexpr int kLookback = AHS_LOOKBACK;  // predecessor statuses loaded per look-back round (B200: 8 beats 16, 32)
+#ifdef AHS_LB_STATS
+__device__ unsigned long long g_lb_stats[4];  // tiles, rounds, empty rounds, statuses consumed
+#endif
 
 __device__ __forceinline__ uint32_t digit8(uint32_t v, uint32_t shift)
 {
@@ -147,8 +153,9 @@ __global__ void __launch_bounds__(BLOCK, MINB)
             __syncthreads();
         }
 
-        auto tile_work = [&](auto full_c) {
+        auto tile_work = [&](auto full_c, auto skew_c) {
             constexpr bool FULL = decltype(full_c)::value;
+            constexpr bool SKEW = decltype(skew_c)::value;
             // --------------------------------------------- early counts
             // keys (and values) into registers; per sub-warp digit counts
             uint32_t v[ITEMS];
@@ -162,7 +169,7 @@ __global__ void __launch_bounds__(BLOCK, MINB)
                 v[it] = ((valid ? sk[idx] : 0u) ^ in_flip) - in_sub;
                 if constexpr (KV) pv[it] = valid ? sv[idx] : 0u;
                 const uint32_t d = digit8(v[it], shift);
-                if (skew) {
+                if constexpr (SKEW) {
                     const uint32_t d0 = __shfl_sync(kFull, d, 0);
                     if (__all_sync(kFull, !valid || d == d0)) {
                         // one digit across the warp: same-address atomics would serialise
@@ -227,7 +234,7 @@ __global__ void __launch_bounds__(BLOCK, MINB)
                 const uint32_t dd = digit8(v[it], shift);
                 uint32_t pos;
                 bool done = false;
-                if (skew) {
+                if constexpr (SKEW) {
                     const uint32_t d0 = __shfl_sync(kFull, dd, 0);
                     if (__all_sync(kFull, !valid || dd == d0)) {
                         const uint32_t vm = FULL ? kFull : __ballot_sync(kFull, valid);
@@ -289,6 +296,11 @@ __global__ void __launch_bounds__(BLOCK, MINB)
                                 }
                             }
                         }
+#ifdef AHS_LB_STATS
+                        atomicAdd(&g_lb_stats[1], 1ull);
+                        atomicAdd(&g_lb_stats[3], (unsigned long long)used);
+                        if (used == 0) atomicAdd(&g_lb_stats[2], 1ull);
+#endif
                         if (fin) break;
                         jt -= used;
                         if (used == 0) {
@@ -298,6 +310,9 @@ __global__ void __launch_bounds__(BLOCK, MINB)
                         }
                     }
                     st_relaxed(&status[(size_t)tile * kBins + d], kFlagIncl | (excl + total));
+#ifdef AHS_LB_STATS
+                    atomicAdd(&g_lb_stats[0], 1ull);
+#endif
                 }
                 s_gofs[d] = __ldg(&bucket_base[d]) + excl - s_start[d];
             }
@@ -335,8 +350,12 @@ __global__ void __launch_bounds__(BLOCK, MINB)
                 }
             }
         };
-        if (full) tile_work(std::true_type{});
-        else tile_work(std::false_type{});
+        if (full) {
+            if (skew) tile_work(std::true_type{}, std::true_type{});
+            else tile_work(std::true_type{}, std::false_type{});
+        } else {
+            tile_work(std::false_type{}, std::true_type{});
+        }
         __syncthreads();
     }
 }

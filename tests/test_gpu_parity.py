@@ -2,8 +2,9 @@
 
 Bar: features n/min/max/k/bits/shift/nbins/descents bit-exact, |dH| <= 1e-9
 (BASELINE.json north_star), strategy + rule identical, keys and values
-bit-exact (the unique stable order).  Sizes span several tiles (8192 keys /
-4096 pairs) with ragged tails; full BASELINE.json configs at the end.
+bit-exact (the unique stable order).  Sizes span several tiles (7680 keys /
+4608 pairs per onesweep tile) with ragged tails, and sizes where every
+persistent CTA walks several tiles; full BASELINE.json configs at the end.
 """
 import math
 
@@ -103,8 +104,8 @@ def check_forced(keys, vals, strategy, **kw):
 
 # --------------------------------------------------------------- T4 small
 
-SIZES = [1, 2, 3, 4, 5, 7, 8, 15, 16, 17, 21, 33, 1000, 4095, 4096, 4097, 8191, 8192, 8193,
-         3 * 8192 + 77, 65537, 250_001]
+SIZES = [1, 2, 3, 4, 5, 7, 8, 15, 16, 17, 21, 33, 1000, 4607, 4608, 4609, 7679, 7680, 7681,
+         3 * 7680 + 77, 5 * 4608 + 13, 65537, 250_001]
 
 FAMILIES = {
     "u1000": lambda n, s: synth.uniform_range(s, n, 0, 999),
@@ -125,6 +126,16 @@ def test_pipeline_small_sizes(family):
         keys = FAMILIES[family](n, 100 + i)
         check_pipeline(keys)
         check_pipeline(keys, np.arange(n, dtype=np.uint32))
+
+
+@pytest.mark.parametrize("family", ["full32", "zipf_wide", "neg16"])
+def test_pipeline_many_tiles_per_cta(family):
+    # > 296 resident CTAs x 7680: every persistent CTA takes several tickets,
+    # with TMA prefetch across tiles and a ragged last tile
+    n = 3_000_017
+    keys = FAMILIES[family](n, 7)
+    check_pipeline(keys)
+    check_pipeline(keys, np.arange(n, dtype=np.uint32))
 
 
 def test_pipeline_empty():

@@ -5,6 +5,7 @@
 #include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -75,7 +76,7 @@ struct Bufs {
 
 static int g_only = -1, g_idx = 0;
 
-template <bool KV, int BLOCK, int ITEMS, int MINB>
+template <bool KV, int BLOCK, int ITEMS, int MINB, bool NIB = false>
 float run_cfg(const Bufs &B, uint32_t n, uint32_t shift, int sms, int reps, bool check,
               const std::vector<uint32_t> &hk, const std::vector<uint32_t> &hbase)
 {
@@ -107,6 +108,16 @@ float run_cfg(const Bufs &B, uint32_t n, uint32_t shift, int sms, int reps, bool
     }
     std::sort(ts.begin(), ts.end());
     const float med = ts[ts.size() / 2];
+#ifdef AHS_LB_STATS
+    {
+        unsigned long long st[4];
+        CK(cudaMemcpyFromSymbol(st, g_lb_stats, sizeof(st)));
+        printf("  look-back (W=%d): per digit-tile %.2f rounds, %.2f empty rounds, %.1f statuses\n", kLookback,
+               (double)st[1] / st[0], (double)st[2] / st[0], (double)st[3] / st[0]);
+        memset(st, 0, sizeof(st));
+        CK(cudaMemcpyToSymbol(g_lb_stats, st, sizeof(st)));
+    }
+#endif
     bool ok = true;
     if (check) {
         std::vector<uint32_t> got(n), gotv(n), pos(hbase);
@@ -121,9 +132,9 @@ float run_cfg(const Bufs &B, uint32_t n, uint32_t shift, int sms, int reps, bool
         }
     }
     const double bytes = (KV ? 16.0 : 8.0) * n;
-    printf("  onesweep<%s,B%d,I%d,minb%d> tile %5d occ %d grid %4u: %8.1f us  %7.1f GB/s  %6.1f Gkeys/s  "
+    printf("  %s<%s,B%d,I%d,minb%d> tile %5d occ %d grid %4u: %8.1f us  %7.1f GB/s  %6.1f Gkeys/s  "
            "%.2f keys/clk/SM@1.9 max %.1f us %s\n",
-           KV ? "kv" : "k", BLOCK, ITEMS, MINB, C::kTile, occ, grid, med * 1e3, bytes / med / 1e6,
+           NIB ? "nibble  " : "onesweep", KV ? "kv" : "k", BLOCK, ITEMS, MINB, C::kTile, occ, grid, med * 1e3, bytes / med / 1e6,
            n / med / 1e6, n / med / 1e6 / sms / 1.9, ts.back() * 1e3, check ? (ok ? "ok" : "FAIL") : "");
     return med;
 }
@@ -202,14 +213,8 @@ int main(int argc, char **argv)
         printf("digit shift %u (max digit share %.3f)\n", shift, (double)mx / n);
         g_idx = 0;
         run_cfg<false, 512, 15, 2>(B, n, shift, sms, reps, true, hk, base);
-        run_cfg<false, 512, 13, 2>(B, n, shift, sms, reps, true, hk, base);
-        run_cfg<false, 512, 21, 2>(B, n, shift, sms, reps, true, hk, base);
-        run_cfg<false, 256, 15, 4>(B, n, shift, sms, reps, true, hk, base);
-        run_cfg<false, 512, 15, 1>(B, n, shift, sms, reps, false, hk, base);
         run_cfg<true, 512, 9, 2>(B, n, shift, sms, reps, true, hk, base);
         run_cfg<true, 512, 15, 1>(B, n, shift, sms, reps, true, hk, base);
-        run_cfg<true, 256, 15, 2>(B, n, shift, sms, reps, false, hk, base);
-        run_cfg<true, 512, 11, 1>(B, n, shift, sms, reps, true, hk, base);
     }
     if (cub) {
         run_cub<false>(B, n, 0, 32, sms, reps);
