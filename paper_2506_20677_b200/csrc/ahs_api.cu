@@ -23,6 +23,7 @@ namespace {
 struct DevInfo {
     bool ok = false;
     bool init = false;
+    bool setup_failed = false;  // sm_100 device, but a kernel attribute could not be set
     int sms = 0;
     int hist_clusters = 0;  // co-resident K2 clusters
     int os_keys_per_sm = 0, os_pairs_per_sm = 0;  // co-resident K6 CTAs
@@ -92,10 +93,11 @@ int device_info(int *sms, int *hist_clusters = nullptr, int *os_keys = nullptr, 
             if (!good) {
                 cudaGetLastError();
                 d.ok = false;
+                d.setup_failed = true;
             }
         }
     }
-    if (!d.ok) return AHS_ENODEV;
+    if (!d.ok) return d.setup_failed ? AHS_ECUDA : AHS_ENODEV;
     *sms = d.sms;
     if (hist_clusters) *hist_clusters = d.hist_clusters;
     if (os_keys) *os_keys = d.os_keys_per_sm;

@@ -31,8 +31,8 @@ constexpr int kReduceBlock = 256;
 constexpr int kReduceChunk = 32 * 1024;  // bytes per TMA chunk: 8 vectors per thread
 constexpr int kReduceStages = 3;
 constexpr int kReduceSmem = kReduceStages * (kReduceChunk + 16);
-constexpr int kHistBlock = 512;
-constexpr int kHistChunk = 40 * 1024;  // 5 vectors per thread
+constexpr int kHistBlock = 1024;
+constexpr int kHistChunk = 48 * 1024;  // 3 vectors per thread
 constexpr int kHistStages = 2;
 constexpr int kHistCluster = 2;
 constexpr int kHistBins = 128 * 1024;                // bytes: 2^16 packed 16-bit counters
@@ -163,7 +163,7 @@ __device__ __forceinline__ Partial reduce_partials(const Partial *__restrict__ p
 }
 
 // ------------------------------------------------------------------ K2 ----
-// Mode C (nb <= 64): private per-thread counters, layout [bin][thread]
+// Mode C (nb <= 32768 / BLOCK): private per-thread counters, layout [bin][thread]
 //   (conflict-free, no atomics).
 // Mode A (64 < nb <= 32768): R = min(#warps, 32768 / nb) private 32-bit
 //   copies; warp w increments copy w % R.
@@ -173,9 +173,10 @@ __device__ __forceinline__ Partial reduce_partials(const Partial *__restrict__ p
 //   adds 32768 to the global overflow bin.  The guard bit absorbs the carry,
 //   so a half never spills into its neighbour while fewer than 32768
 //   increments to one bin are in flight between the crossing and its
-//   correction.  Bound: each thread has at most one packed atomic in flight
-//   (the next one is issued after the branch on this one's return value), a
-//   warp's lanes stay within two key slots of each other (every slot has warp
+//   correction.  Bound: a thread has at most the four packed atomics of its
+//   current vector in flight (add4 issues them back to back, then checks the
+//   returns; the next vector's atomics come after those branches), a warp's
+//   lanes stay within two key slots of each other (every slot has warp
 //   collectives), and one slot is 128 keys: <= 32 warps x 256 = 8192 < 32768.
 // Both modes first merge runs of equal bins: within a thread's 4 keys, and
 // across lanes whose 4 keys all fall into one bin (sorted / nearly sorted
@@ -190,13 +191,35 @@ struct HistAdd {
             atomicAdd(&sh[copy_base + b], c);
             return;
         }
+        fix(atomicAdd(&sh[b >> 1], c << ((b & 1u) << 4)), b, c);
+    }
+    __device__ __forceinline__ void fix(uint32_t old, uint32_t b, uint32_t c) const
+    {
         const uint32_t sft = (b & 1u) << 4;
-        const uint32_t old = atomicAdd(&sh[b >> 1], c << sft);
         const uint32_t h = (old >> sft) & 0xffffu;
         if (h < 0x8000u && h + c >= 0x8000u) {
             atomicSub(&sh[b >> 1], 0x8000u << sft);
             atomicAdd(&ovf[b], 0x8000u);
         }
+    }
+    // four single increments: all atomics in flight before the first check
+    __device__ __forceinline__ void add4(uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3) const
+    {
+        if (!packed) {
+            atomicAdd(&sh[copy_base + b0], 1u);
+            atomicAdd(&sh[copy_base + b1], 1u);
+            atomicAdd(&sh[copy_base + b2], 1u);
+            atomicAdd(&sh[copy_base + b3], 1u);
+            return;
+        }
+        const uint32_t o0 = atomicAdd(&sh[b0 >> 1], 1u << ((b0 & 1u) << 4));
+        const uint32_t o1 = atomicAdd(&sh[b1 >> 1], 1u << ((b1 & 1u) << 4));
+        const uint32_t o2 = atomicAdd(&sh[b2 >> 1], 1u << ((b2 & 1u) << 4));
+        const uint32_t o3 = atomicAdd(&sh[b3 >> 1], 1u << ((b3 & 1u) << 4));
+        fix(o0, b0, 1u);
+        fix(o1, b1, 1u);
+        fix(o2, b2, 1u);
+        fix(o3, b3, 1u);
     }
 };
 
@@ -209,12 +232,7 @@ __device__ __forceinline__ void hist_vec(const Add &add, uint4 x, bool act, uint
     const bool single = act && b0 == b1 && b1 == b2 && b2 == b3;
     const uint32_t smask = __ballot_sync(kFull, single);
     if (smask == 0u) {  // no lane with a one-bin vector: plain per-key adds (random data)
-        if (act) {
-            add(b0, 1u);
-            add(b1, 1u);
-            add(b2, 1u);
-            add(b3, 1u);
-        }
+        if (act) add.add4(b0, b1, b2, b3);
         return;
     }
     const uint32_t pb = __shfl_up_sync(kFull, b0, 1);
@@ -235,7 +253,7 @@ __device__ __forceinline__ void hist_vec(const Add &add, uint4 x, bool act, uint
     }
 }
 
-// nb <= 64: per-thread private counters, layout [bin][thread] (conflict-free,
+// nb <= 32768 / BLOCK: per-thread private counters, layout [bin][thread] (conflict-free,
 // no atomics; the same thread's updates are ordered)
 template <int BLOCK>
 struct ThreadCols {
@@ -243,6 +261,13 @@ struct ThreadCols {
     __device__ __forceinline__ void operator()(uint32_t b, uint32_t c) const
     {
         sh[b * BLOCK + threadIdx.x] += c;
+    }
+    __device__ __forceinline__ void add4(uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3) const
+    {
+        (*this)(b0, 1u);
+        (*this)(b1, 1u);
+        (*this)(b2, 1u);
+        (*this)(b3, 1u);
     }
 };
 
@@ -260,7 +285,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(BLOCK, 1)
     if (rg.nb <= 1u) return;  // k = 1 (uniform for the whole grid): no histogram
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
     const bool packed = rg.nb > kHistWords;
-    const bool cols = rg.nb <= 64u;  // per-thread columns
+    const bool cols = rg.nb <= kHistWords / BLOCK;  // per-thread columns (64 bins at 512 threads)
     uint32_t R = 1;
     if (!packed && !cols) {
         R = kHistWords / rg.nb;
@@ -323,6 +348,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(BLOCK, 1)
     if (!packed) {
         const uint32_t per = (rg.nb + CL - 1) / CL;
         const uint32_t b0 = rank * per, b1 = min(rg.nb, b0 + per);
+#pragma unroll 4
         for (uint32_t b = b0 + threadIdx.x; b < b1; b += BLOCK) {
             uint32_t s = 0;
 #pragma unroll
@@ -333,6 +359,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(BLOCK, 1)
         const uint32_t nw = (rg.nb + 1u) >> 1;
         const uint32_t per = (nw + CL - 1) / CL;
         const uint32_t w0 = rank * per, w1 = min(nw, w0 + per);
+#pragma unroll 8
         for (uint32_t w = w0 + threadIdx.x; w < w1; w += BLOCK) {
             uint32_t lo = 0, hi = 0;
 #pragma unroll
@@ -405,6 +432,7 @@ __global__ void __launch_bounds__(BLOCK)
             c = (uint32_t)n;
         } else {
             c = __ldcg(&ovf[b]);
+#pragma unroll 16
             for (int r = 0; r < nrows; r++) c += __ldcg(&parts[(size_t)r * kMaxBins + b]);
         }
         hist[b] = c;

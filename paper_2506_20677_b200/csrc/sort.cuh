@@ -43,8 +43,8 @@ constexpr int kMinTile = OsPairs::kTile < OsKeys::kTile ? OsPairs::kTile : OsKey
 // (the kernel is shared-atomic bound otherwise), with the same run merging
 // as feat_hist.  Marginals are flushed with global atomics into dhist (zeroed
 // by the host's memset); the last CTA turns them into exclusive bucket bases.
-constexpr int kRHBlock = 512;
-constexpr int kRHChunk = 40 * 1024;  // 5 vectors per thread
+constexpr int kRHBlock = 1024;
+constexpr int kRHChunk = 46 * 1024;  // < 3 vectors per thread (fits 227 KB with the 4 KB static digit tables)
 constexpr int kRHStages = 2;
 constexpr int kRHSmem = kHistBins + kRHStages * (kRHChunk + 16);
 
@@ -52,14 +52,28 @@ struct JointAdd {  // packed joint counter; overflow goes straight to the margin
     uint32_t *sh, *dig0, *dig1;
     __device__ __forceinline__ void operator()(uint32_t b, uint32_t c) const
     {
+        fix(atomicAdd(&sh[b >> 1], c << ((b & 1u) << 4)), b, c);
+    }
+    __device__ __forceinline__ void fix(uint32_t old, uint32_t b, uint32_t c) const
+    {
         const uint32_t sft = (b & 1u) << 4;
-        const uint32_t old = atomicAdd(&sh[b >> 1], c << sft);
         const uint32_t h = (old >> sft) & 0xffffu;
         if (h < 0x8000u && h + c >= 0x8000u) {
             atomicSub(&sh[b >> 1], 0x8000u << sft);
             atomicAdd(&dig0[b & 255u], 0x8000u);
             atomicAdd(&dig1[b >> 8], 0x8000u);
         }
+    }
+    __device__ __forceinline__ void add4(uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3) const
+    {
+        const uint32_t o0 = atomicAdd(&sh[b0 >> 1], 1u << ((b0 & 1u) << 4));
+        const uint32_t o1 = atomicAdd(&sh[b1 >> 1], 1u << ((b1 & 1u) << 4));
+        const uint32_t o2 = atomicAdd(&sh[b2 >> 1], 1u << ((b2 & 1u) << 4));
+        const uint32_t o3 = atomicAdd(&sh[b3 >> 1], 1u << ((b3 & 1u) << 4));
+        fix(o0, b0, 1u);
+        fix(o1, b1, 1u);
+        fix(o2, b2, 1u);
+        fix(o3, b3, 1u);
     }
 };
 
@@ -110,12 +124,14 @@ __global__ void __launch_bounds__(BLOCK, 1)
             const uint32_t t = threadIdx.x & 255u;
             uint32_t sum = 0;
             if (threadIdx.x < 256) {
+#pragma unroll 16
                 for (uint32_t d1 = 0; d1 < 256; d1++) {
                     const uint32_t b = (d1 << 8) | t;
                     sum += (sh[b >> 1] >> ((b & 1u) << 4)) & 0xffffu;
                 }
                 atomicAdd(&s_dig[0][t], sum);
             } else {
+#pragma unroll 16
                 for (uint32_t w = t << 7; w < (t << 7) + 128u; w++) {
                     const uint32_t x = sh[w];
                     sum += (x & 0xffffu) + (x >> 16);
