@@ -2,28 +2,31 @@
 // (one read + one write of the keys per pass; §III.G,
 // each pass a stable counting sort by one base-256 digit, Eq. 4).
 //
-// Persistent CTAs.  A CTA takes tiles from an atomic ticket in increasing
-// order and, while it works on tile t, its next tile is already arriving in
-// the second shared-memory buffer (TMA bulk copy), so HBM latency is hidden
-// behind the work on t.  Per tile:
+// Persistent CTAs (two per SM).  A CTA takes tiles from an atomic ticket in
+// increasing order; the ticket for its next tile is taken only once the
+// current tile's inclusive prefix is published (a held-but-unstarted tile then
+// waits on nothing but this CTA's write-out), and that tile's keys arrive by
+// TMA bulk copy in the second shared-memory buffer during the write-out.
+// Per tile:
 //
-//   rank      each half-warp (a "sub-warp" of 16 lanes) owns a contiguous
-//             segment of 16 x ITEMS keys and a 256-word digit table in shared
-//             memory; word = {bit 16+j: lane j has this digit in the current
-//             item | low 16 bits: running count}.  Per item every lane adds
-//             (1 << (16 + j)) + 1 to its digit's word, reads the word back
-//             (peers = the mask, count after the item) and clears the mask
-//             half: rank = count - popc(peers at or above me).  Stable (items
-//             in order, lanes in order) with three shared-memory operations
-//             per key and no match.any (which costs ~60 cycles per warp
-//             instruction on sm_100).  An item whose 32 keys share one digit
-//             (constant digits, sorted runs) skips the atomics.
-//   publish   per digit: tile count -> status word (aggregate) for look-back.
-//   prefix    per digit: exclusive prefix over the sub-warps, plus the tile's
-//             digit start (scan over the 256 tile counts).
+//   early     keys (and values) into registers; each half-warp ("sub-warp",
+//   counts    16 lanes) owns a contiguous segment of 16 x ITEMS keys and counts
+//             its digits in a 256-word table with shared atomics (a warp whose
+//             32 keys share one digit adds once: same-address atomics serialise).
+//   publish   per digit: tile count -> status word (aggregate) for the
+//             look-back of later tiles, before any ranking.
+//   offsets   tile digit starts (scan over the 256 counts); each sub-warp table
+//             is rewritten as {lane mask 0 | slot = digit start + earlier
+//             sub-warps' count}.
+//   rank +    per item every lane adds (1 << (16 + j)) + 1 to its digit's word,
+//   scatter   reads it back (mask = its peers in this item, slot advanced by
+//             their number) and clears the mask half: tile position = slot -
+//             popc(peers at or above me).  Stable (items in order, lanes in
+//             order), three shared-memory operations per key, no match.any
+//             (~60 cycles per warp instruction on sm_100).  Keys (and values)
+//             go straight to their tile position in shared memory.
 //   look-back decoupled look-back over predecessor tiles (kLookback statuses
 //             per round), inclusive status published.
-//   scatter   keys (and values) into shared memory in digit order.
 //   write     consecutive tile slots of one digit -> consecutive global slots
 //             (coalesced), output transform fused.
 //
