@@ -68,6 +68,8 @@ def lib():
             "ahs_sort_host": ([vp, vp, vp, vp, u64, i32, C.POINTER(Thresholds), vp, sz,
                                C.POINTER(Features), p_i32, p_i32, vp], C.c_int),
             "ahs_launch_count": ([], C.c_uint64),
+            "ahs_rank_mode": ([C.c_int], C.c_int),
+            "ahs_lane_order_ok": ([], C.c_int),
             "ahs_kernel_count": ([], C.c_int),
             "ahs_kernel_name": ([C.c_int], C.c_char_p),
             "ahs_profile_begin": ([], C.c_int),
@@ -114,6 +116,24 @@ def ahs_host_scratch_bytes(n: int, has_vals: bool) -> int:
 
 def ahs_sort_passes(feat: Features, strategy: int, has_vals: bool) -> int:
     return lib().ahs_sort_passes(C.byref(feat), strategy, int(bool(has_vals)))
+
+
+RANK_MASKED, RANK_ORDERED = 0, 1
+
+
+def ahs_rank_mode(mode: int = -1) -> int:
+    """Query (-1) or set (0 masked, 1 ordered) the onesweep ranking mode; returns the mode."""
+    rc = lib().ahs_rank_mode(mode)
+    if rc < 0:
+        raise AhsError(rc, "ahs_rank_mode")
+    return rc
+
+
+def ahs_lane_order_ok() -> bool:
+    rc = lib().ahs_lane_order_ok()
+    if rc < 0:
+        raise AhsError(rc, "ahs_lane_order_ok")
+    return rc == 1
 
 
 def ahs_launch_count() -> int:

@@ -26,13 +26,43 @@ struct DevInfo {
     bool setup_failed = false;  // sm_100 device, but a kernel attribute could not be set
     int sms = 0;
     int hist_clusters = 0;  // co-resident K2 clusters
-    int os_keys_per_sm = 0, os_pairs_per_sm = 0;  // co-resident K6 CTAs
+    // K6 variants: [kv][rank mode]
+    const void *os_fn[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+    size_t os_smem[2][2] = {{0, 0}, {0, 0}};
+    int os_tile[2][2] = {{0, 0}, {0, 0}};
+    int os_per_sm[2][2] = {{0, 0}, {0, 0}};  // co-resident CTAs per SM
+    bool lane_order_ok = false;              // self-test of the ordered ranking passed
+    int rank_mode = kRankMasked;
 };
 std::mutex g_dev_mu;
 DevInfo g_dev[64];
 
 #define K2_KERNEL k_feat_hist<kHistBlock, kHistCluster>
-int device_info(int *sms, int *hist_clusters = nullptr, int *os_keys = nullptr, int *os_pairs = nullptr)
+__device__ uint32_t g_selftest_bad;
+
+// Runs k_lane_order_selftest on a private stream; true iff no violation.
+bool lane_order_selftest(int sms)
+{
+    cudaStream_t st;
+    if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    uint32_t *bad = nullptr, zero = 0, h = 1;
+    bool ok = cudaGetSymbolAddress((void **)&bad, g_selftest_bad) == cudaSuccess &&
+              cudaMemcpyAsync(bad, &zero, 4, cudaMemcpyHostToDevice, st) == cudaSuccess;
+    if (ok) {
+        k_lane_order_selftest<<<sms, 512, 0, st>>>(bad, 288);
+        ok = cudaGetLastError() == cudaSuccess &&
+             cudaMemcpyAsync(&h, bad, 4, cudaMemcpyDeviceToHost, st) == cudaSuccess &&
+             cudaStreamSynchronize(st) == cudaSuccess && h == 0;
+    }
+    cudaGetLastError();
+    cudaStreamDestroy(st);
+    return ok;
+}
+
+int device_info(int *sms, int *hist_clusters = nullptr, DevInfo **info = nullptr)
 {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
@@ -78,17 +108,37 @@ int device_info(int *sms, int *hist_clusters = nullptr, int *os_keys = nullptr, 
                 }
                 d.hist_clusters = nc;
             }
-            good &= cudaFuncSetAttribute(K6_KEYS, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)OsKeys::kSmem) == cudaSuccess;
-            good &= cudaFuncSetAttribute(K6_PAIRS, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)OsPairs::kSmem) == cudaSuccess;
-            // persistent K6 grids: co-resident CTAs per SM
+            d.os_fn[0][kRankMasked] = (const void *)K6_KEYS_M;
+            d.os_fn[1][kRankMasked] = (const void *)K6_PAIRS_M;
+            d.os_fn[0][kRankOrdered] = (const void *)K6_KEYS_O;
+            d.os_fn[1][kRankOrdered] = (const void *)K6_PAIRS_O;
+            d.os_smem[0][kRankMasked] = OsKeysM::kSmem;
+            d.os_smem[1][kRankMasked] = OsPairsM::kSmem;
+            d.os_smem[0][kRankOrdered] = OsKeysO::kSmem;
+            d.os_smem[1][kRankOrdered] = OsPairsO::kSmem;
+            d.os_tile[0][kRankMasked] = OsKeysM::kTile;
+            d.os_tile[1][kRankMasked] = OsPairsM::kTile;
+            d.os_tile[0][kRankOrdered] = OsKeysO::kTile;
+            d.os_tile[1][kRankOrdered] = OsPairsO::kTile;
+            for (int kv = 0; kv < 2; kv++)
+                for (int m = 0; m < 2; m++) {
+                    // persistent K6 grids: co-resident CTAs per SM
+                    good &= cudaFuncSetAttribute(d.os_fn[kv][m], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)d.os_smem[kv][m]) == cudaSuccess;
+                    if (good)
+                        good &= cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                                    &d.os_per_sm[kv][m], d.os_fn[kv][m], kSortBlock, d.os_smem[kv][m]) ==
+                                cudaSuccess;
+                    good &= d.os_per_sm[kv][m] > 0;
+                }
+            // The ordered ranking is used only if the device serves the lanes of
+            // one shared atomic instruction in lane order (onesweep.cuh), checked
+            // here once per device; AHS_RANK=masked forces the masked ranking.
             if (good) {
-                good &= cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.os_keys_per_sm, K6_KEYS, kSortBlock,
-                                                                      OsKeys::kSmem) == cudaSuccess;
-                good &= cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.os_pairs_per_sm, K6_PAIRS, kSortBlock,
-                                                                      OsPairs::kSmem) == cudaSuccess;
-                good &= d.os_keys_per_sm > 0 && d.os_pairs_per_sm > 0;
+                d.lane_order_ok = lane_order_selftest(d.sms);
+                const char *env = std::getenv("AHS_RANK");
+                const bool force_masked = env && std::strcmp(env, "masked") == 0;
+                d.rank_mode = (d.lane_order_ok && !force_masked) ? kRankOrdered : kRankMasked;
             }
             if (!good) {
                 cudaGetLastError();
@@ -100,8 +150,7 @@ int device_info(int *sms, int *hist_clusters = nullptr, int *os_keys = nullptr, 
     if (!d.ok) return d.setup_failed ? AHS_ECUDA : AHS_ENODEV;
     *sms = d.sms;
     if (hist_clusters) *hist_clusters = d.hist_clusters;
-    if (os_keys) *os_keys = d.os_keys_per_sm;
-    if (os_pairs) *os_pairs = d.os_pairs_per_sm;
+    if (info) *info = &d;
     return AHS_OK;
 }
 
@@ -275,6 +324,33 @@ int ahs_sort_passes(const ahs_features_t *f, int32_t strategy, int has_vals)
 }
 
 uint64_t ahs_launch_count(void) { return g_launches.load(); }
+
+int ahs_rank_mode(int mode)
+{
+    int sms = 0;
+    DevInfo *di = nullptr;
+    int rc = device_info(&sms, nullptr, &di);
+    if (rc) return rc;
+    if (mode == -1) return di->rank_mode;
+    if (mode == AHS_RANK_MASKED) {
+        di->rank_mode = kRankMasked;
+    } else if (mode == AHS_RANK_ORDERED) {
+        if (!di->lane_order_ok) return AHS_EINVAL;
+        di->rank_mode = kRankOrdered;
+    } else {
+        return AHS_EINVAL;
+    }
+    return di->rank_mode;
+}
+
+int ahs_lane_order_ok(void)
+{
+    int sms = 0;
+    DevInfo *di = nullptr;
+    int rc = device_info(&sms, nullptr, &di);
+    if (rc) return rc;
+    return di->lane_order_ok ? 1 : 0;
+}
 int ahs_kernel_count(void) { return KID_COUNT; }
 const char *ahs_kernel_name(int id) { return (id >= 0 && id < KID_COUNT) ? kKernelNames[id] : ""; }
 
@@ -455,8 +531,9 @@ int ahs_sort(const void *d_keys_in, const uint32_t *d_vals_in, void *d_keys_out,
         ((uintptr_t)d_keys_out & 3u) || (kv && (((uintptr_t)d_vals_in & 3u) || ((uintptr_t)d_vals_out & 3u))))
         return AHS_EINVAL;
     if (feat->k == 0 || feat->k > (1ull << 32) || feat->nbins == 0) return AHS_EFEAT;
-    int sms = 0, os_keys = 0, os_pairs = 0;
-    int rc = device_info(&sms, nullptr, &os_keys, &os_pairs);
+    int sms = 0;
+    DevInfo *di = nullptr;
+    int rc = device_info(&sms, nullptr, &di);
     if (rc) return rc;
     cudaStream_t s = (cudaStream_t)stream;
     const uint32_t *kin = (const uint32_t *)d_keys_in;
@@ -516,9 +593,12 @@ int ahs_sort(const void *d_keys_in, const uint32_t *d_vals_in, void *d_keys_out,
     }
 
     // zero control words + the status of every pass (one memset)
-    const uint64_t tile = kv ? (uint64_t)OsPairs::kTile : (uint64_t)OsKeys::kTile;
+    const int mode = di->rank_mode;
+    const uint64_t tile = (uint64_t)di->os_tile[kv][mode];
     const uint64_t tiles = (n + tile - 1) / tile;
-    const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)sms * (kv ? os_pairs : os_keys));
+    const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)sms * di->os_per_sm[kv][mode]);
+    const void *k6 = di->os_fn[kv][mode];
+    const size_t k6_smem = di->os_smem[kv][mode];
     const size_t status_words_per_pass = (size_t)tiles * kBins;
     const size_t zero_bytes = (TL.status - TL.ctrl) + status_words_per_pass * 4 * passes;
     if (cudaMemsetAsync(tmp + TL.ctrl, 0, zero_bytes, s) != cudaSuccess) return AHS_ECUDA;
@@ -571,18 +651,17 @@ int ahs_sort(const void *d_keys_in, const uint32_t *d_vals_in, void *d_keys_out,
         uint32_t *tk = tickets + p;
         const uint32_t *bb = count_kv ? bases : bases + 256 * p;
         const uint32_t tma_ok = (((uintptr_t)sk & 15u) == 0) && (!kv || ((uintptr_t)sv & 15u) == 0);
-        cudaError_t e;
-        if (!kv) {
-            e = launch(KID_ONESWEEP, s, [&] {
-                K6_KEYS<<<grid, kSortBlock, OsKeys::kSmem, s>>>(
-                    sk, nullptr, dk, nullptr, n32, shift, in_flip, in_sub, out_flip, out_add, bb, st, tk, tma_ok);
-            });
-        } else {
-            e = launch(count_kv ? KID_COUNT_SCATTER_KV : KID_ONESWEEP_KV, s, [&] {
-                K6_PAIRS<<<grid, kSortBlock, OsPairs::kSmem, s>>>(
-                    sk, sv, dk, dv, n32, shift, in_flip, in_sub, out_flip, out_add, bb, st, tk, tma_ok);
-            });
-        }
+        const void *kin_p = sk, *vin_p = sv;
+        void *kout_p = dk, *vout_p = dv;
+        const void *bb_p = bb;
+        uint32_t n_a = n32, sh_a = shift, if_a = in_flip, is_a = in_sub, of_a = out_flip, oa_a = out_add;
+        void *st_p = st, *tk_p = tk;
+        uint32_t tma_a = tma_ok;
+        void *args[] = {&kin_p, &vin_p, &kout_p, &vout_p, &n_a, &sh_a, &if_a, &is_a, &of_a, &oa_a,
+                        &bb_p, &st_p, &tk_p, &tma_a};
+        const cudaError_t e = launch(kv ? (count_kv ? KID_COUNT_SCATTER_KV : KID_ONESWEEP_KV) : KID_ONESWEEP, s, [&] {
+            cudaLaunchKernel(k6, dim3(grid), dim3(kSortBlock), args, k6_smem, s);
+        });
         if (e != cudaSuccess) return AHS_ECUDA;
     }
     return AHS_OK;

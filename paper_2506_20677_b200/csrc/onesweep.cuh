@@ -58,14 +58,35 @@ __device__ __forceinline__ uint32_t digit8(uint32_t v, uint32_t shift)
     return __byte_perm(v, 0u, 0x4440u | (shift >> 3));
 }
 
-template <bool KV, int BLOCK, int ITEMS>
+// Shared-memory index of tile slot i in the reordered tile: XOR-swizzled so
+// that 32 consecutive slots stay conflict-free (write-out) while slots 32
+// apart land in different banks (an ascending input puts exactly 32 keys per
+// digit into an 8192-key tile: its scatter would otherwise hit one bank).
+__device__ __forceinline__ uint32_t swz(uint32_t i) { return i ^ ((i >> 5) & 31u); }
+
+// RANK: kRankMasked  16-lane sub-warps, {lane mask | slot} words: atomic add,
+//                    read-back, mask clear (makes no assumption about the order
+//                    in which the lanes of one atomic instruction are served).
+//       kRankOrdered whole warps, plain slot counters: one atomic add with
+//                    return per key IS the rank.  Correct only on hardware that
+//                    serves the same-address lanes of one shared-memory atomic
+//                    instruction in ascending lane order (B200 does: 11.6e9 of
+//                    11.6e9 in tools/atomorder.cu); the CUDA model leaves that
+//                    order unspecified, so the host selects this mode only after
+//                    a self-test of the property on the device (ahs_api.cu).
+constexpr int kRankMasked = 0;
+constexpr int kRankOrdered = 1;
+
+template <bool KV, int BLOCK, int ITEMS, int RANK = kRankMasked>
 struct Onesweep {
     static constexpr int kWarps = BLOCK / 32;
-    static constexpr int kSub = kWarps * 2;  // half-warp sub-warps
+    static constexpr int kGroupLanes = RANK == kRankOrdered ? 32 : 16;  // lanes sharing one digit table
+    static constexpr int kSub = BLOCK / kGroupLanes;                     // digit tables per CTA
     static constexpr int kTile = BLOCK * ITEMS;
-    static constexpr int kSeg = 16 * ITEMS;  // keys per sub-warp
+    static constexpr int kSeg = kGroupLanes * ITEMS;  // keys per table owner
     static constexpr int kTPD = BLOCK / kBins;  // threads per digit in the per-tile scans
-    static_assert(ITEMS % 2 == 1, "odd ITEMS: the half-warps of a warp read disjoint bank halves");
+    static_assert(RANK == kRankOrdered || ITEMS % 2 == 1,
+                  "odd ITEMS: the half-warps of a warp read disjoint bank halves");
     static_assert(BLOCK * ITEMS < 65536, "16-bit slot field");
     static_assert(BLOCK == 256 || BLOCK == 512, "one or two threads per digit");
     static_assert((kTile * 4) % 16 == 0, "TMA tile size");
@@ -78,7 +99,7 @@ struct Onesweep {
     static constexpr size_t kSmem = kOffAux + (size_t)(4 * kBins + 8) * 4;
 };
 
-template <bool KV, int BLOCK, int ITEMS, int MINB>
+template <bool KV, int BLOCK, int ITEMS, int MINB, int RANK = kRankMasked>
 __global__ void __launch_bounds__(BLOCK, MINB)
     k_onesweep(const uint32_t *__restrict__ keys_in, const uint32_t *__restrict__ vals_in,
                uint32_t *__restrict__ keys_out, uint32_t *__restrict__ vals_out, uint32_t n,
@@ -86,8 +107,9 @@ __global__ void __launch_bounds__(BLOCK, MINB)
                const uint32_t *__restrict__ bucket_base, uint32_t *__restrict__ status,
                uint32_t *__restrict__ tile_ticket, uint32_t tma_ok)
 {
-    using C = Onesweep<KV, BLOCK, ITEMS>;
-    constexpr int TILE = C::kTile, SEG = C::kSeg;
+    using C = Onesweep<KV, BLOCK, ITEMS, RANK>;
+    constexpr int TILE = C::kTile, SEG = C::kSeg, GL = C::kGroupLanes;
+    constexpr bool ORDERED = RANK == kRankOrdered;
     extern __shared__ __align__(128) uint8_t smem[];
     uint32_t *s_kb = reinterpret_cast<uint32_t *>(smem + C::kOffK);
     uint32_t *s_vb = reinterpret_cast<uint32_t *>(smem + C::kOffV);
@@ -100,10 +122,10 @@ __global__ void __launch_bounds__(BLOCK, MINB)
     __shared__ uint32_t s_ticket[2];
 
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-    const uint32_t h = lane >> 4, j = lane & 15u;
-    const uint32_t sub = warp * 2u + h;
+    const uint32_t h = ORDERED ? 0u : lane >> 4, j = ORDERED ? lane : lane & 15u;
+    const uint32_t sub = ORDERED ? warp : warp * 2u + h;
     const uint32_t ntiles = (n + TILE - 1) / TILE;
-    const uint32_t lt16 = (1u << j) - 1u;
+    const uint32_t ltj = ORDERED ? lanemask_lt() : (1u << j) - 1u;  // lanes before me in my group
 
     auto tile_full = [&](uint32_t t) { return (uint64_t)(t + 1) * TILE <= n; };
     auto issue = [&](uint32_t t, uint32_t b) {  // thread 0
@@ -156,9 +178,12 @@ __global__ void __launch_bounds__(BLOCK, MINB)
             __syncthreads();
         }
 
-        auto tile_work = [&](auto full_c, auto skew_c) {
+        auto tile_work = [&](auto full_c) {
             constexpr bool FULL = decltype(full_c)::value;
-            constexpr bool SKEW = decltype(skew_c)::value;
+            // uniform-digit fast path for this warp and tile: on when the pass is
+            // skewed, or when the warp's first 32 keys share one digit (sorted
+            // runs); decided once per warp, a warp-uniform runtime branch
+            bool wskew = skew;
             // --------------------------------------------- early counts
             // keys (and values) into registers; per sub-warp digit counts
             uint32_t v[ITEMS];
@@ -167,17 +192,18 @@ __global__ void __launch_bounds__(BLOCK, MINB)
             const uint32_t sbase = sub * SEG + j;
     #pragma unroll
             for (int it = 0; it < ITEMS; it++) {
-                const uint32_t idx = sbase + it * 16;
+                const uint32_t idx = sbase + it * GL;
                 const bool valid = FULL || idx < tile_n;
                 v[it] = ((valid ? sk[idx] : 0u) ^ in_flip) - in_sub;
                 if constexpr (KV) pv[it] = valid ? sv[idx] : 0u;
                 const uint32_t d = digit8(v[it], shift);
-                if constexpr (SKEW) {
+                if (it == 0 && !wskew) wskew = __all_sync(kFull, d == __shfl_sync(kFull, d, 0));
+                if (wskew) {
                     const uint32_t d0 = __shfl_sync(kFull, d, 0);
                     if (__all_sync(kFull, !valid || d == d0)) {
                         // one digit across the warp: same-address atomics would serialise
                         const uint32_t vm = FULL ? kFull : __ballot_sync(kFull, valid);
-                        if (j == 0) cw[d0] += __popc((vm >> (h * 16u)) & 0xffffu);
+                        if (j == 0) cw[d0] += __popc(ORDERED ? vm : (vm >> (h * 16u)) & 0xffffu);
                         __syncwarp();
                         continue;
                     }
@@ -232,42 +258,48 @@ __global__ void __launch_bounds__(BLOCK, MINB)
             // word = {bit 16+j: lane j has this digit in this item | low 16: next slot}
     #pragma unroll
             for (int it = 0; it < ITEMS; it++) {
-                const uint32_t idx = sbase + it * 16;
+                const uint32_t idx = sbase + it * GL;
                 const bool valid = FULL || idx < tile_n;
                 const uint32_t dd = digit8(v[it], shift);
-                uint32_t pos;
+                uint32_t pos = 0;
                 bool done = false;
-                if constexpr (SKEW) {
+                if (wskew) {
                     const uint32_t d0 = __shfl_sync(kFull, dd, 0);
                     if (__all_sync(kFull, !valid || dd == d0)) {
                         const uint32_t vm = FULL ? kFull : __ballot_sync(kFull, valid);
-                        const uint32_t mh = (vm >> (h * 16u)) & 0xffffu;
+                        const uint32_t gm = ORDERED ? vm : (vm >> (h * 16u)) & 0xffffu;
                         const uint32_t c = cw[d0];
-                        pos = c + __popc(mh & lt16);
+                        pos = c + __popc(gm & ltj);
                         __syncwarp();
-                        if (j == 0) cw[d0] = c + __popc(mh);
+                        if (j == 0) cw[d0] = c + __popc(gm);
                         done = true;
                     }
                 }
                 if (!done) {
-                    if (valid) atomicAdd(&cw[dd], (1u << (16u + j)) + 1u);
-                    __syncwarp();
-                    const uint32_t w = cw[dd];
-                    __syncwarp();
-                    if (valid) reinterpret_cast<uint16_t *>(cw + dd)[1] = 0;
-                    pos = (w & 0xffffu) - __popc(w >> (16u + j));
+                    if constexpr (ORDERED) {
+                        // lanes of this instruction are served in lane order (self-tested)
+                        if (valid) pos = atomicAdd(&cw[dd], 1u);
+                    } else {
+                        if (valid) atomicAdd(&cw[dd], (1u << (16u + j)) + 1u);
+                        __syncwarp();
+                        const uint32_t w = cw[dd];
+                        __syncwarp();
+                        if (valid) reinterpret_cast<uint16_t *>(cw + dd)[1] = 0;
+                        pos = (w & 0xffffu) - __popc(w >> (16u + j));
+                    }
                 }
                 if (valid) {
-                    sk[pos] = v[it];
-                    if constexpr (KV) sv[pos] = pv[it];
+                    sk[swz(pos)] = v[it];
+                    if constexpr (KV) sv[swz(pos)] = pv[it];
                 }
                 __syncwarp();
             }
-            // this warp's two digit tables are no longer needed: clear for the next tile
+            // this warp's digit tables are no longer needed: clear for the next tile
             {
-                uint4 *t4 = reinterpret_cast<uint4 *>(s_cnt + warp * 2 * kBins);
+                constexpr int TPW = 32 / GL;  // tables per warp
+                uint4 *t4 = reinterpret_cast<uint4 *>(s_cnt + warp * TPW * kBins);
     #pragma unroll
-                for (int q = 0; q < 2 * kBins / 4 / 32; q++) t4[q * 32 + lane] = make_uint4(0u, 0u, 0u, 0u);
+                for (int q = 0; q < TPW * kBins / 4 / 32; q++) t4[q * 32 + lane] = make_uint4(0u, 0u, 0u, 0u);
             }
 
             // ------------------------------------------- decoupled look-back
@@ -339,28 +371,64 @@ __global__ void __launch_bounds__(BLOCK, MINB)
             if constexpr (FULL) {
     #pragma unroll 5
                 for (int i = tid; i < TILE; i += BLOCK) {
-                    const uint32_t x = sk[i];
+                    const uint32_t x = sk[swz(i)];
                     const uint32_t o = s_gofs[digit8(x, shift)] + i;
                     keys_out[o] = (x + out_add) ^ out_flip;
-                    if constexpr (KV) vals_out[o] = sv[i];
+                    if constexpr (KV) vals_out[o] = sv[swz(i)];
                 }
             } else {
                 for (uint32_t i = tid; i < tile_n; i += BLOCK) {
-                    const uint32_t x = sk[i];
+                    const uint32_t x = sk[swz(i)];
                     const uint32_t o = s_gofs[digit8(x, shift)] + i;
                     keys_out[o] = (x + out_add) ^ out_flip;
-                    if constexpr (KV) vals_out[o] = sv[i];
+                    if constexpr (KV) vals_out[o] = sv[swz(i)];
                 }
             }
         };
-        if (full) {
-            if (skew) tile_work(std::true_type{}, std::true_type{});
-            else tile_work(std::true_type{}, std::false_type{});
-        } else {
-            tile_work(std::false_type{}, std::true_type{});
-        }
+        if (full) tile_work(std::true_type{});
+        else tile_work(std::false_type{});
         __syncthreads();
     }
+}
+
+// Self-test of the hardware property kRankOrdered relies on: the lanes of one
+// shared-memory atomicAdd instruction that hit the same address are served in
+// ascending lane order, so the returned old values are lane-ordered ranks.
+// Same source pattern as the ranking loop (per-warp 256-word tables, items in
+// sequence separated by __syncwarp), with digit collision rates from "all 32
+// lanes on one word" to "spread over 256 words".  Expected ranks come from
+// match.any (slow but independent).  *bad counts violations.
+__device__ __forceinline__ uint32_t selftest_hash(uint32_t x)
+{
+    x ^= x >> 16;
+    x *= 0x7feb352du;
+    x ^= x >> 15;
+    x *= 0x846ca68bu;
+    x ^= x >> 16;
+    return x;
+}
+
+__global__ void __launch_bounds__(512)
+    k_lane_order_selftest(uint32_t *__restrict__ bad, int items)
+{
+    __shared__ uint32_t tab[16][kBins];
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < 16 * kBins; i += blockDim.x) (&tab[0][0])[i] = 0u;
+    __syncthreads();
+    const uint32_t lt = lanemask_lt();
+    uint32_t nbad = 0;
+    for (int it = 0; it < items; it++) {
+        const uint32_t r = selftest_hash((blockIdx.x * blockDim.x + threadIdx.x) * 977u + it * 0x9e3779b9u);
+        const uint32_t mask = (1u << (it % 9)) - 1u;  // 1 .. 256 distinct words
+        const uint32_t dd = (r & mask) * (kBins / (mask + 1u));
+        const uint32_t pos = atomicAdd(&tab[warp][dd], 1u);
+        const uint32_t peers = __match_any_sync(kFull, dd);
+        const uint32_t base = __shfl_sync(kFull, pos, __ffs(peers) - 1);
+        nbad += pos != base + __popc(peers & lt);
+        __syncwarp();
+    }
+    nbad = __reduce_add_sync(kFull, nbad);
+    if (lane == 0 && nbad) atomicAdd(bad, nbad);
 }
 
 }  // namespace ahs

@@ -22,16 +22,25 @@
 
 namespace ahs {
 
-// K6 launch configurations (see onesweep.cuh): keys 512 x 15 (tile 7680,
-// two CTAs per SM), pairs 512 x 9 (tile 4608, two CTAs per SM).
+// K6 launch configurations (see onesweep.cuh), measured on B200
+// (tools/passbench.cu, profiles/r01_summary.md):
+//   masked ranking (no assumption on atomic lane order): keys 512 x 15 (tile
+//     7680, 2 CTAs/SM), pairs 512 x 9 (tile 4608, 2 CTAs/SM);
+//   ordered ranking (after the lane-order self-test): keys 512 x 16 (tile
+//     8192, 2 CTAs/SM), pairs 512 x 15 (tile 7680, 1 CTA/SM).
 constexpr int kSortBlock = 512;
-constexpr int kItemsKeys = 15;
-constexpr int kItemsPairs = 9;
-using OsKeys = Onesweep<false, kSortBlock, kItemsKeys>;
-using OsPairs = Onesweep<true, kSortBlock, kItemsPairs>;
-#define K6_KEYS k_onesweep<false, kSortBlock, kItemsKeys, 2>
-#define K6_PAIRS k_onesweep<true, kSortBlock, kItemsPairs, 2>
-constexpr int kMinTile = OsPairs::kTile < OsKeys::kTile ? OsPairs::kTile : OsKeys::kTile;
+using OsKeysM = Onesweep<false, kSortBlock, 15, kRankMasked>;
+using OsPairsM = Onesweep<true, kSortBlock, 9, kRankMasked>;
+using OsKeysO = Onesweep<false, kSortBlock, 16, kRankOrdered>;
+using OsPairsO = Onesweep<true, kSortBlock, 15, kRankOrdered>;
+#define K6_KEYS_M k_onesweep<false, kSortBlock, 15, 2, kRankMasked>
+#define K6_PAIRS_M k_onesweep<true, kSortBlock, 9, 2, kRankMasked>
+#define K6_KEYS_O k_onesweep<false, kSortBlock, 16, 2, kRankOrdered>
+#define K6_PAIRS_O k_onesweep<true, kSortBlock, 15, 1, kRankOrdered>
+constexpr int kMinTile = 4608;  // smallest K6 tile: sizes the look-back status buffer
+static_assert(kMinTile <= OsKeysM::kTile && kMinTile <= OsPairsM::kTile && kMinTile <= OsKeysO::kTile &&
+                  kMinTile <= OsPairsO::kTile,
+              "kMinTile");
 
 // ------------------------------------------------------------------ K5 ----
 // Digit histograms of v = (key ^ flip) - min for the `passes` 8-bit digits.

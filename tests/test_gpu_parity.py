@@ -2,9 +2,11 @@
 
 Bar: features n/min/max/k/bits/shift/nbins/descents bit-exact, |dH| <= 1e-9
 (BASELINE.json north_star), strategy + rule identical, keys and values
-bit-exact (the unique stable order).  Sizes span several tiles (7680 keys /
-4608 pairs per onesweep tile) with ragged tails, and sizes where every
-persistent CTA walks several tiles; full BASELINE.json configs at the end.
+bit-exact (the unique stable order).  Sizes span several tiles (onesweep
+tiles: 8192 keys / 7680 pairs with the ordered ranking, 7680 / 4608 with the
+masked ranking, which has its own parity test) with ragged tails, and sizes
+where every persistent CTA walks several tiles; full BASELINE.json configs at
+the end.
 """
 import math
 
@@ -105,7 +107,7 @@ def check_forced(keys, vals, strategy, **kw):
 # --------------------------------------------------------------- T4 small
 
 SIZES = [1, 2, 3, 4, 5, 7, 8, 15, 16, 17, 21, 33, 1000, 4607, 4608, 4609, 7679, 7680, 7681,
-         3 * 7680 + 77, 5 * 4608 + 13, 65537, 250_001]
+         8191, 8192, 8193, 3 * 7680 + 77, 3 * 8192 + 77, 5 * 4608 + 13, 65537, 250_001]
 
 FAMILIES = {
     "u1000": lambda n, s: synth.uniform_range(s, n, 0, 999),
@@ -136,6 +138,31 @@ def test_pipeline_many_tiles_per_cta(family):
     keys = FAMILIES[family](n, 7)
     check_pipeline(keys)
     check_pipeline(keys, np.arange(n, dtype=np.uint32))
+
+
+@pytest.fixture
+def masked_rank():
+    """Run a test with the masked (order-agnostic) onesweep ranking, then restore."""
+    prev = ahs.ahs_rank_mode()
+    ahs.ahs_rank_mode(ahs.RANK_MASKED)
+    yield
+    ahs.ahs_rank_mode(prev)
+
+
+def test_lane_order_selftest_selects_ordered_ranking():
+    # B200 serves same-address lanes of one shared atomic in lane order
+    # (tools/atomorder.cu); the library then uses the one-atomic ranking
+    assert ahs.ahs_lane_order_ok()
+    assert ahs.ahs_rank_mode() == ahs.RANK_ORDERED
+
+
+@pytest.mark.parametrize("family", ["full32", "zipf_wide", "neg16", "alt_extremes", "const"])
+def test_masked_ranking_parity(family, masked_rank):
+    assert ahs.ahs_rank_mode() == ahs.RANK_MASKED
+    for n in (1, 33, 7679, 7681, 4609, 3 * 7680 + 77, 250_001, 3_000_017):
+        keys = FAMILIES[family](n, 11)
+        check_pipeline(keys)
+        check_pipeline(keys, np.arange(n, dtype=np.uint32))
 
 
 def test_pipeline_empty():

@@ -46,6 +46,8 @@ __global__ void k_gen(uint32_t *k, uint32_t *v, uint32_t n, int dist, uint32_t s
             x = (r << 2) | (x & 0xffffff00u);
         } else if (dist == 2) {
             x = (x & 0xffffff00u) | 42u;
+        } else if (dist == 3) {  // ascending (presorted) keys
+            x = i;
         }
         k[i] = x;
         v[i] = i;
@@ -76,13 +78,13 @@ struct Bufs {
 
 static int g_only = -1, g_idx = 0;
 
-template <bool KV, int BLOCK, int ITEMS, int MINB, bool NIB = false>
+template <bool KV, int BLOCK, int ITEMS, int MINB, int RANK = kRankMasked>
 float run_cfg(const Bufs &B, uint32_t n, uint32_t shift, int sms, int reps, bool check,
               const std::vector<uint32_t> &hk, const std::vector<uint32_t> &hbase)
 {
     if (g_only >= 0 && g_idx++ != g_only) return 0.f;
-    using C = Onesweep<KV, BLOCK, ITEMS>;
-    auto kern = k_onesweep<KV, BLOCK, ITEMS, MINB>;
+    using C = Onesweep<KV, BLOCK, ITEMS, RANK>;
+    auto kern = k_onesweep<KV, BLOCK, ITEMS, MINB, RANK>;
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmem));
     int occ = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, BLOCK, C::kSmem));
@@ -134,7 +136,7 @@ float run_cfg(const Bufs &B, uint32_t n, uint32_t shift, int sms, int reps, bool
     const double bytes = (KV ? 16.0 : 8.0) * n;
     printf("  %s<%s,B%d,I%d,minb%d> tile %5d occ %d grid %4u: %8.1f us  %7.1f GB/s  %6.1f Gkeys/s  "
            "%.2f keys/clk/SM@1.9 max %.1f us %s\n",
-           NIB ? "nibble  " : "onesweep", KV ? "kv" : "k", BLOCK, ITEMS, MINB, C::kTile, occ, grid, med * 1e3, bytes / med / 1e6,
+           RANK == kRankOrdered ? "ordered " : "masked  ", KV ? "kv" : "k", BLOCK, ITEMS, MINB, C::kTile, occ, grid, med * 1e3, bytes / med / 1e6,
            n / med / 1e6, n / med / 1e6 / sms / 1.9, ts.back() * 1e3, check ? (ok ? "ok" : "FAIL") : "");
     return med;
 }
@@ -199,7 +201,7 @@ int main(int argc, char **argv)
     std::vector<uint32_t> hk(n);
     CK(cudaMemcpy(hk.data(), B.k, n * 4ull, cudaMemcpyDeviceToHost));
     printf("n = %u, dist %d, %d SMs\n", n, dist, sms);
-    for (uint32_t shift : {0u, 24u})
+    for (uint32_t shift : {0u, 8u})
         if (g_only < 0 || shift == 0) {
         std::vector<uint32_t> hist(256, 0), base(256);
         for (uint32_t i = 0; i < n; i++) hist[(hk[i] >> shift) & 255u]++;
@@ -213,8 +215,9 @@ int main(int argc, char **argv)
         printf("digit shift %u (max digit share %.3f)\n", shift, (double)mx / n);
         g_idx = 0;
         run_cfg<false, 512, 15, 2>(B, n, shift, sms, reps, true, hk, base);
+        run_cfg<false, 512, 16, 2, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
         run_cfg<true, 512, 9, 2>(B, n, shift, sms, reps, true, hk, base);
-        run_cfg<true, 512, 15, 1>(B, n, shift, sms, reps, true, hk, base);
+        run_cfg<true, 512, 15, 1, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
     }
     if (cub) {
         run_cub<false>(B, n, 0, 32, sms, reps);
