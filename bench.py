@@ -210,8 +210,11 @@ def time_pipeline(torch, ahs, keys_np, vals_np, steps, warmup, device, flush, pr
     total_ms = sum(a.elapsed_time(b) for a, b in ev)
     prof = ahs.ahs_profile_read() if profile else None
     passes = ahs.ahs_sort_passes(f, s, dv is not None)
+    executed = ahs.ahs_sort_executed_passes(ws, stream) if passes > 0 else 0
+    if executed < 0:  # no device plan on this path (COUNTING): the nominal passes all run
+        executed = passes
     return dict(total_ms=total_ms, f=f, s=s, r=r, launches=launches, prof=prof, passes=passes,
-                clocks=clocks, step_ms=[a.elapsed_time(b) for a, b in ev])
+                executed=executed, clocks=clocks, step_ms=[a.elapsed_time(b) for a, b in ev])
 
 
 def time_e2e(torch, ahs, keys_np, vals_np, steps, warmup, device):
@@ -283,6 +286,9 @@ def run_ours(args):
     if prof[kname]["launches"] == 0:
         kname = max(prof, key=lambda k: prof[k]["ms"])
     kl = prof[kname]["launches"]
+    if kname.startswith("onesweep") and res["executed"] < res["passes"]:
+        # NEXT-1 skipped launches return at once: average over the executed ones
+        kl = kl * res["executed"] // res["passes"]
     kms = prof[kname]["ms"] / max(1, kl)
     per_launch_bytes = {"onesweep": 8 * n, "onesweep_kv": 16 * n, "count_fill": 4 * n,
                         "count_scatter_kv": 16 * n, "radix_hist": 4 * n, "feat_reduce": 4 * n,
@@ -293,7 +299,7 @@ def run_ours(args):
     kernels = {k: {"ms_per_launch": v["ms"] / v["launches"], "launches": v["launches"],
                    "share_of_kernel_time": v["ms"] / step_total}
                for k, v in prof.items() if v["launches"]}
-    sb = sort_bytes(s, res["passes"], n, kv)
+    sb = sort_bytes(s, res["executed"], n, kv)
     sort_ms = sum(v["ms"] for k, v in prof.items() if not k.startswith("feat")) / args.steps
     feat_ms = sum(v["ms"] for k, v in prof.items() if k.startswith("feat")) / args.steps
 
@@ -304,6 +310,7 @@ def run_ours(args):
         "data": "synthetic (SplitMix64 recipe of SURVEY.md §8(d))",
         "config": {"workload": args.workload, "n": n, "key_dtype": dt, "kv": kv,
                    "strategy": ahs.STRATEGY_NAMES[s], "rule": ahs.RULE_NAMES[r], "passes": res["passes"],
+                   "passes_executed": res["executed"],
                    "l2": "flushed before every timed step (256 MiB write)",
                    "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU"},
         "roofline": {"bound": "hbm", "kernel": kname, "achieved": round(achieved, 1), "peak": peak,
@@ -338,10 +345,10 @@ def run_ours(args):
             kv2 = v2 is not None
             sort_ms2 = sum(v["ms"] for k, v in p2.items() if not k.startswith("feat")) / args.table_steps
             feat_ms2 = sum(v["ms"] for k, v in p2.items() if k.startswith("feat")) / args.table_steps
-            sb2 = sort_bytes(r2["s"], r2["passes"], n2, kv2)
+            sb2 = sort_bytes(r2["s"], r2["executed"], n2, kv2)
             rows.append({
                 "workload": cfg, "n": n2, "kv": kv2, "strategy": ahs.STRATEGY_NAMES[r2["s"]],
-                "rule": ahs.RULE_NAMES[r2["r"]], "passes": r2["passes"],
+                "rule": ahs.RULE_NAMES[r2["r"]], "passes": r2["passes"], "passes_executed": r2["executed"],
                 "pipeline_Gkeys_s": n2 * args.table_steps / (r2["total_ms"] * 1e-3) / 1e9,
                 "sort_Gkeys_s": n2 / (sort_ms2 * 1e-3) / 1e9 if sort_ms2 > 0 else None,
                 "sort_GBps": sb2 / (sort_ms2 * 1e-3) / 1e9 if sort_ms2 > 0 else None,
@@ -401,7 +408,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg2", choices=sorted(synth.CONFIGS))
-    ap.add_argument("--configs", default="cfg1,cfg2kv,cfg3,cfg4a,cfg4d,cfg5_r8,cfg5_r32",
+    ap.add_argument("--configs", default="cfg1,cfg2kv,cfg3,cfg4a,cfg4b,cfg4d,cfg5_r8,cfg5_r16,cfg5_r24,cfg5_r32",
                     help="per-strategy table rows (single GPU only); '' to skip")
     ap.add_argument("--table-steps", type=int, default=5)
     ap.add_argument("--soak", type=float, default=2.0, help="untimed seconds of load before timing")

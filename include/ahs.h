@@ -199,6 +199,21 @@ AHS_API int ahs_sort_host(const void *h_keys_in, const uint32_t *h_vals_in, void
 AHS_API int ahs_rank_mode(int mode);
 AHS_API int ahs_lane_order_ok(void);
 
+/* ------------------------------------------- trivial-pass skipping (NEXT-1) */
+/* A radix pass whose digit is the same for every key is an identity
+ * permutation.  With skipping on (default; environment AHS_SKIP_TRIVIAL=0
+ * turns it off), K5 writes a device-side pass plan into d_tmp and such passes
+ * return at once; the remaining passes keep the buffer parity so the result
+ * still lands in keys_out.  Not used in place (keys_out == keys_in), where the
+ * parity must be known on the host.  Output is identical either way.
+ * ahs_set_skip_trivial(0/1) sets it (any other value queries); returns the
+ * setting.  ahs_sort_executed_passes() reads the plan of the last ahs_sort on
+ * that d_tmp (synchronizes `stream`): the number of executed digit passes, or
+ * -1 if that sort wrote no plan (COUNTING paths). */
+AHS_API int ahs_set_skip_trivial(int on);
+AHS_API int ahs_sort_executed_passes(const void *d_tmp, size_t tmp_bytes, uint64_t n, int has_vals,
+                                     void *stream);
+
 /* -------------------------------------------------------- instrumentation */
 /* Kernels launched by this library since load (all streams, all threads). */
 AHS_API uint64_t ahs_launch_count(void);

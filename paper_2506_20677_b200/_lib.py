@@ -69,6 +69,8 @@ def lib():
                                C.POINTER(Features), p_i32, p_i32, vp], C.c_int),
             "ahs_launch_count": ([], C.c_uint64),
             "ahs_rank_mode": ([C.c_int], C.c_int),
+            "ahs_set_skip_trivial": ([C.c_int], C.c_int),
+            "ahs_sort_executed_passes": ([vp, sz, u64, C.c_int, vp], C.c_int),
             "ahs_lane_order_ok": ([], C.c_int),
             "ahs_kernel_count": ([], C.c_int),
             "ahs_kernel_name": ([C.c_int], C.c_char_p),
@@ -127,6 +129,17 @@ def ahs_rank_mode(mode: int = -1) -> int:
     if rc < 0:
         raise AhsError(rc, "ahs_rank_mode")
     return rc
+
+
+def ahs_set_skip_trivial(on: int = -1) -> int:
+    """NEXT-1 trivial-pass skipping: 1 on, 0 off, -1 query; returns the setting."""
+    return lib().ahs_set_skip_trivial(on)
+
+
+def ahs_sort_executed_passes(ws: "Workspace", stream=None) -> int:
+    """Executed digit passes of the last ahs_sort that used `ws` (-1: no plan, COUNTING)."""
+    return lib().ahs_sort_executed_passes(_dev_ptr(ws.tmp), ws.tmp.numel(), ws.n, int(ws.has_vals),
+                                          _stream(stream))
 
 
 def ahs_lane_order_ok() -> bool:

@@ -171,6 +171,11 @@ const char *kKernelNames[KID_COUNT] = {"feat_reduce", "feat_hist",   "feat_final
                                        "count_fill",  "count_scatter_kv"};
 
 std::atomic<uint64_t> g_launches{0};
+// NEXT-1 trivial-pass skipping (default on; AHS_SKIP_TRIVIAL=0 or ahs_set_skip_trivial(0) turn it off)
+std::atomic<bool> g_skip_trivial{[] {
+    const char *e = std::getenv("AHS_SKIP_TRIVIAL");
+    return !(e && e[0] == '0');
+}()};
 std::atomic<bool> g_prof{false};
 std::mutex g_prof_mu;
 struct ProfRec {
@@ -341,6 +346,28 @@ int ahs_rank_mode(int mode)
         return AHS_EINVAL;
     }
     return di->rank_mode;
+}
+
+int ahs_set_skip_trivial(int on)
+{
+    if (on != 0 && on != 1) return g_skip_trivial.load() ? 1 : 0;
+    g_skip_trivial.store(on == 1);
+    return on;
+}
+
+int ahs_sort_executed_passes(const void *d_tmp, size_t tmp_bytes, uint64_t n, int has_vals, void *stream)
+{
+    const TmpLayout TL = tmp_layout(n, has_vals);
+    if (!d_tmp || tmp_bytes < TL.total) return AHS_EINVAL;
+    uint32_t w[6];
+    cudaStream_t s = (cudaStream_t)stream;
+    if (cudaMemcpyAsync(w, (const char *)d_tmp + TL.ticket + 8 * 4, sizeof(w), cudaMemcpyDeviceToHost, s) !=
+            cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess) {
+        cudaGetLastError();
+        return AHS_ECUDA;
+    }
+    return w[5] == kPlanMagic ? (int)w[4] : -1;
 }
 
 int ahs_lane_order_ok(void)
@@ -603,10 +630,12 @@ int ahs_sort(const void *d_keys_in, const uint32_t *d_vals_in, void *d_keys_out,
     const size_t zero_bytes = (TL.status - TL.ctrl) + status_words_per_pass * 4 * passes;
     if (cudaMemsetAsync(tmp + TL.ctrl, 0, zero_bytes, s) != cudaSuccess) return AHS_ECUDA;
 
-    // in place with an odd pass count: stream the input to tmp first
+    // in place with an odd pass count: stream the input to tmp first.  In place,
+    // the pass count (and so the buffer parity) must be known here: no skipping.
     const uint32_t *src_k = kin;
     const uint32_t *src_v = d_vals_in;
     const bool inplace = (const void *)kout == d_keys_in || (kv && (const void *)d_vals_out == d_vals_in);
+    const bool skip = !inplace && g_skip_trivial.load() && !count_kv;
     if (inplace && (passes & 1)) {
         if (cudaMemcpyAsync(tkeys, kin, n * 4, cudaMemcpyDeviceToDevice, s) != cudaSuccess) return AHS_ECUDA;
         if (kv && cudaMemcpyAsync(tvals, d_vals_in, n * 4, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
@@ -616,6 +645,7 @@ int ahs_sort(const void *d_keys_in, const uint32_t *d_vals_in, void *d_keys_out,
     }
 
     if (!d_ws || ws_bytes < WL.total) return AHS_ENOSPACE;
+    uint32_t *plan = tickets + 8;
     const uint32_t *bases;
     if (count_kv) {
         bases = (const uint32_t *)((const char *)d_ws + WL.scan);
@@ -630,35 +660,32 @@ int ahs_sort(const void *d_keys_in, const uint32_t *d_vals_in, void *d_keys_out,
         }
         cudaError_t e = launch(KID_RADIX_HIST, s, [&] {
             k_radix_hist<kRHBlock><<<(unsigned)g5, kRHBlock, kRHSmem, s>>>(
-                src_k, n, flip, sub, passes, fhist, feat->nbins, feat->shift, dhist, bucket, tickets + 7);
+                src_k, n, flip, sub, passes, fhist, feat->nbins, feat->shift, dhist, bucket, tickets + 7, plan,
+                skip ? 1 : 0);
         });
         if (e != cudaSuccess) return AHS_ECUDA;
         bases = bucket;
     }
 
     for (int p = 0; p < passes; p++) {
-        const bool first = p == 0, last = p == passes - 1;
-        // destination parity: the last pass always lands in out
-        const bool to_out = ((passes - 1 - p) & 1) == 0;
-        uint32_t *dk = to_out ? kout : tkeys;
-        uint32_t *dv = kv ? (to_out ? d_vals_out : tvals) : nullptr;
-        const uint32_t *sk = first ? src_k : (to_out ? tkeys : kout);
-        const uint32_t *sv = kv ? (first ? src_v : (to_out ? tvals : d_vals_out)) : nullptr;
-        const uint32_t in_flip = first ? flip : 0u, in_sub = first ? sub : 0u;
-        const uint32_t out_flip = last ? flip : 0u, out_add = last ? sub : 0u;
-        const uint32_t shift = count_kv ? 0u : 8u * (uint32_t)p;
-        uint32_t *st = status + (size_t)p * status_words_per_pass;
-        uint32_t *tk = tickets + p;
-        const uint32_t *bb = count_kv ? bases : bases + 256 * p;
-        const uint32_t tma_ok = (((uintptr_t)sk & 15u) == 0) && (!kv || ((uintptr_t)sv & 15u) == 0);
-        const void *kin_p = sk, *vin_p = sv;
-        void *kout_p = dk, *vout_p = dv;
-        const void *bb_p = bb;
-        uint32_t n_a = n32, sh_a = shift, if_a = in_flip, is_a = in_sub, of_a = out_flip, oa_a = out_add;
-        void *st_p = st, *tk_p = tk;
-        uint32_t tma_a = tma_ok;
-        void *args[] = {&kin_p, &vin_p, &kout_p, &vout_p, &n_a, &sh_a, &if_a, &is_a, &of_a, &oa_a,
-                        &bb_p, &st_p, &tk_p, &tma_a};
+        PassArgs pa;
+        pa.keys_in = src_k;
+        pa.vals_in = kv ? src_v : nullptr;
+        pa.keys_out = kout;
+        pa.vals_out = kv ? d_vals_out : nullptr;
+        pa.keys_tmp = tkeys;
+        pa.vals_tmp = kv ? tvals : nullptr;
+        pa.n = n32;
+        pa.pass = (uint32_t)p;
+        pa.npasses = (uint32_t)passes;
+        pa.shift = count_kv ? 0u : 8u * (uint32_t)p;
+        pa.flip = flip;
+        pa.sub = sub;
+        pa.bucket_base = count_kv ? bases : bases + 256 * p;
+        pa.status = status + (size_t)p * status_words_per_pass;
+        pa.ticket = tickets + p;
+        pa.plan = count_kv ? nullptr : plan;  // K5's plan (no skipping when not enabled)
+        void *args[] = {&pa};
         const cudaError_t e = launch(kv ? (count_kv ? KID_COUNT_SCATTER_KV : KID_ONESWEEP_KV) : KID_ONESWEEP, s, [&] {
             cudaLaunchKernel(k6, dim3(grid), dim3(kSortBlock), args, k6_smem, s);
         });

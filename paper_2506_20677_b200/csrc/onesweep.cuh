@@ -99,14 +99,50 @@ struct Onesweep {
     static constexpr size_t kSmem = kOffAux + (size_t)(4 * kBins + 8) * 4;
 };
 
+// One digit pass of a chain of `npasses` LSD passes.  Buffers: the chain reads
+// `keys_in` (first executed pass, input transform v = (key ^ flip) - sub) and
+// ping-pongs between `keys_tmp` and `keys_out` so that the last executed pass
+// (output transform key = (v + sub) ^ flip) lands in `keys_out`.  With a
+// device plan (K5, NEXT-1 trivial-pass skipping) a pass whose digit is the
+// same for every key is an identity permutation: its launch returns at once,
+// and the executed passes are renumbered 0 .. m-1 (plan word: exec index << 8
+// | m, or kPassSkip).  Without a plan, pass p is executed pass p of npasses.
+constexpr uint32_t kPassSkip = 0xffffffffu;
+struct PassArgs {
+    const uint32_t *keys_in, *vals_in;
+    uint32_t *keys_out, *vals_out, *keys_tmp, *vals_tmp;
+    uint32_t n, pass, npasses, shift, flip, sub;
+    const uint32_t *bucket_base;  // this pass's 256 digit bases
+    uint32_t *status, *ticket;    // this pass's look-back statuses and tile ticket (zeroed)
+    const uint32_t *plan;         // nullptr: no skipping
+};
+
 template <bool KV, int BLOCK, int ITEMS, int MINB, int RANK = kRankMasked>
-__global__ void __launch_bounds__(BLOCK, MINB)
-    k_onesweep(const uint32_t *__restrict__ keys_in, const uint32_t *__restrict__ vals_in,
-               uint32_t *__restrict__ keys_out, uint32_t *__restrict__ vals_out, uint32_t n,
-               uint32_t shift, uint32_t in_flip, uint32_t in_sub, uint32_t out_flip, uint32_t out_add,
-               const uint32_t *__restrict__ bucket_base, uint32_t *__restrict__ status,
-               uint32_t *__restrict__ tile_ticket, uint32_t tma_ok)
+__global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(const PassArgs a)
 {
+    // ---- this pass's place in the chain
+    uint32_t e = a.pass, m = a.npasses;
+    if (a.plan) {
+        const uint32_t w = a.plan[a.pass];
+        if (w == kPassSkip) return;  // constant digit: identity
+        e = w >> 8;
+        m = w & 255u;
+    }
+    const bool first = e == 0, last = e + 1 == m;
+    const bool to_out = ((m - 1 - e) & 1u) == 0;        // destination parity: the last lands in out
+    const bool from_out = !first && !to_out;             // source = the previous pass's destination
+    const uint32_t *__restrict__ keys_in = first ? a.keys_in : (from_out ? a.keys_out : a.keys_tmp);
+    const uint32_t *__restrict__ vals_in = first ? a.vals_in : (from_out ? a.vals_out : a.vals_tmp);
+    uint32_t *__restrict__ keys_out = to_out ? a.keys_out : a.keys_tmp;
+    uint32_t *__restrict__ vals_out = to_out ? a.vals_out : a.vals_tmp;
+    const uint32_t n = a.n, shift = a.shift;
+    const uint32_t in_flip = first ? a.flip : 0u, in_sub = first ? a.sub : 0u;
+    const uint32_t out_flip = last ? a.flip : 0u, out_add = last ? a.sub : 0u;
+    const uint32_t *__restrict__ bucket_base = a.bucket_base;
+    uint32_t *__restrict__ status = a.status;
+    uint32_t *__restrict__ tile_ticket = a.ticket;
+    const uint32_t tma_ok = (((uintptr_t)keys_in & 15u) == 0) && (!KV || ((uintptr_t)vals_in & 15u) == 0);
+
     using C = Onesweep<KV, BLOCK, ITEMS, RANK>;
     constexpr int TILE = C::kTile, SEG = C::kSeg, GL = C::kGroupLanes;
     constexpr bool ORDERED = RANK == kRankOrdered;

@@ -52,6 +52,7 @@ static_assert(kMinTile <= OsKeysM::kTile && kMinTile <= OsPairsM::kTile && kMinT
 // (the kernel is shared-atomic bound otherwise), with the same run merging
 // as feat_hist.  Marginals are flushed with global atomics into dhist (zeroed
 // by the host's memset); the last CTA turns them into exclusive bucket bases.
+constexpr uint32_t kPlanMagic = 0xa45c0de1u;  // plan[5] once K5 has written a plan
 constexpr int kRHBlock = 1024;
 constexpr int kRHChunk = 46 * 1024;  // < 3 vectors per thread (fits 227 KB with the 4 KB static digit tables)
 constexpr int kRHStages = 2;
@@ -91,12 +92,13 @@ __global__ void __launch_bounds__(BLOCK, 1)
     k_radix_hist(const uint32_t *__restrict__ keys, uint64_t n, uint32_t flip, uint32_t sub, int passes,
                  const uint32_t *__restrict__ fhist, uint32_t nb, uint32_t fshift,
                  uint32_t *__restrict__ dhist, uint32_t *__restrict__ bucket_base,
-                 uint32_t *__restrict__ ticket)
+                 uint32_t *__restrict__ ticket, uint32_t *__restrict__ plan, int skip_trivial)
 {
     extern __shared__ __align__(128) uint32_t sh[];
     __shared__ uint32_t s_dig[4][256];
     __shared__ __align__(8) uint64_t bars[kRHStages];
     __shared__ bool s_last;
+    __shared__ uint32_t s_triv[4];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
     const bool from_keys = fshift > 0u;  // digits 0 and 1 need the keys
     for (int i = threadIdx.x; i < 4 * 256; i += BLOCK) (&s_dig[0][0])[i] = 0u;
@@ -184,12 +186,29 @@ __global__ void __launch_bounds__(BLOCK, 1)
             const uint32_t t = __shfl_up_sync(kFull, incl, o);
             if (lane >= (uint32_t)o) incl += t;
         }
-        uint32_t run = incl - sum;
+        uint32_t run = incl - sum, mx = 0;
 #pragma unroll
         for (int j = 0; j < 8; j++) {
             bucket_base[warp * 256 + lane * 8 + j] = run;
             run += c[j];
+            mx = max(mx, c[j]);
         }
+        // NEXT-1: a digit that every key shares makes its pass an identity
+        mx = __reduce_max_sync(kFull, mx);
+        if (lane == 0) s_triv[warp] = skip_trivial && (uint64_t)mx == n;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        // device pass plan: executed passes renumbered 0 .. m-1; plan[4] = m, plan[5] = magic
+        uint32_t m = 0;
+        for (int p = 0; p < passes; p++) m += s_triv[p] ? 0u : 1u;
+        uint32_t e = 0;
+        for (int p = 0; p < passes; p++) {
+            plan[p] = s_triv[p] ? kPassSkip : ((e << 8) | m);
+            e += s_triv[p] ? 0u : 1u;
+        }
+        plan[4] = m;
+        plan[5] = kPlanMagic;
     }
 }
 

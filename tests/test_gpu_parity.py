@@ -58,7 +58,7 @@ def check_features(f, of):
     assert f.flags == of.flags
 
 
-def run_gpu(keys, vals=None, strategy=None, misalign=0, inplace=False, th=None, stream=None):
+def run_gpu(keys, vals=None, strategy=None, misalign=0, inplace=False, th=None, stream=None, info=None):
     n = keys.size
     dk = to_dev(keys, misalign)
     dv = to_dev(vals, misalign) if vals is not None else None
@@ -74,6 +74,9 @@ def run_gpu(keys, vals=None, strategy=None, misalign=0, inplace=False, th=None, 
         vo = to_dev(np.zeros_like(vals), misalign) if vals is not None else None
     ahs.ahs_sort(dk, dv, ko, vo, s, f, ws, stream)
     torch.cuda.synchronize()
+    if info is not None:
+        info["executed"] = ahs.ahs_sort_executed_passes(ws, stream)
+        info["nominal"] = ahs.ahs_sort_passes(f, s, vals is not None)
     return f, s, r, to_host(ko), (to_host(vo) if vo is not None else None)
 
 
@@ -163,6 +166,60 @@ def test_masked_ranking_parity(family, masked_rank):
         keys = FAMILIES[family](n, 11)
         check_pipeline(keys)
         check_pipeline(keys, np.arange(n, dtype=np.uint32))
+
+
+@pytest.fixture
+def skip_off():
+    prev = ahs.ahs_set_skip_trivial(-1)
+    ahs.ahs_set_skip_trivial(0)
+    yield
+    ahs.ahs_set_skip_trivial(prev)
+
+
+# NEXT-1: (keys, strategy, expected executed passes with skipping)
+TRIVIAL_CASES = {
+    # key - min = j * 2^18: digits 0 and 1 constant (cfg3's structure) -> RADIX, 2 of 4 passes
+    "cfg3_like": (lambda n: synth.cfg3(n, seed=5), None, 2),
+    # k = 2^16 under GENERAL (4 passes): digits 2 and 3 of key - min are 0
+    "general_16bit": (lambda n: synth.uniform_range(6, n, 1000, 1000 + 65535), 2, 2),
+    # k = 2^20: only digit 3 constant
+    "general_20bit": (lambda n: synth.uniform_range(7, n, -(2 ** 19), 2 ** 19 - 1), 2, 3),
+    # full 32-bit: nothing to skip
+    "general_32bit": (lambda n: synth.uniform_range(8, n, -(2 ** 31), 2 ** 31 - 1), 2, 4),
+}
+
+
+@pytest.mark.parametrize("case", list(TRIVIAL_CASES))
+def test_trivial_pass_skipping(case):
+    gen, strategy, want = TRIVIAL_CASES[case]
+    for n in (33, 7681, 250_001):
+        keys = gen(n)
+        if strategy is None:
+            ok, ov = oracle.sort(keys, np.arange(n, dtype=np.uint32), oracle.QUICK)
+        for vals in (None, np.arange(n, dtype=np.uint32)):
+            info = {}
+            f, s, r, ko, vo = run_gpu(keys, vals, strategy=strategy, info=info)
+            ok, ov = oracle.sort(keys, vals, oracle.QUICK)
+            assert np.array_equal(ko, ok)
+            if vals is not None:
+                assert np.array_equal(vo, ov)
+            if n > 1000:  # tiny inputs may have more constant digits by chance
+                assert info["executed"] == want, (case, n, info)
+            # in place: the parity must be known on the host, no skipping
+            info2 = {}
+            f, s, r, ko, vo = run_gpu(keys, vals, strategy=strategy, inplace=True, info=info2)
+            assert np.array_equal(ko, ok)
+            assert info2["executed"] == info2["nominal"]
+
+
+def test_trivial_pass_skipping_off(skip_off):
+    keys = synth.cfg3(250_001, seed=5)
+    for vals in (None, np.arange(keys.size, dtype=np.uint32)):
+        info = {}
+        f, s, r, ko, vo = run_gpu(keys, vals, info=info)
+        ok, ov = oracle.sort(keys, vals, oracle.QUICK)
+        assert np.array_equal(ko, ok)
+        assert info["executed"] == info["nominal"] == 4
 
 
 def test_pipeline_empty():

@@ -99,8 +99,22 @@ float run_cfg(const Bufs &B, uint32_t n, uint32_t shift, int sms, int reps, bool
         CK(cudaMemsetAsync(B.status, 0, (size_t)tiles * 256 * 4));
         CK(cudaMemsetAsync(B.ticket, 0, 4));
         CK(cudaEventRecord(a));
-        kern<<<grid, BLOCK, C::kSmem>>>(B.k, B.v, B.ko, B.vo, n, shift, 0u, 0u, 0u, 0u, B.bb, B.status, B.ticket,
-                                        1u);
+        PassArgs pa{};
+        pa.keys_in = B.k;
+        pa.vals_in = B.v;
+        pa.keys_out = B.ko;
+        pa.vals_out = B.vo;
+        pa.keys_tmp = B.ko;
+        pa.vals_tmp = B.vo;
+        pa.n = n;
+        pa.pass = 0;
+        pa.npasses = 1;
+        pa.shift = shift;
+        pa.bucket_base = B.bb;
+        pa.status = B.status;
+        pa.ticket = B.ticket;
+        pa.plan = nullptr;
+        kern<<<grid, BLOCK, C::kSmem>>>(pa);
         CK(cudaEventRecord(b));
         CK(cudaEventSynchronize(b));
         CK(cudaGetLastError());
