@@ -245,12 +245,13 @@ def time_e2e(torch, ahs, keys_np, vals_np, steps, warmup, device):
     return ms, nb, nb
 
 
-def sort_bytes(strategy: int, passes: int, n: int, kv: bool) -> int:
-    """Algorithmic HBM bytes of ahs_sort: radix = histogram read 4n +
-    per pass read+write (8n keys, 16n pairs); counting keys-only = write 4n."""
+def sort_bytes(strategy: int, passes: int, n: int, kv: bool, shift: int = 1) -> int:
+    """Algorithmic HBM bytes of ahs_sort: radix = K5's read of the keys
+    (4n, only when the feature buckets are coarser than the keys: shift > 0) + per
+    executed pass read+write (8n keys, 16n pairs); counting keys-only = write 4n."""
     if passes == 0:
         return 4 * n if strategy == 0 else 0
-    hist = 0 if (strategy == 0 and passes == 1) else 4 * n
+    hist = 0 if (strategy == 0 and passes == 1) or shift == 0 else 4 * n
     return hist + passes * (16 if kv else 8) * n
 
 
@@ -299,7 +300,7 @@ def run_ours(args):
     kernels = {k: {"ms_per_launch": v["ms"] / v["launches"], "launches": v["launches"],
                    "share_of_kernel_time": v["ms"] / step_total}
                for k, v in prof.items() if v["launches"]}
-    sb = sort_bytes(s, res["executed"], n, kv)
+    sb = sort_bytes(s, res["executed"], n, kv, f.shift)
     sort_ms = sum(v["ms"] for k, v in prof.items() if not k.startswith("feat")) / args.steps
     feat_ms = sum(v["ms"] for k, v in prof.items() if k.startswith("feat")) / args.steps
 
@@ -345,7 +346,7 @@ def run_ours(args):
             kv2 = v2 is not None
             sort_ms2 = sum(v["ms"] for k, v in p2.items() if not k.startswith("feat")) / args.table_steps
             feat_ms2 = sum(v["ms"] for k, v in p2.items() if k.startswith("feat")) / args.table_steps
-            sb2 = sort_bytes(r2["s"], r2["executed"], n2, kv2)
+            sb2 = sort_bytes(r2["s"], r2["executed"], n2, kv2, r2["f"].shift)
             rows.append({
                 "workload": cfg, "n": n2, "kv": kv2, "strategy": ahs.STRATEGY_NAMES[r2["s"]],
                 "rule": ahs.RULE_NAMES[r2["r"]], "passes": r2["passes"], "passes_executed": r2["executed"],
