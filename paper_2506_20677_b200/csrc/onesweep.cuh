@@ -49,6 +49,24 @@ constexpr int kBins = 256;     // 8-bit digits
 #define AHS_LOOKBACK 8
 #endif
 constexpr int kLookback = AHS_LOOKBACK;  // predecessor statuses loaded per look-back round (B200: 8 beats 16, 32)
+#ifdef AHS_PHASE_STATS
+// development instrumentation (tools/passbench.cu -DAHS_PHASE_STATS): cycles
+// per tile phase and look-back rounds, seen by thread 0 of each CTA
+__device__ unsigned long long g_phase_cycles[8];
+__device__ unsigned long long g_lb_probe[4];  // look-backs, rounds, cycles in rounds, empty rounds
+#define PHASE_MARK(k)                                                       \
+    do {                                                                    \
+        if (threadIdx.x == 0) {                                             \
+            const long long t_ = clock64();                                 \
+            atomicAdd(&g_phase_cycles[k], (unsigned long long)(t_ - t_ph)); \
+            t_ph = t_;                                                      \
+        }                                                                   \
+    } while (0)
+#else
+#define PHASE_MARK(k) \
+    do {              \
+    } while (0)
+#endif
 #ifdef AHS_LB_STATS
 __device__ unsigned long long g_lb_stats[4];  // tiles, rounds, empty rounds, statuses consumed
 #endif
@@ -194,6 +212,9 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(const PassArgs a)
 
     const bool skew = s_skew != 0u;
     uint32_t phase = 0;  // bit b: parity of buffer b's next completion
+#ifdef AHS_PHASE_STATS
+    long long t_ph = clock64();
+#endif
     for (uint32_t iter = 0;; iter++) {
         const uint32_t b = iter & 1u;
         const uint32_t tile = s_ticket[b];
@@ -205,6 +226,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(const PassArgs a)
         uint32_t *sv = s_vb + b * TILE;
         if (tma_ok && full) {
             mbar_wait(&s_bar[b], (phase >> b) & 1u);
+            PHASE_MARK(0);
             phase ^= 1u << b;
         } else {
             for (uint32_t i = tid; i < tile_n; i += BLOCK) {
@@ -247,6 +269,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(const PassArgs a)
                 if (valid) atomicAdd(&cw[d], 1u);
             }
             __syncthreads();
+            PHASE_MARK(1);
 
             // ------------------ per-digit totals, publish aggregate, tile scan
             const uint32_t d = tid & (kBins - 1), part = tid / kBins;
@@ -277,6 +300,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(const PassArgs a)
                 s_start[d] = before + incl - total;
             }
             __syncthreads();
+            PHASE_MARK(2);
             // sub-warp digit offsets in the tile (digit start + earlier sub-warps)
             {
                 uint32_t run = s_start[d] + (part ? s_part[d] : 0u);
@@ -289,6 +313,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(const PassArgs a)
                 }
             }
             __syncthreads();
+            PHASE_MARK(3);
 
             // ------------------------------------- rank + scatter in digit order
             // word = {bit 16+j: lane j has this digit in this item | low 16: next slot}
@@ -338,6 +363,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(const PassArgs a)
                 for (int q = 0; q < TPW * kBins / 4 / 32; q++) t4[q * 32 + lane] = make_uint4(0u, 0u, 0u, 0u);
             }
 
+            PHASE_MARK(4);
             // ------------------------------------------- decoupled look-back
             // kLookback predecessor statuses per round, consumed newest-first: AGG
             // counts accumulate, the first INCL ends the walk, an unpublished one is
@@ -347,7 +373,14 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(const PassArgs a)
                 if (tile > 0) {
                     int jt = (int)tile - 1;
                     uint32_t spins = 0;
+#ifdef AHS_PHASE_STATS
+                    const long long t_lb0 = clock64();
+                    uint32_t n_rounds = 0, n_empty = 0;
+#endif
                     while (true) {
+#ifdef AHS_PHASE_STATS
+                        n_rounds++;
+#endif
                         uint32_t st[kLookback];
     #pragma unroll
                         for (int q = 0; q < kLookback; q++)
@@ -374,6 +407,9 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(const PassArgs a)
 #endif
                         if (fin) break;
                         jt -= used;
+#ifdef AHS_PHASE_STATS
+                        n_empty += used == 0;
+#endif
                         if (used == 0) {
                             // predecessors hold earlier tickets and publish before they wait
                             if (++spins > (1u << 24)) __trap();
@@ -381,6 +417,14 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(const PassArgs a)
                         }
                     }
                     st_relaxed(&status[(size_t)tile * kBins + d], kFlagIncl | (excl + total));
+#ifdef AHS_PHASE_STATS
+                    if (tid == 0) {
+                        atomicAdd(&g_lb_probe[0], 1ull);
+                        atomicAdd(&g_lb_probe[1], (unsigned long long)n_rounds);
+                        atomicAdd(&g_lb_probe[2], (unsigned long long)(clock64() - t_lb0));
+                        atomicAdd(&g_lb_probe[3], (unsigned long long)n_empty);
+                    }
+#endif
 #ifdef AHS_LB_STATS
                     atomicAdd(&g_lb_stats[0], 1ull);
 #endif
@@ -388,6 +432,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(const PassArgs a)
                 s_gofs[d] = __ldg(&bucket_base[d]) + excl - s_start[d];
             }
             __syncthreads();
+            PHASE_MARK(5);
             // Next tile: its ticket is taken only now, after this tile's inclusive
             // prefix is published, so a tile whose ticket is held but not yet
             // started never waits on anything but this CTA's write-out (taking it
@@ -424,6 +469,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(const PassArgs a)
         if (full) tile_work(std::true_type{});
         else tile_work(std::false_type{});
         __syncthreads();
+        PHASE_MARK(6);
     }
 }
 

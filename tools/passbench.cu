@@ -124,6 +124,28 @@ float run_cfg(const Bufs &B, uint32_t n, uint32_t shift, int sms, int reps, bool
     }
     std::sort(ts.begin(), ts.end());
     const float med = ts[ts.size() / 2];
+#ifdef AHS_PHASE_STATS
+    {
+        unsigned long long ph[8];
+        CK(cudaMemcpyFromSymbol(ph, g_phase_cycles, sizeof(ph)));
+        const double per = (double)tiles * (reps + 2);
+        const char *nm[7] = {"tma wait", "early counts", "totals+scan", "offsets", "rank+scatter",
+                             "look-back+sync", "write-out+sync"};
+        double tot = 0;
+        for (int k = 0; k < 7; k++) tot += ph[k] / per;
+        printf("  phases (cycles per tile, thread 0):");
+        for (int k = 0; k < 7; k++) printf(" %s %.0f (%.0f%%)", nm[k], ph[k] / per, 100.0 * ph[k] / per / tot);
+        printf("  total %.0f\n", tot);
+        memset(ph, 0, sizeof(ph));
+        CK(cudaMemcpyToSymbol(g_phase_cycles, ph, sizeof(ph)));
+        unsigned long long lp[4];
+        CK(cudaMemcpyFromSymbol(lp, g_lb_probe, sizeof(lp)));
+        printf("  look-back (thread 0): %.2f rounds, %.0f cycles, %.0f cycles/round, %.2f empty rounds per tile\n",
+               (double)lp[1] / lp[0], (double)lp[2] / lp[0], (double)lp[2] / lp[1], (double)lp[3] / lp[0]);
+        memset(lp, 0, sizeof(lp));
+        CK(cudaMemcpyToSymbol(g_lb_probe, lp, sizeof(lp)));
+    }
+#endif
 #ifdef AHS_LB_STATS
     {
         unsigned long long st[4];
@@ -228,10 +250,14 @@ int main(int argc, char **argv)
         CK(cudaMemcpy(B.bb, base.data(), 1024, cudaMemcpyHostToDevice));
         printf("digit shift %u (max digit share %.3f)\n", shift, (double)mx / n);
         g_idx = 0;
-        run_cfg<false, 512, 15, 2>(B, n, shift, sms, reps, true, hk, base);
         run_cfg<false, 512, 16, 2, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
-        run_cfg<true, 512, 9, 2>(B, n, shift, sms, reps, true, hk, base);
+        run_cfg<false, 256, 24, 3, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
+        run_cfg<false, 256, 20, 3, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
+        run_cfg<false, 256, 32, 2, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
+        run_cfg<false, 512, 32, 1, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
         run_cfg<true, 512, 15, 1, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
+        run_cfg<true, 256, 15, 2, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
+        run_cfg<true, 256, 12, 3, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
     }
     if (cub) {
         run_cub<false>(B, n, 0, 32, sms, reps);
