@@ -87,8 +87,6 @@ int device_info(int *sms, int *hist_clusters = nullptr, DevInfo **info = nullptr
                                          kHistSmemBytes) == cudaSuccess;
             good &= cudaFuncSetAttribute(k_feat_reduce<kReduceBlock>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          kReduceSmem) == cudaSuccess;
-            good &= cudaFuncSetAttribute(k_radix_hist<kRHBlock>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         kRHSmem) == cudaSuccess;
             if (good) {
                 cudaLaunchConfig_t cfg = {};
                 cfg.gridDim = dim3(kHistCluster * 128);
@@ -210,7 +208,7 @@ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 constexpr int kMaxReduceBlocks = 2048;
 constexpr int kMaxHistRows = 80;  // K2 clusters (rows of partial histograms)
 struct WsLayout {
-    size_t feat, partials, fctrl, ovf, hist, scan, parts, total;
+    size_t feat, partials, fctrl, ovf, hist, scan, parts, byte0, digit1, total;
 };
 WsLayout ws_layout()
 {
@@ -230,6 +228,10 @@ WsLayout ws_layout()
     o += align_up((size_t)(kMaxBins + 1) * 4, 256);
     L.parts = o;
     o += (size_t)kMaxHistRows * kMaxBins * 4;
+    L.byte0 = o;  // K1: per-CTA histograms of the raw low byte (radix digit 0)
+    o += (size_t)kMaxReduceBlocks * 256 * 4;
+    L.digit1 = o;  // K2: per-CTA histograms of digit 1 of key - min (when shift > 8)
+    o += (size_t)kMaxHistRows * kHistCluster * 256 * 4;
     L.total = o;
     return L;
 }
@@ -456,8 +458,8 @@ int ahs_features(const void *d_keys, uint64_t n, int32_t dtype, void *d_ws, size
     const uint64_t g1 = std::max<uint64_t>(1, std::min<uint64_t>(nch1, (uint64_t)sms * 2));
 
     cudaError_t e = launch(KID_FEAT_REDUCE, s, [&] {
-        k_feat_reduce<kReduceBlock><<<(unsigned)g1, kReduceBlock, kReduceSmem, s>>>(keys, n, flip, partials, ovf,
-                                                                                     kMaxBins, fctrl);
+        k_feat_reduce<kReduceBlock><<<(unsigned)g1, kReduceBlock, kReduceSmem, s>>>(
+            keys, n, flip, partials, ovf, kMaxBins, fctrl, (uint32_t *)(ws + L.byte0));
     });
     if (e != cudaSuccess) return AHS_ECUDA;
     // K2: clusters of kHistCluster CTAs, one partial-histogram row per cluster
@@ -465,8 +467,8 @@ int ahs_features(const void *d_keys, uint64_t n, int32_t dtype, void *d_ws, size
     uint64_t rows = (nch2 + kHistCluster - 1) / kHistCluster;
     rows = std::max<uint64_t>(1, std::min<uint64_t>(rows, (uint64_t)std::min(hclusters, kMaxHistRows)));
     e = launch(KID_FEAT_HIST, s, [&] {
-        K2_KERNEL<<<(unsigned)(rows * kHistCluster), kHistBlock, kHistSmemBytes, s>>>(keys, n, flip, partials,
-                                                                                       (int)g1, ovf, parts);
+        K2_KERNEL<<<(unsigned)(rows * kHistCluster), kHistBlock, kHistSmemBytes, s>>>(
+            keys, n, flip, partials, (int)g1, ovf, parts, (uint32_t *)(ws + L.digit1));
     });
     if (e != cudaSuccess) return AHS_ECUDA;
     e = launch(KID_FEAT_FINALIZE, s, [&] {
@@ -650,18 +652,14 @@ int ahs_sort(const void *d_keys_in, const uint32_t *d_vals_in, void *d_keys_out,
     if (count_kv) {
         bases = (const uint32_t *)((const char *)d_ws + WL.scan);
     } else {
-        const uint32_t *fhist = (const uint32_t *)((const char *)d_ws + WL.hist);
-        uint64_t g5;
-        if (feat->shift > 0) {
-            const uint64_t nch = (n / 4 + kRHChunk / 16 - 1) / (kRHChunk / 16);
-            g5 = std::max<uint64_t>(1, std::min<uint64_t>(nch, (uint64_t)sms));
-        } else {
-            g5 = std::max<uint64_t>(1, ((uint64_t)feat->nbins + kRHBlock - 1) / kRHBlock);
-        }
+        const char *wsc = (const char *)d_ws;
+        const uint32_t *fhist = (const uint32_t *)(wsc + WL.hist);
+        const uint64_t g5 = std::max<uint64_t>(2 * kRowCtas, ((uint64_t)feat->nbins + kRHBlock - 1) / kRHBlock);
         cudaError_t e = launch(KID_RADIX_HIST, s, [&] {
-            k_radix_hist<kRHBlock><<<(unsigned)g5, kRHBlock, kRHSmem, s>>>(
-                src_k, n, flip, sub, passes, fhist, feat->nbins, feat->shift, dhist, bucket, tickets + 7, plan,
-                skip ? 1 : 0);
+            k_radix_hist<kRHBlock><<<(unsigned)g5, kRHBlock, 0, s>>>(
+                n, sub, passes, fhist, feat->nbins, feat->shift, (const DevFeatures *)(wsc + WL.feat),
+                (const uint32_t *)(wsc + WL.byte0), (const uint32_t *)(wsc + WL.digit1), dhist, bucket, tickets + 7,
+                plan, skip ? 1 : 0);
         });
         if (e != cudaSuccess) return AHS_ECUDA;
         bases = bucket;

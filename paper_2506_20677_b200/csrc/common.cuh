@@ -23,9 +23,9 @@ struct DevFeatures {
     uint32_t umin, umax;
     uint64_t descents;
     uint64_t k;
-    uint32_t bits, shift, nb, pad0;
+    uint32_t bits, shift, nb, pad0;  // pad0: K1 CTA count (rows of the low-byte histograms)
     double entropy;
-    uint64_t pad1[2];
+    uint64_t pad1[2];                // pad1[0]: K2 CTA count (rows of the digit-1 histograms)
 };
 static_assert(sizeof(DevFeatures) == 64, "DevFeatures is 64 bytes");
 

@@ -59,10 +59,16 @@ template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK)
     k_feat_reduce(const uint32_t *__restrict__ keys, uint64_t n, uint32_t flip,
                   Partial *__restrict__ partials, uint32_t *__restrict__ zero_words, uint32_t nzero,
-                  FinalCtrl *__restrict__ fctrl)
+                  FinalCtrl *__restrict__ fctrl, uint32_t *__restrict__ byte0_rows)
 {
     extern __shared__ __align__(128) uint8_t smem_raw[];
     __shared__ __align__(8) uint64_t bars[kReduceStages];
+    // histogram of the raw low byte of every key (for the radix sort: digit 0 of
+    // key - min is this byte minus min's low byte, mod 256 -- no borrow -- so it
+    // is known before min is); one row per CTA, no atomics across CTAs
+    __shared__ uint32_t s_b0[256];
+    for (int i = threadIdx.x; i < 256; i += BLOCK) s_b0[i] = 0u;
+    __syncthreads();
     for (uint32_t i = blockIdx.x * BLOCK + threadIdx.x; i < nzero; i += gridDim.x * BLOCK)
         zero_words[i] = 0u;
     if (blockIdx.x == 0 && threadIdx.x == 0) fctrl->barrier = 0u;
@@ -86,6 +92,10 @@ __global__ void __launch_bounds__(BLOCK)
                 }
                 mn = min(mn, min(min(a0, a1), min(a2, a3)));
                 mx = max(mx, max(max(a0, a1), max(a2, a3)));
+                atomicAdd(&s_b0[a0 & 255u], 1u);
+                atomicAdd(&s_b0[a1 & 255u], 1u);
+                atomicAdd(&s_b0[a2 & 255u], 1u);
+                atomicAdd(&s_b0[a3 & 255u], 1u);
                 desc += (uint32_t)(a0 > a1) + (uint32_t)(a1 > a2) + (uint32_t)(a2 > a3) +
                         (uint32_t)(has_next && a3 > nxt);
             }
@@ -98,10 +108,13 @@ __global__ void __launch_bounds__(BLOCK)
             const uint32_t a = keys[i] ^ flip;
             mn = min(mn, a);
             mx = max(mx, a);
+            atomicAdd(&s_b0[a & 255u], 1u);
             if (i + 1 < n) desc += (uint32_t)(a > (keys[i + 1] ^ flip));
         }
     }
 
+    __syncthreads();
+    for (int i = threadIdx.x; i < 256; i += BLOCK) byte0_rows[(size_t)blockIdx.x * 256 + i] = s_b0[i];
     __shared__ uint32_t s_mn[BLOCK / 32], s_mx[BLOCK / 32], s_d[BLOCK / 32];
     mn = __reduce_min_sync(kFull, mn);
     mx = __reduce_max_sync(kFull, mx);
@@ -275,7 +288,7 @@ template <int BLOCK, int CL>
 __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(BLOCK, 1)
     k_feat_hist(const uint32_t *__restrict__ keys, uint64_t n, uint32_t flip,
                 const Partial *__restrict__ partials, int nparts, uint32_t *__restrict__ ovf,
-                uint32_t *__restrict__ parts)
+                uint32_t *__restrict__ parts, uint32_t *__restrict__ digit1_rows)
 {
     extern __shared__ __align__(128) uint32_t sh[];
     __shared__ __align__(8) uint64_t bars[kHistStages];
@@ -293,6 +306,12 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(BLOCK, 1)
     }
     const uint32_t words = packed ? (rg.nb + 1u) >> 1 : (cols ? rg.nb * BLOCK : R * rg.nb);
     for (uint32_t i = threadIdx.x; i < words; i += BLOCK) sh[i] = 0u;
+    // Digit 1 of v = key - min for the radix sort, counted here when the feature
+    // buckets are coarser than 2^8 (shift > 8, always the packed mode) and the
+    // histogram can therefore not supply it; one row per CTA.
+    __shared__ uint32_t s_d1[256];
+    const bool cnt1 = rg.shift > 8u;
+    for (int i = threadIdx.x; i < 256; i += BLOCK) s_d1[i] = 0u;
     __syncthreads();
 
     const uint32_t umin = p.mn, shift = rg.shift;
@@ -307,12 +326,22 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(BLOCK, 1)
                 const uint32_t j = j0 + threadIdx.x;
                 const bool act = j < nv;
                 const uint4 x = act ? c[j] : make_uint4(c0, c0, c0, c0);
-                hist_vec(add, make_uint4(x.x - c0, x.y - c0, x.z - c0, x.w - c0), act, shift);
+                const uint4 v = make_uint4(x.x - c0, x.y - c0, x.z - c0, x.w - c0);
+                if (cnt1 && act) {
+                    atomicAdd(&s_d1[(v.x >> 8) & 255u], 1u);
+                    atomicAdd(&s_d1[(v.y >> 8) & 255u], 1u);
+                    atomicAdd(&s_d1[(v.z >> 8) & 255u], 1u);
+                    atomicAdd(&s_d1[(v.w >> 8) & 255u], 1u);
+                }
+                hist_vec(add, v, act, shift);
             }
         });
         if (blockIdx.x == 0 && warp == 0) {  // head / tail keys, one per lane
             const uint64_t i = lane < 3 ? lane : sp.tail0 + (lane - 3);
-            if (lane < 3 ? i < sp.head : (lane < 6 && i < n)) add((keys[i] - c0) >> shift, 1u);
+            if (lane < 3 ? i < sp.head : (lane < 6 && i < n)) {
+                add((keys[i] - c0) >> shift, 1u);
+                if (cnt1) atomicAdd(&s_d1[((keys[i] - c0) >> 8) & 255u], 1u);
+            }
         }
     };
     if (cols) {
@@ -338,6 +367,8 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(BLOCK, 1)
             sh[b] = s;
         }
     }
+    if (cnt1)
+        for (int i = threadIdx.x; i < 256; i += BLOCK) digit1_rows[(size_t)blockIdx.x * 256 + i] = s_d1[i];
     // merge the cluster's histograms over DSMEM: CTA rank r owns a slice
     cluster.sync();
     const uint32_t rank = cluster.block_rank();
@@ -490,6 +521,8 @@ __global__ void __launch_bounds__(BLOCK)
             f.shift = rg.shift;
             f.nb = rg.nb;
             f.entropy = H;
+            f.pad0 = (uint32_t)nparts;            // K1 CTAs = rows of byte0_rows
+            f.pad1[0] = (uint64_t)nrows * kHistCluster;  // K2 CTAs = rows of digit1_rows
             *out = f;
         }
     }

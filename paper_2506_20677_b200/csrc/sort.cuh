@@ -43,112 +43,49 @@ static_assert(kMinTile <= OsKeysM::kTile && kMinTile <= OsPairsM::kTile && kMinT
               "kMinTile");
 
 // ------------------------------------------------------------------ K5 ----
-// Digit histograms of v = (key ^ flip) - min for the `passes` 8-bit digits.
-// Digits whose bits lie inside [fshift, 32) are read off the feature
-// histogram (ws, exact counts of v >> fshift): a bucket's keys share those
-// bits.  Only when fshift > 0 (k > 2^16) are the keys read again, for the
-// joint histogram of their low 16 bits (digits 0 and 1) in 2^16 packed
-// guard-bit counters: ONE shared atomic per key instead of one per digit
-// (the kernel is shared-atomic bound otherwise), with the same run merging
-// as feat_hist.  Marginals are flushed with global atomics into dhist (zeroed
-// by the host's memset); the last CTA turns them into exclusive bucket bases.
+// Digit histograms of v = (key ^ flip) - min for the `passes` 8-bit digits,
+// without reading the keys:
+//   digits whose bits lie inside [fshift, 32) are read off the feature
+//     histogram (exact counts of v >> fshift: a bucket's keys share those bits);
+//   digit 0 when fshift > 0: K1's per-CTA histograms of the raw low byte,
+//     rotated by min's low byte (v's low byte = raw low byte - min's, mod 256);
+//   digit 1 when fshift > 8: K2's per-CTA histograms of digit 1 of v.
+// (fshift <= 16, so no other digit needs the keys.)  Marginals are flushed with
+// global atomics into dhist (zeroed by the host's memset); the last CTA turns
+// them into exclusive bucket bases and writes the pass plan (NEXT-1).
 constexpr uint32_t kPlanMagic = 0xa45c0de1u;  // plan[5] once K5 has written a plan
 constexpr int kRHBlock = 1024;
-constexpr int kRHChunk = 46 * 1024;  // < 3 vectors per thread (fits 227 KB with the 4 KB static digit tables)
-constexpr int kRHStages = 2;
-constexpr int kRHSmem = kHistBins + kRHStages * (kRHChunk + 16);
-
-struct JointAdd {  // packed joint counter; overflow goes straight to the marginals
-    uint32_t *sh, *dig0, *dig1;
-    __device__ __forceinline__ void operator()(uint32_t b, uint32_t c) const
-    {
-        fix(atomicAdd(&sh[b >> 1], c << ((b & 1u) << 4)), b, c);
-    }
-    __device__ __forceinline__ void fix(uint32_t old, uint32_t b, uint32_t c) const
-    {
-        const uint32_t sft = (b & 1u) << 4;
-        const uint32_t h = (old >> sft) & 0xffffu;
-        if (h < 0x8000u && h + c >= 0x8000u) {
-            atomicSub(&sh[b >> 1], 0x8000u << sft);
-            atomicAdd(&dig0[b & 255u], 0x8000u);
-            atomicAdd(&dig1[b >> 8], 0x8000u);
-        }
-    }
-    __device__ __forceinline__ void add4(uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3) const
-    {
-        const uint32_t o0 = atomicAdd(&sh[b0 >> 1], 1u << ((b0 & 1u) << 4));
-        const uint32_t o1 = atomicAdd(&sh[b1 >> 1], 1u << ((b1 & 1u) << 4));
-        const uint32_t o2 = atomicAdd(&sh[b2 >> 1], 1u << ((b2 & 1u) << 4));
-        const uint32_t o3 = atomicAdd(&sh[b3 >> 1], 1u << ((b3 & 1u) << 4));
-        fix(o0, b0, 1u);
-        fix(o1, b1, 1u);
-        fix(o2, b2, 1u);
-        fix(o3, b3, 1u);
-    }
-};
+constexpr int kRowCtas = 4;  // K5 CTAs per row set (K1 low bytes, K2 digit 1)
 
 template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK, 1)
-    k_radix_hist(const uint32_t *__restrict__ keys, uint64_t n, uint32_t flip, uint32_t sub, int passes,
-                 const uint32_t *__restrict__ fhist, uint32_t nb, uint32_t fshift,
-                 uint32_t *__restrict__ dhist, uint32_t *__restrict__ bucket_base,
-                 uint32_t *__restrict__ ticket, uint32_t *__restrict__ plan, int skip_trivial)
+    k_radix_hist(uint64_t n, uint32_t sub, int passes, const uint32_t *__restrict__ fhist, uint32_t nb,
+                 uint32_t fshift, const DevFeatures *__restrict__ dfeat, const uint32_t *__restrict__ byte0_rows,
+                 const uint32_t *__restrict__ digit1_rows, uint32_t *__restrict__ dhist,
+                 uint32_t *__restrict__ bucket_base, uint32_t *__restrict__ ticket, uint32_t *__restrict__ plan,
+                 int skip_trivial)
 {
-    extern __shared__ __align__(128) uint32_t sh[];
     __shared__ uint32_t s_dig[4][256];
-    __shared__ __align__(8) uint64_t bars[kRHStages];
     __shared__ bool s_last;
     __shared__ uint32_t s_triv[4];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
-    const bool from_keys = fshift > 0u;  // digits 0 and 1 need the keys
     for (int i = threadIdx.x; i < 4 * 256; i += BLOCK) (&s_dig[0][0])[i] = 0u;
-    if (from_keys)
-        for (int i = threadIdx.x; i < (int)kHistWords; i += BLOCK) sh[i] = 0u;
     __syncthreads();
-
-    if (from_keys) {
-        const JointAdd add{sh, s_dig[0], s_dig[1]};
-        const uint32_t c0 = sub - flip;
-        const VecSplit sp = vec_split(keys, n);
-        const uint4 *body = reinterpret_cast<const uint4 *>(keys + sp.head);
-        uint8_t *stage = reinterpret_cast<uint8_t *>(sh) + kHistBins;
-        stream_chunks<kRHStages, kRHChunk>(body, sp.nvec, stage, bars, [&](const uint4 *c, uint32_t nv, uint64_t) {
-            for (uint32_t j0 = 0; j0 < nv; j0 += BLOCK) {
-                const uint32_t j = j0 + threadIdx.x;
-                const bool act = j < nv;
-                const uint4 x = act ? c[j] : make_uint4(0u, 0u, 0u, 0u);
-                // bins = low 16 bits of v = key - (sub - flip)  (mod 2^32)
-                hist_vec(add,
-                         make_uint4((x.x - c0) & 0xffffu, (x.y - c0) & 0xffffu, (x.z - c0) & 0xffffu,
-                                    (x.w - c0) & 0xffffu),
-                         act, 0u);
-            }
-        });
-        if (blockIdx.x == 0 && warp == 0) {  // head / tail keys, one per lane
-            const uint64_t i = lane < 3 ? lane : sp.tail0 + (lane - 3);
-            const bool act = lane < 3 ? i < sp.head : (lane < 6 && i < n);
-            if (act) add((keys[i] - c0) & 0xffffu, 1u);
-        }
-        __syncthreads();
-        // marginals: threads 0..255 own digit-0 value t, 256..511 digit-1 value t - 256
-        if (threadIdx.x < 512) {
+    // rows of K1 (digit 0): CTAs 0 .. kRowCtas-1; rows of K2 (digit 1): the next
+    // kRowCtas (the grid has >= 2 kRowCtas); four threads per bin and CTA, each
+    // summing every (4 kRowCtas)-th row: few dependent L2 round trips
+    if (blockIdx.x < 2 * kRowCtas) {
+        const bool d1 = blockIdx.x >= kRowCtas;
+        if (d1 ? fshift > 8u : fshift > 0u) {
+            constexpr uint32_t PARTS = BLOCK / 256;
             const uint32_t t = threadIdx.x & 255u;
+            const uint32_t part = (blockIdx.x % kRowCtas) * PARTS + (threadIdx.x >> 8);
+            const int rows = d1 ? (int)__ldcg(&dfeat->pad1[0]) : (int)__ldcg(&dfeat->pad0);
+            const uint32_t *rp = d1 ? digit1_rows : byte0_rows;
             uint32_t sum = 0;
-            if (threadIdx.x < 256) {
-#pragma unroll 16
-                for (uint32_t d1 = 0; d1 < 256; d1++) {
-                    const uint32_t b = (d1 << 8) | t;
-                    sum += (sh[b >> 1] >> ((b & 1u) << 4)) & 0xffffu;
-                }
-                atomicAdd(&s_dig[0][t], sum);
-            } else {
-#pragma unroll 16
-                for (uint32_t w = t << 7; w < (t << 7) + 128u; w++) {
-                    const uint32_t x = sh[w];
-                    sum += (x & 0xffffu) + (x >> 16);
-                }
-                atomicAdd(&s_dig[1][t], sum);
-            }
+#pragma unroll 8
+            for (int r = (int)part; r < rows; r += PARTS * kRowCtas) sum += __ldcg(&rp[(size_t)r * 256 + t]);
+            if (sum) atomicAdd(&s_dig[d1 ? 1 : 0][d1 ? t : ((t - sub) & 255u)], sum);
         }
     }
     // digits inside the feature buckets: this CTA's slice of the bins
@@ -158,8 +95,7 @@ __global__ void __launch_bounds__(BLOCK, 1)
         const uint32_t base = b << fshift;
 #pragma unroll
         for (int p = 0; p < 4; p++)
-            if (p < passes && (uint32_t)(8 * p) >= fshift && !(from_keys && p < 2))
-                atomicAdd(&s_dig[p][(base >> (8 * p)) & 255u], c);
+            if (p < passes && (uint32_t)(8 * p) >= fshift) atomicAdd(&s_dig[p][(base >> (8 * p)) & 255u], c);
     }
     __syncthreads();
     for (int i = threadIdx.x; i < passes * 256; i += BLOCK) {
