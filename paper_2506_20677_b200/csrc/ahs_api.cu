@@ -480,12 +480,21 @@ int ahs_features(const void *d_keys, uint64_t n, int32_t dtype, void *d_ws, size
     });
     if (e != cudaSuccess) return AHS_ECUDA;
 
+    // the one host sync of the pipeline: 64 bytes into a pinned per-thread
+    // buffer (a pageable destination costs a staged, slower copy)
+    thread_local DevFeatures *pinned = nullptr;
+    if (!pinned && cudaHostAlloc((void **)&pinned, sizeof(DevFeatures), cudaHostAllocDefault) != cudaSuccess) {
+        cudaGetLastError();
+        pinned = nullptr;
+    }
     DevFeatures hf;
-    if (cudaMemcpyAsync(&hf, dfeat, sizeof(hf), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+    DevFeatures *dst = pinned ? pinned : &hf;
+    if (cudaMemcpyAsync(dst, dfeat, sizeof(hf), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
         cudaStreamSynchronize(s) != cudaSuccess) {
         cudaGetLastError();
         return AHS_ECUDA;
     }
+    hf = *dst;
     if (dtype == AHS_I32) {
         feat->min = (int64_t)(int32_t)(hf.umin ^ 0x80000000u);
         feat->max = (int64_t)(int32_t)(hf.umax ^ 0x80000000u);

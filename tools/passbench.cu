@@ -250,14 +250,10 @@ int main(int argc, char **argv)
         CK(cudaMemcpy(B.bb, base.data(), 1024, cudaMemcpyHostToDevice));
         printf("digit shift %u (max digit share %.3f)\n", shift, (double)mx / n);
         g_idx = 0;
+        run_cfg<false, 512, 15, 2>(B, n, shift, sms, reps, true, hk, base);
         run_cfg<false, 512, 16, 2, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
-        run_cfg<false, 256, 24, 3, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
-        run_cfg<false, 256, 20, 3, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
-        run_cfg<false, 256, 32, 2, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
-        run_cfg<false, 512, 32, 1, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
+        run_cfg<true, 512, 9, 2>(B, n, shift, sms, reps, true, hk, base);
         run_cfg<true, 512, 15, 1, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
-        run_cfg<true, 256, 15, 2, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
-        run_cfg<true, 256, 12, 3, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
     }
     if (cub) {
         run_cub<false>(B, n, 0, 32, sms, reps);
