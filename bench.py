@@ -225,6 +225,38 @@ def time_pipeline(torch, ahs, keys_np, vals_np, steps, warmup, device, flush, pr
                 executed=executed, clocks=clocks, step_ms=step_ms)
 
 
+def entropy_exact_report(torch, ahs, keys_np, vals_np, device, reps=5):
+    """NEXT-2: the paper-literal entropy (over distinct values) of the sorted output, the FSM
+    branch it would give under the paper's own normalisation (RANGE: 0.7 log2 k), and the
+    K8 kernel's time (it reads the 4n-byte output about twice)."""
+    n = keys_np.size
+    dk = upload(torch, keys_np, device)
+    ws = ahs.Workspace(n, False, device)
+    stream = torch.cuda.current_stream(device)
+    f = ahs.ahs_features(dk, ws, stream)
+    s, r = ahs.ahs_select(f)
+    ko = torch.empty_like(dk)
+    ahs.ahs_sort(dk, None, ko, None, s, f, ws, stream)
+    hx = ahs.ahs_entropy_sorted(ko, ws, stream)
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        ahs.ahs_entropy_sorted(ko, ws, stream)  # synchronizes
+        b.record(stream)
+        torch.cuda.synchronize(device)
+        ts.append(a.elapsed_time(b))
+    ms = statistics.median(ts)
+    fp = ahs.Features.from_buffer_copy(f)
+    fp.entropy = hx
+    sp, rp = ahs.ahs_select(fp, ahs.ahs_thresholds_default(entropy_norm=1))
+    return {"H_exact": hx, "H16": f.entropy, "branch": ahs.STRATEGY_NAMES[s],
+            "branch_paper_literal": ahs.STRATEGY_NAMES[sp], "agree": sp == s,
+            "ms": ms, "GBps_one_read": 4 * n / (ms * 1e-3) / 1e9,
+            "note": "K8 ahs_entropy_sorted on ahs_sort's output, incl. its 8-byte readback; "
+                    "paper-literal FSM = RANGE norm (0.7 log2 k) with H over distinct values"}
+
+
 def time_e2e(torch, ahs, keys_np, vals_np, steps, warmup, device):
     """Same metric through the C-ABI host entry point: pinned host buffers, H2D and D2H
     inside the timed region every step."""
@@ -338,6 +370,9 @@ def run_ours(args):
         "clocks": res["clocks"],
         "features": {"k": f.k, "nbins": f.nbins, "H": f.entropy, "descents": f.descents},
     }
+    # NEXT-2: paper-literal entropy of the output and the branch it implies
+    if rank == 0:
+        out["entropy_exact"] = entropy_exact_report(torch, ahs, keys, vals, device)
     # end to end through the C ABI with host buffers
     if not args.no_e2e:
         e_ms, bi, bo = time_e2e(torch, ahs, keys, vals, max(3, args.steps // 2), 2, device)
@@ -368,6 +403,9 @@ def run_ours(args):
                 "features_GBps": 8 * n2 / (feat_ms2 * 1e-3) / 1e9 if feat_ms2 > 0 else None,
                 "kernels_ms": {k: v["ms"] / v["launches"] for k, v in p2.items() if v["launches"]},
             })
+            ee = entropy_exact_report(torch, ahs, k2, v2, device, reps=2)
+            rows[-1].update({"H16": ee["H16"], "H_exact": ee["H_exact"],
+                             "branch_paper_literal": ee["branch_paper_literal"], "branch_agree": ee["agree"]})
             del k2, v2
         out["strategies"] = rows
     # CPU oracle baseline (rank 0, N = 1 only)

@@ -181,6 +181,19 @@ AHS_API int ahs_sort_host(const void *h_keys_in, const uint32_t *h_vals_in, void
                   void *d_scratch, size_t scratch_bytes, ahs_features_t *feat,
                   int32_t *strategy, int32_t *rule, void *stream);
 
+/* ------------------------------------------ paper-literal entropy (NEXT-2) */
+/* H over the DISTINCT key values (§III.A line 96, H = -sum_v p_v
+ * log2 p_v; reading "P" of SURVEY Appendix A, where ahs_features computes the
+ * bucketed H16 of reading "B"), from a device key array in which equal keys
+ * are contiguous, e.g. the keys_out of ahs_sort:
+ *   H = log2 n - (1/n) sum over runs of c log2 c,  clamped to >= 0.
+ * Key equality only (int32 and uint32 alike).  d_ws: an ahs_features workspace
+ * (this call uses its own scratch area in it).  Synchronizes `stream`; *H on
+ * return.  n = 0 gives H = 0.  Errors: EINVAL (NULL / misaligned pointer),
+ * ENOSPACE, ERANGE (n > AHS_MAX_N), ENODEV, ECUDA. */
+AHS_API int ahs_entropy_sorted(const void *d_keys, uint64_t n, void *d_ws, size_t ws_bytes, double *H,
+                               void *stream);
+
 /* ------------------------------------------------------- ranking mode (K6) */
 /* The onesweep pass ranks keys stably in one of two ways (onesweep.cuh):
  *   AHS_RANK_MASKED   {lane mask, slot} words: atomic add, read-back, clear;

@@ -70,6 +70,7 @@ def lib():
             "ahs_launch_count": ([], C.c_uint64),
             "ahs_rank_mode": ([C.c_int], C.c_int),
             "ahs_set_skip_trivial": ([C.c_int], C.c_int),
+            "ahs_entropy_sorted": ([vp, u64, vp, sz, C.POINTER(C.c_double), vp], C.c_int),
             "ahs_sort_executed_passes": ([vp, sz, u64, C.c_int, vp], C.c_int),
             "ahs_lane_order_ok": ([], C.c_int),
             "ahs_kernel_count": ([], C.c_int),
@@ -129,6 +130,15 @@ def ahs_rank_mode(mode: int = -1) -> int:
     if rc < 0:
         raise AhsError(rc, "ahs_rank_mode")
     return rc
+
+
+def ahs_entropy_sorted(keys, ws: "Workspace", stream=None) -> float:
+    """NEXT-2: per-distinct-value entropy of a CUDA key array whose equal keys are contiguous."""
+    h = C.c_double()
+    rc = lib().ahs_entropy_sorted(_dev_ptr(keys), keys.numel(), _dev_ptr(ws.ws), ws.ws_bytes, C.byref(h),
+                                  _stream(stream))
+    _check(rc, "ahs_entropy_sorted")
+    return h.value
 
 
 def ahs_set_skip_trivial(on: int = -1) -> int:

@@ -14,6 +14,7 @@
 #include "../../include/ahs.h"
 #include "features.cuh"
 #include "sort.cuh"
+#include "entropy.cuh"
 
 using namespace ahs;
 
@@ -32,6 +33,7 @@ struct DevInfo {
     int os_tile[2][2] = {{0, 0}, {0, 0}};
     int os_per_sm[2][2] = {{0, 0}, {0, 0}};  // co-resident CTAs per SM
     bool lane_order_ok = false;              // self-test of the ordered ranking passed
+    int ent_grid = 0;                        // K8 cooperative grid
     int rank_mode = kRankMasked;
 };
 std::mutex g_dev_mu;
@@ -138,6 +140,13 @@ int device_info(int *sms, int *hist_clusters = nullptr, DevInfo **info = nullptr
                 const bool force_masked = env && std::strcmp(env, "masked") == 0;
                 d.rank_mode = (d.lane_order_ok && !force_masked) ? kRankOrdered : kRankMasked;
             }
+            if (good) {  // K8: co-resident CTAs for its cooperative launch
+                int per = 0;
+                good &= cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_entropy_sorted<kEntBlock>,
+                                                                      kEntBlock, 0) == cudaSuccess;
+                d.ent_grid = std::min(kEntMaxGrid, per * d.sms);
+                good &= d.ent_grid > 0;
+            }
             if (!good) {
                 cudaGetLastError();
                 d.ok = false;
@@ -162,11 +171,12 @@ enum KernelId {
     KID_ONESWEEP_KV,
     KID_COUNT_FILL,
     KID_COUNT_SCATTER_KV,
+    KID_ENTROPY_SORTED,
     KID_COUNT
 };
 const char *kKernelNames[KID_COUNT] = {"feat_reduce", "feat_hist",   "feat_finalize",
                                        "radix_hist",  "onesweep",    "onesweep_kv",
-                                       "count_fill",  "count_scatter_kv"};
+                                       "count_fill",  "count_scatter_kv", "entropy_sorted"};
 
 std::atomic<uint64_t> g_launches{0};
 // NEXT-1 trivial-pass skipping (default on; AHS_SKIP_TRIVIAL=0 or ahs_set_skip_trivial(0) turn it off)
@@ -208,7 +218,7 @@ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 constexpr int kMaxReduceBlocks = 2048;
 constexpr int kMaxHistRows = 80;  // K2 clusters (rows of partial histograms)
 struct WsLayout {
-    size_t feat, partials, fctrl, ovf, hist, scan, parts, byte0, digit1, total;
+    size_t feat, partials, fctrl, ovf, hist, scan, parts, byte0, digit1, ent, total;
 };
 WsLayout ws_layout()
 {
@@ -232,6 +242,8 @@ WsLayout ws_layout()
     o += (size_t)kMaxReduceBlocks * 256 * 4;
     L.digit1 = o;  // K2: per-CTA histograms of digit 1 of key - min (when shift > 8)
     o += (size_t)kMaxHistRows * kHistCluster * 256 * 4;
+    L.ent = o;  // K8 (NEXT-2): per-chunk run pieces, per-chunk sums, result
+    o += align_up((size_t)kEntMaxGrid * (sizeof(RunPieces) + 8) + 256, 256);
     L.total = o;
     return L;
 }
@@ -697,6 +709,47 @@ int ahs_sort(const void *d_keys_in, const uint32_t *d_vals_in, void *d_keys_out,
             cudaLaunchKernel(k6, dim3(grid), dim3(kSortBlock), args, k6_smem, s);
         });
         if (e != cudaSuccess) return AHS_ECUDA;
+    }
+    return AHS_OK;
+}
+
+// ------------------------------------------------------------ NEXT-2
+int ahs_entropy_sorted(const void *d_keys, uint64_t n, void *d_ws, size_t ws_bytes, double *H, void *stream)
+{
+    if (!H) return AHS_EINVAL;
+    *H = 0.0;
+    if (n == 0) return AHS_OK;
+    if (n > AHS_MAX_N) return AHS_ERANGE;
+    if (!d_keys || !d_ws || ((uintptr_t)d_keys & 3u) || ((uintptr_t)d_ws & 15u)) return AHS_EINVAL;
+    const WsLayout L = ws_layout();
+    if (ws_bytes < L.total) return AHS_ENOSPACE;
+    int sms = 0;
+    DevInfo *di = nullptr;
+    int rc = device_info(&sms, nullptr, &di);
+    if (rc) return rc;
+    constexpr uint64_t kTileKeys = (uint64_t)kEntBlock * kEntItems;
+    uint64_t grid = std::min<uint64_t>((n + kTileKeys - 1) / kTileKeys, (uint64_t)di->ent_grid);
+    grid = std::max<uint64_t>(1, grid);
+    uint64_t chunk = (n + grid - 1) / grid;
+    chunk = (chunk + kEntItems - 1) / kEntItems * kEntItems;  // chunk starts stay 16-key aligned
+    grid = (n + chunk - 1) / chunk;
+    char *ws = (char *)d_ws;
+    RunPieces *pieces = (RunPieces *)(ws + L.ent);
+    double *csum = (double *)(ws + L.ent + kEntMaxGrid * sizeof(RunPieces));
+    double *dH = csum + kEntMaxGrid;
+    cudaStream_t s = (cudaStream_t)stream;
+    const uint32_t *keys = (const uint32_t *)d_keys;
+    uint64_t nn = n;
+    void *args[] = {&keys, &nn, &chunk, &pieces, &csum, &dH};
+    cudaError_t e = launch(KID_ENTROPY_SORTED, s, [&] {
+        cudaLaunchCooperativeKernel((void *)k_entropy_sorted<kEntBlock>, dim3((unsigned)grid), dim3(kEntBlock),
+                                    args, 0, s);
+    });
+    if (e != cudaSuccess) return AHS_ECUDA;
+    if (cudaMemcpyAsync(H, dH, sizeof(double), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess) {
+        cudaGetLastError();
+        return AHS_ECUDA;
     }
     return AHS_OK;
 }

@@ -1,0 +1,203 @@
+// entropy.cuh — K8, NEXT-2: the paper-literal entropy (§III.A line
+// 96, H = -sum_v p_v log2 p_v over the DISTINCT key values: reading "P" of
+// SURVEY Appendix A) from a key array in which equal keys are contiguous
+// (ahs_sort's output):  H = log2 n - (1/n) sum_runs c log2 c.
+//
+// One cooperative launch of G CTAs, CTA c owning the contiguous chunk
+// [c0, c1) = [c * chunk, (c + 1) * chunk), one read of the keys:
+//   per chunk   tiles of BLOCK x 16 keys (next tile prefetched); a run starts at
+//               i when i == 0 or key[i] != key[i-1] and ends at i when i == n-1
+//               or key[i] != key[i+1]; a block max-scan gives every thread the
+//               start of its first run.  Runs that start AND end inside the
+//               chunk add c log2 c (fp64, fixed order) -> S[c].  The chunk's
+//               first run, when it began in an earlier chunk, is only measured
+//               (its length inside the chunk, and whether it ends here); so is
+//               the last run when it continues into the next chunk.
+//   grid sync
+//   CTA 0       thread 0 stitches the runs that cross chunk boundaries in chunk
+//               order, then sums S[0..G) in a fixed tree: H = log2 n - S / n,
+//               clamped >= 0.
+// Deterministic for a given G.  Work is independent of the run lengths.
+#pragma once
+
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+
+namespace ahs {
+
+constexpr int kEntBlock = 256;
+constexpr int kEntItems = 16;
+constexpr int kEntMaxGrid = 1024;
+
+// per-chunk boundary record (global scratch)
+struct RunPieces {
+    uint64_t pre;       // length of the first run inside the chunk when it began earlier (0: a run starts at c0)
+    uint64_t suf;       // length of the last run inside the chunk when it continues past c1 (0 otherwise)
+    uint32_t pre_ends;  // that first run ends inside the chunk
+    uint32_t pad;
+};
+
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK)
+    k_entropy_sorted(const uint32_t *__restrict__ keys, uint64_t n, uint64_t chunk,
+                     RunPieces *__restrict__ pieces, double *__restrict__ chunk_S, double *__restrict__ out_H)
+{
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    __shared__ uint32_t s_w[BLOCK / 32];
+    __shared__ double s_d[BLOCK / 32];
+    __shared__ RunPieces s_rp;
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const uint64_t c0 = (uint64_t)blockIdx.x * chunk;
+    const uint64_t c1 = min(n, c0 + chunk);
+    if (threadIdx.x == 0) s_rp = RunPieces{0ull, 0ull, 0u, 0u};
+    __syncthreads();
+    // a run that began before the chunk enters it unless key[c0] starts a new run
+    const bool virt = c0 > 0 && c0 < c1 && keys[c0] == keys[c0 - 1];
+
+    // positions below are chunk-local (32-bit: chunk < 2^32)
+    const uint32_t len = (uint32_t)(c1 - c0);
+    uint32_t carry = 0;  // local start of the run in progress (0 also when it entered the chunk)
+    double S = 0.0;
+    const bool vec = ((uintptr_t)keys & 15u) == 0;  // chunk and tile starts are multiples of 16 keys
+    constexpr uint32_t TILE = (uint32_t)BLOCK * kEntItems;
+    const uint32_t *kc = keys + c0;
+    // keys of tile t0 for this thread (keys past the chunk, up to n, are read
+    // too: a run end looks one key ahead)
+    auto load = [&](uint32_t t0, uint32_t (&k)[kEntItems]) {
+        const uint32_t i0 = t0 + threadIdx.x * kEntItems;
+        if (vec && c0 + i0 + kEntItems <= n) {
+            const uint4 *p4 = reinterpret_cast<const uint4 *>(kc + i0);
+#pragma unroll
+            for (int q = 0; q < kEntItems / 4; q++) {
+                const uint4 x = ld_nc_v4(p4 + q);
+                k[4 * q] = x.x;
+                k[4 * q + 1] = x.y;
+                k[4 * q + 2] = x.z;
+                k[4 * q + 3] = x.w;
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < kEntItems; q++) k[q] = (c0 + i0 + q < n) ? kc[i0 + q] : 0u;
+        }
+    };
+    const bool last_chunk = c1 == n;
+    uint32_t k[kEntItems], kn[kEntItems];
+    if (len > 0) load(0, kn);
+    for (uint32_t t0 = 0; t0 < len; t0 += TILE) {
+        const uint32_t i0 = t0 + threadIdx.x * kEntItems;
+#pragma unroll
+        for (int q = 0; q < kEntItems; q++) k[q] = kn[q];
+        if (t0 + TILE < len) load(t0 + TILE, kn);  // next tile in flight while this one is scanned
+        // neighbours: the previous / next thread's keys; global loads only at warp edges
+        uint32_t prev = __shfl_up_sync(kFull, k[kEntItems - 1], 1);
+        uint32_t next = __shfl_down_sync(kFull, k[0], 1);
+        if (lane == 0) prev = (c0 + i0 > 0 && i0 < len) ? kc[(int64_t)i0 - 1] : 0u;
+        if (lane == 31) next = (c0 + i0 + kEntItems < n) ? kc[i0 + kEntItems] : 0u;
+        // a start at local 0 of chunk 0 is real; elsewhere starts compare with the previous key
+        uint32_t mine = 0;  // last local start among my keys (0: none; neutral, carry >= 0)
+#pragma unroll
+        for (int q = 0; q < kEntItems; q++) {
+            const uint32_t i = i0 + q;
+            const bool st = i < len && k[q] != (q ? k[q - 1] : prev);
+            if (st) mine = i;
+        }
+        // exclusive max-scan over the block (thread order = key order)
+        uint32_t incl = mine;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t x = __shfl_up_sync(kFull, incl, o);
+            if (lane >= (uint32_t)o) incl = max(incl, x);
+        }
+        if (lane == 31) s_w[warp] = incl;
+        __syncthreads();
+        uint32_t before = carry, tile_max = carry;
+        for (int w = 0; w < BLOCK / 32; w++) {
+            if (w < (int)warp) before = max(before, (uint32_t)s_w[w]);
+            tile_max = max(tile_max, (uint32_t)s_w[w]);
+        }
+        const uint32_t up = __shfl_up_sync(kFull, incl, 1);
+        uint32_t cur = lane ? max(before, up) : before;
+#pragma unroll
+        for (int q = 0; q < kEntItems; q++) {
+            const uint32_t i = i0 + q;
+            if (i < len) {
+                const bool st = k[q] != (q ? k[q - 1] : prev) || (c0 + i == 0);
+                if (st) cur = i;
+                const bool end = (last_chunk && i + 1 == len) ||
+                                 (q + 1 < kEntItems ? k[q + 1] != k[q] : next != k[q]);
+                const bool entered = virt && cur == 0 && !st;  // the run that entered the chunk
+                if (end) {
+                    if (entered) {
+                        s_rp.pre = i + 1;
+                        s_rp.pre_ends = 1u;
+                    } else if (i > cur) {  // runs of one key contribute 1 log2 1 = 0
+                        const double c = (double)(i - cur + 1);
+                        S += c * log2(c);
+                    }
+                } else if (i + 1 == len) {  // the last run continues into the next chunk
+                    if (entered) s_rp.pre = len;  // ... and entered it: it crosses the whole chunk
+                    else s_rp.suf = len - cur;
+                }
+            }
+        }
+        carry = tile_max;
+        __syncthreads();
+    }
+    // fixed-order block sum
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) S += __shfl_down_sync(kFull, S, o);
+    if (lane == 0) s_d[warp] = S;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < BLOCK / 32; w++) t += s_d[w];
+        chunk_S[blockIdx.x] = t;
+        pieces[blockIdx.x] = s_rp;
+    }
+    grid.sync();
+
+    // ---- CTA 0: stitch the runs crossing chunk boundaries (chunk order), then
+    // a fixed tree over the chunk sums
+    if (blockIdx.x == 0) {
+        __shared__ RunPieces s_pieces[kEntMaxGrid];
+        for (uint32_t c = threadIdx.x; c < gridDim.x; c += BLOCK) {
+            RunPieces rp;
+            rp.pre = __ldcg(&pieces[c].pre);
+            rp.suf = __ldcg(&pieces[c].suf);
+            rp.pre_ends = __ldcg(&pieces[c].pre_ends);
+            s_pieces[c] = rp;
+        }
+        __syncthreads();
+        double t = 0.0;
+        if (threadIdx.x == 0) {
+            uint64_t run = 0;  // length so far of the run crossing into the next chunk
+            for (uint32_t c = 0; c < gridDim.x; c++) {
+                const RunPieces rp = s_pieces[c];
+                if (rp.pre > 0) {  // the crossing run continues here
+                    run += rp.pre;
+                    if (!rp.pre_ends) continue;  // ... and crosses this chunk too
+                }
+                // the crossing run (if any) ended at the start of this chunk or inside it
+                if (run > 1) t += (double)run * log2((double)run);
+                run = rp.suf;
+            }
+            if (run > 1) t += (double)run * log2((double)run);
+        }
+        for (uint32_t c = threadIdx.x; c < gridDim.x; c += BLOCK) t += __ldcg(&chunk_S[c]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(kFull, t, o);
+        if (lane == 0) s_d[warp] = t;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double tot = 0.0;
+            for (int w = 0; w < BLOCK / 32; w++) tot += s_d[w];
+            const double dn = (double)n;
+            const double H = log2(dn) - tot / dn;
+            *out_H = H < 0.0 ? 0.0 : H;
+        }
+    }
+}
+
+}  // namespace ahs

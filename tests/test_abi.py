@@ -143,12 +143,24 @@ def test_bad_arguments_fail_loudly():
                       None, 0, None) == -1                                                  # bad strategy
 
 
+def test_entropy_sorted_arguments():
+    L = ahs.lib()
+    h = C.c_double(-1.0)
+    assert L.ahs_entropy_sorted(None, 0, None, 0, C.byref(h), None) == 0 and h.value == 0.0  # empty
+    assert L.ahs_entropy_sorted(None, 10, None, 0, C.byref(h), None) == -1                    # NULL keys
+    assert L.ahs_entropy_sorted(C.c_void_p(4098), 10, C.c_void_p(4096), 1 << 30, C.byref(h), None) == -1
+    assert L.ahs_entropy_sorted(C.c_void_p(4096), 10, C.c_void_p(4096), 16, C.byref(h), None) == -2
+    assert L.ahs_entropy_sorted(C.c_void_p(4096), 10, C.c_void_p(4096), 1 << 30, None, None) == -1
+
+
 @pytest.mark.skipif(os.path.exists("/dev/nvidia0"), reason="checks the no-GPU path")
 def test_no_device_is_an_error_not_a_fallback():
     L = ahs.lib()
     f = ahs.Features()
     rc = L.ahs_features(C.c_void_p(4096), 10, 0, C.c_void_p(4096), 1 << 30, C.byref(f), None)
     assert rc == -6   # AHS_ENODEV
+    h = C.c_double()
+    assert L.ahs_entropy_sorted(C.c_void_p(4096), 10, C.c_void_p(4096), 1 << 30, C.byref(h), None) == -6
 
 
 def test_product_does_not_import_oracle():

@@ -370,3 +370,57 @@ def test_cfg5_full_size(r):
         idx = synth.uniform_below(synth.stream(99, 4096), n).astype(np.int64)
         b = np.searchsorted(cum, idx, side="right")
         assert np.array_equal(ko[idx].astype(np.int64), b + of.min)
+
+
+# ------------------------------------------------------ NEXT-2: H over distinct values
+
+ENT_CASES = {
+    "u1000": lambda n: synth.uniform_range(31, n, 0, 999),
+    "full32": lambda n: synth.uniform_range(32, n, -(2 ** 31), 2 ** 31 - 1),
+    "zipf_wide": lambda n: synth.cfg3(n, seed=33),
+    "two_values": lambda n: synth.uniform_range(34, n, 5, 6),
+    "const": lambda n: synth.cfg4c(n),
+    # one long run in the middle: spans many chunks of the cooperative grid
+    "long_run": lambda n: np.concatenate([np.arange(n // 4, dtype=np.int32),
+                                          np.full(n - n // 2, 7 * n, np.int32),
+                                          np.arange(n // 2 - n // 4, dtype=np.int32) + 8 * n]),
+}
+
+
+@pytest.mark.parametrize("case", list(ENT_CASES))
+def test_entropy_sorted_matches_oracle(case):
+    """ahs_entropy_sorted vs the oracle's H_exact (run lengths of the sorted keys, Kahan), 1e-9."""
+    for n in (1, 2, 17, 4095, 4097, 65537, 1_000_003, 5_000_011):
+        keys = ENT_CASES[case](n)
+        ok = np.sort(keys, kind="stable")  # any order with equal keys contiguous
+        want = oracle.h_exact_sorted(ok)
+        ws = ahs.Workspace(n, False)
+        got = ahs.ahs_entropy_sorted(to_dev(ok), ws)
+        assert abs(got - want) <= H_TOL, (case, n, got, want)
+        # misaligned start (scalar load path)
+        got2 = ahs.ahs_entropy_sorted(to_dev(ok, misalign=1), ws)
+        assert abs(got2 - want) <= H_TOL, (case, n, got2, want)
+
+
+def test_entropy_sorted_on_pipeline_output_and_paper_branch():
+    """NEXT-2 on ahs_sort's output: H_exact; the paper-literal FSM (RANGE norm with H_exact)
+    picks the same branch as reading B here."""
+    for cfg in ("cfg1", "cfg2"):
+        keys, vals, _ = synth.make(cfg)
+        dk = to_dev(keys)
+        ws = ahs.Workspace(keys.size, False)
+        f = ahs.ahs_features(dk, ws)
+        s, r = ahs.ahs_select(f)
+        ko = torch.empty_like(dk)
+        ahs.ahs_sort(dk, None, ko, None, s, f, ws)
+        hx = ahs.ahs_entropy_sorted(ko, ws)
+        assert abs(hx - oracle.h_exact_sorted(np.sort(keys))) <= H_TOL
+        fp = ahs.Features.from_buffer_copy(f)
+        fp.entropy = hx
+        sp, _ = ahs.ahs_select(fp, ahs.ahs_thresholds_default(entropy_norm=1))
+        assert sp == s, cfg
+
+
+def test_entropy_sorted_empty():
+    ws = ahs.Workspace(1, False)
+    assert ahs.ahs_entropy_sorted(torch.empty(0, dtype=torch.int32, device="cuda"), ws) == 0.0
