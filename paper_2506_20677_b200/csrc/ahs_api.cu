@@ -32,6 +32,7 @@ struct DevInfo {
     size_t os_smem[2][2] = {{0, 0}, {0, 0}};
     int os_tile[2][2] = {{0, 0}, {0, 0}};
     int os_per_sm[2][2] = {{0, 0}, {0, 0}};  // co-resident CTAs per SM
+    int os_block[2][2] = {{0, 0}, {0, 0}};
     bool lane_order_ok = false;              // self-test of the ordered ranking passed
     int ent_grid = 0;                        // K8 cooperative grid
     int rank_mode = kRankMasked;
@@ -120,15 +121,19 @@ int device_info(int *sms, int *hist_clusters = nullptr, DevInfo **info = nullptr
             d.os_tile[1][kRankMasked] = OsPairsM::kTile;
             d.os_tile[0][kRankOrdered] = OsKeysO::kTile;
             d.os_tile[1][kRankOrdered] = OsPairsO::kTile;
+            d.os_block[0][kRankMasked] = kSortBlock;
+            d.os_block[1][kRankMasked] = kSortBlock;
+            d.os_block[0][kRankOrdered] = kSortBlock;
+            d.os_block[1][kRankOrdered] = kSortBlockPairsO;
             for (int kv = 0; kv < 2; kv++)
                 for (int m = 0; m < 2; m++) {
                     // persistent K6 grids: co-resident CTAs per SM
                     good &= cudaFuncSetAttribute(d.os_fn[kv][m], cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)d.os_smem[kv][m]) == cudaSuccess;
                     if (good)
-                        good &= cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                                    &d.os_per_sm[kv][m], d.os_fn[kv][m], kSortBlock, d.os_smem[kv][m]) ==
-                                cudaSuccess;
+                        good &= cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.os_per_sm[kv][m], d.os_fn[kv][m],
+                                                                              d.os_block[kv][m],
+                                                                              d.os_smem[kv][m]) == cudaSuccess;
                     good &= d.os_per_sm[kv][m] > 0;
                 }
             // The ordered ranking is used only if the device serves the lanes of
@@ -706,7 +711,7 @@ int ahs_sort(const void *d_keys_in, const uint32_t *d_vals_in, void *d_keys_out,
         pa.plan = count_kv ? nullptr : plan;  // K5's plan (no skipping when not enabled)
         void *args[] = {&pa};
         const cudaError_t e = launch(kv ? (count_kv ? KID_COUNT_SCATTER_KV : KID_ONESWEEP_KV) : KID_ONESWEEP, s, [&] {
-            cudaLaunchKernel(k6, dim3(grid), dim3(kSortBlock), args, k6_smem, s);
+            cudaLaunchKernel(k6, dim3(grid), dim3(di->os_block[kv][mode]), args, k6_smem, s);
         });
         if (e != cudaSuccess) return AHS_ECUDA;
     }

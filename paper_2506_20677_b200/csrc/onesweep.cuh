@@ -106,7 +106,7 @@ struct Onesweep {
     static_assert(RANK == kRankOrdered || ITEMS % 2 == 1,
                   "odd ITEMS: the half-warps of a warp read disjoint bank halves");
     static_assert(BLOCK * ITEMS < 65536, "16-bit slot field");
-    static_assert(BLOCK == 256 || BLOCK == 512, "one or two threads per digit");
+    static_assert(BLOCK >= 256 && BLOCK <= 512 && BLOCK % 128 == 0, "256, 384 or 512 threads");
     static_assert((kTile * 4) % 16 == 0, "TMA tile size");
     static constexpr size_t kBuf = (size_t)kTile * 4;
     static constexpr size_t kOffK = 0;                                   // keys   [2][TILE]
@@ -275,8 +275,10 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(const PassArgs a)
             const uint32_t d = tid & (kBins - 1), part = tid / kBins;
             constexpr int SPP = C::kSub / C::kTPD;  // sub-warps per thread
             uint32_t psum = 0;
+            if (C::kTPD == 2 || tid < kBins) {
     #pragma unroll 8
-            for (int s = 0; s < SPP; s++) psum += s_cnt[(part * SPP + s) * kBins + d];
+                for (int s = 0; s < SPP; s++) psum += s_cnt[(part * SPP + s) * kBins + d];
+            }
             if constexpr (C::kTPD == 2) {
                 s_part[part * kBins + d] = psum;
                 __syncthreads();
@@ -302,7 +304,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(const PassArgs a)
             __syncthreads();
             PHASE_MARK(2);
             // sub-warp digit offsets in the tile (digit start + earlier sub-warps)
-            {
+            if (C::kTPD == 2 || tid < kBins) {
                 uint32_t run = s_start[d] + (part ? s_part[d] : 0u);
     #pragma unroll 8
                 for (int s = 0; s < SPP; s++) {

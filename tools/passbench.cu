@@ -250,10 +250,12 @@ int main(int argc, char **argv)
         CK(cudaMemcpy(B.bb, base.data(), 1024, cudaMemcpyHostToDevice));
         printf("digit shift %u (max digit share %.3f)\n", shift, (double)mx / n);
         g_idx = 0;
-        run_cfg<false, 512, 15, 2>(B, n, shift, sms, reps, true, hk, base);
         run_cfg<false, 512, 16, 2, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
-        run_cfg<true, 512, 9, 2>(B, n, shift, sms, reps, true, hk, base);
+        run_cfg<false, 384, 16, 3, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
+        run_cfg<false, 384, 14, 3, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
         run_cfg<true, 512, 15, 1, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
+        run_cfg<true, 384, 12, 2, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
+        run_cfg<true, 384, 9, 3, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
     }
     if (cub) {
         run_cub<false>(B, n, 0, 32, sms, reps);
