@@ -141,10 +141,14 @@ AHS_API int ahs_sort_passes(const ahs_features_t *feat, int32_t strategy, int ha
 /* ---------------------------------------------------------- the hot path */
 
 /* Feature extraction.  Reads d_keys[0..n) twice (min/max/descents, then the
- * histogram of (key - min) >> shift), computes H in fp64 on the device, then
- * copies the ~72-byte result to *feat and SYNCHRONIZES `stream` (the one host
- * sync of the pipeline: the FSM runs on the host).  d_ws (>= ahs_workspace_bytes)
- * keeps the histogram and its exclusive scan for a following ahs_sort(COUNTING).
+ * histogram of (key - min) >> shift), computes H in fp64 on the device, and
+ * WAITS for the result on the host (the one host sync of the pipeline: the FSM
+ * runs on the host): the last kernel writes the 64-byte record into a mapped
+ * pinned per-thread buffer that the call polls (falling back to a copy + stream
+ * sync when mapped memory is unavailable).  On return every read of d_keys is
+ * complete; later work on `stream` is ordered after the kernels as usual.
+ * d_ws (>= ahs_workspace_bytes) keeps the histogram and the digit rows for a
+ * following ahs_sort on the same keys.
  * n = 0 returns AHS_OK with feat->flags = EMPTY and launches nothing. */
 AHS_API int ahs_features(const void *d_keys, uint64_t n, int32_t dtype, void *d_ws, size_t ws_bytes,
                  ahs_features_t *feat, void *stream);
@@ -162,14 +166,16 @@ AHS_API int ahs_select(const ahs_features_t *feat, const ahs_thresholds_t *th, i
  *                             then cost one extra device copy)
  *   feat                      from ahs_features on the same keys (n, dtype, min,
  *                             bits, shift must match; AHS_EFEAT otherwise)
- *   d_ws                      the ahs_features workspace (read for COUNTING)
+ *   d_ws                      the ahs_features workspace (COUNTING reads its
+ *                             histogram and writes the exclusive scan of it
+ *                             there; RADIX / GENERAL read its digit rows)
  *   d_tmp                     >= ahs_sort_tmp_bytes(n, d_vals_in != NULL)
  * COUNTING with shift > 0 (only reachable with k_counting > 65536) runs as
  * radix passes on key - min; the output is identical.  Empty and constant
  * inputs are copies.  The keys must not change between the two calls. */
 AHS_API int ahs_sort(const void *d_keys_in, const uint32_t *d_vals_in, void *d_keys_out,
              uint32_t *d_vals_out, uint64_t n, int32_t strategy, const ahs_features_t *feat,
-             const void *d_ws, size_t ws_bytes, void *d_tmp, size_t tmp_bytes, void *stream);
+             void *d_ws, size_t ws_bytes, void *d_tmp, size_t tmp_bytes, void *stream);
 
 /* End to end from HOST buffers: H2D copy, ahs_features, ahs_select, ahs_sort,
  * D2H copy, stream sync.  h_* are host pointers (pinned for full speed);

@@ -177,16 +177,24 @@ enum KernelId {
     KID_COUNT_FILL,
     KID_COUNT_SCATTER_KV,
     KID_ENTROPY_SORTED,
+    KID_HIST_SCAN,
     KID_COUNT
 };
 const char *kKernelNames[KID_COUNT] = {"feat_reduce", "feat_hist",   "feat_finalize",
                                        "radix_hist",  "onesweep",    "onesweep_kv",
-                                       "count_fill",  "count_scatter_kv", "entropy_sorted"};
+                                       "count_fill",  "count_scatter_kv", "entropy_sorted",
+                                       "hist_scan"};
 
 std::atomic<uint64_t> g_launches{0};
 // NEXT-1 trivial-pass skipping (default on; AHS_SKIP_TRIVIAL=0 or ahs_set_skip_trivial(0) turn it off)
 std::atomic<bool> g_skip_trivial{[] {
     const char *e = std::getenv("AHS_SKIP_TRIVIAL");
+    return !(e && e[0] == '0');
+}()};
+// programmatic dependent launch between the kernels of a step (default on;
+// AHS_PDL=0 turns it off: plain stream serialization)
+std::atomic<bool> g_pdl{[] {
+    const char *e = std::getenv("AHS_PDL");
     return !(e && e[0] == '0');
 }()};
 std::atomic<bool> g_prof{false};
@@ -215,6 +223,32 @@ cudaError_t launch(int kid, cudaStream_t s, F &&f)
     std::lock_guard<std::mutex> lk(g_prof_mu);
     g_prof_recs.push_back(r);
     return e;
+}
+
+// Launch a libahs kernel (every one starts with pdl_begin()) on stream s,
+// with programmatic stream serialization unless AHS_PDL=0.
+void pdl_config(cudaLaunchConfig_t &cfg, cudaLaunchAttribute *attr, dim3 grid, dim3 block, size_t smem,
+                cudaStream_t s)
+{
+    cfg = cudaLaunchConfig_t{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = g_pdl.load(std::memory_order_relaxed) ? 1 : 0;
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                     Args &&...args)
+{
+    cudaLaunchConfig_t cfg;
+    cudaLaunchAttribute attr[1];
+    pdl_config(cfg, attr, grid, block, smem, s);
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -466,7 +500,6 @@ int ahs_features(const void *d_keys, uint64_t n, int32_t dtype, void *d_ws, size
     FinalCtrl *fctrl = (FinalCtrl *)(ws + L.fctrl);
     uint32_t *ovf = (uint32_t *)(ws + L.ovf);
     uint32_t *hist = (uint32_t *)(ws + L.hist);
-    uint32_t *scan = (uint32_t *)(ws + L.scan);
     uint32_t *parts = (uint32_t *)(ws + L.parts);
     DevFeatures *dfeat = (DevFeatures *)(ws + L.feat);
 
@@ -475,8 +508,8 @@ int ahs_features(const void *d_keys, uint64_t n, int32_t dtype, void *d_ws, size
     const uint64_t g1 = std::max<uint64_t>(1, std::min<uint64_t>(nch1, (uint64_t)sms * 2));
 
     cudaError_t e = launch(KID_FEAT_REDUCE, s, [&] {
-        k_feat_reduce<kReduceBlock><<<(unsigned)g1, kReduceBlock, kReduceSmem, s>>>(
-            keys, n, flip, partials, ovf, kMaxBins, fctrl, (uint32_t *)(ws + L.byte0));
+        launch_k(k_feat_reduce<kReduceBlock>, dim3((unsigned)g1), dim3(kReduceBlock), kReduceSmem, s, keys, n,
+                 flip, partials, ovf, kMaxBins, fctrl, (uint32_t *)(ws + L.byte0));
     });
     if (e != cudaSuccess) return AHS_ECUDA;
     // K2: clusters of kHistCluster CTAs, one partial-histogram row per cluster
@@ -484,34 +517,65 @@ int ahs_features(const void *d_keys, uint64_t n, int32_t dtype, void *d_ws, size
     uint64_t rows = (nch2 + kHistCluster - 1) / kHistCluster;
     rows = std::max<uint64_t>(1, std::min<uint64_t>(rows, (uint64_t)std::min(hclusters, kMaxHistRows)));
     e = launch(KID_FEAT_HIST, s, [&] {
-        K2_KERNEL<<<(unsigned)(rows * kHistCluster), kHistBlock, kHistSmemBytes, s>>>(
-            keys, n, flip, partials, (int)g1, ovf, parts, (uint32_t *)(ws + L.digit1));
+        launch_k(K2_KERNEL, dim3((unsigned)(rows * kHistCluster)), dim3(kHistBlock), kHistSmemBytes, s, keys, n,
+                 flip, (const Partial *)partials, (int)g1, ovf, parts, (uint32_t *)(ws + L.digit1));
     });
     if (e != cudaSuccess) return AHS_ECUDA;
+    // the one host sync of the pipeline: K3's last CTA writes the 64-byte
+    // feature record straight into a per-thread mapped pinned buffer and
+    // releases its sequence word; the host polls that word (no copy, no
+    // stream sync).  Without a mapped buffer: copy + stream sync.
+    struct HostFeat {
+        DevFeatures *h = nullptr, *d = nullptr;
+        uint64_t seq = 0;
+        bool tried = false;
+    };
+    thread_local HostFeat hfb;
+    if (!hfb.tried) {
+        hfb.tried = true;
+        if (cudaHostAlloc((void **)&hfb.h, sizeof(DevFeatures), cudaHostAllocMapped) != cudaSuccess ||
+            cudaHostGetDevicePointer((void **)&hfb.d, hfb.h, 0) != cudaSuccess) {
+            cudaGetLastError();
+            if (hfb.h) cudaFreeHost(hfb.h);
+            hfb.h = hfb.d = nullptr;
+        } else {
+            std::memset(hfb.h, 0, sizeof(DevFeatures));
+        }
+    }
+    const uint64_t seq = ++hfb.seq;
     e = launch(KID_FEAT_FINALIZE, s, [&] {
-        int np = (int)g1, nr = (int)rows;
-        uint64_t nn = n;
-        void *args[] = {&nn, &partials, &np, &parts, &nr, &ovf, &hist, &scan, &fctrl, &dfeat};
-        cudaLaunchCooperativeKernel((void *)k_feat_finalize<kFinalBlock>, dim3(kFinalGrid),
-                                    dim3(kFinalBlock), args, 0, s);
+        launch_k(k_feat_finalize<kFinalBlock, kFinalGroups>, dim3(kFinalGrid), dim3(kFinalBlock), 0, s, n,
+                 (const Partial *)partials, (int)g1, (const uint32_t *)parts, (int)rows, (const uint32_t *)ovf,
+                 hist, fctrl, dfeat, hfb.d, seq);
     });
     if (e != cudaSuccess) return AHS_ECUDA;
 
-    // the one host sync of the pipeline: 64 bytes into a pinned per-thread
-    // buffer (a pageable destination costs a staged, slower copy)
-    thread_local DevFeatures *pinned = nullptr;
-    if (!pinned && cudaHostAlloc((void **)&pinned, sizeof(DevFeatures), cudaHostAllocDefault) != cudaSuccess) {
-        cudaGetLastError();
-        pinned = nullptr;
-    }
     DevFeatures hf;
-    DevFeatures *dst = pinned ? pinned : &hf;
-    if (cudaMemcpyAsync(dst, dfeat, sizeof(hf), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-        cudaStreamSynchronize(s) != cudaSuccess) {
-        cudaGetLastError();
-        return AHS_ECUDA;
+    if (hfb.h) {
+        volatile uint64_t *flag = &hfb.h->pad1[1];
+        for (uint32_t spin = 0;; spin++) {
+            if (*flag == seq) break;
+            if ((spin & 255u) == 255u) {  // the kernel may have failed: stream state
+                const cudaError_t q = cudaStreamQuery(s);
+                if (q == cudaSuccess) {
+                    if (*flag == seq) break;
+                    return AHS_ECUDA;  // stream drained without the record
+                }
+                if (q != cudaErrorNotReady) {
+                    cudaGetLastError();
+                    return AHS_ECUDA;
+                }
+            }
+        }
+        std::atomic_thread_fence(std::memory_order_acquire);
+        std::memcpy(&hf, (const void *)hfb.h, sizeof(hf));
+    } else {
+        if (cudaMemcpyAsync(&hf, dfeat, sizeof(hf), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+            cudaStreamSynchronize(s) != cudaSuccess) {
+            cudaGetLastError();
+            return AHS_ECUDA;
+        }
     }
-    hf = *dst;
     if (dtype == AHS_I32) {
         feat->min = (int64_t)(int32_t)(hf.umin ^ 0x80000000u);
         feat->max = (int64_t)(int32_t)(hf.umax ^ 0x80000000u);
@@ -530,6 +594,21 @@ int ahs_features(const void *d_keys, uint64_t n, int32_t dtype, void *d_ws, size
     if (hf.descents == 0) feat->flags |= AHS_FLAG_SORTED;
     if (n >= 2 && hf.descents == n - 1) feat->flags |= AHS_FLAG_STRICT_DESC;
     return AHS_OK;
+}
+
+// K3s: the exclusive scan of the feature histogram (COUNTING only); returns
+// the device scan array in ws, or nullptr on a launch error.
+static const uint32_t *hist_scan(void *d_ws, const ahs_features_t *feat, cudaStream_t s)
+{
+    const WsLayout L = ws_layout();
+    char *ws = (char *)d_ws;
+    uint32_t *scan = (uint32_t *)(ws + L.scan);
+    const unsigned g = (unsigned)((feat->nbins + kScanBlock - 1) / kScanBlock);
+    const cudaError_t e = launch(KID_HIST_SCAN, s, [&] {
+        launch_k(k_hist_scan<kScanBlock>, dim3(g), dim3(kScanBlock), 0, s, (const uint32_t *)(ws + L.hist),
+                 (const FinalCtrl *)(ws + L.fctrl), feat->nbins, (uint32_t)feat->n, scan);
+    });
+    return e == cudaSuccess ? scan : nullptr;
 }
 
 // ----------------------------------------------------------------- select
@@ -571,7 +650,7 @@ int ahs_select(const ahs_features_t *f, const ahs_thresholds_t *th, int32_t *str
 
 // ------------------------------------------------------------------- sort
 int ahs_sort(const void *d_keys_in, const uint32_t *d_vals_in, void *d_keys_out, uint32_t *d_vals_out,
-             uint64_t n, int32_t strategy, const ahs_features_t *feat, const void *d_ws, size_t ws_bytes,
+             uint64_t n, int32_t strategy, const ahs_features_t *feat, void *d_ws, size_t ws_bytes,
              void *d_tmp, size_t tmp_bytes, void *stream)
 {
     if (!feat) return AHS_EINVAL;
@@ -612,12 +691,14 @@ int ahs_sort(const void *d_keys_in, const uint32_t *d_vals_in, void *d_keys_out,
     // ---- keys-only COUNTING from the feature histogram (Listing 2)
     if (strategy == AHS_COUNTING && exact_hist && !kv) {
         if (!d_ws || ws_bytes < WL.total) return AHS_ENOSPACE;
-        const uint32_t *scan = (const uint32_t *)((const char *)d_ws + WL.scan);
+        const uint32_t *scan = hist_scan(d_ws, feat, s);
+        if (!scan) return AHS_ECUDA;
         const uint64_t nvec = n / 4;
         uint64_t g = (4 * nvec + kFillChunk - 1) / kFillChunk;
         g = std::max<uint64_t>(1, g);
         cudaError_t e = launch(KID_COUNT_FILL, s, [&] {
-            k_count_fill<<<(unsigned)g, kFillBlock, 0, s>>>(kout, n32, scan, feat->nbins, flip, umin);
+            launch_k(k_count_fill, dim3((unsigned)g), dim3(kFillBlock), 0, s, kout, n32, scan, feat->nbins, flip,
+                     umin);
         });
         return e == cudaSuccess ? AHS_OK : AHS_ECUDA;
     }
@@ -676,16 +757,17 @@ int ahs_sort(const void *d_keys_in, const uint32_t *d_vals_in, void *d_keys_out,
     uint32_t *plan = tickets + 8;
     const uint32_t *bases;
     if (count_kv) {
-        bases = (const uint32_t *)((const char *)d_ws + WL.scan);
+        bases = hist_scan(d_ws, feat, s);
+        if (!bases) return AHS_ECUDA;
     } else {
         const char *wsc = (const char *)d_ws;
         const uint32_t *fhist = (const uint32_t *)(wsc + WL.hist);
         const uint64_t g5 = std::max<uint64_t>(2 * kRowCtas, ((uint64_t)feat->nbins + kRHBlock - 1) / kRHBlock);
         cudaError_t e = launch(KID_RADIX_HIST, s, [&] {
-            k_radix_hist<kRHBlock><<<(unsigned)g5, kRHBlock, 0, s>>>(
-                n, sub, passes, fhist, feat->nbins, feat->shift, (const DevFeatures *)(wsc + WL.feat),
-                (const uint32_t *)(wsc + WL.byte0), (const uint32_t *)(wsc + WL.digit1), dhist, bucket, tickets + 7,
-                plan, skip ? 1 : 0);
+            launch_k(k_radix_hist<kRHBlock>, dim3((unsigned)g5), dim3(kRHBlock), 0, s, n, sub, passes, fhist,
+                     feat->nbins, feat->shift, (const DevFeatures *)(wsc + WL.feat),
+                     (const uint32_t *)(wsc + WL.byte0), (const uint32_t *)(wsc + WL.digit1), dhist, bucket,
+                     tickets + 7, plan, skip ? 1 : 0);
         });
         if (e != cudaSuccess) return AHS_ECUDA;
         bases = bucket;
@@ -711,7 +793,10 @@ int ahs_sort(const void *d_keys_in, const uint32_t *d_vals_in, void *d_keys_out,
         pa.plan = count_kv ? nullptr : plan;  // K5's plan (no skipping when not enabled)
         void *args[] = {&pa};
         const cudaError_t e = launch(kv ? (count_kv ? KID_COUNT_SCATTER_KV : KID_ONESWEEP_KV) : KID_ONESWEEP, s, [&] {
-            cudaLaunchKernel(k6, dim3(grid), dim3(di->os_block[kv][mode]), args, k6_smem, s);
+            cudaLaunchConfig_t cfg;
+            cudaLaunchAttribute attr[1];
+            pdl_config(cfg, attr, dim3(grid), dim3(di->os_block[kv][mode]), k6_smem, s);
+            cudaLaunchKernelExC(&cfg, k6, args);
         });
         if (e != cudaSuccess) return AHS_ECUDA;
     }

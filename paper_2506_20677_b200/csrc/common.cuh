@@ -52,6 +52,19 @@ __host__ __device__ __forceinline__ Range derive_range(uint32_t umin, uint32_t u
     return r;
 }
 
+// ------------------------------------------- programmatic dependent launch
+// Every libahs kernel starts with pdl_begin(): wait until the previous grid in
+// the stream has completed and its memory is visible (a no-op unless launched
+// with programmatic stream serialization), then let the next grid launch: its
+// CTAs become resident as resources free up and wait in their own pdl_begin(),
+// which hides the launch latency between the kernels of a step.  Nothing
+// touches global memory before the wait.
+__device__ __forceinline__ void pdl_begin()
+{
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ---------------------------------------------------------------- memory ops
 __device__ __forceinline__ uint4 ld_nc_v4(const uint4 *p)
 {

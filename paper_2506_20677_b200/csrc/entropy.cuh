@@ -43,6 +43,7 @@ __global__ void __launch_bounds__(BLOCK)
     k_entropy_sorted(const uint32_t *__restrict__ keys, uint64_t n, uint64_t chunk,
                      RunPieces *__restrict__ pieces, double *__restrict__ chunk_S, double *__restrict__ out_H)
 {
+    pdl_begin();
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
     __shared__ uint32_t s_w[BLOCK / 32];

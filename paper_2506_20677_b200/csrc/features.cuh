@@ -38,13 +38,15 @@ constexpr int kHistCluster = 2;
 constexpr int kHistBins = 128 * 1024;                // bytes: 2^16 packed 16-bit counters
 constexpr uint32_t kHistWords = kHistBins / 4;       // 32768
 constexpr int kHistSmemBytes = kHistBins + kHistStages * (kHistChunk + 16);
-constexpr int kFinalBlock = 256;
+constexpr int kFinalBins = 256;                      // K3 bins per CTA
+constexpr int kFinalGroups = 4;                      // K3 row groups (threads per bin)
+constexpr int kFinalBlock = kFinalBins * kFinalGroups;
 constexpr uint32_t kMaxBins = 1u << 16;
-constexpr int kFinalGrid = (int)(kMaxBins / kFinalBlock);  // 256
+constexpr int kFinalGrid = (int)(kMaxBins / kFinalBins);  // 256
 
 // K3 control block in ws (zeroed by K1 where noted)
 struct FinalCtrl {
-    uint32_t barrier;       // zeroed by K1
+    uint32_t barrier;       // K3's finished-CTA count, zeroed by K1
     uint32_t pad[31];
     uint32_t chunk_tot[kFinalGrid];
     double chunk_S[kFinalGrid];
@@ -61,6 +63,7 @@ __global__ void __launch_bounds__(BLOCK)
                   Partial *__restrict__ partials, uint32_t *__restrict__ zero_words, uint32_t nzero,
                   FinalCtrl *__restrict__ fctrl, uint32_t *__restrict__ byte0_rows)
 {
+    pdl_begin();
     extern __shared__ __align__(128) uint8_t smem_raw[];
     __shared__ __align__(8) uint64_t bars[kReduceStages];
     // histogram of the raw low byte of every key (for the radix sort: digit 0 of
@@ -290,6 +293,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(BLOCK, 1)
                 const Partial *__restrict__ partials, int nparts, uint32_t *__restrict__ ovf,
                 uint32_t *__restrict__ parts, uint32_t *__restrict__ digit1_rows)
 {
+    pdl_begin();
     extern __shared__ __align__(128) uint32_t sh[];
     __shared__ __align__(8) uint64_t bars[kHistStages];
     cg::cluster_group cluster = cg::this_cluster();
@@ -407,14 +411,19 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(BLOCK, 1)
 }
 
 // ------------------------------------------------------------------ K3 ----
-// Cooperative launch of kFinalGrid CTAs x kFinalBlock threads (co-resident by
-// construction); thread b owns bin b.
-//   phase 1: c_b = sum of the cluster rows + overflow; hist[b] = c_b; per-CTA
-//            chunk total and chunk sum of c_b log2 c_b (fixed tree).
-//   barrier (atomic counter zeroed by K1; all CTAs are resident)
-//   phase 2: scan[b] = exclusive prefix (chunk offset + local), scan[nb] = n;
-//            CTA 0: H = log2 n - (1/n) sum_j S_j (fixed order), clamped to
-//            [0, log2 nb] (R11), written with the other features.
+// kFinalGrid CTAs x kFinalBlock threads; CTA j owns bins [j * BINS, (j + 1) * BINS),
+// and the GROUPS row groups of its threads sum every GROUPS-th cluster row of
+// them (the row sums are latency bound: GROUPS independent load streams per
+// bin).  CTAs past the last bin (nb < 2^16) return at once; `active` remain.
+//   c_b = sum of the cluster rows + overflow; hist[b] = c_b; per-CTA chunk
+//   total and chunk sum S_j of c_b log2 c_b (fixed tree).
+//   The last active CTA to finish (atomic count, zeroed by K1; no grid
+//   barrier, no co-residency needed): H = log2 n - (1/n) sum_j S_j (fixed
+//   order, independent of which CTA is last), clamped to [0, log2 nb]
+//   (R11), written with the other features to `out` and, when
+//   given, to the host-mapped `hout` (its seq word last, system-scope release).
+// The exclusive scan of the histogram is K3s (k_hist_scan), run by ahs_sort
+// only where COUNTING needs it.
 template <int BLOCK>
 __device__ __forceinline__ uint32_t block_sum_u32(uint32_t x, uint32_t *s_tmp)
 {
@@ -442,32 +451,114 @@ __device__ __forceinline__ double block_sum_f64_fixed(double x, double *s_tmp)
     return t;
 }
 
-template <int BLOCK>
-__global__ void __launch_bounds__(BLOCK)
+__device__ __forceinline__ void st_release_sys_u64(uint64_t *p, uint64_t v)
+{
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+template <int BLOCK, int GROUPS>
+__global__ void __launch_bounds__(BLOCK, 2)
     k_feat_finalize(uint64_t n, const Partial *__restrict__ partials, int nparts,
                     const uint32_t *__restrict__ parts, int nrows, const uint32_t *__restrict__ ovf,
-                    uint32_t *__restrict__ hist, uint32_t *__restrict__ scan, FinalCtrl *__restrict__ fctrl,
-                    DevFeatures *__restrict__ out)
+                    uint32_t *__restrict__ hist, FinalCtrl *__restrict__ fctrl, DevFeatures *__restrict__ out,
+                    DevFeatures *__restrict__ hout, uint64_t seq)
 {
+    pdl_begin();
+    constexpr uint32_t BINS = BLOCK / GROUPS;
     const Partial p = reduce_partials<BLOCK>(partials, nparts);
     const Range rg = derive_range(p.mn, p.mx, 16u);
+    const uint32_t active = (rg.nb + BINS - 1u) / BINS;
+    if (blockIdx.x >= active) return;  // no bins here (uniform per CTA)
     __shared__ uint32_t s_u[BLOCK / 32];
     __shared__ double s_d[BLOCK / 32];
-    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    const uint32_t b = blockIdx.x * BLOCK + threadIdx.x;
+    __shared__ uint32_t s_part[GROUPS - 1][BINS];
+    __shared__ uint32_t s_last;
+    const uint32_t grp = threadIdx.x / BINS;
+    const uint32_t b = blockIdx.x * BINS + threadIdx.x % BINS;
 
-    // ---- phase 1
     uint32_t c = 0;
-    if (b < rg.nb) {
+    if (b < rg.nb && rg.nb > 1u) {
+#pragma unroll 8
+        for (int r = (int)grp; r < nrows; r += GROUPS) c += __ldcg(&parts[(size_t)r * kMaxBins + b]);
+    }
+    if (grp > 0) s_part[grp - 1][threadIdx.x % BINS] = c;
+    __syncthreads();
+    if (grp > 0) {
+        c = 0;
+    } else if (b < rg.nb) {  // group 0 holds the bin's count
         if (rg.nb == 1u) {
             c = (uint32_t)n;
         } else {
-            c = __ldcg(&ovf[b]);
-#pragma unroll 16
-            for (int r = 0; r < nrows; r++) c += __ldcg(&parts[(size_t)r * kMaxBins + b]);
+            c += __ldcg(&ovf[b]);
+#pragma unroll
+            for (int q = 0; q < GROUPS - 1; q++) c += s_part[q][threadIdx.x];
         }
         hist[b] = c;
     }
+    const uint32_t tot = block_sum_u32<BLOCK>(c, s_u);
+    const double S = block_sum_f64_fixed<BLOCK>(c > 1u ? (double)c * log2((double)c) : 0.0, s_d);
+    if (threadIdx.x == 0) {
+        fctrl->chunk_tot[blockIdx.x] = tot;
+        fctrl->chunk_S[blockIdx.x] = S;
+        __threadfence();
+        s_last = atomicAdd(&fctrl->barrier, 1u) == active - 1u;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const double cs = threadIdx.x < active ? __ldcg(&fctrl->chunk_S[threadIdx.x]) : 0.0;
+    const double tot_S = block_sum_f64_fixed<BLOCK>(cs, s_d);
+    if (threadIdx.x == 0) {
+        double H = 0.0;
+        if (rg.nb > 1u) {
+            const double dn = (double)n;
+            H = log2(dn) - tot_S / dn;
+            const double hmax = log2((double)rg.nb);
+            if (H < 0.0) H = 0.0;
+            if (H > hmax) H = hmax;
+        }
+        DevFeatures f{};
+        f.umin = p.mn;
+        f.umax = p.mx;
+        f.descents = p.desc;
+        f.k = rg.k;
+        f.bits = rg.bits;
+        f.shift = rg.shift;
+        f.nb = rg.nb;
+        f.entropy = H;
+        f.pad0 = (uint32_t)nparts;                   // K1 CTAs = rows of byte0_rows
+        f.pad1[0] = (uint64_t)nrows * kHistCluster;  // K2 CTAs = rows of digit1_rows
+        f.pad1[1] = seq;
+        *out = f;
+        if (hout) {
+            uint64_t *hw = reinterpret_cast<uint64_t *>(hout);
+            const uint64_t *fw = reinterpret_cast<const uint64_t *>(&f);
+#pragma unroll
+            for (int w = 0; w < 7; w++) hw[w] = fw[w];
+            st_release_sys_u64(hw + 7, seq);  // pad1[1]: the host polls this word
+        }
+    }
+}
+
+// ----------------------------------------------------------------- K3s ----
+// scan[b] = exclusive prefix of hist over bins (scan[nb] = n), for COUNTING.
+// CTA j owns bins [j * BLOCK, (j + 1) * BLOCK); its offset is the sum of K3's
+// chunk totals before it (BLOCK / kFinalBins chunks per CTA).
+constexpr int kScanBlock = 1024;
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK)
+    k_hist_scan(const uint32_t *__restrict__ hist, const FinalCtrl *__restrict__ fctrl, uint32_t nb, uint32_t n,
+                uint32_t *__restrict__ scan)
+{
+    pdl_begin();
+    static_assert(BLOCK % kFinalBins == 0 && BLOCK >= kFinalGrid, "one chunk total per thread");
+    __shared__ uint32_t s_u[BLOCK / 32];
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const uint32_t b = blockIdx.x * BLOCK + threadIdx.x;
+    const uint32_t nchunks = blockIdx.x * (BLOCK / kFinalBins);
+    const uint32_t before = threadIdx.x < nchunks ? __ldcg(&fctrl->chunk_tot[threadIdx.x]) : 0u;
+    const uint32_t c = b < nb ? __ldcg(&hist[b]) : 0u;
+    const uint32_t off = block_sum_u32<BLOCK>(before, s_u);
     uint32_t incl = c;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -476,56 +567,10 @@ __global__ void __launch_bounds__(BLOCK)
     }
     if (lane == 31) s_u[warp] = incl;
     __syncthreads();
-    uint32_t wofs = 0, tot = 0;
-    for (uint32_t w = 0; w < BLOCK / 32; w++) {
-        wofs += w < warp ? s_u[w] : 0u;
-        tot += s_u[w];
-    }
-    const uint32_t local_excl = wofs + incl - c;
-    __syncthreads();
-    const double S = block_sum_f64_fixed<BLOCK>(c > 1u ? (double)c * log2((double)c) : 0.0, s_d);
-    if (threadIdx.x == 0) {
-        fctrl->chunk_tot[blockIdx.x] = tot;
-        fctrl->chunk_S[blockIdx.x] = S;
-        __threadfence();
-        atomicAdd(&fctrl->barrier, 1u);
-        uint32_t spins = 0;
-        while (ld_relaxed(&fctrl->barrier) < gridDim.x)
-            if (++spins > (1u << 28)) __trap();
-        __threadfence();
-    }
-    __syncthreads();
-    // ---- phase 2
-    const uint32_t mine = threadIdx.x < blockIdx.x ? __ldcg(&fctrl->chunk_tot[threadIdx.x]) : 0u;
-    const uint32_t off = block_sum_u32<BLOCK>(mine, s_u);
-    if (b < rg.nb) scan[b] = off + local_excl;
-    if (b == rg.nb - 1u) scan[rg.nb] = (uint32_t)n;
-    if (blockIdx.x == 0) {
-        const double cs = threadIdx.x < gridDim.x ? __ldcg(&fctrl->chunk_S[threadIdx.x]) : 0.0;
-        const double tot_S = block_sum_f64_fixed<BLOCK>(cs, s_d);
-        if (threadIdx.x == 0) {
-            double H = 0.0;
-            if (rg.nb > 1u) {
-                const double dn = (double)n;
-                H = log2(dn) - tot_S / dn;
-                const double hmax = log2((double)rg.nb);
-                if (H < 0.0) H = 0.0;
-                if (H > hmax) H = hmax;
-            }
-            DevFeatures f{};
-            f.umin = p.mn;
-            f.umax = p.mx;
-            f.descents = p.desc;
-            f.k = rg.k;
-            f.bits = rg.bits;
-            f.shift = rg.shift;
-            f.nb = rg.nb;
-            f.entropy = H;
-            f.pad0 = (uint32_t)nparts;            // K1 CTAs = rows of byte0_rows
-            f.pad1[0] = (uint64_t)nrows * kHistCluster;  // K2 CTAs = rows of digit1_rows
-            *out = f;
-        }
-    }
+    uint32_t wofs = 0;
+    for (uint32_t w = 0; w < warp; w++) wofs += s_u[w];
+    if (b < nb) scan[b] = off + wofs + incl - c;
+    if (b == nb - 1u) scan[nb] = n;
 }
 
 }  // namespace ahs

@@ -138,6 +138,7 @@ struct PassArgs {
 template <bool KV, int BLOCK, int ITEMS, int MINB, int RANK = kRankMasked>
 __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(const PassArgs a)
 {
+    pdl_begin();
     // ---- this pass's place in the chain
     uint32_t e = a.pass, m = a.npasses;
     if (a.plan) {

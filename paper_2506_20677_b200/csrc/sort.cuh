@@ -67,6 +67,7 @@ __global__ void __launch_bounds__(BLOCK, 1)
                  uint32_t *__restrict__ bucket_base, uint32_t *__restrict__ ticket, uint32_t *__restrict__ plan,
                  int skip_trivial)
 {
+    pdl_begin();
     __shared__ uint32_t s_dig[4][256];
     __shared__ bool s_last;
     __shared__ uint32_t s_triv[4];
@@ -176,6 +177,7 @@ __global__ void __launch_bounds__(kFillBlock)
     k_count_fill(uint32_t *__restrict__ out, uint32_t n, const uint32_t *__restrict__ scan,
                  uint32_t nb, uint32_t out_flip, uint32_t out_add)
 {
+    pdl_begin();
     __shared__ uint32_t s_lo, s_hi;
     // output positions are counted from the first 16-byte aligned element
     const uint32_t head = min(n, (uint32_t)(((16u - ((uintptr_t)out & 15u)) & 15u) >> 2));

@@ -1,4 +1,7 @@
-"""Step time vs kernel time of the pipeline (development tool): how much of a step is host round trip."""
+"""Step time vs kernel time of the pipeline (development tool): how much of a step is host round trip.
+
+    python tools/gapbench.py [cfg ...]     (AHS_PDL=0 etc. pass through)
+"""
 import os
 import sys
 
@@ -9,47 +12,42 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2506_20677_b200 as ahs  # noqa: E402
 import synth  # noqa: E402
 
-cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
-keys, vals, _ = synth.make(cfg)
-dk = torch.from_numpy(keys.view(np.int32)).cuda()
-if keys.dtype == np.uint32:
-    dk = dk.view(torch.uint32)
-ko = torch.empty_like(dk)
-ws = ahs.Workspace(keys.size, False)
-st = torch.cuda.current_stream()
-for _ in range(3):
-    f = ahs.ahs_features(dk, ws)
-    s, r = ahs.ahs_select(f)
-    ahs.ahs_sort(dk, None, ko, None, s, f, ws)
-torch.cuda.synchronize()
-a, b, c = (torch.cuda.Event(enable_timing=True) for _ in range(3))
-tf, ts = [], []
-ahs.ahs_profile_begin()
-for _ in range(20):
-    a.record(st)
-    f = ahs.ahs_features(dk, ws)
-    b.record(st)
-    s, r = ahs.ahs_select(f)
-    ahs.ahs_sort(dk, None, ko, None, s, f, ws)
-    c.record(st)
+
+def run(cfg, reps=30):
+    keys, vals, _ = synth.make(cfg)
+    dk = torch.from_numpy(keys.view(np.int32)).cuda()
+    if keys.dtype == np.uint32:
+        dk = dk.view(torch.uint32)
+    dv = torch.from_numpy(vals.view(np.int32)).cuda().view(torch.uint32) if vals is not None else None
+    ko = torch.empty_like(dk)
+    vo = torch.empty_like(dv) if dv is not None else None
+    ws = ahs.Workspace(keys.size, dv is not None)
+    st = torch.cuda.current_stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    for _ in range(3):
+        f = ahs.ahs_features(dk, ws)
+        s, r = ahs.ahs_select(f)
+        ahs.ahs_sort(dk, dv, ko, vo, s, f, ws)
     torch.cuda.synchronize()
-    tf.append(a.elapsed_time(b))
-    ts.append(b.elapsed_time(c))
-ahs.ahs_profile_end()
-prof = ahs.ahs_profile_read()
-kf = sum(v["ms"] for k, v in prof.items() if k.startswith("feat")) / 20
-ks = sum(v["ms"] for k, v in prof.items() if not k.startswith("feat")) / 20
-tf2, ts2 = [], []
-for _ in range(20):
-    a.record(st)
-    f = ahs.ahs_features(dk, ws)
-    b.record(st)
-    s, r = ahs.ahs_select(f)
-    ahs.ahs_sort(dk, None, ko, None, s, f, ws)
-    c.record(st)
-    torch.cuda.synchronize()
-    tf2.append(a.elapsed_time(b))
-    ts2.append(b.elapsed_time(c))
-print(f"{cfg} (no per-kernel events): features step {np.median(tf2)*1e3:.1f} us, sort step {np.median(ts2)*1e3:.1f} us")
-print(f"{cfg}: features step {np.median(tf)*1e3:.1f} us (kernels {kf*1e3:.1f}), "
-      f"sort step {np.median(ts)*1e3:.1f} us (kernels {ks*1e3:.1f})")
+    a, b, c = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+    tf, ts, tt = [], [], []
+    for _ in range(reps):
+        flush.fill_(1)
+        a.record(st)
+        f = ahs.ahs_features(dk, ws)
+        b.record(st)
+        s, r = ahs.ahs_select(f)
+        ahs.ahs_sort(dk, dv, ko, vo, s, f, ws)
+        c.record(st)
+        torch.cuda.synchronize()
+        tf.append(a.elapsed_time(b))
+        ts.append(b.elapsed_time(c))
+        tt.append(a.elapsed_time(c))
+    print(f"{cfg:10s} {ahs.STRATEGY_NAMES[s] if hasattr(ahs, 'STRATEGY_NAMES') else s}: "
+          f"features {np.median(tf)*1e3:7.1f} us, sort {np.median(ts)*1e3:7.1f} us, "
+          f"step {np.median(tt)*1e3:7.1f} us (min {np.min(tt)*1e3:7.1f}) pdl={os.environ.get('AHS_PDL', '1')}",
+          flush=True)
+
+
+for cfg in (sys.argv[1:] or ["cfg2"]):
+    run(cfg)
