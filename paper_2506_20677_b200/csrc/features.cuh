@@ -541,7 +541,7 @@ __global__ void __launch_bounds__(BLOCK, 2)
 }
 
 // ----------------------------------------------------------------- K3s ----
-// scan[b] = exclusive prefix of hist over bins (scan[nb] = n), for COUNTING.
+// scan[b] = exclusive prefix of hist over bins (scan[b] = n for nb <= b <= max(nb, 256)), for COUNTING.
 // CTA j owns bins [j * BLOCK, (j + 1) * BLOCK); its offset is the sum of K3's
 // chunk totals before it (BLOCK / kFinalBins chunks per CTA).
 constexpr int kScanBlock = 1024;
@@ -571,6 +571,7 @@ __global__ void __launch_bounds__(BLOCK)
     for (uint32_t w = 0; w < warp; w++) wofs += s_u[w];
     if (b < nb) scan[b] = off + wofs + incl - c;
     if (b == nb - 1u) scan[nb] = n;
+    if (b > nb && b <= 256u) scan[b] = n;  // K6 reads 257 bucket bases when it scatters COUNTING pairs
 }
 
 }  // namespace ahs

@@ -5,6 +5,7 @@
 #include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
+#include <cmath>
 #include <type_traits>
 #include <cstdio>
 #include <cstdlib>
@@ -236,9 +237,24 @@ int main(int argc, char **argv)
     CK(cudaDeviceSynchronize());
     std::vector<uint32_t> hk(n);
     CK(cudaMemcpy(hk.data(), B.k, n * 4ull, cudaMemcpyDeviceToHost));
+    std::vector<uint32_t> shifts = {0u, 8u};
+    if (dist == 4) {  // cfg3-like: j * 2^18, j ~ Zipf(1.1) on [0, 4096) by inverse CDF (digits 2 and 3 vary)
+        std::vector<double> cdf(4096);
+        double acc = 0.0;
+        for (int j = 0; j < 4096; j++) cdf[j] = (acc += std::pow(j + 1.0, -1.1));
+        for (int j = 0; j < 4096; j++) cdf[j] /= acc;
+        cdf[4095] = 1.0;
+        for (uint32_t i = 0; i < n; i++) {
+            const double u = (hash32(i * 2654435761u + 777u) >> 8) * (1.0 / 16777216.0);
+            const uint32_t j = (uint32_t)(std::upper_bound(cdf.begin(), cdf.end(), u) - cdf.begin());
+            hk[i] = std::min(j, 4095u) << 18;
+        }
+        CK(cudaMemcpy(B.k, hk.data(), n * 4ull, cudaMemcpyHostToDevice));
+        shifts = {16u, 24u};
+    }
     printf("n = %u, dist %d, %d SMs\n", n, dist, sms);
-    for (uint32_t shift : {0u, 8u})
-        if (g_only < 0 || shift == 0) {
+    for (uint32_t shift : shifts)
+        if (g_only < 0 || shift == shifts[0]) {
         std::vector<uint32_t> hist(256, 0), base(256);
         for (uint32_t i = 0; i < n; i++) hist[(hk[i] >> shift) & 255u]++;
         uint32_t run = 0, mx = 0;
