@@ -14,9 +14,9 @@
 //               (its length inside the chunk, and whether it ends here); so is
 //               the last run when it continues into the next chunk.
 //   grid sync
-//   CTA 0       thread 0 stitches the runs that cross chunk boundaries in chunk
-//               order, then sums S[0..G) in a fixed tree: H = log2 n - S / n,
-//               clamped >= 0.
+//   CTA 0       the runs that cross chunk boundaries: the thread of each run's
+//               origin chunk follows it forward to its end; then a fixed tree
+//               over the chunk sums and those runs: H = log2 n - S / n, >= 0.
 // Deterministic for a given G.  Work is independent of the run lengths.
 #pragma once
 
@@ -66,7 +66,10 @@ __global__ void __launch_bounds__(BLOCK)
     const uint32_t *kc = keys + c0;
     // keys of tile t0 for this thread (keys past the chunk, up to n, are read
     // too: a run end looks one key ahead)
-    auto load = [&](uint32_t t0, uint32_t (&k)[kEntItems]) {
+    // keys of tile t0 for this thread, plus the warp's edge neighbours (lane 0:
+    // the key before its first, lane 31: the key after its last; keys past the
+    // chunk, up to n, are read too: a run end looks one key ahead)
+    auto load = [&](uint32_t t0, uint32_t (&k)[kEntItems], uint32_t &edge) {
         const uint32_t i0 = t0 + threadIdx.x * kEntItems;
         if (vec && c0 + i0 + kEntItems <= n) {
             const uint4 *p4 = reinterpret_cast<const uint4 *>(kc + i0);
@@ -82,20 +85,24 @@ __global__ void __launch_bounds__(BLOCK)
 #pragma unroll
             for (int q = 0; q < kEntItems; q++) k[q] = (c0 + i0 + q < n) ? kc[i0 + q] : 0u;
         }
+        edge = 0u;
+        if (lane == 0 && c0 + i0 > 0 && i0 < len) edge = kc[(int64_t)i0 - 1];
+        if (lane == 31 && c0 + i0 + kEntItems < n) edge = kc[i0 + kEntItems];
     };
     const bool last_chunk = c1 == n;
-    uint32_t k[kEntItems], kn[kEntItems];
-    if (len > 0) load(0, kn);
+    uint32_t k[kEntItems], kn[kEntItems], edge = 0u, edge_n = 0u;
+    if (len > 0) load(0, kn, edge_n);
     for (uint32_t t0 = 0; t0 < len; t0 += TILE) {
         const uint32_t i0 = t0 + threadIdx.x * kEntItems;
 #pragma unroll
         for (int q = 0; q < kEntItems; q++) k[q] = kn[q];
-        if (t0 + TILE < len) load(t0 + TILE, kn);  // next tile in flight while this one is scanned
-        // neighbours: the previous / next thread's keys; global loads only at warp edges
+        edge = edge_n;
+        if (t0 + TILE < len) load(t0 + TILE, kn, edge_n);  // next tile in flight while this one is scanned
+        // neighbours: the previous / next thread's keys; the loaded edges at warp edges
         uint32_t prev = __shfl_up_sync(kFull, k[kEntItems - 1], 1);
         uint32_t next = __shfl_down_sync(kFull, k[0], 1);
-        if (lane == 0) prev = (c0 + i0 > 0 && i0 < len) ? kc[(int64_t)i0 - 1] : 0u;
-        if (lane == 31) next = (c0 + i0 + kEntItems < n) ? kc[i0 + kEntItems] : 0u;
+        if (lane == 0) prev = edge;
+        if (lane == 31) next = edge;
         // a start at local 0 of chunk 0 is real; elsewhere starts compare with the previous key
         uint32_t mine = 0;  // last local start among my keys (0: none; neutral, carry >= 0)
 #pragma unroll
@@ -159,8 +166,10 @@ __global__ void __launch_bounds__(BLOCK)
     }
     grid.sync();
 
-    // ---- CTA 0: stitch the runs crossing chunk boundaries (chunk order), then
-    // a fixed tree over the chunk sums
+    // ---- CTA 0: the runs crossing chunk boundaries, then a fixed tree over the
+    // chunk sums.  A crossing run has exactly one origin chunk (suf > 0, where
+    // it starts); the thread of that chunk follows it forward through chunks it
+    // crosses whole (pre > 0, !pre_ends) to the one it ends in.
     if (blockIdx.x == 0) {
         __shared__ RunPieces s_pieces[kEntMaxGrid];
         for (uint32_t c = threadIdx.x; c < gridDim.x; c += BLOCK) {
@@ -172,21 +181,16 @@ __global__ void __launch_bounds__(BLOCK)
         }
         __syncthreads();
         double t = 0.0;
-        if (threadIdx.x == 0) {
-            uint64_t run = 0;  // length so far of the run crossing into the next chunk
-            for (uint32_t c = 0; c < gridDim.x; c++) {
-                const RunPieces rp = s_pieces[c];
-                if (rp.pre > 0) {  // the crossing run continues here
-                    run += rp.pre;
-                    if (!rp.pre_ends) continue;  // ... and crosses this chunk too
-                }
-                // the crossing run (if any) ended at the start of this chunk or inside it
-                if (run > 1) t += (double)run * log2((double)run);
-                run = rp.suf;
+        for (uint32_t c = threadIdx.x; c < gridDim.x; c += BLOCK) {
+            t += __ldcg(&chunk_S[c]);
+            uint64_t run = s_pieces[c].suf;
+            if (run == 0) continue;
+            for (uint32_t e = c + 1; e < gridDim.x; e++) {  // the run continues into chunk e
+                run += s_pieces[e].pre;
+                if (s_pieces[e].pre_ends) break;
             }
-            if (run > 1) t += (double)run * log2((double)run);
+            t += (double)run * log2((double)run);  // run >= 2: it spans a boundary
         }
-        for (uint32_t c = threadIdx.x; c < gridDim.x; c += BLOCK) t += __ldcg(&chunk_S[c]);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(kFull, t, o);
         if (lane == 0) s_d[warp] = t;
