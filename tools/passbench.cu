@@ -78,6 +78,7 @@ struct Bufs {
 };
 
 static int g_only = -1, g_idx = 0;
+static bool g_noflush = false;  // env PB_NOFLUSH=1: the pass input stays L2-warm (as inside a sort)
 
 template <bool KV, int BLOCK, int ITEMS, int MINB, int RANK = kRankMasked>
 float run_cfg(const Bufs &B, uint32_t n, uint32_t shift, int sms, int reps, bool check,
@@ -96,7 +97,7 @@ float run_cfg(const Bufs &B, uint32_t n, uint32_t shift, int sms, int reps, bool
     CK(cudaEventCreate(&b));
     std::vector<float> ts;
     for (int r = 0; r < reps + 2; r++) {
-        k_flush<<<sms * 4, 512>>>(B.flush, B.flush_n);
+        if (!g_noflush) k_flush<<<sms * 4, 512>>>(B.flush, B.flush_n);
         CK(cudaMemsetAsync(B.status, 0, (size_t)tiles * 256 * 4));
         CK(cudaMemsetAsync(B.ticket, 0, 4));
         CK(cudaEventRecord(a));
@@ -221,6 +222,7 @@ int main(int argc, char **argv)
     const int reps = argc > 3 ? atoi(argv[3]) : 10;
     const bool cub = argc > 4 ? atoi(argv[4]) != 0 : true;
     g_only = argc > 5 ? atoi(argv[5]) : -1;
+    g_noflush = getenv("PB_NOFLUSH") && getenv("PB_NOFLUSH")[0] == '1';
     int sms;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
     Bufs B;
