@@ -21,11 +21,12 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 _lock = threading.Lock()
 _lib = None
 
-I32, U32 = 0, 1
+I32, U32, I64, U64 = 0, 1, 2, 3
 INSERTION, COUNTING, RADIX, QUICK = 0, 1, 2, 3
 STRATEGY4_NAMES = {INSERTION: "insertion", COUNTING: "counting", RADIX: "radix", QUICK: "quick"}
 RULE_NAMES = {0: "EMPTY", 1: "CONSTANT", 2: "SMALL_N", 3: "SMALL_RANGE", 4: "LOW_ENTROPY", 5: "DEFAULT"}
 FLAG_EMPTY, FLAG_CONSTANT, FLAG_BUCKETED, FLAG_SORTED, FLAG_STRICT_DESC, FLAG_SIGNED = 1, 2, 4, 8, 16, 32
+FLAG_K_SATURATED = 64  # k = 2^64 (64-bit keys spanning the whole range): reported as 2^64 - 1
 
 # Table II / reading A3-A5 defaults
 DEFAULT_THRESHOLDS = dict(n_insertion=20, k_counting=1024, k_radix=1_000_000,
@@ -40,6 +41,13 @@ class Features(C.Structure):
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_ if f != "pad"}
+
+    def key_min(self):
+        """min as a Python int in the key's own type (uint64: min holds the bit pattern)."""
+        return self.min & 0xFFFFFFFFFFFFFFFF if self.dtype == U64 else self.min
+
+    def key_max(self):
+        return self.max & 0xFFFFFFFFFFFFFFFF if self.dtype == U64 else self.max
 
 
 def build(force: bool = False) -> str:
@@ -74,12 +82,14 @@ def lib():
     return _lib
 
 
+_DTYPES = {np.dtype(np.int32): I32, np.dtype(np.uint32): U32, np.dtype(np.int64): I64, np.dtype(np.uint64): U64}
+
+
 def _dtype_code(keys: np.ndarray) -> int:
-    if keys.dtype == np.int32:
-        return I32
-    if keys.dtype == np.uint32:
-        return U32
-    raise TypeError(f"oracle keys must be int32 or uint32, got {keys.dtype}")
+    try:
+        return _DTYPES[keys.dtype]
+    except KeyError:  # P:409 integers only; 64-bit per S:20 (NEXT-3)
+        raise TypeError(f"oracle keys must be int32, uint32, int64 or uint64, got {keys.dtype}") from None
 
 
 def _ptr(a):

@@ -31,6 +31,13 @@
  *                     (reading A13).  Records compare (key, original index),
  *                     so the result is the unique stable order.
  *
+ * Key types: int32, uint32, int64, uint64 (SPEC's SortKey is i64, S:20;
+ * NEXT-3 in SURVEY §8(f)).  Every function works on the ORDER-PRESERVING
+ * UNSIGNED IMAGE u of a key (signed types: the sign bit flipped), so unsigned
+ * comparison of images is the keys' order and u - u_min = key - min exactly.
+ * k = max - min + 1 can be 2^64 for 64-bit keys: it is computed in 128-bit
+ * arithmetic and reported saturated at 2^64 - 1 with ORF_K_SATURATED.
+ *
  * Parity pins: tests/test_oracle.py (brute force over all permutations for
  * n <= 8 against Python's sorted(), entropy closed forms, SPEC worked examples,
  * golden fixtures in tests/golden/).  H_exact is context only ("parity
@@ -53,24 +60,50 @@ typedef struct {
     uint32_t pad;
 } oracle_features_t;
 
-enum { OR_I32 = 0, OR_U32 = 1 };
+enum { OR_I32 = 0, OR_U32 = 1, OR_I64 = 2, OR_U64 = 3 };
 enum { ORF_EMPTY = 1, ORF_CONSTANT = 2, ORF_BUCKETED = 4, ORF_SORTED = 8,
-       ORF_STRICT_DESC = 16, ORF_SIGNED = 32 };
+       ORF_STRICT_DESC = 16, ORF_SIGNED = 32, ORF_K_SATURATED = 64 };
 /* the paper's four algorithms, §III.A */
 enum { OR_INSERTION = 0, OR_COUNTING = 1, OR_RADIX = 2, OR_QUICK = 3 };
 enum { ORR_EMPTY = 0, ORR_CONSTANT = 1, ORR_SMALL_N = 2, ORR_SMALL_RANGE = 3,
        ORR_LOW_ENTROPY = 4, ORR_DEFAULT = 5 };
 
-static int64_t key_at(const void *keys, int dtype, uint64_t i)
+static int dtype_ok(int dtype) { return dtype >= OR_I32 && dtype <= OR_U64; }
+static int dtype_signed(int dtype) { return dtype == OR_I32 || dtype == OR_I64; }
+static size_t key_bytes(int dtype) { return dtype >= OR_I64 ? 8 : 4; }
+
+/* order-preserving unsigned image of key i (sign bit flipped for signed types) */
+static uint64_t key_at(const void *keys, int dtype, uint64_t i)
 {
-    if (dtype == OR_I32) return (int64_t)((const int32_t *)keys)[i];
-    return (int64_t)((const uint32_t *)keys)[i];
+    switch (dtype) {
+    case OR_I32: return (uint64_t)(((const uint32_t *)keys)[i] ^ 0x80000000u);
+    case OR_U32: return (uint64_t)((const uint32_t *)keys)[i];
+    case OR_I64: return ((const uint64_t *)keys)[i] ^ 0x8000000000000000ull;
+    default: return ((const uint64_t *)keys)[i];
+    }
 }
 
-static void key_put(void *keys, int dtype, uint64_t i, int64_t v)
+/* inverse of key_at: store the key whose image is u */
+static void key_put(void *keys, int dtype, uint64_t i, uint64_t u)
 {
-    if (dtype == OR_I32) ((int32_t *)keys)[i] = (int32_t)v;
-    else ((uint32_t *)keys)[i] = (uint32_t)v;
+    switch (dtype) {
+    case OR_I32: ((uint32_t *)keys)[i] = (uint32_t)u ^ 0x80000000u; break;
+    case OR_U32: ((uint32_t *)keys)[i] = (uint32_t)u; break;
+    case OR_I64: ((uint64_t *)keys)[i] = u ^ 0x8000000000000000ull; break;
+    default: ((uint64_t *)keys)[i] = u; break;
+    }
+}
+
+/* the key with image u as a 64-bit integer: its value for the signed types
+ * and uint32, its bit pattern for uint64 */
+static int64_t key_value(int dtype, uint64_t u)
+{
+    switch (dtype) {
+    case OR_I32: return (int64_t)(int32_t)((uint32_t)u ^ 0x80000000u);
+    case OR_U32: return (int64_t)u;
+    case OR_I64: return (int64_t)(u ^ 0x8000000000000000ull);
+    default: return (int64_t)u;
+    }
 }
 
 /* number of bits needed to write x in binary; bitlen(0) = 0 */
@@ -89,12 +122,12 @@ static uint32_t bitlen(uint64_t x)
 int oracle_features(const void *keys, uint64_t n, int dtype, uint32_t entropy_bits,
                     oracle_features_t *out, uint64_t *hist_out)
 {
-    if (!out || (dtype != OR_I32 && dtype != OR_U32) || entropy_bits == 0 || entropy_bits > 32)
+    if (!out || !dtype_ok(dtype) || entropy_bits == 0 || entropy_bits > 32)
         return -1;
     memset(out, 0, sizeof(*out));
     out->n = n;
     out->dtype = (uint32_t)dtype;
-    if (dtype == OR_I32) out->flags |= ORF_SIGNED;
+    if (dtype_signed(dtype)) out->flags |= ORF_SIGNED;
     if (n == 0) {                      /* empty array, O(1) exit */
         out->flags |= ORF_EMPTY;
         return 0;
@@ -102,23 +135,25 @@ int oracle_features(const void *keys, uint64_t n, int dtype, uint32_t entropy_bi
     if (!keys) return -1;
 
     /* pass 1: min, max (P:397 Math.min/max), descents (reading A14) */
-    int64_t mn = key_at(keys, dtype, 0), mx = mn;
+    uint64_t mn = key_at(keys, dtype, 0), mx = mn;
     uint64_t desc = 0;
     for (uint64_t i = 0; i < n; i++) {
-        int64_t v = key_at(keys, dtype, i);
+        uint64_t v = key_at(keys, dtype, i);
         if (v < mn) mn = v;
         if (v > mx) mx = v;
         if (i + 1 < n && v > key_at(keys, dtype, i + 1)) desc++;
     }
-    out->min = mn;
-    out->max = mx;
+    out->min = key_value(dtype, mn);
+    out->max = key_value(dtype, mx);
     out->descents = desc;
-    /* k = max(arr) - min(arr) + 1 — at most 2^32, fits u64 */
-    uint64_t k = (uint64_t)(mx - mn) + 1;
-    out->k = k;
-    out->bits = bitlen(k - 1);
+    /* k = max(arr) - min(arr) + 1, in 128-bit arithmetic: up to
+     * 2^64 for 64-bit keys, reported saturated at 2^64 - 1 */
+    unsigned __int128 k = (unsigned __int128)(mx - mn) + 1u;
+    out->k = k > (unsigned __int128)UINT64_MAX ? UINT64_MAX : (uint64_t)k;
+    if (k > (unsigned __int128)UINT64_MAX) out->flags |= ORF_K_SATURATED;
+    out->bits = bitlen(mx - mn); /* = bitlen(k - 1) */
     out->shift = out->bits > entropy_bits ? out->bits - entropy_bits : 0;
-    out->nb = (uint32_t)(((k - 1) >> out->shift) + 1);
+    out->nb = (uint32_t)(((mx - mn) >> out->shift) + 1);
     if (out->shift > 0) out->flags |= ORF_BUCKETED;
     if (k == 1) out->flags |= ORF_CONSTANT;
     if (desc == 0) out->flags |= ORF_SORTED;
@@ -128,7 +163,7 @@ int oracle_features(const void *keys, uint64_t n, int dtype, uint32_t entropy_bi
     uint64_t *c = (uint64_t *)calloc(out->nb, sizeof(uint64_t));
     if (!c) return -2;
     for (uint64_t i = 0; i < n; i++) {
-        uint64_t off = (uint64_t)(key_at(keys, dtype, i) - mn);
+        uint64_t off = key_at(keys, dtype, i) - mn;
         c[off >> out->shift]++;
     }
 
@@ -208,7 +243,7 @@ int oracle_select(const oracle_features_t *f, uint64_t n_insertion, uint64_t k_c
 void oracle_insertion(void *keys, uint32_t *vals, uint64_t n, int dtype)
 {
     for (uint64_t i = 1; i < n; i++) {
-        int64_t key = key_at(keys, dtype, i);
+        uint64_t key = key_at(keys, dtype, i);
         uint32_t val = vals ? vals[i] : 0;
         int64_t j = (int64_t)i - 1;
         while (j >= 0 && key_at(keys, dtype, (uint64_t)j) > key) {
@@ -231,20 +266,20 @@ int oracle_counting(const void *keys, const uint32_t *vals, uint64_t n, int dtyp
                     void *out_keys, uint32_t *out_vals)
 {
     if (n == 0) return 0;
-    int64_t mn = key_at(keys, dtype, 0), mx = mn;
+    uint64_t mn = key_at(keys, dtype, 0), mx = mn;
     for (uint64_t i = 0; i < n; i++) {
-        int64_t v = key_at(keys, dtype, i);
+        uint64_t v = key_at(keys, dtype, i);
         if (v < mn) mn = v;
         if (v > mx) mx = v;
     }
-    uint64_t range = (uint64_t)(mx - mn) + 1;
-    if (range > ORACLE_COUNTING_MAX_RANGE) return -3;
+    if (mx - mn >= ORACLE_COUNTING_MAX_RANGE) return -3;
+    uint64_t range = mx - mn + 1;
     uint64_t *count = (uint64_t *)calloc(range, sizeof(uint64_t));
     if (!count) return -2;
     for (uint64_t i = 0; i < n; i++) count[key_at(keys, dtype, i) - mn]++;      /* count */
     for (uint64_t i = 1; i < range; i++) count[i] += count[i - 1];             /* prefix */
     for (uint64_t i = n; i-- > 0;) {                                           /* output */
-        int64_t x = key_at(keys, dtype, i);
+        uint64_t x = key_at(keys, dtype, i);
         uint64_t pos = --count[x - mn];
         key_put(out_keys, dtype, pos, x);
         if (out_vals) out_vals[pos] = vals[i];
@@ -263,16 +298,16 @@ int oracle_radix(const void *keys, const uint32_t *vals, uint64_t n, int dtype,
                  void *out_keys, uint32_t *out_vals)
 {
     if (n == 0) return 0;
-    int64_t mn = key_at(keys, dtype, 0), mx = mn;
+    uint64_t mn = key_at(keys, dtype, 0), mx = mn;
     for (uint64_t i = 0; i < n; i++) {
-        int64_t v = key_at(keys, dtype, i);
+        uint64_t v = key_at(keys, dtype, i);
         if (v < mn) mn = v;
         if (v > mx) mx = v;
     }
-    uint64_t k = (uint64_t)(mx - mn) + 1;
+    unsigned __int128 k = (unsigned __int128)(mx - mn) + 1u; /* up to 2^64 */
     /* Eq. 4: d = ceil(log_256 k) = least d with 256^d >= k */
     uint32_t d = 0;
-    for (uint64_t p = 1; p < k; p *= 256) d++;
+    for (unsigned __int128 p = 1; p < k; p *= 256) d++;
 
     uint64_t *a = (uint64_t *)malloc(n * sizeof(uint64_t));
     uint64_t *b = (uint64_t *)malloc(n * sizeof(uint64_t));
@@ -280,7 +315,7 @@ int oracle_radix(const void *keys, const uint32_t *vals, uint64_t n, int dtype,
     uint32_t *vb = vals ? (uint32_t *)malloc(n * sizeof(uint32_t)) : NULL;
     if (!a || !b || (vals && (!va || !vb))) { free(a); free(b); free(va); free(vb); return -2; }
     for (uint64_t i = 0; i < n; i++) {
-        a[i] = (uint64_t)(key_at(keys, dtype, i) - mn);
+        a[i] = key_at(keys, dtype, i) - mn;
         if (vals) va[i] = vals[i];
     }
     for (uint32_t digit = 0; digit < d; digit++) {
@@ -298,7 +333,7 @@ int oracle_radix(const void *keys, const uint32_t *vals, uint64_t n, int dtype,
         if (vals) { uint32_t *tv = va; va = vb; vb = tv; }
     }
     for (uint64_t i = 0; i < n; i++) {
-        key_put(out_keys, dtype, i, (int64_t)a[i] + mn);
+        key_put(out_keys, dtype, i, a[i] + mn);
         if (vals) out_vals[i] = va[i];
     }
     free(a); free(b); free(va); free(vb);
@@ -312,7 +347,7 @@ int oracle_radix(const void *keys, const uint32_t *vals, uint64_t n, int dtype,
  * on the smaller side / loop on the larger, heapsort past depth
  * 2*log2(n) + 64 (reading A13).
  * ------------------------------------------------------------------------- */
-typedef struct { int64_t key; uint64_t idx; } rec_t;
+typedef struct { uint64_t key; uint64_t idx; } rec_t; /* key: the ordered image */
 
 static int rec_lt(const rec_t *x, const rec_t *y)
 {
@@ -402,7 +437,8 @@ int oracle_sort(const void *keys, const uint32_t *vals, uint64_t n, int dtype, i
                 void *out_keys, uint32_t *out_vals)
 {
     if (n == 0) return 0;
-    size_t kb = dtype == OR_I32 ? sizeof(int32_t) : sizeof(uint32_t);
+    if (!dtype_ok(dtype)) return -1;
+    size_t kb = key_bytes(dtype);
     switch (strategy4) {
     case OR_INSERTION:
         memcpy(out_keys, keys, n * kb);
@@ -431,7 +467,7 @@ int oracle_ahs(const void *keys, const uint32_t *vals, uint64_t n, int dtype,
     if (rc) return rc;
     if (n == 0) return 0;
     if (*rule == ORR_CONSTANT) {
-        size_t kb = dtype == OR_I32 ? sizeof(int32_t) : sizeof(uint32_t);
+        size_t kb = key_bytes(dtype);
         memcpy(out_keys, keys, n * kb);
         if (vals) memcpy(out_vals, vals, n * sizeof(uint32_t));
         return 0;
