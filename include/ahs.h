@@ -58,7 +58,9 @@ typedef enum {
     AHS_ENODEV = -6    /* no CUDA device or not an sm_100 device */
 } ahs_status;
 
-typedef enum { AHS_I32 = 0, AHS_U32 = 1 } ahs_dtype;
+/* Key types: 32-bit keys (PAPER.md P:409 integers) and, NEXT-3, 64-bit keys
+ * (SPEC.md S:20 SortKey is i64).  Values are always uint32. */
+typedef enum { AHS_I32 = 0, AHS_U32 = 1, AHS_I64 = 2, AHS_U64 = 3 } ahs_dtype;
 
 /* The GPU's three strategies.  The paper's Insertion (n <= 20) and QuickSort
  * branches both run as AHS_GENERAL; ahs_rule keeps which rule fired. */
@@ -84,15 +86,19 @@ typedef enum { AHS_NORM_BUCKETS = 0, AHS_NORM_RANGE = 1 } ahs_entropy_norm;
 #define AHS_FLAG_BUCKETED 4u     /* shift > 0: H is a 2^16-bucket entropy */
 #define AHS_FLAG_SORTED 8u       /* descents = 0 */
 #define AHS_FLAG_STRICT_DESC 16u /* descents = n - 1 (n >= 2) */
-#define AHS_FLAG_SIGNED 32u      /* dtype = AHS_I32 */
+#define AHS_FLAG_SIGNED 32u      /* dtype = AHS_I32 or AHS_I64 */
+#define AHS_FLAG_K_SATURATED 64u /* 64-bit keys spanning the whole range: k = 2^64, reported
+                                    as 2^64 - 1 */
 
 #define AHS_ENTROPY_BITS 16u     /* at most 2^16 histogram bins (reading R1) */
 #define AHS_MAX_N ((1ull << 30) - 1) /* look-back counts are 30-bit */
 
 /* ------------------------------------------------------------------ types */
 /* The state vector v = (n, k, H) of PAPER.md §III.A (line 96) and friends.
- *   min, max   in the key's own signedness (sign-extended for AHS_I32)
- *   k          max - min + 1 (up to 2^32, hence 64-bit)
+ *   min, max   in the key's own signedness (sign-extended for AHS_I32); for
+ *              AHS_U64 the key's bit pattern (reinterpret as uint64)
+ *   k          max - min + 1 (up to 2^32 for 32-bit keys; for 64-bit keys up
+ *              to 2^64, saturated at 2^64 - 1 with AHS_FLAG_K_SATURATED)
  *   bits       bitlen(k - 1); shift = max(0, bits - 16);
  *   nbins      ((k - 1) >> shift) + 1  — histogram bins of (key - min) >> shift
  *   entropy    H = -sum_b p_b log2 p_b over those bins, fp64, clamped to
@@ -131,8 +137,11 @@ AHS_API void ahs_thresholds_default(ahs_thresholds_t *th);
 AHS_API size_t ahs_workspace_bytes(uint64_t n);
 
 /* Device scratch for ahs_sort: a second key buffer (and value buffer when
- * has_vals) plus per-tile look-back status.  Sufficient for every strategy. */
+ * has_vals) plus per-tile look-back status.  Sufficient for every strategy.
+ * ahs_sort_tmp_bytes assumes 32-bit keys; ahs_sort_tmp_bytes_dtype takes the
+ * key type (0 for an invalid dtype). */
 AHS_API size_t ahs_sort_tmp_bytes(uint64_t n, int has_vals);
+AHS_API size_t ahs_sort_tmp_bytes_dtype(uint64_t n, int has_vals, int32_t dtype);
 
 /* Number of 8-bit digit passes ahs_sort will run for this strategy
  * (RADIX: ceil(bits/8) per Eq. 4; GENERAL: 4; COUNTING: 0 keys-only or 1 KV). */
@@ -181,7 +190,8 @@ AHS_API int ahs_sort(const void *d_keys_in, const uint32_t *d_vals_in, void *d_k
  * D2H copy, stream sync.  h_* are host pointers (pinned for full speed);
  * d_scratch (>= ahs_host_scratch_bytes) is carved into the device buffers.
  * feat / strategy / rule may be NULL. */
-AHS_API size_t ahs_host_scratch_bytes(uint64_t n, int has_vals);
+AHS_API size_t ahs_host_scratch_bytes(uint64_t n, int has_vals);                 /* 32-bit keys */
+AHS_API size_t ahs_host_scratch_bytes_dtype(uint64_t n, int has_vals, int32_t dtype); /* any key type */
 AHS_API int ahs_sort_host(const void *h_keys_in, const uint32_t *h_vals_in, void *h_keys_out,
                   uint32_t *h_vals_out, uint64_t n, int32_t dtype, const ahs_thresholds_t *th,
                   void *d_scratch, size_t scratch_bytes, ahs_features_t *feat,

@@ -9,11 +9,13 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "lib", "libahs.so")
 
-AHS_I32, AHS_U32 = 0, 1
+AHS_I32, AHS_U32, AHS_I64, AHS_U64 = 0, 1, 2, 3
 AHS_COUNTING, AHS_RADIX, AHS_GENERAL = 0, 1, 2
 STRATEGY_NAMES = {AHS_COUNTING: "COUNTING", AHS_RADIX: "RADIX", AHS_GENERAL: "GENERAL"}
 RULE_NAMES = {0: "EMPTY", 1: "CONSTANT", 2: "SMALL_N", 3: "SMALL_RANGE", 4: "LOW_ENTROPY", 5: "DEFAULT"}
-FLAG_NAMES = {1: "EMPTY", 2: "CONSTANT", 4: "BUCKETED", 8: "SORTED", 16: "STRICT_DESC", 32: "SIGNED"}
+FLAG_NAMES = {1: "EMPTY", 2: "CONSTANT", 4: "BUCKETED", 8: "SORTED", 16: "STRICT_DESC", 32: "SIGNED",
+              64: "K_SATURATED"}
+FLAG_K_SATURATED = 64
 
 
 class AhsError(RuntimeError):
@@ -31,6 +33,13 @@ class Features(C.Structure):
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
+
+    def key_min(self):
+        """min in the key's own type (uint64 keys: min holds the bit pattern)."""
+        return self.min & 0xFFFFFFFFFFFFFFFF if self.dtype == AHS_U64 else self.min
+
+    def key_max(self):
+        return self.max & 0xFFFFFFFFFFFFFFFF if self.dtype == AHS_U64 else self.max
 
 
 class Thresholds(C.Structure):
@@ -60,6 +69,8 @@ def lib():
             "ahs_thresholds_default": ([C.POINTER(Thresholds)], None),
             "ahs_workspace_bytes": ([u64], sz),
             "ahs_sort_tmp_bytes": ([u64, C.c_int], sz),
+            "ahs_sort_tmp_bytes_dtype": ([u64, C.c_int, i32], sz),
+            "ahs_host_scratch_bytes_dtype": ([u64, C.c_int, i32], sz),
             "ahs_sort_passes": ([C.POINTER(Features), i32, C.c_int], C.c_int),
             "ahs_features": ([vp, u64, i32, vp, sz, C.POINTER(Features), vp], C.c_int),
             "ahs_select": ([C.POINTER(Features), C.POINTER(Thresholds), p_i32, p_i32], C.c_int),
@@ -113,8 +124,14 @@ def ahs_sort_tmp_bytes(n: int, has_vals: bool) -> int:
     return lib().ahs_sort_tmp_bytes(n, int(bool(has_vals)))
 
 
-def ahs_host_scratch_bytes(n: int, has_vals: bool) -> int:
-    return lib().ahs_host_scratch_bytes(n, int(bool(has_vals)))
+def ahs_host_scratch_bytes(n: int, has_vals: bool, key_dtype=None) -> int:
+    if key_dtype is None:
+        return lib().ahs_host_scratch_bytes(n, int(bool(has_vals)))
+    return lib().ahs_host_scratch_bytes_dtype(n, int(bool(has_vals)), _code_of(key_dtype))
+
+
+def ahs_sort_tmp_bytes_dtype(n: int, has_vals: bool, key_dtype) -> int:
+    return lib().ahs_sort_tmp_bytes_dtype(n, int(bool(has_vals)), _code_of(key_dtype))
 
 
 def ahs_sort_passes(feat: Features, strategy: int, has_vals: bool) -> int:
@@ -192,13 +209,21 @@ def _torch():
     return torch
 
 
+def _code_of(dt) -> int:
+    """ahs dtype code of a torch / numpy dtype (or an ahs code)."""
+    if isinstance(dt, int):
+        if dt in (AHS_I32, AHS_U32, AHS_I64, AHS_U64):
+            return dt
+        raise TypeError(f"not an ahs dtype code: {dt}")
+    name = str(dt).replace("torch.", "")
+    codes = {"int32": AHS_I32, "uint32": AHS_U32, "int64": AHS_I64, "uint64": AHS_U64}
+    if name not in codes:  # PAPER.md P:409 integer keys; 64-bit per S:20 (NEXT-3)
+        raise TypeError(f"keys must be int32, uint32, int64 or uint64, got {dt}")
+    return codes[name]
+
+
 def _dtype_code(t) -> int:
-    torch = _torch()
-    if t.dtype == torch.int32:
-        return AHS_I32
-    if t.dtype == torch.uint32:
-        return AHS_U32
-    raise TypeError(f"keys must be int32 or uint32 (PAPER.md P:409 integer-only), got {t.dtype}")
+    return _code_of(t.dtype)
 
 
 def _dev_ptr(t):
@@ -221,12 +246,14 @@ def _stream(stream):
 class Workspace:
     """Device buffers for one n: ws (features) and tmp (sort), owned by torch."""
 
-    def __init__(self, n: int, has_vals: bool, device=None):
+    def __init__(self, n: int, has_vals: bool, device=None, key_dtype=None):
         torch = _torch()
         device = device or torch.device("cuda", torch.cuda.current_device())
         self.n, self.has_vals = n, has_vals
         self.ws_bytes = ahs_workspace_bytes(n)
-        self.tmp_bytes = ahs_sort_tmp_bytes(n, has_vals)
+        # key_dtype: None = 32-bit keys; else a torch / numpy dtype or ahs code (64-bit keys need more)
+        self.tmp_bytes = (ahs_sort_tmp_bytes(n, has_vals) if key_dtype is None
+                          else ahs_sort_tmp_bytes_dtype(n, has_vals, key_dtype))
         self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=device)
         self.tmp = torch.empty(self.tmp_bytes, dtype=torch.uint8, device=device)
 
@@ -263,7 +290,7 @@ def sort(keys, vals=None, th: Thresholds | None = None, ws: Workspace | None = N
     torch = _torch()
     n = keys.numel()
     if ws is None:
-        ws = Workspace(n, vals is not None, keys.device)
+        ws = Workspace(n, vals is not None, keys.device, key_dtype=keys.dtype)
     feat = ahs_features(keys, ws, stream)
     strategy, rule = ahs_select(feat, th)
     if out is None:
@@ -286,12 +313,7 @@ def ahs_sort_host(keys: np.ndarray, vals: np.ndarray | None, keys_out: np.ndarra
         return C.c_void_p(a.data_ptr())
 
     def code(a):
-        dt = str(a.dtype)
-        if "uint32" in dt:
-            return AHS_U32
-        if "int32" in dt:
-            return AHS_I32
-        raise TypeError(f"keys must be int32 or uint32, got {dt}")
+        return _code_of(a.dtype)
 
     n = keys.size if isinstance(keys, np.ndarray) else keys.numel()
     f = Features()

@@ -28,11 +28,12 @@ struct DevInfo {
     int sms = 0;
     int hist_clusters = 0;  // co-resident K2 clusters
     // K6 variants: [kv][rank mode]
-    const void *os_fn[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
-    size_t os_smem[2][2] = {{0, 0}, {0, 0}};
-    int os_tile[2][2] = {{0, 0}, {0, 0}};
-    int os_per_sm[2][2] = {{0, 0}, {0, 0}};  // co-resident CTAs per SM
-    int os_block[2][2] = {{0, 0}, {0, 0}};
+    // K6 variants [key width: 0 = 32-bit, 1 = 64-bit][kv][rank mode]
+    const void *os_fn[2][2][2] = {};
+    size_t os_smem[2][2][2] = {};
+    int os_tile[2][2][2] = {};
+    int os_per_sm[2][2][2] = {};  // co-resident CTAs per SM
+    int os_block[2][2][2] = {};
     bool lane_order_ok = false;              // self-test of the ordered ranking passed
     int ent_grid = 0;                        // K8 cooperative grid
     int rank_mode = kRankMasked;
@@ -41,6 +42,7 @@ std::mutex g_dev_mu;
 DevInfo g_dev[64];
 
 #define K2_KERNEL k_feat_hist<kHistBlock, kHistCluster>
+#define K2_KERNEL64 k_feat_hist<kHistBlock, kHistCluster, uint64_t>
 __device__ uint32_t g_selftest_bad;
 
 // Runs k_lane_order_selftest on a private stream; true iff no violation.
@@ -90,6 +92,10 @@ int device_info(int *sms, int *hist_clusters = nullptr, DevInfo **info = nullptr
                                          kHistSmemBytes) == cudaSuccess;
             good &= cudaFuncSetAttribute(k_feat_reduce<kReduceBlock>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          kReduceSmem) == cudaSuccess;
+            good &= cudaFuncSetAttribute(K2_KERNEL64, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kHistSmemBytes) == cudaSuccess;
+            good &= cudaFuncSetAttribute(k_feat_reduce64<kReduceBlock>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kReduceSmem) == cudaSuccess;
             if (good) {
                 cudaLaunchConfig_t cfg = {};
                 cfg.gridDim = dim3(kHistCluster * 128);
@@ -109,33 +115,33 @@ int device_info(int *sms, int *hist_clusters = nullptr, DevInfo **info = nullptr
                 }
                 d.hist_clusters = nc;
             }
-            d.os_fn[0][kRankMasked] = (const void *)K6_KEYS_M;
-            d.os_fn[1][kRankMasked] = (const void *)K6_PAIRS_M;
-            d.os_fn[0][kRankOrdered] = (const void *)K6_KEYS_O;
-            d.os_fn[1][kRankOrdered] = (const void *)K6_PAIRS_O;
-            d.os_smem[0][kRankMasked] = OsKeysM::kSmem;
-            d.os_smem[1][kRankMasked] = OsPairsM::kSmem;
-            d.os_smem[0][kRankOrdered] = OsKeysO::kSmem;
-            d.os_smem[1][kRankOrdered] = OsPairsO::kSmem;
-            d.os_tile[0][kRankMasked] = OsKeysM::kTile;
-            d.os_tile[1][kRankMasked] = OsPairsM::kTile;
-            d.os_tile[0][kRankOrdered] = OsKeysO::kTile;
-            d.os_tile[1][kRankOrdered] = OsPairsO::kTile;
-            d.os_block[0][kRankMasked] = kSortBlock;
-            d.os_block[1][kRankMasked] = kSortBlock;
-            d.os_block[0][kRankOrdered] = kSortBlock;
-            d.os_block[1][kRankOrdered] = kSortBlockPairsO;
-            for (int kv = 0; kv < 2; kv++)
-                for (int m = 0; m < 2; m++) {
-                    // persistent K6 grids: co-resident CTAs per SM
-                    good &= cudaFuncSetAttribute(d.os_fn[kv][m], cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)d.os_smem[kv][m]) == cudaSuccess;
-                    if (good)
-                        good &= cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.os_per_sm[kv][m], d.os_fn[kv][m],
-                                                                              d.os_block[kv][m],
-                                                                              d.os_smem[kv][m]) == cudaSuccess;
-                    good &= d.os_per_sm[kv][m] > 0;
-                }
+            auto set_k6 = [&](int w, int kv, int m, const void *fn, size_t smem, int tile, int block) {
+                d.os_fn[w][kv][m] = fn;
+                d.os_smem[w][kv][m] = smem;
+                d.os_tile[w][kv][m] = tile;
+                d.os_block[w][kv][m] = block;
+            };
+            set_k6(0, 0, kRankMasked, (const void *)K6_KEYS_M, OsKeysM::kSmem, OsKeysM::kTile, kSortBlock);
+            set_k6(0, 1, kRankMasked, (const void *)K6_PAIRS_M, OsPairsM::kSmem, OsPairsM::kTile, kSortBlock);
+            set_k6(0, 0, kRankOrdered, (const void *)K6_KEYS_O, OsKeysO::kSmem, OsKeysO::kTile, kSortBlock);
+            set_k6(0, 1, kRankOrdered, (const void *)K6_PAIRS_O, OsPairsO::kSmem, OsPairsO::kTile, kSortBlockPairsO);
+            set_k6(1, 0, kRankMasked, (const void *)K6W_KEYS_M, OsKeys64M::kSmem, OsKeys64M::kTile, kSortBlock);
+            set_k6(1, 1, kRankMasked, (const void *)K6W_PAIRS_M, OsPairs64M::kSmem, OsPairs64M::kTile, kSortBlock);
+            set_k6(1, 0, kRankOrdered, (const void *)K6W_KEYS_O, OsKeys64O::kSmem, OsKeys64O::kTile, kSortBlock);
+            set_k6(1, 1, kRankOrdered, (const void *)K6W_PAIRS_O, OsPairs64O::kSmem, OsPairs64O::kTile,
+                   kSortBlockPairsO);
+            for (int w = 0; w < 2; w++)
+                for (int kv = 0; kv < 2; kv++)
+                    for (int m = 0; m < 2; m++) {
+                        // persistent K6 grids: co-resident CTAs per SM
+                        good &= cudaFuncSetAttribute(d.os_fn[w][kv][m], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                     (int)d.os_smem[w][kv][m]) == cudaSuccess;
+                        if (good)
+                            good &= cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                                        &d.os_per_sm[w][kv][m], d.os_fn[w][kv][m], d.os_block[w][kv][m],
+                                        d.os_smem[w][kv][m]) == cudaSuccess;
+                        good &= d.os_per_sm[w][kv][m] > 0;
+                    }
             // The ordered ranking is used only if the device serves the lanes of
             // one shared atomic instruction in lane order (onesweep.cuh), checked
             // here once per device; AHS_RANK=masked forces the masked ranking.
@@ -178,12 +184,13 @@ enum KernelId {
     KID_COUNT_SCATTER_KV,
     KID_ENTROPY_SORTED,
     KID_HIST_SCAN,
+    KID_DIGIT_COUNT,
     KID_COUNT
 };
 const char *kKernelNames[KID_COUNT] = {"feat_reduce", "feat_hist",   "feat_finalize",
                                        "radix_hist",  "onesweep",    "onesweep_kv",
                                        "count_fill",  "count_scatter_kv", "entropy_sorted",
-                                       "hist_scan"};
+                                       "hist_scan",   "digit_count64"};
 
 std::atomic<uint64_t> g_launches{0};
 // NEXT-1 trivial-pass skipping (default on; AHS_SKIP_TRIVIAL=0 or ahs_set_skip_trivial(0) turn it off)
@@ -266,7 +273,7 @@ WsLayout ws_layout()
     L.feat = o;
     o += align_up(sizeof(DevFeatures), 256);
     L.partials = o;
-    o += align_up(sizeof(Partial) * kMaxReduceBlocks, 256);
+    o += align_up(sizeof(Partial64) * kMaxReduceBlocks, 256);  // 32- or 64-bit partials
     L.fctrl = o;
     o += align_up(sizeof(FinalCtrl), 256);
     L.ovf = o;
@@ -288,33 +295,46 @@ WsLayout ws_layout()
 }
 
 // ------------------------------------------------------------ tmp layout
+// [ctrl: digit histograms, bucket bases (kMaxPasses x 256 u32 each), 256 B of
+//  tickets (passes 0..7, K5 at [8]) and the pass plan (at [16], kMaxPasses + 2
+//  words)] [look-back status: two regions, used by alternate passes]
+// [second key buffer (n x key bytes)] [second value buffer]
+// The ctrl block sits at offset 0 whatever n and the key width.
 struct TmpLayout {
-    size_t keys, vals, ctrl, dhist, bucket, ticket, status, status_bytes, total;
+    size_t ctrl, dhist, bucket, ticket, status, status_region_bytes, keys, vals, total;
 };
-constexpr int kStatusWordsPerTile = 4 * kBins;  // up to 4 passes
-TmpLayout tmp_layout(uint64_t n, int has_vals)
+constexpr int kTicketPlan = 16;  // plan offset in the ticket block (words)
+TmpLayout tmp_layout(uint64_t n, int has_vals, size_t key_bytes = 4)
 {
     TmpLayout L;
     size_t o = 0;
-    L.keys = o;
-    o += align_up(n * 4, 256);
-    L.vals = o;
-    if (has_vals) o += align_up(n * 4, 256);
     L.ctrl = o;
     L.dhist = o;
-    L.bucket = o + 4 * 256 * 4;
-    L.ticket = o + 2 * 4 * 256 * 4;  // 8 tickets
-    o += 2 * 4 * 256 * 4 + 256;
+    L.bucket = o + (size_t)kMaxPasses * 256 * 4;
+    L.ticket = o + 2 * (size_t)kMaxPasses * 256 * 4;
+    o += 2 * (size_t)kMaxPasses * 256 * 4 + 256;
     L.status = o;
     const uint64_t tiles = (n + kMinTile - 1) / kMinTile;
-    L.status_bytes = (size_t)tiles * kStatusWordsPerTile * 4;
-    o += align_up(L.status_bytes, 256);
+    L.status_region_bytes = align_up((size_t)tiles * kBins * 4, 256);
+    o += 2 * L.status_region_bytes;
+    L.keys = o;
+    o += align_up(n * key_bytes, 256);
+    L.vals = o;
+    if (has_vals) o += align_up(n * 4, 256);
     L.total = o;
     return L;
 }
 
+inline bool dtype_valid(int32_t dtype)
+{
+    return dtype == AHS_I32 || dtype == AHS_U32 || dtype == AHS_I64 || dtype == AHS_U64;
+}
+inline bool dtype_wide(int32_t dtype) { return dtype == AHS_I64 || dtype == AHS_U64; }
+inline size_t key_bytes_of(int32_t dtype) { return dtype_wide(dtype) ? 8 : 4; }
 inline uint32_t flip_of(int32_t dtype) { return dtype == AHS_I32 ? 0x80000000u : 0u; }
+inline uint64_t flip64_of(int32_t dtype) { return dtype == AHS_I64 ? 0x8000000000000000ull : 0ull; }
 inline uint32_t umin_of(const ahs_features_t *f) { return (uint32_t)f->min ^ flip_of((int32_t)f->dtype); }
+inline uint64_t umin64_of(const ahs_features_t *f) { return (uint64_t)f->min ^ flip64_of((int32_t)f->dtype); }
 
 bool thresholds_valid(const ahs_thresholds_t *th)
 {
@@ -366,12 +386,17 @@ size_t ahs_workspace_bytes(uint64_t) { return ws_layout().total; }
 
 size_t ahs_sort_tmp_bytes(uint64_t n, int has_vals) { return tmp_layout(n, has_vals).total; }
 
+size_t ahs_sort_tmp_bytes_dtype(uint64_t n, int has_vals, int32_t dtype)
+{
+    return dtype_valid(dtype) ? tmp_layout(n, has_vals, key_bytes_of(dtype)).total : 0;
+}
+
 int ahs_sort_passes(const ahs_features_t *f, int32_t strategy, int has_vals)
 {
     if (!f) return AHS_EINVAL;
     if (f->n == 0 || f->k <= 1) return 0;
     switch (strategy) {
-    case AHS_GENERAL: return 4;
+    case AHS_GENERAL: return dtype_wide((int32_t)f->dtype) ? 8 : 4;
     case AHS_RADIX: return radix_passes(f->bits);
     case AHS_COUNTING:
         if (f->shift > 0) return radix_passes(f->bits);
@@ -410,17 +435,19 @@ int ahs_set_skip_trivial(int on)
 
 int ahs_sort_executed_passes(const void *d_tmp, size_t tmp_bytes, uint64_t n, int has_vals, void *stream)
 {
-    const TmpLayout TL = tmp_layout(n, has_vals);
-    if (!d_tmp || tmp_bytes < TL.total) return AHS_EINVAL;
-    uint32_t w[6];
+    (void)n;
+    (void)has_vals;
+    const TmpLayout TL = tmp_layout(0, 0);  // the ctrl block does not depend on n or the key width
+    if (!d_tmp || tmp_bytes < TL.status) return AHS_EINVAL;
+    uint32_t w[kMaxPasses + 2];
     cudaStream_t s = (cudaStream_t)stream;
-    if (cudaMemcpyAsync(w, (const char *)d_tmp + TL.ticket + 8 * 4, sizeof(w), cudaMemcpyDeviceToHost, s) !=
-            cudaSuccess ||
+    if (cudaMemcpyAsync(w, (const char *)d_tmp + TL.ticket + kTicketPlan * 4, sizeof(w), cudaMemcpyDeviceToHost,
+                        s) != cudaSuccess ||
         cudaStreamSynchronize(s) != cudaSuccess) {
         cudaGetLastError();
         return AHS_ECUDA;
     }
-    return w[5] == kPlanMagic ? (int)w[4] : -1;
+    return w[kMaxPasses + 1] == kPlanMagic ? (int)w[kMaxPasses] : -1;
 }
 
 int ahs_lane_order_ok(void)
@@ -474,18 +501,20 @@ int ahs_profile_read(double *ms, uint64_t *launches, int n_ids)
 int ahs_features(const void *d_keys, uint64_t n, int32_t dtype, void *d_ws, size_t ws_bytes,
                  ahs_features_t *feat, void *stream)
 {
-    if (!feat || (dtype != AHS_I32 && dtype != AHS_U32)) return AHS_EINVAL;
+    if (!feat || !dtype_valid(dtype)) return AHS_EINVAL;
     std::memset(feat, 0, sizeof(*feat));
     feat->n = n;
     feat->dtype = (uint32_t)dtype;
     feat->entropy_bits = AHS_ENTROPY_BITS;
-    if (dtype == AHS_I32) feat->flags |= AHS_FLAG_SIGNED;
+    if (dtype == AHS_I32 || dtype == AHS_I64) feat->flags |= AHS_FLAG_SIGNED;
+    const bool wide = dtype_wide(dtype);
     if (n == 0) {  // empty input exits in O(1)
         feat->flags |= AHS_FLAG_EMPTY | AHS_FLAG_SORTED;
         return AHS_OK;
     }
     if (n > AHS_MAX_N) return AHS_ERANGE;
-    if (!d_keys || !d_ws || ((uintptr_t)d_keys & 3u) || ((uintptr_t)d_ws & 15u)) return AHS_EINVAL;
+    if (!d_keys || !d_ws || ((uintptr_t)d_keys & (key_bytes_of(dtype) - 1)) || ((uintptr_t)d_ws & 15u))
+        return AHS_EINVAL;
     const WsLayout L = ws_layout();
     if (ws_bytes < L.total) return AHS_ENOSPACE;
     int sms = 0, hclusters = 0;
@@ -503,13 +532,20 @@ int ahs_features(const void *d_keys, uint64_t n, int32_t dtype, void *d_ws, size
     uint32_t *parts = (uint32_t *)(ws + L.parts);
     DevFeatures *dfeat = (DevFeatures *)(ws + L.feat);
 
-    const uint64_t nvec = n / 4;
+    const uint64_t nvec = wide ? n / 2 : n / 4;  // 16-byte vectors
     const uint64_t nch1 = (nvec + kReduceChunk / 16 - 1) / (kReduceChunk / 16);
     const uint64_t g1 = std::max<uint64_t>(1, std::min<uint64_t>(nch1, (uint64_t)sms * 2));
+    const uint64_t *keys64 = (const uint64_t *)d_keys;
+    Partial64 *partials64 = (Partial64 *)(ws + L.partials);
+    const uint64_t flip64 = flip64_of(dtype);
 
     cudaError_t e = launch(KID_FEAT_REDUCE, s, [&] {
-        launch_k(k_feat_reduce<kReduceBlock>, dim3((unsigned)g1), dim3(kReduceBlock), kReduceSmem, s, keys, n,
-                 flip, partials, ovf, kMaxBins, fctrl, (uint32_t *)(ws + L.byte0));
+        if (wide)
+            launch_k(k_feat_reduce64<kReduceBlock>, dim3((unsigned)g1), dim3(kReduceBlock), kReduceSmem, s, keys64,
+                     n, flip64, partials64, ovf, kMaxBins, fctrl, (uint32_t *)(ws + L.byte0));
+        else
+            launch_k(k_feat_reduce<kReduceBlock>, dim3((unsigned)g1), dim3(kReduceBlock), kReduceSmem, s, keys, n,
+                     flip, partials, ovf, kMaxBins, fctrl, (uint32_t *)(ws + L.byte0));
     });
     if (e != cudaSuccess) return AHS_ECUDA;
     // K2: clusters of kHistCluster CTAs, one partial-histogram row per cluster
@@ -517,8 +553,12 @@ int ahs_features(const void *d_keys, uint64_t n, int32_t dtype, void *d_ws, size
     uint64_t rows = (nch2 + kHistCluster - 1) / kHistCluster;
     rows = std::max<uint64_t>(1, std::min<uint64_t>(rows, (uint64_t)std::min(hclusters, kMaxHistRows)));
     e = launch(KID_FEAT_HIST, s, [&] {
-        launch_k(K2_KERNEL, dim3((unsigned)(rows * kHistCluster)), dim3(kHistBlock), kHistSmemBytes, s, keys, n,
-                 flip, (const Partial *)partials, (int)g1, ovf, parts, (uint32_t *)(ws + L.digit1));
+        if (wide)
+            launch_k(K2_KERNEL64, dim3((unsigned)(rows * kHistCluster)), dim3(kHistBlock), kHistSmemBytes, s, keys64,
+                     n, flip64, (const Partial64 *)partials64, (int)g1, ovf, parts, (uint32_t *)(ws + L.digit1));
+        else
+            launch_k(K2_KERNEL, dim3((unsigned)(rows * kHistCluster)), dim3(kHistBlock), kHistSmemBytes, s, keys, n,
+                     flip, (const Partial *)partials, (int)g1, ovf, parts, (uint32_t *)(ws + L.digit1));
     });
     if (e != cudaSuccess) return AHS_ECUDA;
     // the one host sync of the pipeline: K3's last CTA writes the 64-byte
@@ -544,15 +584,20 @@ int ahs_features(const void *d_keys, uint64_t n, int32_t dtype, void *d_ws, size
     }
     const uint64_t seq = ++hfb.seq;
     e = launch(KID_FEAT_FINALIZE, s, [&] {
-        launch_k(k_feat_finalize<kFinalBlock, kFinalGroups>, dim3(kFinalGrid), dim3(kFinalBlock), 0, s, n,
-                 (const Partial *)partials, (int)g1, (const uint32_t *)parts, (int)rows, (const uint32_t *)ovf,
-                 hist, fctrl, dfeat, hfb.d, seq);
+        if (wide)
+            launch_k(k_feat_finalize<kFinalBlock, kFinalGroups, uint64_t>, dim3(kFinalGrid), dim3(kFinalBlock), 0,
+                     s, n, (const Partial64 *)partials64, (int)g1, (const uint32_t *)parts, (int)rows,
+                     (const uint32_t *)ovf, hist, fctrl, dfeat, hfb.d, seq);
+        else
+            launch_k(k_feat_finalize<kFinalBlock, kFinalGroups>, dim3(kFinalGrid), dim3(kFinalBlock), 0, s, n,
+                     (const Partial *)partials, (int)g1, (const uint32_t *)parts, (int)rows, (const uint32_t *)ovf,
+                     hist, fctrl, dfeat, hfb.d, seq);
     });
     if (e != cudaSuccess) return AHS_ECUDA;
 
     DevFeatures hf;
     if (hfb.h) {
-        volatile uint64_t *flag = &hfb.h->pad1[1];
+        volatile uint64_t *flag = &hfb.h->seq;
         for (uint32_t spin = 0;; spin++) {
             if (*flag == seq) break;
             if ((spin & 255u) == 255u) {  // the kernel may have failed: stream state
@@ -576,13 +621,22 @@ int ahs_features(const void *d_keys, uint64_t n, int32_t dtype, void *d_ws, size
             return AHS_ECUDA;
         }
     }
-    if (dtype == AHS_I32) {
-        feat->min = (int64_t)(int32_t)(hf.umin ^ 0x80000000u);
-        feat->max = (int64_t)(int32_t)(hf.umax ^ 0x80000000u);
-    } else {
+    // min / max from the ordered images: the key's value (uint64: its bit pattern)
+    switch (dtype) {
+    case AHS_I32:
+        feat->min = (int64_t)(int32_t)((uint32_t)hf.umin ^ 0x80000000u);
+        feat->max = (int64_t)(int32_t)((uint32_t)hf.umax ^ 0x80000000u);
+        break;
+    case AHS_I64:
+        feat->min = (int64_t)(hf.umin ^ 0x8000000000000000ull);
+        feat->max = (int64_t)(hf.umax ^ 0x8000000000000000ull);
+        break;
+    default:
         feat->min = (int64_t)hf.umin;
         feat->max = (int64_t)hf.umax;
+        break;
     }
+    if (hf.ksat) feat->flags |= AHS_FLAG_K_SATURATED;
     feat->k = hf.k;
     feat->bits = hf.bits;
     feat->shift = hf.shift;
@@ -649,36 +703,30 @@ int ahs_select(const ahs_features_t *f, const ahs_thresholds_t *th, int32_t *str
 }
 
 // ------------------------------------------------------------------- sort
-int ahs_sort(const void *d_keys_in, const uint32_t *d_vals_in, void *d_keys_out, uint32_t *d_vals_out,
-             uint64_t n, int32_t strategy, const ahs_features_t *feat, void *d_ws, size_t ws_bytes,
-             void *d_tmp, size_t tmp_bytes, void *stream)
+}  // extern "C"
+
+namespace {
+// The digit passes of ahs_sort for key type K (uint32_t, or uint64_t: NEXT-3).
+template <typename K>
+int sort_impl(const K *kin, const uint32_t *d_vals_in, K *kout, uint32_t *d_vals_out, uint64_t n, int32_t strategy,
+              const ahs_features_t *feat, void *d_ws, size_t ws_bytes, void *d_tmp, size_t tmp_bytes,
+              cudaStream_t s)
 {
-    if (!feat) return AHS_EINVAL;
-    if (strategy != AHS_COUNTING && strategy != AHS_RADIX && strategy != AHS_GENERAL) return AHS_EINVAL;
-    if (feat->n != n) return AHS_EFEAT;
-    if (n == 0) return AHS_OK;
-    if (n > AHS_MAX_N) return AHS_ERANGE;
+    constexpr bool kWide = sizeof(K) == 8;
+    constexpr int W = kWide ? 1 : 0;
     const int32_t dtype = (int32_t)feat->dtype;
-    if (dtype != AHS_I32 && dtype != AHS_U32) return AHS_EFEAT;
     const bool kv = d_vals_in != nullptr;
-    if (!d_keys_in || !d_keys_out || (kv && !d_vals_out) || ((uintptr_t)d_keys_in & 3u) ||
-        ((uintptr_t)d_keys_out & 3u) || (kv && (((uintptr_t)d_vals_in & 3u) || ((uintptr_t)d_vals_out & 3u))))
-        return AHS_EINVAL;
-    if (feat->k == 0 || feat->k > (1ull << 32) || feat->nbins == 0) return AHS_EFEAT;
     int sms = 0;
     DevInfo *di = nullptr;
     int rc = device_info(&sms, nullptr, &di);
     if (rc) return rc;
-    cudaStream_t s = (cudaStream_t)stream;
-    const uint32_t *kin = (const uint32_t *)d_keys_in;
-    uint32_t *kout = (uint32_t *)d_keys_out;
-    const uint32_t flip = flip_of(dtype);
-    const uint32_t umin = umin_of(feat);
+    const K flip = kWide ? (K)flip64_of(dtype) : (K)flip_of(dtype);
+    const K umin = kWide ? (K)umin64_of(feat) : (K)umin_of(feat);
     const uint32_t n32 = (uint32_t)n;
 
     // constant input: stable identity
     if (feat->k == 1) {
-        if (kout != kin && cudaMemcpyAsync(kout, kin, n * 4, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+        if (kout != kin && cudaMemcpyAsync(kout, kin, n * sizeof(K), cudaMemcpyDeviceToDevice, s) != cudaSuccess)
             return AHS_ECUDA;
         if (kv && d_vals_out != d_vals_in &&
             cudaMemcpyAsync(d_vals_out, d_vals_in, n * 4, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
@@ -693,21 +741,31 @@ int ahs_sort(const void *d_keys_in, const uint32_t *d_vals_in, void *d_keys_out,
         if (!d_ws || ws_bytes < WL.total) return AHS_ENOSPACE;
         const uint32_t *scan = hist_scan(d_ws, feat, s);
         if (!scan) return AHS_ECUDA;
-        const uint64_t nvec = n / 4;
-        uint64_t g = (4 * nvec + kFillChunk - 1) / kFillChunk;
-        g = std::max<uint64_t>(1, g);
-        cudaError_t e = launch(KID_COUNT_FILL, s, [&] {
-            launch_k(k_count_fill, dim3((unsigned)g), dim3(kFillBlock), 0, s, kout, n32, scan, feat->nbins, flip,
-                     umin);
-        });
+        cudaError_t e;
+        if constexpr (kWide) {
+            const uint64_t g = std::max<uint64_t>(1, std::min<uint64_t>((n + kFill64Block - 1) / kFill64Block,
+                                                                        (uint64_t)sms * 8));
+            e = launch(KID_COUNT_FILL, s, [&] {
+                launch_k(k_count_fill64, dim3((unsigned)g), dim3(kFill64Block), 0, s, kout, n32, scan, feat->nbins,
+                         flip, umin);
+            });
+        } else {
+            const uint64_t nvec = n / 4;
+            uint64_t g = (4 * nvec + kFillChunk - 1) / kFillChunk;
+            g = std::max<uint64_t>(1, g);
+            e = launch(KID_COUNT_FILL, s, [&] {
+                launch_k(k_count_fill, dim3((unsigned)g), dim3(kFillBlock), 0, s, kout, n32, scan, feat->nbins, flip,
+                         umin);
+            });
+        }
         return e == cudaSuccess ? AHS_OK : AHS_ECUDA;
     }
 
     // ---- digit passes: plan
-    const TmpLayout TL = tmp_layout(n, kv);
+    const TmpLayout TL = tmp_layout(n, kv, sizeof(K));
     if (!d_tmp || tmp_bytes < TL.total || ((uintptr_t)d_tmp & 255u)) return AHS_ENOSPACE;
     char *tmp = (char *)d_tmp;
-    uint32_t *tkeys = (uint32_t *)(tmp + TL.keys);
+    K *tkeys = (K *)(tmp + TL.keys);
     uint32_t *tvals = kv ? (uint32_t *)(tmp + TL.vals) : nullptr;
     uint32_t *dhist = (uint32_t *)(tmp + TL.dhist);
     uint32_t *bucket = (uint32_t *)(tmp + TL.bucket);
@@ -716,37 +774,31 @@ int ahs_sort(const void *d_keys_in, const uint32_t *d_vals_in, void *d_keys_out,
 
     const bool count_kv = strategy == AHS_COUNTING && exact_hist && kv && feat->bits <= 8;
     int passes;
-    uint32_t sub;
-    if (count_kv) {
-        passes = 1;
-        sub = umin;
-    } else if (strategy == AHS_GENERAL) {
-        passes = 4;  // full width; on key - min (same order, lets K5 reuse the feature histogram)
-        sub = umin;
-    } else {  // RADIX, or COUNTING that cannot use the histogram directly
-        passes = radix_passes(feat->bits);
-        sub = umin;
-    }
+    if (count_kv) passes = 1;
+    else if (strategy == AHS_GENERAL) passes = kWide ? 8 : 4;  // full width, on key - min (R14)
+    else passes = radix_passes(feat->bits);                     // RADIX, or COUNTING without the histogram
 
-    // zero control words + the status of every pass (one memset)
+    // zero the control words and both status regions (one memset); passes
+    // alternate between the regions, each clearing the previous pass's
     const int mode = di->rank_mode;
-    const uint64_t tile = (uint64_t)di->os_tile[kv][mode];
+    const uint64_t tile = (uint64_t)di->os_tile[W][kv][mode];
     const uint64_t tiles = (n + tile - 1) / tile;
-    const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)sms * di->os_per_sm[kv][mode]);
-    const void *k6 = di->os_fn[kv][mode];
-    const size_t k6_smem = di->os_smem[kv][mode];
+    const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)sms * di->os_per_sm[W][kv][mode]);
+    const void *k6 = di->os_fn[W][kv][mode];
+    const size_t k6_smem = di->os_smem[W][kv][mode];
     const size_t status_words_per_pass = (size_t)tiles * kBins;
-    const size_t zero_bytes = (TL.status - TL.ctrl) + status_words_per_pass * 4 * passes;
+    const size_t zero_bytes = (TL.status - TL.ctrl) + status_words_per_pass * 4 * (passes > 1 ? 2 : 1);
     if (cudaMemsetAsync(tmp + TL.ctrl, 0, zero_bytes, s) != cudaSuccess) return AHS_ECUDA;
 
     // in place with an odd pass count: stream the input to tmp first.  In place,
     // the pass count (and so the buffer parity) must be known here: no skipping.
-    const uint32_t *src_k = kin;
+    const K *src_k = kin;
     const uint32_t *src_v = d_vals_in;
-    const bool inplace = (const void *)kout == d_keys_in || (kv && (const void *)d_vals_out == d_vals_in);
+    const bool inplace = kout == kin || (kv && d_vals_out == d_vals_in);
     const bool skip = !inplace && g_skip_trivial.load() && !count_kv;
     if (inplace && (passes & 1)) {
-        if (cudaMemcpyAsync(tkeys, kin, n * 4, cudaMemcpyDeviceToDevice, s) != cudaSuccess) return AHS_ECUDA;
+        if (cudaMemcpyAsync(tkeys, kin, n * sizeof(K), cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+            return AHS_ECUDA;
         if (kv && cudaMemcpyAsync(tvals, d_vals_in, n * 4, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
             return AHS_ECUDA;
         src_k = tkeys;
@@ -754,7 +806,7 @@ int ahs_sort(const void *d_keys_in, const uint32_t *d_vals_in, void *d_keys_out,
     }
 
     if (!d_ws || ws_bytes < WL.total) return AHS_ENOSPACE;
-    uint32_t *plan = tickets + 8;
+    uint32_t *plan = tickets + kTicketPlan;
     const uint32_t *bases;
     if (count_kv) {
         bases = hist_scan(d_ws, feat, s);
@@ -762,19 +814,33 @@ int ahs_sort(const void *d_keys_in, const uint32_t *d_vals_in, void *d_keys_out,
     } else {
         const char *wsc = (const char *)d_ws;
         const uint32_t *fhist = (const uint32_t *)(wsc + WL.hist);
+        cudaError_t e = cudaSuccess;
+        if constexpr (kWide) {
+            // K5b: digits 2 .. below the feature buckets come from the keys
+            const int p1 = std::min(passes, (int)((feat->shift + 7) / 8));
+            if (p1 > 2) {
+                const uint64_t g = std::max<uint64_t>(
+                    1, std::min<uint64_t>((n + kDC64Block - 1) / kDC64Block, (uint64_t)sms * 4));
+                e = launch(KID_DIGIT_COUNT, s, [&] {
+                    launch_k(k_digit_count64<kDC64Block>, dim3((unsigned)g), dim3(kDC64Block), 0, s,
+                             (const uint64_t *)src_k, n, (uint64_t)(umin - flip), 2, p1, dhist);
+                });
+                if (e != cudaSuccess) return AHS_ECUDA;
+            }
+        }
         const uint64_t g5 = std::max<uint64_t>(2 * kRowCtas, ((uint64_t)feat->nbins + kRHBlock - 1) / kRHBlock);
-        cudaError_t e = launch(KID_RADIX_HIST, s, [&] {
-            launch_k(k_radix_hist<kRHBlock>, dim3((unsigned)g5), dim3(kRHBlock), 0, s, n, sub, passes, fhist,
-                     feat->nbins, feat->shift, (const DevFeatures *)(wsc + WL.feat),
+        e = launch(KID_RADIX_HIST, s, [&] {
+            launch_k(k_radix_hist<kRHBlock, kWide ? 8 : 4>, dim3((unsigned)g5), dim3(kRHBlock), 0, s, n,
+                     (uint32_t)umin, passes, fhist, feat->nbins, feat->shift, (const DevFeatures *)(wsc + WL.feat),
                      (const uint32_t *)(wsc + WL.byte0), (const uint32_t *)(wsc + WL.digit1), dhist, bucket,
-                     tickets + 7, plan, skip ? 1 : 0);
+                     tickets + kMaxPasses, plan, skip ? 1 : 0);
         });
         if (e != cudaSuccess) return AHS_ECUDA;
         bases = bucket;
     }
 
     for (int p = 0; p < passes; p++) {
-        PassArgs pa;
+        PassArgsT<K> pa;
         pa.keys_in = src_k;
         pa.vals_in = kv ? src_v : nullptr;
         pa.keys_out = kout;
@@ -786,21 +852,51 @@ int ahs_sort(const void *d_keys_in, const uint32_t *d_vals_in, void *d_keys_out,
         pa.npasses = (uint32_t)passes;
         pa.shift = count_kv ? 0u : 8u * (uint32_t)p;
         pa.flip = flip;
-        pa.sub = sub;
+        pa.sub = umin;
         pa.bucket_base = count_kv ? bases : bases + 256 * p;
-        pa.status = status + (size_t)p * status_words_per_pass;
+        // regions [0, spw) and [spw, 2 spw) of this sort's tile count: both inside the memset
+        pa.status = status + (size_t)(p & 1) * status_words_per_pass;
         pa.ticket = tickets + p;
         pa.plan = count_kv ? nullptr : plan;  // K5's plan (no skipping when not enabled)
+        pa.status_clear = p > 0 ? status + (size_t)((p - 1) & 1) * status_words_per_pass : nullptr;
+        pa.clear_words = p > 0 && p + 1 < passes ? (uint32_t)status_words_per_pass : 0u;
         void *args[] = {&pa};
         const cudaError_t e = launch(kv ? (count_kv ? KID_COUNT_SCATTER_KV : KID_ONESWEEP_KV) : KID_ONESWEEP, s, [&] {
             cudaLaunchConfig_t cfg;
             cudaLaunchAttribute attr[1];
-            pdl_config(cfg, attr, dim3(grid), dim3(di->os_block[kv][mode]), k6_smem, s);
+            pdl_config(cfg, attr, dim3(grid), dim3(di->os_block[W][kv][mode]), k6_smem, s);
             cudaLaunchKernelExC(&cfg, k6, args);
         });
         if (e != cudaSuccess) return AHS_ECUDA;
     }
     return AHS_OK;
+}
+}  // namespace
+
+extern "C" {
+int ahs_sort(const void *d_keys_in, const uint32_t *d_vals_in, void *d_keys_out, uint32_t *d_vals_out,
+             uint64_t n, int32_t strategy, const ahs_features_t *feat, void *d_ws, size_t ws_bytes,
+             void *d_tmp, size_t tmp_bytes, void *stream)
+{
+    if (!feat) return AHS_EINVAL;
+    if (strategy != AHS_COUNTING && strategy != AHS_RADIX && strategy != AHS_GENERAL) return AHS_EINVAL;
+    if (feat->n != n) return AHS_EFEAT;
+    if (n == 0) return AHS_OK;
+    if (n > AHS_MAX_N) return AHS_ERANGE;
+    const int32_t dtype = (int32_t)feat->dtype;
+    if (!dtype_valid(dtype)) return AHS_EFEAT;
+    const bool kv = d_vals_in != nullptr;
+    const uintptr_t kal = key_bytes_of(dtype) - 1;
+    if (!d_keys_in || !d_keys_out || (kv && !d_vals_out) || ((uintptr_t)d_keys_in & kal) ||
+        ((uintptr_t)d_keys_out & kal) || (kv && (((uintptr_t)d_vals_in & 3u) || ((uintptr_t)d_vals_out & 3u))))
+        return AHS_EINVAL;
+    if (feat->k == 0 || feat->nbins == 0 || (!dtype_wide(dtype) && feat->k > (1ull << 32))) return AHS_EFEAT;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (dtype_wide(dtype))
+        return sort_impl<uint64_t>((const uint64_t *)d_keys_in, d_vals_in, (uint64_t *)d_keys_out, d_vals_out, n,
+                                   strategy, feat, d_ws, ws_bytes, d_tmp, tmp_bytes, s);
+    return sort_impl<uint32_t>((const uint32_t *)d_keys_in, d_vals_in, (uint32_t *)d_keys_out, d_vals_out, n,
+                               strategy, feat, d_ws, ws_bytes, d_tmp, tmp_bytes, s);
 }
 
 // ------------------------------------------------------------ NEXT-2
@@ -845,21 +941,26 @@ int ahs_entropy_sorted(const void *d_keys, uint64_t n, void *d_ws, size_t ws_byt
 }
 
 // -------------------------------------------------------------- host e2e
-size_t ahs_host_scratch_bytes(uint64_t n, int has_vals)
+size_t ahs_host_scratch_bytes_dtype(uint64_t n, int has_vals, int32_t dtype)
 {
-    const size_t kb = align_up(n * 4, 256);
-    return kb * (has_vals ? 4 : 2) + ws_layout().total + tmp_layout(n, has_vals).total;
+    if (!dtype_valid(dtype)) return 0;
+    const size_t kbytes = key_bytes_of(dtype);
+    const size_t kb = align_up(n * kbytes, 256), vb = align_up(n * 4, 256);
+    return 2 * kb + (has_vals ? 2 * vb : 0) + ws_layout().total + tmp_layout(n, has_vals, kbytes).total;
 }
+
+size_t ahs_host_scratch_bytes(uint64_t n, int has_vals) { return ahs_host_scratch_bytes_dtype(n, has_vals, AHS_U32); }
 
 int ahs_sort_host(const void *h_keys_in, const uint32_t *h_vals_in, void *h_keys_out, uint32_t *h_vals_out,
                   uint64_t n, int32_t dtype, const ahs_thresholds_t *th, void *d_scratch, size_t scratch_bytes,
                   ahs_features_t *feat, int32_t *strategy, int32_t *rule, void *stream)
 {
-    if (dtype != AHS_I32 && dtype != AHS_U32) return AHS_EINVAL;
+    if (!dtype_valid(dtype)) return AHS_EINVAL;
     const bool kv = h_vals_in != nullptr;
     if (n > 0 && (!h_keys_in || !h_keys_out || (kv && !h_vals_out) || !d_scratch)) return AHS_EINVAL;
     if (n > AHS_MAX_N) return AHS_ERANGE;
-    if (n > 0 && scratch_bytes < ahs_host_scratch_bytes(n, kv)) return AHS_ENOSPACE;
+    if (n > 0 && scratch_bytes < ahs_host_scratch_bytes_dtype(n, kv, dtype)) return AHS_ENOSPACE;
+    const size_t kbytes = key_bytes_of(dtype);
     if ((uintptr_t)d_scratch & 255u) return AHS_EINVAL;
     cudaStream_t s = (cudaStream_t)stream;
     ahs_features_t f;
@@ -870,7 +971,7 @@ int ahs_sort_host(const void *h_keys_in, const uint32_t *h_vals_in, void *h_keys
         rc = ahs_select(&f, th, &st, &ru);
         if (rc) return rc;
     } else {
-        const size_t kb = align_up(n * 4, 256);
+        const size_t kb = align_up(n * kbytes, 256), vb = align_up(n * 4, 256);
         char *p = (char *)d_scratch;
         void *dk_in = p;
         p += kb;
@@ -879,15 +980,16 @@ int ahs_sort_host(const void *h_keys_in, const uint32_t *h_vals_in, void *h_keys
         uint32_t *dv_in = nullptr, *dv_out = nullptr;
         if (kv) {
             dv_in = (uint32_t *)p;
-            p += kb;
+            p += vb;
             dv_out = (uint32_t *)p;
-            p += kb;
+            p += vb;
         }
         void *ws = p;
         p += ws_layout().total;
         void *tmp = p;
-        const size_t tmpb = tmp_layout(n, kv).total;
-        if (cudaMemcpyAsync(dk_in, h_keys_in, n * 4, cudaMemcpyHostToDevice, s) != cudaSuccess) return AHS_ECUDA;
+        const size_t tmpb = tmp_layout(n, kv, kbytes).total;
+        if (cudaMemcpyAsync(dk_in, h_keys_in, n * kbytes, cudaMemcpyHostToDevice, s) != cudaSuccess)
+            return AHS_ECUDA;
         if (kv && cudaMemcpyAsync(dv_in, h_vals_in, n * 4, cudaMemcpyHostToDevice, s) != cudaSuccess)
             return AHS_ECUDA;
         int rc = ahs_features(dk_in, n, dtype, ws, ws_layout().total, &f, stream);
@@ -896,7 +998,7 @@ int ahs_sort_host(const void *h_keys_in, const uint32_t *h_vals_in, void *h_keys
         if (rc) return rc;
         rc = ahs_sort(dk_in, dv_in, dk_out, dv_out, n, st, &f, ws, ws_layout().total, tmp, tmpb, stream);
         if (rc) return rc;
-        if (cudaMemcpyAsync(h_keys_out, dk_out, n * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+        if (cudaMemcpyAsync(h_keys_out, dk_out, n * kbytes, cudaMemcpyDeviceToHost, s) != cudaSuccess)
             return AHS_ECUDA;
         if (kv && cudaMemcpyAsync(h_vals_out, dv_out, n * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess)
             return AHS_ECUDA;

@@ -18,16 +18,24 @@ struct Partial {
     uint64_t desc;
 };
 
-// Device-side feature record, written by K3 into ws and copied to the host.
+// Device-side feature record, written by K3 into ws and into the host's
+// mapped buffer (seq last).  umin/umax: ordered images (32-bit keys zero-extended).
 struct DevFeatures {
-    uint32_t umin, umax;
+    uint64_t umin, umax;
     uint64_t descents;
-    uint64_t k;
-    uint32_t bits, shift, nb, pad0;  // pad0: K1 CTA count (rows of the low-byte histograms)
+    uint64_t k;                       // saturated at 2^64 - 1 (64-bit keys spanning the range)
+    uint32_t bits, shift, nb, nparts; // nparts: K1 CTA count (rows of the low-byte histograms)
     double entropy;
-    uint64_t pad1[2];                // pad1[0]: K2 CTA count (rows of the digit-1 histograms)
+    uint32_t nrows2, ksat;            // nrows2: K2 CTA count (rows of the digit-1 histograms)
+    uint64_t seq;                     // the host polls this word
 };
-static_assert(sizeof(DevFeatures) == 64, "DevFeatures is 64 bytes");
+static_assert(sizeof(DevFeatures) == 72, "DevFeatures is 72 bytes (9 words, seq last)");
+
+// 64-bit keys (NEXT-3): per-block result of K1 (ordered images)
+struct Partial64 {
+    uint64_t mn, mx;
+    uint64_t desc;
+};
 
 // Derived range quantities (§III.A line 96 k = max - min + 1;
 // DESIGN.md R1: shift = max(0, bitlen(k-1) - 16), nb = ((k-1) >> shift) + 1).
@@ -65,6 +73,29 @@ __device__ __forceinline__ void pdl_begin()
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+// 64-bit keys: k = umax - umin + 1 can be 2^64: reported saturated
+struct Range64 {
+    uint64_t k;
+    uint32_t bits, shift, nb, ksat;
+};
+
+__host__ __device__ __forceinline__ Range64 derive_range64(uint64_t umin, uint64_t umax, uint32_t entropy_bits)
+{
+    Range64 r;
+    const uint64_t km1 = umax - umin;
+    r.ksat = km1 == ~0ull ? 1u : 0u;
+    r.k = r.ksat ? km1 : km1 + 1ull;
+#ifdef __CUDA_ARCH__
+    r.bits = km1 ? 64u - (uint32_t)__clzll((long long)km1) : 0u;
+#else
+    r.bits = 0;
+    while (r.bits < 64 && (km1 >> r.bits)) r.bits++;
+#endif
+    r.shift = r.bits > entropy_bits ? r.bits - entropy_bits : 0u;
+    r.nb = (uint32_t)((km1 >> r.shift) + 1ull);
+    return r;
+}
+
 // ---------------------------------------------------------------- memory ops
 __device__ __forceinline__ uint4 ld_nc_v4(const uint4 *p)
 {
@@ -79,6 +110,13 @@ __device__ __forceinline__ uint32_t ld_nc(const uint32_t *p)
 {
     uint32_t r;
     asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
+    return r;
+}
+
+__device__ __forceinline__ uint64_t ld_nc(const uint64_t *p)
+{
+    uint64_t r;
+    asm("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(r) : "l"(p));
     return r;
 }
 

@@ -139,6 +139,160 @@ __global__ void __launch_bounds__(BLOCK)
     }
 }
 
+// 64-bit keys (NEXT-3): the same pass over uint4 vectors of two keys each
+// (u = key ^ flip, flip = 2^63 for int64); head and tail are at most one key.
+__device__ __forceinline__ VecSplit vec_split64(const uint64_t *p, uint64_t n)
+{
+    VecSplit s;
+    const uint64_t mis = ((16u - ((uintptr_t)p & 15u)) & 15u) >> 3;
+    s.head = mis < n ? mis : n;
+    s.nvec = (n - s.head) >> 1;
+    s.tail0 = s.head + 2ull * s.nvec;
+    return s;
+}
+
+__device__ __forceinline__ uint64_t lo_hi(uint32_t lo, uint32_t hi) { return ((uint64_t)hi << 32) | lo; }
+
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK)
+    k_feat_reduce64(const uint64_t *__restrict__ keys, uint64_t n, uint64_t flip,
+                    Partial64 *__restrict__ partials, uint32_t *__restrict__ zero_words, uint32_t nzero,
+                    FinalCtrl *__restrict__ fctrl, uint32_t *__restrict__ byte0_rows)
+{
+    pdl_begin();
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    __shared__ __align__(8) uint64_t bars[kReduceStages];
+    __shared__ uint32_t s_b0[256];  // raw low byte (digit 0 of key - min up to a rotation), as in K1
+    for (int i = threadIdx.x; i < 256; i += BLOCK) s_b0[i] = 0u;
+    __syncthreads();
+    for (uint32_t i = blockIdx.x * BLOCK + threadIdx.x; i < nzero; i += gridDim.x * BLOCK)
+        zero_words[i] = 0u;
+    if (blockIdx.x == 0 && threadIdx.x == 0) fctrl->barrier = 0u;
+
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const VecSplit sp = vec_split64(keys, n);
+    const uint4 *body = reinterpret_cast<const uint4 *>(keys + sp.head);
+    uint64_t mn = ~0ull, mx = 0ull;
+    uint32_t desc = 0u;
+    stream_chunks<kReduceStages, kReduceChunk>(
+        body, sp.nvec, smem_raw, bars, [&](const uint4 *c, uint32_t nv, uint64_t v0) {
+            for (uint32_t j = threadIdx.x; j < nv; j += BLOCK) {
+                const uint4 x = c[j];
+                const uint64_t a0 = lo_hi(x.x, x.y) ^ flip, a1 = lo_hi(x.z, x.w) ^ flip;
+                bool has_next = true;
+                uint64_t nxt;
+                if (v0 + j + 1 < sp.nvec) {
+                    const uint4 y = c[j + 1];  // in-chunk or the chunk's successor vector
+                    nxt = lo_hi(y.x, y.y) ^ flip;
+                } else {
+                    has_next = sp.tail0 < n;
+                    nxt = has_next ? (keys[sp.tail0] ^ flip) : 0ull;
+                }
+                mn = min(mn, min(a0, a1));
+                mx = max(mx, max(a0, a1));
+                atomicAdd(&s_b0[x.x & 255u], 1u);
+                atomicAdd(&s_b0[x.z & 255u], 1u);
+                desc += (uint32_t)(a0 > a1) + (uint32_t)(has_next && a1 > nxt);
+            }
+        });
+    if (blockIdx.x == 0 && threadIdx.x < 2) {  // unaligned head / tail key
+        const uint64_t i = threadIdx.x == 0 ? 0ull : sp.tail0;
+        const bool act = threadIdx.x == 0 ? sp.head > 0 : sp.tail0 < n;
+        if (act) {
+            const uint64_t a = keys[i] ^ flip;
+            mn = min(mn, a);
+            mx = max(mx, a);
+            atomicAdd(&s_b0[(uint32_t)a & 255u], 1u);
+            if (i + 1 < n) desc += (uint32_t)(a > (keys[i + 1] ^ flip));
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 256; i += BLOCK) byte0_rows[(size_t)blockIdx.x * 256 + i] = s_b0[i];
+    __shared__ uint64_t s_mn[BLOCK / 32], s_mx[BLOCK / 32];
+    __shared__ uint32_t s_d[BLOCK / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        mn = min(mn, __shfl_down_sync(kFull, mn, o));
+        mx = max(mx, __shfl_down_sync(kFull, mx, o));
+    }
+    desc = __reduce_add_sync(kFull, desc);
+    if (lane == 0) {
+        s_mn[warp] = mn;
+        s_mx[warp] = mx;
+        s_d[warp] = desc;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        Partial64 p{~0ull, 0ull, 0ull};
+        for (int w = 0; w < BLOCK / 32; w++) {
+            p.mn = min(p.mn, s_mn[w]);
+            p.mx = max(p.mx, s_mx[w]);
+            p.desc += s_d[w];
+        }
+        partials[blockIdx.x] = p;
+    }
+}
+
+// Reduce the 64-bit K1 partials inside one block (all threads get the result).
+template <int BLOCK>
+__device__ __forceinline__ Partial64 reduce_partials64(const Partial64 *__restrict__ partials, int nparts)
+{
+    __shared__ unsigned long long r_mn[BLOCK / 32], r_mx[BLOCK / 32], r_d[BLOCK / 32];
+    __shared__ Partial64 r_out;
+    unsigned long long mn = ~0ull, mx = 0ull, d = 0ull;
+    for (int i = threadIdx.x; i < nparts; i += BLOCK) {
+        mn = min(mn, (unsigned long long)__ldcg(&partials[i].mn));
+        mx = max(mx, (unsigned long long)__ldcg(&partials[i].mx));
+        d += __ldcg(&partials[i].desc);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        mn = min(mn, __shfl_down_sync(kFull, mn, o));
+        mx = max(mx, __shfl_down_sync(kFull, mx, o));
+        d += __shfl_down_sync(kFull, d, o);
+    }
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    if (lane == 0) {
+        r_mn[warp] = mn;
+        r_mx[warp] = mx;
+        r_d[warp] = d;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        Partial64 p{~0ull, 0ull, 0ull};
+        for (int w = 0; w < BLOCK / 32; w++) {
+            p.mn = min(p.mn, (uint64_t)r_mn[w]);
+            p.mx = max(p.mx, (uint64_t)r_mx[w]);
+            p.desc += r_d[w];
+        }
+        r_out = p;
+    }
+    __syncthreads();
+    return r_out;
+}
+
+// Key-type traits for K2 / K3: partial record, its reduction, the derived range
+template <typename K>
+struct KeyTraits;
+template <>
+struct KeyTraits<uint32_t> {
+    using P = Partial;
+    template <int BLOCK>
+    __device__ static P reduce(const P *p, int n);
+    __device__ static Range64 range(const P &p)
+    {
+        const Range r = derive_range(p.mn, p.mx, 16u);
+        return Range64{r.k, r.bits, r.shift, r.nb, 0u};
+    }
+};
+template <>
+struct KeyTraits<uint64_t> {
+    using P = Partial64;
+    template <int BLOCK>
+    __device__ static P reduce(const P *p, int n);
+    __device__ static Range64 range(const P &p) { return derive_range64(p.mn, p.mx, 16u); }
+};
+
 // Reduce the K1 partials inside one block (all threads get the result).
 template <int BLOCK>
 __device__ __forceinline__ Partial reduce_partials(const Partial *__restrict__ partials, int nparts)
@@ -176,6 +330,17 @@ __device__ __forceinline__ Partial reduce_partials(const Partial *__restrict__ p
     }
     __syncthreads();
     return r_out;
+}
+
+template <int BLOCK>
+__device__ __forceinline__ Partial KeyTraits<uint32_t>::reduce(const Partial *p, int n)
+{
+    return reduce_partials<BLOCK>(p, n);
+}
+template <int BLOCK>
+__device__ __forceinline__ Partial64 KeyTraits<uint64_t>::reduce(const Partial64 *p, int n)
+{
+    return reduce_partials64<BLOCK>(p, n);
 }
 
 // ------------------------------------------------------------------ K2 ----
@@ -287,18 +452,20 @@ struct ThreadCols {
     }
 };
 
-template <int BLOCK, int CL>
+// K: uint32_t, or uint64_t for 64-bit keys (NEXT-3: two keys per uint4, bins
+// (key - min) >> shift with shift <= 48)
+template <int BLOCK, int CL, typename K = uint32_t>
 __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(BLOCK, 1)
-    k_feat_hist(const uint32_t *__restrict__ keys, uint64_t n, uint32_t flip,
-                const Partial *__restrict__ partials, int nparts, uint32_t *__restrict__ ovf,
+    k_feat_hist(const K *__restrict__ keys, uint64_t n, K flip,
+                const typename KeyTraits<K>::P *__restrict__ partials, int nparts, uint32_t *__restrict__ ovf,
                 uint32_t *__restrict__ parts, uint32_t *__restrict__ digit1_rows)
 {
     pdl_begin();
     extern __shared__ __align__(128) uint32_t sh[];
     __shared__ __align__(8) uint64_t bars[kHistStages];
     cg::cluster_group cluster = cg::this_cluster();
-    const Partial p = reduce_partials<BLOCK>(partials, nparts);
-    const Range rg = derive_range(p.mn, p.mx, 16u);
+    const auto p = KeyTraits<K>::template reduce<BLOCK>(partials, nparts);
+    const Range64 rg = KeyTraits<K>::range(p);
     if (rg.nb <= 1u) return;  // k = 1 (uniform for the whole grid): no histogram
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
     const bool packed = rg.nb > kHistWords;
@@ -318,14 +485,17 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(BLOCK, 1)
     for (int i = threadIdx.x; i < 256; i += BLOCK) s_d1[i] = 0u;
     __syncthreads();
 
-    const uint32_t umin = p.mn, shift = rg.shift;
-    const uint32_t c0 = umin - flip;  // (key ^ flip) - umin == key - (umin - flip)  (mod 2^32)
-    const VecSplit sp = vec_split(keys, n);
+    const uint32_t shift = rg.shift;
+    const K c0 = (K)p.mn - flip;  // (key ^ flip) - umin == key - (umin - flip)  (mod 2^32 / 2^64)
+    VecSplit sp;
+    if constexpr (sizeof(K) == 4) sp = vec_split(keys, n);
+    else sp = vec_split64(keys, n);
     const uint4 *body = reinterpret_cast<const uint4 *>(keys + sp.head);
     uint8_t *stage = reinterpret_cast<uint8_t *>(sh) + kHistBins;
     auto run = [&](const auto &add) {
         stream_chunks<kHistStages, kHistChunk>(body, sp.nvec, stage, bars,
                                                [&](const uint4 *c, uint32_t nv, uint64_t) {
+            if constexpr (sizeof(K) == 4) {
             for (uint32_t j0 = 0; j0 < nv; j0 += BLOCK) {  // block-uniform trip count
                 const uint32_t j = j0 + threadIdx.x;
                 const bool act = j < nv;
@@ -339,12 +509,40 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(BLOCK, 1)
                 }
                 hist_vec(add, v, act, shift);
             }
+            } else {
+            // 64-bit keys: a thread takes two consecutive vectors (4 keys), bins computed here
+            for (uint32_t j0 = 0; j0 < nv; j0 += 2 * BLOCK) {  // block-uniform trip count
+                const uint32_t j = j0 + 2 * threadIdx.x;
+                const bool a0 = j < nv, a1 = j + 1 < nv;
+                const uint4 x = a0 ? c[j] : make_uint4(0u, 0u, 0u, 0u);
+                const uint4 y = a1 ? c[j + 1] : make_uint4(0u, 0u, 0u, 0u);
+                const uint64_t v0 = lo_hi(x.x, x.y) - c0, v1 = lo_hi(x.z, x.w) - c0;
+                const uint64_t v2 = lo_hi(y.x, y.y) - c0, v3 = lo_hi(y.z, y.w) - c0;
+                if (cnt1) {
+                    if (a0) {
+                        atomicAdd(&s_d1[(uint32_t)(v0 >> 8) & 255u], 1u);
+                        atomicAdd(&s_d1[(uint32_t)(v1 >> 8) & 255u], 1u);
+                    }
+                    if (a1) {
+                        atomicAdd(&s_d1[(uint32_t)(v2 >> 8) & 255u], 1u);
+                        atomicAdd(&s_d1[(uint32_t)(v3 >> 8) & 255u], 1u);
+                    }
+                }
+                const uint4 bq = make_uint4((uint32_t)(v0 >> shift), (uint32_t)(v1 >> shift),
+                                            (uint32_t)(v2 >> shift), (uint32_t)(v3 >> shift));
+                hist_vec(add, bq, a0 && a1, 0u);
+                if (a0 && !a1) {  // the chunk's odd last vector
+                    add(bq.x, 1u);
+                    add(bq.y, 1u);
+                }
+            }
+            }
         });
         if (blockIdx.x == 0 && warp == 0) {  // head / tail keys, one per lane
             const uint64_t i = lane < 3 ? lane : sp.tail0 + (lane - 3);
             if (lane < 3 ? i < sp.head : (lane < 6 && i < n)) {
-                add((keys[i] - c0) >> shift, 1u);
-                if (cnt1) atomicAdd(&s_d1[((keys[i] - c0) >> 8) & 255u], 1u);
+                add((uint32_t)((keys[i] - c0) >> shift), 1u);
+                if (cnt1) atomicAdd(&s_d1[(uint32_t)((keys[i] - c0) >> 8) & 255u], 1u);
             }
         }
     };
@@ -456,17 +654,29 @@ __device__ __forceinline__ void st_release_sys_u64(uint64_t *p, uint64_t v)
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-template <int BLOCK, int GROUPS>
+// the record into the host's mapped buffer: seq (the word the host polls) last,
+// with a system-scope release
+__device__ __forceinline__ void write_host_features(DevFeatures *hout, const DevFeatures &f)
+{
+    uint64_t *hw = reinterpret_cast<uint64_t *>(hout);
+    const uint64_t *fw = reinterpret_cast<const uint64_t *>(&f);
+    constexpr int W = (int)(sizeof(DevFeatures) / 8);
+#pragma unroll
+    for (int w = 0; w < W - 1; w++) hw[w] = fw[w];
+    st_release_sys_u64(hw + W - 1, f.seq);
+}
+
+template <int BLOCK, int GROUPS, typename K = uint32_t>
 __global__ void __launch_bounds__(BLOCK, 2)
-    k_feat_finalize(uint64_t n, const Partial *__restrict__ partials, int nparts,
+    k_feat_finalize(uint64_t n, const typename KeyTraits<K>::P *__restrict__ partials, int nparts,
                     const uint32_t *__restrict__ parts, int nrows, const uint32_t *__restrict__ ovf,
                     uint32_t *__restrict__ hist, FinalCtrl *__restrict__ fctrl, DevFeatures *__restrict__ out,
                     DevFeatures *__restrict__ hout, uint64_t seq)
 {
     pdl_begin();
     constexpr uint32_t BINS = BLOCK / GROUPS;
-    const Partial p = reduce_partials<BLOCK>(partials, nparts);
-    const Range rg = derive_range(p.mn, p.mx, 16u);
+    const auto p = KeyTraits<K>::template reduce<BLOCK>(partials, nparts);
+    const Range64 rg = KeyTraits<K>::range(p);
     const uint32_t active = (rg.nb + BINS - 1u) / BINS;
     if (blockIdx.x >= active) return;  // no bins here (uniform per CTA)
     __shared__ uint32_t s_u[BLOCK / 32];
@@ -522,21 +732,16 @@ __global__ void __launch_bounds__(BLOCK, 2)
         f.umax = p.mx;
         f.descents = p.desc;
         f.k = rg.k;
+        f.ksat = rg.ksat;
         f.bits = rg.bits;
         f.shift = rg.shift;
         f.nb = rg.nb;
         f.entropy = H;
-        f.pad0 = (uint32_t)nparts;                   // K1 CTAs = rows of byte0_rows
-        f.pad1[0] = (uint64_t)nrows * kHistCluster;  // K2 CTAs = rows of digit1_rows
-        f.pad1[1] = seq;
+        f.nparts = (uint32_t)nparts;               // K1 CTAs = rows of byte0_rows
+        f.nrows2 = (uint32_t)nrows * kHistCluster;  // K2 CTAs = rows of digit1_rows
+        f.seq = seq;
         *out = f;
-        if (hout) {
-            uint64_t *hw = reinterpret_cast<uint64_t *>(hout);
-            const uint64_t *fw = reinterpret_cast<const uint64_t *>(&f);
-#pragma unroll
-            for (int w = 0; w < 7; w++) hw[w] = fw[w];
-            st_release_sys_u64(hw + 7, seq);  // pad1[1]: the host polls this word
-        }
+        if (hout) write_host_features(hout, f);
     }
 }
 

@@ -76,6 +76,12 @@ __device__ __forceinline__ uint32_t digit8(uint32_t v, uint32_t shift)
     return __byte_perm(v, 0u, 0x4440u | (shift >> 3));
 }
 
+// 64-bit keys (NEXT-3): digit at bit `shift` (a multiple of 8, < 64)
+__device__ __forceinline__ uint32_t digit8(uint64_t v, uint32_t shift)
+{
+    return (uint32_t)(v >> shift) & 255u;
+}
+
 // Shared-memory index of tile slot i in the reordered tile: XOR-swizzled so
 // that 32 consecutive slots stay conflict-free (write-out) while slots 32
 // apart land in different banks (an ascending input puts exactly 32 keys per
@@ -95,7 +101,7 @@ __device__ __forceinline__ uint32_t swz(uint32_t i) { return i ^ ((i >> 5) & 31u
 constexpr int kRankMasked = 0;
 constexpr int kRankOrdered = 1;
 
-template <bool KV, int BLOCK, int ITEMS, int RANK = kRankMasked>
+template <bool KV, int BLOCK, int ITEMS, int RANK = kRankMasked, typename K = uint32_t>
 struct Onesweep {
     static constexpr int kWarps = BLOCK / 32;
     static constexpr int kGroupLanes = RANK == kRankOrdered ? 32 : 16;  // lanes sharing one digit table
@@ -108,9 +114,10 @@ struct Onesweep {
     static_assert(BLOCK * ITEMS < 65536, "16-bit slot field");
     static_assert(BLOCK >= 256 && BLOCK <= 512 && BLOCK % 128 == 0, "256, 384 or 512 threads");
     static_assert((kTile * 4) % 16 == 0, "TMA tile size");
-    static constexpr size_t kBuf = (size_t)kTile * 4;
+    static constexpr size_t kBufK = (size_t)kTile * sizeof(K);           // keys: 4 or 8 bytes
+    static constexpr size_t kBuf = (size_t)kTile * 4;                    // values: 4 bytes
     static constexpr size_t kOffK = 0;                                   // keys   [2][TILE]
-    static constexpr size_t kOffV = kOffK + 2 * kBuf;                    // values [2][TILE]
+    static constexpr size_t kOffV = kOffK + 2 * kBufK;                   // values [2][TILE]
     static constexpr size_t kOffCnt = kOffV + (KV ? 2 * kBuf : 0);       // digit tables [SUB][256]
     static constexpr size_t kOffAux = kOffCnt + (size_t)kSub * kBins * 4;
     // aux: part[2][256], start[256], gofs[256], wsum[8]
@@ -126,19 +133,33 @@ struct Onesweep {
 // and the executed passes are renumbered 0 .. m-1 (plan word: exec index << 8
 // | m, or kPassSkip).  Without a plan, pass p is executed pass p of npasses.
 constexpr uint32_t kPassSkip = 0xffffffffu;
-struct PassArgs {
-    const uint32_t *keys_in, *vals_in;
-    uint32_t *keys_out, *vals_out, *keys_tmp, *vals_tmp;
-    uint32_t n, pass, npasses, shift, flip, sub;
+template <typename K>
+struct PassArgsT {
+    const K *keys_in;
+    const uint32_t *vals_in;
+    K *keys_out;
+    uint32_t *vals_out;
+    K *keys_tmp;
+    uint32_t *vals_tmp;
+    uint32_t n, pass, npasses, shift;
+    K flip, sub;
     const uint32_t *bucket_base;  // this pass's 256 digit bases
     uint32_t *status, *ticket;    // this pass's look-back statuses and tile ticket (zeroed)
     const uint32_t *plan;         // nullptr: no skipping
+    uint32_t *status_clear;       // the previous pass's status region: zeroed here for the next pass
+    uint32_t clear_words;         //   (passes alternate between two regions; 0: nothing to clear)
 };
+using PassArgs = PassArgsT<uint32_t>;
 
-template <bool KV, int BLOCK, int ITEMS, int MINB, int RANK = kRankMasked>
-__global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(const PassArgs a)
+// K: uint32_t (32-bit keys) or uint64_t (64-bit keys, NEXT-3); values are 32-bit
+template <bool KV, int BLOCK, int ITEMS, int MINB, int RANK = kRankMasked, typename K = uint32_t>
+__global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(const PassArgsT<K> a)
 {
     pdl_begin();
+    // the previous pass is complete (pdl_begin): its status region is free and
+    // is cleared for the pass after this one (also when this pass is skipped)
+    for (uint32_t i = blockIdx.x * BLOCK + threadIdx.x; i < a.clear_words; i += gridDim.x * BLOCK)
+        a.status_clear[i] = 0u;
     // ---- this pass's place in the chain
     uint32_t e = a.pass, m = a.npasses;
     if (a.plan) {
@@ -150,23 +171,23 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(const PassArgs a)
     const bool first = e == 0, last = e + 1 == m;
     const bool to_out = ((m - 1 - e) & 1u) == 0;        // destination parity: the last lands in out
     const bool from_out = !first && !to_out;             // source = the previous pass's destination
-    const uint32_t *__restrict__ keys_in = first ? a.keys_in : (from_out ? a.keys_out : a.keys_tmp);
+    const K *__restrict__ keys_in = first ? a.keys_in : (from_out ? a.keys_out : a.keys_tmp);
     const uint32_t *__restrict__ vals_in = first ? a.vals_in : (from_out ? a.vals_out : a.vals_tmp);
-    uint32_t *__restrict__ keys_out = to_out ? a.keys_out : a.keys_tmp;
+    K *__restrict__ keys_out = to_out ? a.keys_out : a.keys_tmp;
     uint32_t *__restrict__ vals_out = to_out ? a.vals_out : a.vals_tmp;
     const uint32_t n = a.n, shift = a.shift;
-    const uint32_t in_flip = first ? a.flip : 0u, in_sub = first ? a.sub : 0u;
-    const uint32_t out_flip = last ? a.flip : 0u, out_add = last ? a.sub : 0u;
+    const K in_flip = first ? a.flip : K(0), in_sub = first ? a.sub : K(0);
+    const K out_flip = last ? a.flip : K(0), out_add = last ? a.sub : K(0);
     const uint32_t *__restrict__ bucket_base = a.bucket_base;
     uint32_t *__restrict__ status = a.status;
     uint32_t *__restrict__ tile_ticket = a.ticket;
     const uint32_t tma_ok = (((uintptr_t)keys_in & 15u) == 0) && (!KV || ((uintptr_t)vals_in & 15u) == 0);
 
-    using C = Onesweep<KV, BLOCK, ITEMS, RANK>;
+    using C = Onesweep<KV, BLOCK, ITEMS, RANK, K>;
     constexpr int TILE = C::kTile, SEG = C::kSeg, GL = C::kGroupLanes;
     constexpr bool ORDERED = RANK == kRankOrdered;
     extern __shared__ __align__(128) uint8_t smem[];
-    uint32_t *s_kb = reinterpret_cast<uint32_t *>(smem + C::kOffK);
+    K *s_kb = reinterpret_cast<K *>(smem + C::kOffK);
     uint32_t *s_vb = reinterpret_cast<uint32_t *>(smem + C::kOffV);
     uint32_t *s_cnt = reinterpret_cast<uint32_t *>(smem + C::kOffCnt);
     uint32_t *s_part = reinterpret_cast<uint32_t *>(smem + C::kOffAux);
@@ -184,10 +205,10 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(const PassArgs a)
 
     auto tile_full = [&](uint32_t t) { return (uint64_t)(t + 1) * TILE <= n; };
     auto issue = [&](uint32_t t, uint32_t b) {  // thread 0
-        const uint32_t bytes = (uint32_t)TILE * 4u;
-        mbar_expect_tx(&s_bar[b], bytes * (KV ? 2u : 1u));
-        tma_load_1d(s_kb + b * TILE, keys_in + (size_t)t * TILE, bytes, &s_bar[b]);
-        if constexpr (KV) tma_load_1d(s_vb + b * TILE, vals_in + (size_t)t * TILE, bytes, &s_bar[b]);
+        const uint32_t kbytes = (uint32_t)(TILE * sizeof(K)), vbytes = (uint32_t)TILE * 4u;
+        mbar_expect_tx(&s_bar[b], kbytes + (KV ? vbytes : 0u));
+        tma_load_1d(s_kb + b * TILE, keys_in + (size_t)t * TILE, kbytes, &s_bar[b]);
+        if constexpr (KV) tma_load_1d(s_vb + b * TILE, vals_in + (size_t)t * TILE, vbytes, &s_bar[b]);
     };
 
     // skewed digit distribution (a digit holds > 1/16 of the keys): enable the
@@ -223,7 +244,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(const PassArgs a)
         const uint32_t tile_base = tile * (uint32_t)TILE;
         const uint32_t tile_n = min((uint32_t)TILE, n - tile_base);
         const bool full = tile_n == (uint32_t)TILE;
-        uint32_t *sk = s_kb + b * TILE;
+        K *sk = s_kb + b * TILE;
         uint32_t *sv = s_vb + b * TILE;
         if (tma_ok && full) {
             mbar_wait(&s_bar[b], (phase >> b) & 1u);
@@ -245,7 +266,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(const PassArgs a)
             bool wskew = skew;
             // --------------------------------------------- early counts
             // keys (and values) into registers; per sub-warp digit counts
-            uint32_t v[ITEMS];
+            K v[ITEMS];
             [[maybe_unused]] uint32_t pv[KV ? ITEMS : 1];
             uint32_t *cw = s_cnt + sub * kBins;
             const uint32_t sbase = sub * SEG + j;
@@ -253,7 +274,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(const PassArgs a)
             for (int it = 0; it < ITEMS; it++) {
                 const uint32_t idx = sbase + it * GL;
                 const bool valid = FULL || idx < tile_n;
-                v[it] = ((valid ? sk[idx] : 0u) ^ in_flip) - in_sub;
+                v[it] = ((valid ? sk[idx] : K(0)) ^ in_flip) - in_sub;
                 if constexpr (KV) pv[it] = valid ? sv[idx] : 0u;
                 const uint32_t d = digit8(v[it], shift);
                 if (it == 0 && !wskew) wskew = __all_sync(kFull, d == __shfl_sync(kFull, d, 0));
@@ -455,14 +476,14 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(const PassArgs a)
             if constexpr (FULL) {
     #pragma unroll 5
                 for (int i = tid; i < TILE; i += BLOCK) {
-                    const uint32_t x = sk[swz(i)];
+                    const K x = sk[swz(i)];
                     const uint32_t o = s_gofs[digit8(x, shift)] + i;
                     keys_out[o] = (x + out_add) ^ out_flip;
                     if constexpr (KV) vals_out[o] = sv[swz(i)];
                 }
             } else {
                 for (uint32_t i = tid; i < tile_n; i += BLOCK) {
-                    const uint32_t x = sk[swz(i)];
+                    const K x = sk[swz(i)];
                     const uint32_t o = s_gofs[digit8(x, shift)] + i;
                     keys_out[o] = (x + out_add) ^ out_flip;
                     if constexpr (KV) vals_out[o] = sv[swz(i)];

@@ -39,9 +39,21 @@ using OsPairsO = Onesweep<true, kSortBlockPairsO, 12, kRankOrdered>;
 #define K6_PAIRS_M k_onesweep<true, kSortBlock, 9, 2, kRankMasked>
 #define K6_KEYS_O k_onesweep<false, kSortBlock, 16, 2, kRankOrdered>
 #define K6_PAIRS_O k_onesweep<true, kSortBlockPairsO, 12, 2, kRankOrdered>
-constexpr int kMinTile = 4608;  // smallest K6 tile: sizes the look-back status buffer
+// 64-bit keys (NEXT-3), 2 CTAs/SM each: ordered keys 512 x 9 (tile 4608, 94 KB
+// of shared memory), ordered pairs 384 x 8 (3072), masked keys 512 x 9 (4608,
+// 111 KB), masked pairs 512 x 5 (2560).
+using OsKeys64M = Onesweep<false, kSortBlock, 9, kRankMasked, uint64_t>;
+using OsPairs64M = Onesweep<true, kSortBlock, 5, kRankMasked, uint64_t>;
+using OsKeys64O = Onesweep<false, kSortBlock, 9, kRankOrdered, uint64_t>;
+using OsPairs64O = Onesweep<true, kSortBlockPairsO, 8, kRankOrdered, uint64_t>;
+#define K6W_KEYS_M k_onesweep<false, kSortBlock, 9, 2, kRankMasked, uint64_t>
+#define K6W_PAIRS_M k_onesweep<true, kSortBlock, 5, 2, kRankMasked, uint64_t>
+#define K6W_KEYS_O k_onesweep<false, kSortBlock, 9, 2, kRankOrdered, uint64_t>
+#define K6W_PAIRS_O k_onesweep<true, kSortBlockPairsO, 8, 2, kRankOrdered, uint64_t>
+constexpr int kMinTile = 2560;  // smallest K6 tile: sizes the look-back status regions
 static_assert(kMinTile <= OsKeysM::kTile && kMinTile <= OsPairsM::kTile && kMinTile <= OsKeysO::kTile &&
-                  kMinTile <= OsPairsO::kTile,
+                  kMinTile <= OsPairsO::kTile && kMinTile <= OsKeys64M::kTile &&
+                  kMinTile <= OsPairs64M::kTile && kMinTile <= OsKeys64O::kTile && kMinTile <= OsPairs64O::kTile,
               "kMinTile");
 
 // ------------------------------------------------------------------ K5 ----
@@ -52,14 +64,19 @@ static_assert(kMinTile <= OsKeysM::kTile && kMinTile <= OsPairsM::kTile && kMinT
 //   digit 0 when fshift > 0: K1's per-CTA histograms of the raw low byte,
 //     rotated by min's low byte (v's low byte = raw low byte - min's, mod 256);
 //   digit 1 when fshift > 8: K2's per-CTA histograms of digit 1 of v.
-// (fshift <= 16, so no other digit needs the keys.)  Marginals are flushed with
+// (32-bit keys: fshift <= 16, so no other digit needs the keys.  64-bit keys
+// (NEXT-3): digits 2 .. of v below fshift are counted from the keys by K5b,
+// k_digit_count64, into dhist before K5 runs.)  Marginals are flushed with
 // global atomics into dhist (zeroed by the host's memset); the last CTA turns
-// them into exclusive bucket bases and writes the pass plan (NEXT-1).
-constexpr uint32_t kPlanMagic = 0xa45c0de1u;  // plan[5] once K5 has written a plan
+// them into exclusive bucket bases and writes the pass plan (NEXT-1):
+// plan[p] for p < kMaxPasses, plan[kMaxPasses] = executed passes m,
+// plan[kMaxPasses + 1] = kPlanMagic.
+constexpr int kMaxPasses = 8;                 // 64-bit keys
+constexpr uint32_t kPlanMagic = 0xa45c0de1u;  // plan[kMaxPasses + 1] once K5 has written a plan
 constexpr int kRHBlock = 1024;
 constexpr int kRowCtas = 4;  // K5 CTAs per row set (K1 low bytes, K2 digit 1)
 
-template <int BLOCK>
+template <int BLOCK, int MAXP = 4>
 __global__ void __launch_bounds__(BLOCK, 1)
     k_radix_hist(uint64_t n, uint32_t sub, int passes, const uint32_t *__restrict__ fhist, uint32_t nb,
                  uint32_t fshift, const DevFeatures *__restrict__ dfeat, const uint32_t *__restrict__ byte0_rows,
@@ -68,11 +85,12 @@ __global__ void __launch_bounds__(BLOCK, 1)
                  int skip_trivial)
 {
     pdl_begin();
-    __shared__ uint32_t s_dig[4][256];
+    static_assert(MAXP <= kMaxPasses && MAXP * 32 <= BLOCK, "one warp per pass in the final scan");
+    __shared__ uint32_t s_dig[MAXP][256];
     __shared__ bool s_last;
-    __shared__ uint32_t s_triv[4];
+    __shared__ uint32_t s_triv[MAXP];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
-    for (int i = threadIdx.x; i < 4 * 256; i += BLOCK) (&s_dig[0][0])[i] = 0u;
+    for (int i = threadIdx.x; i < MAXP * 256; i += BLOCK) (&s_dig[0][0])[i] = 0u;
     __syncthreads();
     // rows of K1 (digit 0): CTAs 0 .. kRowCtas-1; rows of K2 (digit 1): the next
     // kRowCtas (the grid has >= 2 kRowCtas); four threads per bin and CTA, each
@@ -83,7 +101,7 @@ __global__ void __launch_bounds__(BLOCK, 1)
             constexpr uint32_t PARTS = BLOCK / 256;
             const uint32_t t = threadIdx.x & 255u;
             const uint32_t part = (blockIdx.x % kRowCtas) * PARTS + (threadIdx.x >> 8);
-            const int rows = d1 ? (int)__ldcg(&dfeat->pad1[0]) : (int)__ldcg(&dfeat->pad0);
+            const int rows = d1 ? (int)__ldcg(&dfeat->nrows2) : (int)__ldcg(&dfeat->nparts);
             const uint32_t *rp = d1 ? digit1_rows : byte0_rows;
             uint32_t sum = 0;
 #pragma unroll 8
@@ -95,10 +113,11 @@ __global__ void __launch_bounds__(BLOCK, 1)
     for (uint32_t b = blockIdx.x * BLOCK + threadIdx.x; b < nb; b += gridDim.x * BLOCK) {
         const uint32_t c = __ldg(&fhist[b]);
         if (!c) continue;
-        const uint32_t base = b << fshift;
+        const uint64_t base = (uint64_t)b << fshift;
 #pragma unroll
-        for (int p = 0; p < 4; p++)
-            if (p < passes && (uint32_t)(8 * p) >= fshift) atomicAdd(&s_dig[p][(base >> (8 * p)) & 255u], c);
+        for (int p = 0; p < MAXP; p++)
+            if (p < passes && (uint32_t)(8 * p) >= fshift)
+                atomicAdd(&s_dig[p][(uint32_t)(base >> (8 * p)) & 255u], c);
     }
     __syncthreads();
     for (int i = threadIdx.x; i < passes * 256; i += BLOCK) {
@@ -138,7 +157,7 @@ __global__ void __launch_bounds__(BLOCK, 1)
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        // device pass plan: executed passes renumbered 0 .. m-1; plan[4] = m, plan[5] = magic
+        // device pass plan: executed passes renumbered 0 .. m-1
         uint32_t m = 0;
         for (int p = 0; p < passes; p++) m += s_triv[p] ? 0u : 1u;
         uint32_t e = 0;
@@ -146,8 +165,8 @@ __global__ void __launch_bounds__(BLOCK, 1)
             plan[p] = s_triv[p] ? kPassSkip : ((e << 8) | m);
             e += s_triv[p] ? 0u : 1u;
         }
-        plan[4] = m;
-        plan[5] = kPlanMagic;
+        plan[kMaxPasses] = m;
+        plan[kMaxPasses + 1] = kPlanMagic;
     }
 }
 
@@ -213,6 +232,47 @@ __global__ void __launch_bounds__(kFillBlock)
         const bool act = threadIdx.x < 4 ? i < head : i < n;
         if (act) out[i] = (upper_bin(scan, 0, nb - 1u, i) + out_add) ^ out_flip;
     }
+}
+
+// ----------------------------------------------------------- K5b / K4w ----
+// 64-bit keys (NEXT-3).
+// K5b: digit histograms of v = (key ^ flip) - min for the digits p in [p0, p1)
+// that neither the feature histogram nor the K1 / K2 rows give (bits between
+// 16 and the feature bucket shift): one read of the keys, per-CTA shared
+// tables, global atomics into dhist (zeroed; K5 adds the other digits and scans).
+constexpr int kDC64Block = 512;
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK)
+    k_digit_count64(const uint64_t *__restrict__ keys, uint64_t n, uint64_t c0, int p0, int p1,
+                    uint32_t *__restrict__ dhist)
+{
+    pdl_begin();
+    __shared__ uint32_t s_dig[kMaxPasses - 2][256];
+    for (int i = threadIdx.x; i < (kMaxPasses - 2) * 256; i += BLOCK) (&s_dig[0][0])[i] = 0u;
+    __syncthreads();
+    const uint64_t stride = (uint64_t)gridDim.x * BLOCK;
+    for (uint64_t i = (uint64_t)blockIdx.x * BLOCK + threadIdx.x; i < n; i += stride) {
+        const uint64_t v = ld_nc(keys + i) - c0;  // (key ^ flip) - min = key - (min - flip)
+        for (int p = p0; p < p1; p++) atomicAdd(&s_dig[p - 2][(uint32_t)(v >> (8 * p)) & 255u], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < (p1 - p0) * 256; i += BLOCK) {
+        const uint32_t c = s_dig[p0 - 2 + i / 256][i % 256];
+        if (c) atomicAdd(&dhist[(p0 + i / 256) * 256 + i % 256], c);
+    }
+}
+
+// K4w: keys-only COUNTING for 64-bit keys: out[i] = min + v for scan[v] <= i <
+// scan[v+1] (as K4; k <= k_counting, so the binary search is short).
+constexpr int kFill64Block = 256;
+__global__ void __launch_bounds__(kFill64Block)
+    k_count_fill64(uint64_t *__restrict__ out, uint32_t n, const uint32_t *__restrict__ scan, uint32_t nb,
+                   uint64_t out_flip, uint64_t out_add)
+{
+    pdl_begin();
+    const uint32_t stride = gridDim.x * kFill64Block;
+    for (uint32_t i = blockIdx.x * kFill64Block + threadIdx.x; i < n; i += stride)
+        out[i] = ((uint64_t)upper_bin(scan, 0u, nb - 1u, i) + out_add) ^ out_flip;
 }
 
 }  // namespace ahs

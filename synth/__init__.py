@@ -200,3 +200,31 @@ def uniform_range(seed: int, n: int, lo: int, hi: int, dtype=np.int32):
     x = stream(seed, n)
     v = uniform_below(x, m).astype(np.int64) + lo
     return v.astype(dtype)
+
+
+# ---------------------------------------------------------- 64-bit keys (NEXT-3)
+def wide_u64(seed: int, n: int) -> np.ndarray:
+    """Full-range uint64 keys: the SplitMix64 words themselves."""
+    return stream(seed, n)
+
+
+def wide_i64(seed: int, n: int) -> np.ndarray:
+    """Full-range int64 keys (the same words reinterpreted)."""
+    return stream(seed, n).view(np.int64)
+
+
+def kmers(seed: int, n: int, k: int = 30) -> np.ndarray:
+    """Genomic-like 2-bit-packed k-mer codes, uniform over [0, 4^k), uint64."""
+    assert 1 <= k <= 32
+    return stream(seed, n) >> np.uint64(64 - 2 * k)
+
+
+def uniform_range64(seed: int, n: int, lo: int, hi: int, dtype=np.int64) -> np.ndarray:
+    """Uniform integers in [lo, hi] for spans up to 2^32 (uniform_below), as int64 / uint64."""
+    m = hi - lo + 1
+    x = stream(seed, n)
+    v = uniform_below(x, m)
+    if dtype == np.uint64:
+        with np.errstate(over="ignore"):
+            return v + np.uint64(lo)
+    return (v.astype(np.int64) + np.int64(lo)).astype(dtype)
