@@ -157,6 +157,9 @@ def cpu_oracle_rate(keys, vals, budget_s: float, max_n: int):
 
 # ------------------------------------------------------------ GPU timing
 def upload(torch, a: np.ndarray, device):
+    if a.dtype in (np.int64, np.uint64):  # NEXT-3 64-bit keys
+        t = torch.from_numpy(a.view(np.int64)).to(device)
+        return t.view(torch.uint64) if a.dtype == np.uint64 else t
     t = torch.from_numpy(a.view(np.int32)).to(device)
     return t.view(torch.uint32) if a.dtype == np.uint32 else t
 
@@ -168,7 +171,7 @@ def time_pipeline(torch, ahs, keys_np, vals_np, steps, warmup, device, flush, pr
     dv = upload(torch, vals_np, device) if vals_np is not None else None
     ko = torch.empty_like(dk)
     vo = torch.empty_like(dv) if dv is not None else None
-    ws = ahs.Workspace(n, dv is not None, device)
+    ws = ahs.Workspace(n, dv is not None, device, key_dtype=keys_np.dtype)
     stream = torch.cuda.current_stream(device)
 
     def step():
@@ -285,14 +288,15 @@ def time_e2e(torch, ahs, keys_np, vals_np, steps, warmup, device):
     return ms, nb, nb
 
 
-def sort_bytes(strategy: int, passes: int, n: int, kv: bool, shift: int = 1) -> int:
-    """Algorithmic HBM bytes of ahs_sort: radix = K5's read of the keys
-    (4n, only when the feature buckets are coarser than the keys: shift > 0) + per
-    executed pass read+write (8n keys, 16n pairs); counting keys-only = write 4n."""
+def sort_bytes(strategy: int, passes: int, n: int, kv: bool, shift: int = 1, kb: int = 4) -> int:
+    """Algorithmic HBM bytes of ahs_sort: per executed pass read + write of
+    the keys (2 kb n, kb = key bytes) and values (8n); counting keys-only = write kb n.
+    K5 reads no keys for 32-bit keys; for 64-bit keys K5b reads them once (8n) when the
+    feature buckets are coarser than 16 bits (shift > 16)."""
     if passes == 0:
-        return 4 * n if strategy == 0 else 0
-    hist = 0 if (strategy == 0 and passes == 1) or shift == 0 else 4 * n
-    return hist + passes * (16 if kv else 8) * n
+        return kb * n if strategy == 0 else 0
+    hist = kb * n if (kb == 8 and shift > 16) else 0
+    return hist + passes * (2 * kb + (8 if kv else 0)) * n
 
 
 def traffic_from_profiles(workload: str):
@@ -392,7 +396,8 @@ def run_ours(args):
             kv2 = v2 is not None
             sort_ms2 = sum(v["ms"] for k, v in p2.items() if not k.startswith("feat")) / args.table_steps
             feat_ms2 = sum(v["ms"] for k, v in p2.items() if k.startswith("feat")) / args.table_steps
-            sb2 = sort_bytes(r2["s"], r2["executed"], n2, kv2, r2["f"].shift)
+            kb2 = k2.dtype.itemsize
+            sb2 = sort_bytes(r2["s"], r2["executed"], n2, kv2, r2["f"].shift, kb2)
             rows.append({
                 "workload": cfg, "n": n2, "kv": kv2, "strategy": ahs.STRATEGY_NAMES[r2["s"]],
                 "rule": ahs.RULE_NAMES[r2["r"]], "passes": r2["passes"], "passes_executed": r2["executed"],
@@ -400,12 +405,16 @@ def run_ours(args):
                 "sort_Gkeys_s": n2 / (sort_ms2 * 1e-3) / 1e9 if sort_ms2 > 0 else None,
                 "sort_GBps": sb2 / (sort_ms2 * 1e-3) / 1e9 if sort_ms2 > 0 else None,
                 "sort_frac_of_peak": (sb2 / (sort_ms2 * 1e-3) / 1e9) / peak if sort_ms2 > 0 else None,
-                "features_GBps": 8 * n2 / (feat_ms2 * 1e-3) / 1e9 if feat_ms2 > 0 else None,
+                "key_bytes": kb2,
+                "features_GBps": 2 * kb2 * n2 / (feat_ms2 * 1e-3) / 1e9 if feat_ms2 > 0 else None,
                 "kernels_ms": {k: v["ms"] / v["launches"] for k, v in p2.items() if v["launches"]},
             })
-            ee = entropy_exact_report(torch, ahs, k2, v2, device, reps=2)
-            rows[-1].update({"H16": ee["H16"], "H_exact": ee["H_exact"],
-                             "branch_paper_literal": ee["branch_paper_literal"], "branch_agree": ee["agree"]})
+            if kb2 == 4:  # K8 (NEXT-2) is built for 32-bit keys
+                ee = entropy_exact_report(torch, ahs, k2, v2, device, reps=2)
+                rows[-1].update({"H16": ee["H16"], "H_exact": ee["H_exact"],
+                                 "branch_paper_literal": ee["branch_paper_literal"], "branch_agree": ee["agree"]})
+            else:
+                rows[-1].update({"H16": r2["f"].entropy})
             del k2, v2
         out["strategies"] = rows
     # CPU oracle baseline (rank 0, N = 1 only)
@@ -458,7 +467,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg2", choices=sorted(synth.CONFIGS))
-    ap.add_argument("--configs", default="cfg1,cfg2kv,cfg3,cfg4a,cfg4b,cfg4d,cfg5_r8,cfg5_r16,cfg5_r24,cfg5_r32",
+    ap.add_argument("--configs", default="cfg1,cfg2kv,cfg3,cfg4a,cfg4b,cfg4d,cfg5_r8,cfg5_r16,cfg5_r24,cfg5_r32,cfg6,cfg6kv",
                     help="per-strategy table rows (single GPU only); '' to skip")
     ap.add_argument("--table-steps", type=int, default=5)
     ap.add_argument("--soak", type=float, default=2.0, help="untimed seconds of load before timing")

@@ -170,8 +170,17 @@ for _r in CFG5_R:
     CONFIGS[f"cfg5_r{_r}"] = ("u32", 1 << 28, (lambda r: (lambda n: cfg5(r, n)))(_r))
 
 
+def _cfg6(n: int, kv: bool):
+    keys = kmers(6, n)  # NEXT-3: genomic-like 30-mers, k = 4^30, uint64
+    return keys, (np.arange(n, dtype=np.uint32) if kv else None)
+
+
+CONFIGS["cfg6"] = ("u64", 1 << 26, lambda n: _cfg6(n, False))
+CONFIGS["cfg6kv"] = ("u64", 1 << 26, lambda n: _cfg6(n, True))
+
+
 def make(name: str, n: int | None = None):
-    """Return (keys ndarray, vals ndarray or None, dtype 'i32'|'u32') for a config."""
+    """Return (keys ndarray, vals ndarray or None, dtype 'i32'|'u32'|'u64') for a config."""
     dtype, n0, fn = CONFIGS[name]
     keys, vals = fn(n0 if n is None else n)
     return keys, vals, dtype

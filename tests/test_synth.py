@@ -40,7 +40,7 @@ def test_config_shapes_small():
     for name in synth.CONFIGS:
         keys, vals, dt = synth.make(name, n=4096)
         assert keys.shape == (4096,)
-        assert keys.dtype == (np.int32 if dt == "i32" else np.uint32)
+        assert keys.dtype == {"i32": np.int32, "u32": np.uint32, "i64": np.int64, "u64": np.uint64}[dt]
         if vals is not None:
             assert np.array_equal(vals, np.arange(4096, dtype=np.uint32))
     assert (synth.cfg4c(100) == 42).all()
@@ -62,3 +62,11 @@ def test_zipf_cdf():
     cdf = synth.zipf_cdf()
     assert cdf.shape == (4096,) and cdf[-1] == 1.0
     assert np.all(np.diff(cdf) > 0)
+
+
+def test_kmers_cover_4pow30():
+    """cfg6 (NEXT-3): 30-mer codes are the top 60 bits of the SplitMix64 words."""
+    x = synth.stream(6, 1000)
+    k = synth.kmers(6, 1000)
+    assert k.dtype == np.uint64 and int(k.max()) < 4 ** 30
+    assert np.array_equal(k, x >> np.uint64(4))
