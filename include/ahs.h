@@ -55,7 +55,9 @@ typedef enum {
     AHS_ERANGE = -3,   /* n > AHS_MAX_N */
     AHS_EFEAT = -4,    /* feat does not describe these keys (n or dtype mismatch) */
     AHS_ECUDA = -5,    /* CUDA launch / runtime error (cudaGetLastError) */
-    AHS_ENODEV = -6    /* no CUDA device or not an sm_100 device */
+    AHS_ENODEV = -6,   /* no CUDA device or not an sm_100 device */
+    AHS_EMODEL = -7,   /* ahs_model_load: malformed JSON or a schema violation (err names the tree / node) */
+    AHS_EMODELVER = -8 /* ahs_model_load: version other than "ahs-model/1" */
 } ahs_status;
 
 /* Key types: 32-bit keys (PAPER.md P:409 integers) and, NEXT-3, 64-bit keys
@@ -72,7 +74,8 @@ typedef enum {
     AHS_RULE_SMALL_N = 2,     /* n <= n_insertion   -> GENERAL (Insertion) */
     AHS_RULE_SMALL_RANGE = 3, /* k <= k_counting   -> COUNTING         */
     AHS_RULE_LOW_ENTROPY = 4, /* k > k_radix and H < c*log2(norm) -> RADIX */
-    AHS_RULE_DEFAULT = 5      /* otherwise   -> GENERAL (QuickSort) */
+    AHS_RULE_DEFAULT = 5,     /* otherwise   -> GENERAL (QuickSort) */
+    AHS_RULE_MODEL = 6        /* the classifier chose (ahs_select_model) */
 } ahs_rule;
 
 /* Entropy normalisation of the RADIX rule (reading R2):
@@ -209,6 +212,36 @@ AHS_API int ahs_sort_host(const void *h_keys_in, const uint32_t *h_vals_in, void
  * ENOSPACE, ERANGE (n > AHS_MAX_N), ENODEV, ECUDA. */
 AHS_API int ahs_entropy_sorted(const void *d_keys, uint64_t n, void *d_ws, size_t ws_bytes, double *H,
                                void *stream);
+
+/* --------------------------------------- strategy classifier (NEXT-4, host) */
+/* PAPER.md §III.H (lines 290-332, Listing 5 loadModel / predictStrategy): a
+ * gradient-boosted tree ensemble over the raw features (n, k, H), used for
+ * n >= 1000 beside the static rules (Table IV).  Model format: SPEC.md's
+ * "ahs-model/1" JSON (classifier.hpp states it); validated eagerly on load.
+ * The library ships no trained model (none exists offline); the tests use an
+ * FSM-consistent fixture.  Host only, no device work, thread-safe after load. */
+typedef struct ahs_model ahs_model_t;
+
+/* Parse + validate json[0..len).  *model receives a handle to free with
+ * ahs_model_free.  err (nullable) receives a NUL-terminated message naming the
+ * offending tree / node.  Errors: EINVAL (NULL json / model), EMODEL,
+ * EMODELVER. */
+AHS_API int ahs_model_load(const char *json, size_t len, ahs_model_t **model, char *err, size_t err_len);
+AHS_API void ahs_model_free(ahs_model_t *model);
+
+/* score_c = base_c + sum over trees of the reached leaf's score (left iff
+ * feature < threshold); *algo4 = argmax (ties: earlier class) as the paper's
+ * algorithm: 0 insertion, 1 counting, 2 radix, 3 quick.  scores4 (nullable)
+ * receives the 4 scores in the model's class order. */
+AHS_API int ahs_model_predict(const ahs_model_t *model, double n, double k, double H, int32_t *algo4,
+                              double *scores4);
+
+/* Strategy selection with the classifier: the P:411 shortcuts (EMPTY,
+ * CONSTANT) first; then, when model != NULL and n >= ml_min_n (Table IV: 1000),
+ * the classifier (rule AHS_RULE_MODEL; insertion and quick map to GENERAL);
+ * otherwise ahs_select.  *source (nullable): 0 = rules, 1 = classifier. */
+AHS_API int ahs_select_model(const ahs_features_t *feat, const ahs_thresholds_t *th, const ahs_model_t *model,
+                             uint64_t ml_min_n, int32_t *strategy, int32_t *rule, int32_t *source);
 
 /* ------------------------------------------------------- ranking mode (K6) */
 /* The onesweep pass ranks keys stably in one of two ways (onesweep.cuh):

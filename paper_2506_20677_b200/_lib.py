@@ -12,7 +12,10 @@ _LIB_PATH = os.path.join(_HERE, "lib", "libahs.so")
 AHS_I32, AHS_U32, AHS_I64, AHS_U64 = 0, 1, 2, 3
 AHS_COUNTING, AHS_RADIX, AHS_GENERAL = 0, 1, 2
 STRATEGY_NAMES = {AHS_COUNTING: "COUNTING", AHS_RADIX: "RADIX", AHS_GENERAL: "GENERAL"}
-RULE_NAMES = {0: "EMPTY", 1: "CONSTANT", 2: "SMALL_N", 3: "SMALL_RANGE", 4: "LOW_ENTROPY", 5: "DEFAULT"}
+RULE_NAMES = {0: "EMPTY", 1: "CONSTANT", 2: "SMALL_N", 3: "SMALL_RANGE", 4: "LOW_ENTROPY", 5: "DEFAULT",
+              6: "MODEL"}
+AHS_EMODEL, AHS_EMODELVER = -7, -8
+ALGO4_NAMES = {0: "insertion", 1: "counting", 2: "radix", 3: "quick"}
 FLAG_NAMES = {1: "EMPTY", 2: "CONSTANT", 4: "BUCKETED", 8: "SORTED", 16: "STRICT_DESC", 32: "SIGNED",
               64: "K_SATURATED"}
 FLAG_K_SATURATED = 64
@@ -70,6 +73,12 @@ def lib():
             "ahs_workspace_bytes": ([u64], sz),
             "ahs_sort_tmp_bytes": ([u64, C.c_int], sz),
             "ahs_sort_tmp_bytes_dtype": ([u64, C.c_int, i32], sz),
+            "ahs_model_load": ([C.c_char_p, sz, C.POINTER(vp), C.c_char_p, sz], C.c_int),
+            "ahs_model_free": ([vp], None),
+            "ahs_model_predict": ([vp, C.c_double, C.c_double, C.c_double, p_i32, C.POINTER(C.c_double)],
+                                  C.c_int),
+            "ahs_select_model": ([C.POINTER(Features), C.POINTER(Thresholds), vp, u64, p_i32, p_i32, p_i32],
+                                 C.c_int),
             "ahs_host_scratch_bytes_dtype": ([u64, C.c_int, i32], sz),
             "ahs_sort_passes": ([C.POINTER(Features), i32, C.c_int], C.c_int),
             "ahs_features": ([vp, u64, i32, vp, sz, C.POINTER(Features), vp], C.c_int),
@@ -324,3 +333,42 @@ def ahs_sort_host(keys: np.ndarray, vals: np.ndarray | None, keys_out: np.ndarra
                              C.byref(s), C.byref(r), _stream(stream))
     _check(rc, "ahs_sort_host")
     return f, s.value, r.value
+
+
+# ------------------------------------------------ strategy classifier (NEXT-4)
+class Model:
+    """A loaded "ahs-model/1" tree ensemble (host; include/ahs.h ahs_model_*)."""
+
+    def __init__(self, json_bytes: bytes | str):
+        if isinstance(json_bytes, str):
+            json_bytes = json_bytes.encode()
+        h = C.c_void_p()
+        err = C.create_string_buffer(512)
+        rc = lib().ahs_model_load(json_bytes, len(json_bytes), C.byref(h), err, 512)
+        if rc:
+            raise AhsError(rc, f"ahs_model_load: {err.value.decode(errors='replace')}")
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.ahs_model_free(self._h)
+            self._h = None
+
+    def predict(self, n: float, k: float, H: float) -> tuple[int, list[float]]:
+        """(the paper's algorithm 0..3, the 4 scores in the model's class order)"""
+        a = C.c_int32()
+        sc = (C.c_double * 4)()
+        _check(lib().ahs_model_predict(self._h, n, k, H, C.byref(a), sc), "ahs_model_predict")
+        return a.value, list(sc)
+
+
+def ahs_select_model(feat: Features, model: Model | None, ml_min_n: int = 1000,
+                     th: Thresholds | None = None) -> tuple[int, int, int]:
+    """(strategy, rule, source: 0 rules / 1 classifier)"""
+    s, r, src = C.c_int32(), C.c_int32(), C.c_int32()
+    rc = lib().ahs_select_model(C.byref(feat), None if th is None else C.byref(th),
+                                None if model is None else model._h, ml_min_n, C.byref(s), C.byref(r),
+                                C.byref(src))
+    _check(rc, "ahs_select_model")
+    return s.value, r.value, src.value
+

@@ -15,6 +15,7 @@
 #include "features.cuh"
 #include "sort.cuh"
 #include "entropy.cuh"
+#include "classifier.hpp"
 
 using namespace ahs;
 
@@ -367,6 +368,8 @@ const char *ahs_status_string(int s)
     case AHS_EFEAT: return "features do not match the keys (n or dtype)";
     case AHS_ECUDA: return "CUDA error";
     case AHS_ENODEV: return "no sm_100 CUDA device";
+    case AHS_EMODEL: return "malformed or invalid model";
+    case AHS_EMODELVER: return "unsupported model version";
     default: return "unknown status";
     }
 }
@@ -1007,6 +1010,62 @@ int ahs_sort_host(const void *h_keys_in, const uint32_t *h_vals_in, void *h_keys
     if (feat) *feat = f;
     if (strategy) *strategy = st;
     if (rule) *rule = ru;
+    return AHS_OK;
+}
+
+// ------------------------------------------------------ classifier (NEXT-4)
+}  // extern "C"
+struct ahs_model {
+    ahs::model::Model m;
+};
+extern "C" {
+
+int ahs_model_load(const char *json, size_t len, ahs_model_t **model, char *err, size_t err_len)
+{
+    if (err && err_len) err[0] = 0;
+    if (!json || !model) return AHS_EINVAL;
+    *model = nullptr;
+    std::unique_ptr<ahs_model> h(new (std::nothrow) ahs_model());
+    if (!h) return AHS_EINVAL;
+    std::string msg;
+    const ahs::model::LoadStatus st = ahs::model::load(json, len, h->m, msg);
+    if (st != ahs::model::LOAD_OK) {
+        if (err && err_len) std::snprintf(err, err_len, "%s", msg.c_str());
+        return st == ahs::model::LOAD_VERSION ? AHS_EMODELVER : AHS_EMODEL;
+    }
+    *model = h.release();
+    return AHS_OK;
+}
+
+void ahs_model_free(ahs_model_t *model) { delete model; }
+
+int ahs_model_predict(const ahs_model_t *model, double n, double k, double H, int32_t *algo4, double *scores4)
+{
+    if (!model || !algo4) return AHS_EINVAL;
+    double sc[4];
+    *algo4 = model->m.predict(n, k, H, sc);
+    if (scores4)
+        for (int c = 0; c < 4; c++) scores4[c] = sc[c];
+    return AHS_OK;
+}
+
+int ahs_select_model(const ahs_features_t *feat, const ahs_thresholds_t *th, const ahs_model_t *model,
+                     uint64_t ml_min_n, int32_t *strategy, int32_t *rule, int32_t *source)
+{
+    if (!feat || !strategy) return AHS_EINVAL;
+    if (source) *source = 0;
+    if (!model || feat->n == 0 || feat->k == 1 || feat->n < ml_min_n)  // P:411 shortcuts, then Table IV's n range
+        return ahs_select(feat, th, strategy, rule);
+    if (th) {  // the thresholds are still validated (they govern the fallback path)
+        int32_t s0, r0;
+        const int rc = ahs_select(feat, th, &s0, &r0);
+        if (rc) return rc;
+    }
+    int32_t a = 0;
+    ahs_model_predict(model, (double)feat->n, (double)feat->k, feat->entropy, &a, nullptr);
+    *strategy = a == ahs::model::COUNTING ? AHS_COUNTING : a == ahs::model::RADIX ? AHS_RADIX : AHS_GENERAL;
+    if (rule) *rule = AHS_RULE_MODEL;
+    if (source) *source = 1;
     return AHS_OK;
 }
 
