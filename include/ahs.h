@@ -213,6 +213,23 @@ AHS_API int ahs_sort_host(const void *h_keys_in, const uint32_t *h_vals_in, void
 AHS_API int ahs_entropy_sorted(const void *d_keys, uint64_t n, void *d_ws, size_t ws_bytes, double *H,
                                void *stream);
 
+/* ------------------------------------------- batched segment sort (NEXT-4) */
+/* Many small independent sorts in one call: the GPU form of the paper's small-n
+ * path (Insertion Sort for n <= 20, §III.E Listing 1).
+ * Segment s = keys[d_offsets[s] .. d_offsets[s+1]) (device uint32 array of
+ * num_segments + 1 non-decreasing offsets <= n; segments need not start at 0),
+ * each sorted ascending and stably, values travelling with their keys; keys
+ * outside every segment are not touched.  max_segment: an upper bound on the
+ * segment lengths, <= 2048 (ERANGE above); <= 32 runs one thread per segment
+ * with Listing 1's insertion sort in shared memory, otherwise one CTA per
+ * segment (bitonic network on (key, index): stable).  Out may alias in.
+ * d_bad (device uint32, required) receives the number of segments found longer
+ * than max_segment or reaching past n: those are left unsorted (never an
+ * out-of-bounds access).  Asynchronous.  Errors: EINVAL, ERANGE, ENODEV, ECUDA. */
+AHS_API int ahs_sort_segments(const void *d_keys_in, const uint32_t *d_vals_in, void *d_keys_out,
+                              uint32_t *d_vals_out, uint64_t n, const uint32_t *d_offsets, uint32_t num_segments,
+                              uint32_t max_segment, int32_t dtype, uint32_t *d_bad, void *stream);
+
 /* --------------------------------------- strategy classifier (NEXT-4, host) */
 /* PAPER.md §III.H (lines 290-332, Listing 5 loadModel / predictStrategy): a
  * gradient-boosted tree ensemble over the raw features (n, k, H), used for

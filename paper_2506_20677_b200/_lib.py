@@ -74,6 +74,7 @@ def lib():
             "ahs_sort_tmp_bytes": ([u64, C.c_int], sz),
             "ahs_sort_tmp_bytes_dtype": ([u64, C.c_int, i32], sz),
             "ahs_model_load": ([C.c_char_p, sz, C.POINTER(vp), C.c_char_p, sz], C.c_int),
+            "ahs_sort_segments": ([vp, vp, vp, vp, u64, vp, C.c_uint32, C.c_uint32, i32, vp, vp], C.c_int),
             "ahs_model_free": ([vp], None),
             "ahs_model_predict": ([vp, C.c_double, C.c_double, C.c_double, p_i32, C.POINTER(C.c_double)],
                                   C.c_int),
@@ -371,4 +372,20 @@ def ahs_select_model(feat: Features, model: Model | None, ml_min_n: int = 1000,
                                 C.byref(src))
     _check(rc, "ahs_select_model")
     return s.value, r.value, src.value
+
+
+# ------------------------------------------------ batched segment sort (NEXT-4)
+def ahs_sort_segments(keys_in, vals_in, keys_out, vals_out, offsets, max_segment: int, bad=None, stream=None):
+    """Sort keys[offsets[s]:offsets[s+1]) for every s (device tensors; offsets uint32/int32 with
+    num_segments + 1 entries).  Asynchronous; returns the device uint32 counter of segments left
+    unsorted (longer than max_segment or past n)."""
+    torch = _torch()
+    if bad is None:
+        bad = torch.zeros(1, dtype=torch.int32, device=keys_in.device)
+    nseg = offsets.numel() - 1
+    rc = lib().ahs_sort_segments(_dev_ptr(keys_in), _dev_ptr(vals_in), _dev_ptr(keys_out), _dev_ptr(vals_out),
+                                 keys_in.numel(), _dev_ptr(offsets), max(nseg, 0), max_segment,
+                                 _dtype_code(keys_in), _dev_ptr(bad), _stream(stream))
+    _check(rc, "ahs_sort_segments")
+    return bad
 

@@ -16,6 +16,7 @@
 #include "sort.cuh"
 #include "entropy.cuh"
 #include "classifier.hpp"
+#include "segsort.cuh"
 
 using namespace ahs;
 
@@ -186,12 +187,13 @@ enum KernelId {
     KID_ENTROPY_SORTED,
     KID_HIST_SCAN,
     KID_DIGIT_COUNT,
+    KID_SEG_SORT,
     KID_COUNT
 };
 const char *kKernelNames[KID_COUNT] = {"feat_reduce", "feat_hist",   "feat_finalize",
                                        "radix_hist",  "onesweep",    "onesweep_kv",
                                        "count_fill",  "count_scatter_kv", "entropy_sorted",
-                                       "hist_scan",   "digit_count64"};
+                                       "hist_scan",   "digit_count64", "seg_sort"};
 
 std::atomic<uint64_t> g_launches{0};
 // NEXT-1 trivial-pass skipping (default on; AHS_SKIP_TRIVIAL=0 or ahs_set_skip_trivial(0) turn it off)
@@ -1011,6 +1013,67 @@ int ahs_sort_host(const void *h_keys_in, const uint32_t *h_vals_in, void *h_keys
     if (strategy) *strategy = st;
     if (rule) *rule = ru;
     return AHS_OK;
+}
+
+// --------------------------------------------------- segment sort (NEXT-4)
+}  // extern "C"
+namespace {
+template <typename K, bool KV>
+cudaError_t seg_launch(const void *kin, const uint32_t *vin, void *kout, uint32_t *vout, uint64_t n,
+                       const uint32_t *offsets, uint32_t nseg, uint32_t max_segment, K flip, uint32_t *bad,
+                       cudaStream_t s)
+{
+    if (max_segment <= (uint32_t)kSegSmallMax) {
+        constexpr size_t smem = seg_small_smem<K, KV>();
+        static bool attr = [] {
+            return cudaFuncSetAttribute(k_seg_small<K, KV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smem) == cudaSuccess;
+        }();
+        if (!attr) return cudaErrorInvalidValue;
+        const unsigned g = (nseg + kSegSmallBlock - 1) / kSegSmallBlock;
+        return launch_k(k_seg_small<K, KV>, dim3(g), dim3(kSegSmallBlock), smem, s, (const K *)kin, vin, (K *)kout,
+                        vout, offsets, nseg, n, flip, max_segment, bad);
+    }
+    return launch_k(k_seg_medium<K, KV>, dim3(nseg), dim3(kSegMedBlock), 0, s, (const K *)kin, vin, (K *)kout, vout,
+                    offsets, nseg, n, flip, max_segment, bad);
+}
+}  // namespace
+extern "C" {
+
+int ahs_sort_segments(const void *d_keys_in, const uint32_t *d_vals_in, void *d_keys_out, uint32_t *d_vals_out,
+                      uint64_t n, const uint32_t *d_offsets, uint32_t num_segments, uint32_t max_segment,
+                      int32_t dtype, uint32_t *d_bad, void *stream)
+{
+    if (!dtype_valid(dtype)) return AHS_EINVAL;
+    if (max_segment > (uint32_t)kSegMedMax) return AHS_ERANGE;
+    if (n > AHS_MAX_N) return AHS_ERANGE;
+    const bool kv = d_vals_in != nullptr;
+    const uintptr_t kal = key_bytes_of(dtype) - 1;
+    if (!d_bad || (num_segments > 0 && (!d_offsets || !d_keys_in || !d_keys_out || (kv && !d_vals_out))) ||
+        ((uintptr_t)d_keys_in & kal) || ((uintptr_t)d_keys_out & kal))
+        return AHS_EINVAL;
+    int sms = 0;
+    int rc = device_info(&sms, nullptr);
+    if (rc) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (cudaMemsetAsync(d_bad, 0, 4, s) != cudaSuccess) return AHS_ECUDA;
+    if (num_segments == 0) return AHS_OK;
+    const cudaError_t e = launch(KID_SEG_SORT, s, [&] {
+        if (dtype_wide(dtype)) {
+            const uint64_t flip = flip64_of(dtype);
+            if (kv) seg_launch<uint64_t, true>(d_keys_in, d_vals_in, d_keys_out, d_vals_out, n, d_offsets,
+                                               num_segments, max_segment, flip, d_bad, s);
+            else seg_launch<uint64_t, false>(d_keys_in, nullptr, d_keys_out, nullptr, n, d_offsets, num_segments,
+                                             max_segment, flip, d_bad, s);
+        } else {
+            const uint32_t flip = flip_of(dtype);
+            if (kv) seg_launch<uint32_t, true>(d_keys_in, d_vals_in, d_keys_out, d_vals_out, n, d_offsets,
+                                               num_segments, max_segment, flip, d_bad, s);
+            else seg_launch<uint32_t, false>(d_keys_in, nullptr, d_keys_out, nullptr, n, d_offsets, num_segments,
+                                             max_segment, flip, d_bad, s);
+        }
+    });
+    return e == cudaSuccess ? AHS_OK : AHS_ECUDA;
 }
 
 // ------------------------------------------------------ classifier (NEXT-4)

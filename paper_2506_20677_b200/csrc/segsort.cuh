@@ -1,0 +1,155 @@
+// segsort.cuh — K9 (NEXT-4): batched sorts of many small independent segments,
+// the GPU form of the paper's small-n path (Insertion Sort for n <= 20,
+// PAPER.md §III.E Listing 1; the small-n results, line 490).
+// Segment s is keys[offsets[s] .. offsets[s+1]), sorted ascending and stably
+// (values travel with their keys); segments are disjoint and in order.
+//
+//   K9s  max segment <= 32: a CTA of 256 threads owns 256 consecutive segments
+//        (<= 8192 keys, one contiguous range): coalesced load of the range into
+//        shared memory, one thread per segment runs Listing 1's insertion sort
+//        (strict > : stable) in shared memory, coalesced store.
+//   K9m  max segment <= 2048: one CTA (512 threads) per segment: bitonic sort
+//        in shared memory on (key, original index) -- unique, so the result is
+//        the stable order -- padded to a power of two with (max, max) records;
+//        values gathered by the sorted indices.
+// Keys compare as unsigned after `flip` (the sign bit for signed types).  A
+// segment longer than the declared maximum (or reaching past n) is left as is
+// and counted in *bad (device word): never an out-of-bounds access.
+#pragma once
+
+#include "common.cuh"
+
+namespace ahs {
+
+constexpr int kSegSmallBlock = 256;
+constexpr int kSegSmallMax = 32;
+constexpr int kSegMedBlock = 512;
+constexpr int kSegMedMax = 2048;
+
+template <typename K, bool KV>
+constexpr size_t seg_small_smem()
+{
+    return (size_t)kSegSmallBlock * kSegSmallMax * (sizeof(K) + (KV ? 4 : 0));
+}
+
+template <typename K, bool KV>
+__global__ void __launch_bounds__(kSegSmallBlock)
+    k_seg_small(const K *__restrict__ kin, const uint32_t *__restrict__ vin, K *__restrict__ kout,
+                uint32_t *__restrict__ vout, const uint32_t *__restrict__ offsets, uint32_t nseg, uint64_t n, K flip,
+                uint32_t maxlen, uint32_t *__restrict__ bad)
+{
+    pdl_begin();
+    constexpr uint32_t CAP = kSegSmallBlock * kSegSmallMax;
+    extern __shared__ __align__(16) uint8_t seg_smem[];  // keys [CAP] then values [CAP]: seg_small_smem<K, KV>()
+    K *sk = reinterpret_cast<K *>(seg_smem);
+    [[maybe_unused]] uint32_t *sv = reinterpret_cast<uint32_t *>(seg_smem + CAP * sizeof(K));
+    __shared__ uint32_t s_ok;
+    const uint32_t s0 = blockIdx.x * kSegSmallBlock, s1 = min(nseg, s0 + kSegSmallBlock);
+    const uint32_t base = __ldg(&offsets[s0]), end = __ldg(&offsets[s1]);
+    // the range must hold the CTA's segments (each <= kSegSmallMax, inside [0, n))
+    if (threadIdx.x == 0) s_ok = (end >= base && (uint64_t)end <= n && end - base <= CAP) ? 1u : 0u;
+    const uint32_t my = s0 + threadIdx.x;
+    uint32_t lo = 0, hi = 0;
+    bool mine = my < s1;
+    if (mine) {
+        lo = __ldg(&offsets[my]);
+        hi = __ldg(&offsets[my + 1]);
+        if (hi < lo || hi - lo > maxlen || lo < base || hi > end) mine = false;  // maxlen <= kSegSmallMax
+    }
+    __syncthreads();
+    if (!s_ok) {
+        if (my < s1) atomicAdd(bad, 1u);
+        return;
+    }
+    if (my < s1 && !mine) atomicAdd(bad, 1u);
+    const uint32_t len = end - base;
+    for (uint32_t i = threadIdx.x; i < len; i += kSegSmallBlock) {
+        sk[i] = kin[base + i] ^ flip;
+        if constexpr (KV) sv[i] = vin[base + i];
+    }
+    __syncthreads();
+    if (mine) {  // Listing 1 on [lo, hi): shift larger keys right, insert (stable: strict >)
+        const uint32_t a = lo - base, b = hi - base;
+        for (uint32_t i = a + 1; i < b; i++) {
+            const K key = sk[i];
+            [[maybe_unused]] uint32_t val = 0;
+            if constexpr (KV) val = sv[i];
+            uint32_t j = i;
+            while (j > a && sk[j - 1] > key) {
+                sk[j] = sk[j - 1];
+                if constexpr (KV) sv[j] = sv[j - 1];
+                j--;
+            }
+            sk[j] = key;
+            if constexpr (KV) sv[j] = val;
+        }
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < len; i += kSegSmallBlock) {
+        kout[base + i] = sk[i] ^ flip;
+        if constexpr (KV) vout[base + i] = sv[i];
+    }
+}
+
+template <typename K, bool KV>
+__global__ void __launch_bounds__(kSegMedBlock)
+    k_seg_medium(const K *__restrict__ kin, const uint32_t *__restrict__ vin, K *__restrict__ kout,
+                 uint32_t *__restrict__ vout, const uint32_t *__restrict__ offsets, uint32_t nseg, uint64_t n, K flip,
+                 uint32_t maxlen, uint32_t *__restrict__ bad)
+{
+    pdl_begin();
+    __shared__ K sk[kSegMedMax];
+    __shared__ uint16_t si[kSegMedMax];
+    __shared__ uint32_t sv[KV ? kSegMedMax : 1];  // values staged too: in place is safe
+    const uint32_t seg = blockIdx.x;
+    if (seg >= nseg) return;
+    const uint32_t lo = __ldg(&offsets[seg]), hi = __ldg(&offsets[seg + 1]);
+    if (hi < lo || (uint64_t)hi > n || hi - lo > maxlen) {  // maxlen <= kSegMedMax
+        if (threadIdx.x == 0) atomicAdd(bad, 1u);
+        return;
+    }
+    const uint32_t len = hi - lo;
+    if (len < 2) {
+        if (len == 1 && threadIdx.x == 0) {
+            kout[lo] = kin[lo];
+            if constexpr (KV) vout[lo] = vin[lo];
+        }
+        return;
+    }
+    uint32_t P = 2;
+    while (P < len) P <<= 1;
+    const K kmax = ~K(0);
+    for (uint32_t i = threadIdx.x; i < P; i += kSegMedBlock) {
+        sk[i] = i < len ? (kin[lo + i] ^ flip) : kmax;
+        si[i] = (uint16_t)i;  // padding sorts after every real record: (max, index >= len)
+        if constexpr (KV)
+            if (i < len) sv[i] = vin[lo + i];
+    }
+    __syncthreads();
+    // bitonic network over (key, index): compare-exchange pairs (i, i ^ j)
+    for (uint32_t k = 2; k <= P; k <<= 1) {
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            for (uint32_t t = threadIdx.x; t < P / 2; t += kSegMedBlock) {
+                const uint32_t i = 2 * j * (t / j) + (t % j);  // lower index of the pair
+                const uint32_t l = i + j;
+                const bool up = (i & k) == 0;
+                const K a = sk[i], b = sk[l];
+                const uint16_t ia = si[i], ib = si[l];
+                const bool gt = a > b || (a == b && ia > ib);
+                if (gt == up) {
+                    sk[i] = b;
+                    sk[l] = a;
+                    si[i] = ib;
+                    si[l] = ia;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (uint32_t i = threadIdx.x; i < len; i += kSegMedBlock) {
+        kout[lo + i] = sk[i] ^ flip;
+        if constexpr (KV) vout[lo + i] = sv[si[i]];
+    }
+}
+
+}  // namespace ahs
