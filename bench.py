@@ -260,6 +260,46 @@ def entropy_exact_report(torch, ahs, keys_np, vals_np, device, reps=5):
                     "paper-literal FSM = RANGE norm (0.7 log2 k) with H over distinct values"}
 
 
+def segments_report(torch, ahs, device, reps=10):
+    """NEXT-4: ahs_sort_segments on two segment-length mixes (L2 flushed per run): the
+    paper's small-n regime (2^20 segments of 1..20 keys: Listing 1's insertion sort, one
+    thread per segment) and 2^13 segments of 1000..2048 keys (one CTA each).  Algorithmic
+    bytes: read + write of keys (and values) + the offsets."""
+    rows = []
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
+    for name, nseg, lo, hi, kv in (("insertion_1_20", 1 << 20, 1, 20, False),
+                                   ("insertion_1_20_kv", 1 << 20, 1, 20, True),
+                                   ("bitonic_1000_2048", 1 << 13, 1000, 2048, False)):
+        lens = np.random.default_rng(7).integers(lo, hi + 1, nseg)
+        off = np.zeros(nseg + 1, dtype=np.int64)
+        off[1:] = np.cumsum(lens)
+        n = int(off[-1])
+        keys = (synth.stream(5, n) >> np.uint64(32)).astype(np.uint32).view(np.int32)
+        dk = upload(torch, keys, device)
+        dv = torch.arange(n, dtype=torch.int32, device=device).view(torch.uint32) if kv else None
+        ko, vo = torch.empty_like(dk), (torch.empty_like(dv) if kv else None)
+        doff = torch.from_numpy(off.astype(np.uint32).view(np.int32)).to(device)
+        bad = torch.zeros(1, dtype=torch.int32, device=device)
+        for _ in range(3):
+            ahs.ahs_sort_segments(dk, dv, ko, vo, doff, hi, bad)
+        torch.cuda.synchronize(device)
+        ts = []
+        for _ in range(reps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            ahs.ahs_sort_segments(dk, dv, ko, vo, doff, hi, bad)
+            b.record()
+            torch.cuda.synchronize(device)
+            ts.append(a.elapsed_time(b))
+        ms = statistics.median(ts)
+        byts = n * (8 + (8 if kv else 0)) + 4 * (nseg + 1)
+        rows.append({"case": name, "segments": nseg, "n": n, "kv": kv, "max_segment": hi, "us": ms * 1e3,
+                     "Gkeys_s": n / (ms * 1e-3) / 1e9, "GBps": byts / (ms * 1e-3) / 1e9,
+                     "bad": int(bad.item())})
+    return rows
+
+
 def time_e2e(torch, ahs, keys_np, vals_np, steps, warmup, device):
     """Same metric through the C-ABI host entry point: pinned host buffers, H2D and D2H
     inside the timed region every step."""
@@ -377,6 +417,11 @@ def run_ours(args):
     # NEXT-2: paper-literal entropy of the output and the branch it implies
     if rank == 0:
         out["entropy_exact"] = entropy_exact_report(torch, ahs, keys, vals, device)
+    # NEXT-4: batched small-n segment sorts
+    if rank == 0 and args.configs:
+        out["segments"] = segments_report(torch, ahs, device)
+        for r in out["segments"]:
+            r["frac_of_peak"] = r["GBps"] / peak
     # end to end through the C ABI with host buffers
     if not args.no_e2e:
         e_ms, bi, bo = time_e2e(torch, ahs, keys, vals, max(3, args.steps // 2), 2, device)

@@ -1018,24 +1018,46 @@ int ahs_sort_host(const void *h_keys_in, const uint32_t *h_vals_in, void *h_keys
 // --------------------------------------------------- segment sort (NEXT-4)
 }  // extern "C"
 namespace {
+template <typename K, bool KV, int L>
+cudaError_t seg_small(const void *kin, const uint32_t *vin, void *kout, uint32_t *vout, uint64_t n,
+                      const uint32_t *offsets, uint32_t nseg, uint32_t max_segment, K flip, uint32_t *bad,
+                      cudaStream_t s)
+{
+    constexpr size_t smem = seg_small_smem<K, KV>();
+    static const bool attr = cudaFuncSetAttribute(k_seg_small<K, KV, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  (int)smem) == cudaSuccess;
+    if (!attr) return cudaErrorInvalidValue;
+    const unsigned g = (nseg + kSegSmallBlock - 1) / kSegSmallBlock;
+    return launch_k(k_seg_small<K, KV, L>, dim3(g), dim3(kSegSmallBlock), smem, s, (const K *)kin, vin, (K *)kout,
+                    vout, offsets, nseg, n, flip, max_segment, bad);
+}
+
+template <typename K, bool KV, int BLOCK>
+cudaError_t seg_medium(const void *kin, const uint32_t *vin, void *kout, uint32_t *vout, uint64_t n,
+                       const uint32_t *offsets, uint32_t nseg, uint32_t max_segment, K flip, uint32_t *bad,
+                       cudaStream_t s)
+{
+    return launch_k(k_seg_medium<K, KV, BLOCK>, dim3(nseg), dim3(BLOCK), 0, s, (const K *)kin, vin, (K *)kout, vout,
+                    offsets, nseg, n, flip, max_segment, bad);
+}
+
+// register network length / CTA size from the declared maximum segment
 template <typename K, bool KV>
 cudaError_t seg_launch(const void *kin, const uint32_t *vin, void *kout, uint32_t *vout, uint64_t n,
                        const uint32_t *offsets, uint32_t nseg, uint32_t max_segment, K flip, uint32_t *bad,
                        cudaStream_t s)
 {
-    if (max_segment <= (uint32_t)kSegSmallMax) {
-        constexpr size_t smem = seg_small_smem<K, KV>();
-        static bool attr = [] {
-            return cudaFuncSetAttribute(k_seg_small<K, KV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)smem) == cudaSuccess;
-        }();
-        if (!attr) return cudaErrorInvalidValue;
-        const unsigned g = (nseg + kSegSmallBlock - 1) / kSegSmallBlock;
-        return launch_k(k_seg_small<K, KV>, dim3(g), dim3(kSegSmallBlock), smem, s, (const K *)kin, vin, (K *)kout,
-                        vout, offsets, nseg, n, flip, max_segment, bad);
-    }
-    return launch_k(k_seg_medium<K, KV>, dim3(nseg), dim3(kSegMedBlock), 0, s, (const K *)kin, vin, (K *)kout, vout,
-                    offsets, nseg, n, flip, max_segment, bad);
+#define AHS_SEG_ARGS kin, vin, kout, vout, n, offsets, nseg, max_segment, flip, bad, s
+    if (max_segment <= 8) return seg_small<K, KV, 8>(AHS_SEG_ARGS);
+    if (max_segment <= 16) return seg_small<K, KV, 16>(AHS_SEG_ARGS);
+    if (max_segment <= 20) return seg_small<K, KV, 20>(AHS_SEG_ARGS);  // the paper's n <= 20 Insertion branch
+    if (max_segment <= 24) return seg_small<K, KV, 24>(AHS_SEG_ARGS);
+    if (max_segment <= (uint32_t)kSegSmallMax) return seg_small<K, KV, 32>(AHS_SEG_ARGS);
+    if (max_segment <= 128) return seg_medium<K, KV, 64>(AHS_SEG_ARGS);
+    if (max_segment <= 256) return seg_medium<K, KV, 128>(AHS_SEG_ARGS);
+    if (max_segment <= 512) return seg_medium<K, KV, 256>(AHS_SEG_ARGS);
+    return seg_medium<K, KV, 512>(AHS_SEG_ARGS);
+#undef AHS_SEG_ARGS
 }
 }  // namespace
 extern "C" {

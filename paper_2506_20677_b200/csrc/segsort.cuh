@@ -6,9 +6,12 @@
 //
 //   K9s  max segment <= 32: a CTA of 256 threads owns 256 consecutive segments
 //        (<= 8192 keys, one contiguous range): coalesced load of the range into
-//        shared memory, one thread per segment runs Listing 1's insertion sort
-//        (strict > : stable) in shared memory, coalesced store.
-//   K9m  max segment <= 2048: one CTA (512 threads) per segment: bitonic sort
+//        shared memory; each thread takes its segment into registers (padded to
+//        L in {8, 16, 20, 24, 32} with the largest key) and runs Listing 1's
+//        insertion sort as unrolled adjacent swaps (strict > : stable); coalesced
+//        store.
+//   K9m  max segment <= 2048: one CTA per segment (P/2 threads for the padded
+//        length P, 64 .. 512): bitonic sort
 //        in shared memory on (key, original index) -- unique, so the result is
 //        the stable order -- padded to a power of two with (max, max) records;
 //        values gathered by the sorted indices.
@@ -32,12 +35,13 @@ constexpr size_t seg_small_smem()
     return (size_t)kSegSmallBlock * kSegSmallMax * (sizeof(K) + (KV ? 4 : 0));
 }
 
-template <typename K, bool KV>
+template <typename K, bool KV, int L>
 __global__ void __launch_bounds__(kSegSmallBlock)
     k_seg_small(const K *__restrict__ kin, const uint32_t *__restrict__ vin, K *__restrict__ kout,
                 uint32_t *__restrict__ vout, const uint32_t *__restrict__ offsets, uint32_t nseg, uint64_t n, K flip,
                 uint32_t maxlen, uint32_t *__restrict__ bad)
 {
+    static_assert(L >= 2 && L <= kSegSmallMax, "register network length");
     pdl_begin();
     constexpr uint32_t CAP = kSegSmallBlock * kSegSmallMax;
     extern __shared__ __align__(16) uint8_t seg_smem[];  // keys [CAP] then values [CAP]: seg_small_smem<K, KV>()
@@ -46,7 +50,7 @@ __global__ void __launch_bounds__(kSegSmallBlock)
     __shared__ uint32_t s_ok;
     const uint32_t s0 = blockIdx.x * kSegSmallBlock, s1 = min(nseg, s0 + kSegSmallBlock);
     const uint32_t base = __ldg(&offsets[s0]), end = __ldg(&offsets[s1]);
-    // the range must hold the CTA's segments (each <= kSegSmallMax, inside [0, n))
+    // the range must hold the CTA's segments (each <= L keys, inside [0, n))
     if (threadIdx.x == 0) s_ok = (end >= base && (uint64_t)end <= n && end - base <= CAP) ? 1u : 0u;
     const uint32_t my = s0 + threadIdx.x;
     uint32_t lo = 0, hi = 0;
@@ -54,7 +58,7 @@ __global__ void __launch_bounds__(kSegSmallBlock)
     if (mine) {
         lo = __ldg(&offsets[my]);
         hi = __ldg(&offsets[my + 1]);
-        if (hi < lo || hi - lo > maxlen || lo < base || hi > end) mine = false;  // maxlen <= kSegSmallMax
+        if (hi < lo || hi - lo > maxlen || lo < base || hi > end) mine = false;  // maxlen <= L
     }
     __syncthreads();
     if (!s_ok) {
@@ -68,21 +72,40 @@ __global__ void __launch_bounds__(kSegSmallBlock)
         if constexpr (KV) sv[i] = vin[base + i];
     }
     __syncthreads();
-    if (mine) {  // Listing 1 on [lo, hi): shift larger keys right, insert (stable: strict >)
-        const uint32_t a = lo - base, b = hi - base;
-        for (uint32_t i = a + 1; i < b; i++) {
-            const K key = sk[i];
-            [[maybe_unused]] uint32_t val = 0;
-            if constexpr (KV) val = sv[i];
-            uint32_t j = i;
-            while (j > a && sk[j - 1] > key) {
-                sk[j] = sk[j - 1];
-                if constexpr (KV) sv[j] = sv[j - 1];
-                j--;
-            }
-            sk[j] = key;
-            if constexpr (KV) sv[j] = val;
+    if (mine) {
+        // the segment into registers, padded with the largest key (padding stays
+        // last: the network only moves a key past a strictly greater one)
+        const uint32_t a = lo - base, m = hi - lo;
+        K r[L];
+        [[maybe_unused]] uint32_t q[KV ? L : 1];
+#pragma unroll
+        for (int i = 0; i < L; i++) {
+            r[i] = (uint32_t)i < m ? sk[a + i] : ~K(0);
+            if constexpr (KV) q[i] = (uint32_t)i < m ? sv[a + i] : 0u;
         }
+        // Listing 1 as adjacent swaps: key i moves left past every
+        // strictly greater key (stable); unrolled so the array stays in registers
+#pragma unroll
+        for (int i = 1; i < L; i++) {
+#pragma unroll
+            for (int j = i; j > 0; j--) {
+                const bool sw = r[j - 1] > r[j];
+                const K x = r[j - 1], y = r[j];
+                r[j - 1] = sw ? y : x;
+                r[j] = sw ? x : y;
+                if constexpr (KV) {
+                    const uint32_t u = q[j - 1], w = q[j];
+                    q[j - 1] = sw ? w : u;
+                    q[j] = sw ? u : w;
+                }
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < L; i++)
+            if ((uint32_t)i < m) {
+                sk[a + i] = r[i];
+                if constexpr (KV) sv[a + i] = q[i];
+            }
     }
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < len; i += kSegSmallBlock) {
@@ -91,8 +114,8 @@ __global__ void __launch_bounds__(kSegSmallBlock)
     }
 }
 
-template <typename K, bool KV>
-__global__ void __launch_bounds__(kSegMedBlock)
+template <typename K, bool KV, int BLOCK>
+__global__ void __launch_bounds__(BLOCK)
     k_seg_medium(const K *__restrict__ kin, const uint32_t *__restrict__ vin, K *__restrict__ kout,
                  uint32_t *__restrict__ vout, const uint32_t *__restrict__ offsets, uint32_t nseg, uint64_t n, K flip,
                  uint32_t maxlen, uint32_t *__restrict__ bad)
@@ -119,7 +142,7 @@ __global__ void __launch_bounds__(kSegMedBlock)
     uint32_t P = 2;
     while (P < len) P <<= 1;
     const K kmax = ~K(0);
-    for (uint32_t i = threadIdx.x; i < P; i += kSegMedBlock) {
+    for (uint32_t i = threadIdx.x; i < P; i += BLOCK) {
         sk[i] = i < len ? (kin[lo + i] ^ flip) : kmax;
         si[i] = (uint16_t)i;  // padding sorts after every real record: (max, index >= len)
         if constexpr (KV)
@@ -129,8 +152,8 @@ __global__ void __launch_bounds__(kSegMedBlock)
     // bitonic network over (key, index): compare-exchange pairs (i, i ^ j)
     for (uint32_t k = 2; k <= P; k <<= 1) {
         for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-            for (uint32_t t = threadIdx.x; t < P / 2; t += kSegMedBlock) {
-                const uint32_t i = 2 * j * (t / j) + (t % j);  // lower index of the pair
+            for (uint32_t t = threadIdx.x; t < P / 2; t += BLOCK) {
+                const uint32_t i = ((t & ~(j - 1)) << 1) | (t & (j - 1));  // lower index of the pair (j = 2^m)
                 const uint32_t l = i + j;
                 const bool up = (i & k) == 0;
                 const K a = sk[i], b = sk[l];
@@ -146,7 +169,7 @@ __global__ void __launch_bounds__(kSegMedBlock)
             __syncthreads();
         }
     }
-    for (uint32_t i = threadIdx.x; i < len; i += kSegMedBlock) {
+    for (uint32_t i = threadIdx.x; i < len; i += BLOCK) {
         kout[lo + i] = sk[i] ^ flip;
         if constexpr (KV) vout[lo + i] = sv[si[i]];
     }
