@@ -212,6 +212,9 @@ AHS_API int ahs_sort_host(const void *h_keys_in, const uint32_t *h_vals_in, void
  * ENOSPACE, ERANGE (n > AHS_MAX_N), ENODEV, ECUDA. */
 AHS_API int ahs_entropy_sorted(const void *d_keys, uint64_t n, void *d_ws, size_t ws_bytes, double *H,
                                void *stream);
+/* The same for any key type (64-bit keys: NEXT-3); ahs_entropy_sorted = AHS_U32. */
+AHS_API int ahs_entropy_sorted_dtype(const void *d_keys, uint64_t n, int32_t dtype, void *d_ws, size_t ws_bytes,
+                                     double *H, void *stream);
 
 /* ------------------------------------------- batched segment sort (NEXT-4) */
 /* Many small independent sorts in one call: the GPU form of the paper's small-n

@@ -73,6 +73,7 @@ def lib():
             "ahs_workspace_bytes": ([u64], sz),
             "ahs_sort_tmp_bytes": ([u64, C.c_int], sz),
             "ahs_sort_tmp_bytes_dtype": ([u64, C.c_int, i32], sz),
+            "ahs_entropy_sorted_dtype": ([vp, u64, i32, vp, sz, C.POINTER(C.c_double), vp], C.c_int),
             "ahs_model_load": ([C.c_char_p, sz, C.POINTER(vp), C.c_char_p, sz], C.c_int),
             "ahs_sort_segments": ([vp, vp, vp, vp, u64, vp, C.c_uint32, C.c_uint32, i32, vp, vp], C.c_int),
             "ahs_model_free": ([vp], None),
@@ -162,8 +163,8 @@ def ahs_rank_mode(mode: int = -1) -> int:
 def ahs_entropy_sorted(keys, ws: "Workspace", stream=None) -> float:
     """NEXT-2: per-distinct-value entropy of a CUDA key array whose equal keys are contiguous."""
     h = C.c_double()
-    rc = lib().ahs_entropy_sorted(_dev_ptr(keys), keys.numel(), _dev_ptr(ws.ws), ws.ws_bytes, C.byref(h),
-                                  _stream(stream))
+    rc = lib().ahs_entropy_sorted_dtype(_dev_ptr(keys), keys.numel(), _dtype_code(keys), _dev_ptr(ws.ws),
+                                        ws.ws_bytes, C.byref(h), _stream(stream))
     _check(rc, "ahs_entropy_sorted")
     return h.value
 

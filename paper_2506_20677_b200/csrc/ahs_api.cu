@@ -155,8 +155,12 @@ int device_info(int *sms, int *hist_clusters = nullptr, DevInfo **info = nullptr
             }
             if (good) {  // K8: co-resident CTAs for its cooperative launch
                 int per = 0;
+                int per64 = 0;
                 good &= cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_entropy_sorted<kEntBlock>,
                                                                       kEntBlock, 0) == cudaSuccess;
+                good &= cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                            &per64, k_entropy_sorted<kEntBlock, uint64_t>, kEntBlock, 0) == cudaSuccess;
+                per = std::min(per, per64);  // one cooperative grid size for both key widths
                 d.ent_grid = std::min(kEntMaxGrid, per * d.sms);
                 good &= d.ent_grid > 0;
             }
@@ -907,11 +911,20 @@ int ahs_sort(const void *d_keys_in, const uint32_t *d_vals_in, void *d_keys_out,
 // ------------------------------------------------------------ NEXT-2
 int ahs_entropy_sorted(const void *d_keys, uint64_t n, void *d_ws, size_t ws_bytes, double *H, void *stream)
 {
+    return ahs_entropy_sorted_dtype(d_keys, n, AHS_U32, d_ws, ws_bytes, H, stream);
+}
+
+int ahs_entropy_sorted_dtype(const void *d_keys, uint64_t n, int32_t dtype, void *d_ws, size_t ws_bytes, double *H,
+                             void *stream)
+{
     if (!H) return AHS_EINVAL;
     *H = 0.0;
+    if (!dtype_valid(dtype)) return AHS_EINVAL;
     if (n == 0) return AHS_OK;
     if (n > AHS_MAX_N) return AHS_ERANGE;
-    if (!d_keys || !d_ws || ((uintptr_t)d_keys & 3u) || ((uintptr_t)d_ws & 15u)) return AHS_EINVAL;
+    if (!d_keys || !d_ws || ((uintptr_t)d_keys & (key_bytes_of(dtype) - 1)) || ((uintptr_t)d_ws & 15u))
+        return AHS_EINVAL;
+    const bool wide = dtype_wide(dtype);
     const WsLayout L = ws_layout();
     if (ws_bytes < L.total) return AHS_ENOSPACE;
     int sms = 0;
@@ -929,12 +942,13 @@ int ahs_entropy_sorted(const void *d_keys, uint64_t n, void *d_ws, size_t ws_byt
     double *csum = (double *)(ws + L.ent + kEntMaxGrid * sizeof(RunPieces));
     double *dH = csum + kEntMaxGrid;
     cudaStream_t s = (cudaStream_t)stream;
-    const uint32_t *keys = (const uint32_t *)d_keys;
+    const void *keys = d_keys;
     uint64_t nn = n;
     void *args[] = {&keys, &nn, &chunk, &pieces, &csum, &dH};
     cudaError_t e = launch(KID_ENTROPY_SORTED, s, [&] {
-        cudaLaunchCooperativeKernel((void *)k_entropy_sorted<kEntBlock>, dim3((unsigned)grid), dim3(kEntBlock),
-                                    args, 0, s);
+        cudaLaunchCooperativeKernel(wide ? (void *)k_entropy_sorted<kEntBlock, uint64_t>
+                                         : (void *)k_entropy_sorted<kEntBlock, uint32_t>,
+                                    dim3((unsigned)grid), dim3(kEntBlock), args, 0, s);
     });
     if (e != cudaSuccess) return AHS_ECUDA;
     if (cudaMemcpyAsync(H, dH, sizeof(double), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
@@ -1053,9 +1067,9 @@ cudaError_t seg_launch(const void *kin, const uint32_t *vin, void *kout, uint32_
     if (max_segment <= 20) return seg_small<K, KV, 20>(AHS_SEG_ARGS);  // the paper's n <= 20 Insertion branch
     if (max_segment <= 24) return seg_small<K, KV, 24>(AHS_SEG_ARGS);
     if (max_segment <= (uint32_t)kSegSmallMax) return seg_small<K, KV, 32>(AHS_SEG_ARGS);
-    if (max_segment <= 128) return seg_medium<K, KV, 64>(AHS_SEG_ARGS);
-    if (max_segment <= 256) return seg_medium<K, KV, 128>(AHS_SEG_ARGS);
-    if (max_segment <= 512) return seg_medium<K, KV, 256>(AHS_SEG_ARGS);
+    if (max_segment <= 256) return seg_medium<K, KV, 64>(AHS_SEG_ARGS);  // padded length 4 x BLOCK
+    if (max_segment <= 512) return seg_medium<K, KV, 128>(AHS_SEG_ARGS);
+    if (max_segment <= 1024) return seg_medium<K, KV, 256>(AHS_SEG_ARGS);
     return seg_medium<K, KV, 512>(AHS_SEG_ARGS);
 #undef AHS_SEG_ARGS
 }

@@ -38,9 +38,10 @@ struct RunPieces {
     uint32_t pad;
 };
 
-template <int BLOCK>
+// K: uint32_t, or uint64_t for 64-bit keys (NEXT-3); only key equality is used
+template <int BLOCK, typename K = uint32_t>
 __global__ void __launch_bounds__(BLOCK)
-    k_entropy_sorted(const uint32_t *__restrict__ keys, uint64_t n, uint64_t chunk,
+    k_entropy_sorted(const K *__restrict__ keys, uint64_t n, uint64_t chunk,
                      RunPieces *__restrict__ pieces, double *__restrict__ chunk_S, double *__restrict__ out_H)
 {
     pdl_begin();
@@ -63,34 +64,43 @@ __global__ void __launch_bounds__(BLOCK)
     double S = 0.0;
     const bool vec = ((uintptr_t)keys & 15u) == 0;  // chunk and tile starts are multiples of 16 keys
     constexpr uint32_t TILE = (uint32_t)BLOCK * kEntItems;
-    const uint32_t *kc = keys + c0;
+    const K *kc = keys + c0;
     // keys of tile t0 for this thread (keys past the chunk, up to n, are read
     // too: a run end looks one key ahead)
     // keys of tile t0 for this thread, plus the warp's edge neighbours (lane 0:
     // the key before its first, lane 31: the key after its last; keys past the
     // chunk, up to n, are read too: a run end looks one key ahead)
-    auto load = [&](uint32_t t0, uint32_t (&k)[kEntItems], uint32_t &edge) {
+    auto load = [&](uint32_t t0, K (&k)[kEntItems], K &edge) {
         const uint32_t i0 = t0 + threadIdx.x * kEntItems;
         if (vec && c0 + i0 + kEntItems <= n) {
             const uint4 *p4 = reinterpret_cast<const uint4 *>(kc + i0);
+            if constexpr (sizeof(K) == 4) {
 #pragma unroll
-            for (int q = 0; q < kEntItems / 4; q++) {
-                const uint4 x = ld_nc_v4(p4 + q);
-                k[4 * q] = x.x;
-                k[4 * q + 1] = x.y;
-                k[4 * q + 2] = x.z;
-                k[4 * q + 3] = x.w;
+                for (int q = 0; q < kEntItems / 4; q++) {
+                    const uint4 x = ld_nc_v4(p4 + q);
+                    k[4 * q] = x.x;
+                    k[4 * q + 1] = x.y;
+                    k[4 * q + 2] = x.z;
+                    k[4 * q + 3] = x.w;
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < kEntItems / 2; q++) {
+                    const uint4 x = ld_nc_v4(p4 + q);
+                    k[2 * q] = ((uint64_t)x.y << 32) | x.x;
+                    k[2 * q + 1] = ((uint64_t)x.w << 32) | x.z;
+                }
             }
         } else {
 #pragma unroll
-            for (int q = 0; q < kEntItems; q++) k[q] = (c0 + i0 + q < n) ? kc[i0 + q] : 0u;
+            for (int q = 0; q < kEntItems; q++) k[q] = (c0 + i0 + q < n) ? kc[i0 + q] : K(0);
         }
-        edge = 0u;
+        edge = K(0);
         if (lane == 0 && c0 + i0 > 0 && i0 < len) edge = kc[(int64_t)i0 - 1];
         if (lane == 31 && c0 + i0 + kEntItems < n) edge = kc[i0 + kEntItems];
     };
     const bool last_chunk = c1 == n;
-    uint32_t k[kEntItems], kn[kEntItems], edge = 0u, edge_n = 0u;
+    K k[kEntItems], kn[kEntItems], edge = K(0), edge_n = K(0);
     if (len > 0) load(0, kn, edge_n);
     for (uint32_t t0 = 0; t0 < len; t0 += TILE) {
         const uint32_t i0 = t0 + threadIdx.x * kEntItems;
@@ -99,8 +109,8 @@ __global__ void __launch_bounds__(BLOCK)
         edge = edge_n;
         if (t0 + TILE < len) load(t0 + TILE, kn, edge_n);  // next tile in flight while this one is scanned
         // neighbours: the previous / next thread's keys; the loaded edges at warp edges
-        uint32_t prev = __shfl_up_sync(kFull, k[kEntItems - 1], 1);
-        uint32_t next = __shfl_down_sync(kFull, k[0], 1);
+        K prev = __shfl_up_sync(kFull, k[kEntItems - 1], 1);
+        K next = __shfl_down_sync(kFull, k[0], 1);
         if (lane == 0) prev = edge;
         if (lane == 31) next = edge;
         // a start at local 0 of chunk 0 is real; elsewhere starts compare with the previous key

@@ -10,8 +10,10 @@
 //        L in {8, 16, 20, 24, 32} with the largest key) and runs Listing 1's
 //        insertion sort as unrolled adjacent swaps (strict > : stable); coalesced
 //        store.
-//   K9m  max segment <= 2048: one CTA per segment (P/2 threads for the padded
-//        length P, 64 .. 512): bitonic sort
+//   K9m  max segment <= 2048: one CTA per segment, every segment padded to
+//        P = 4 BLOCK (256 .. 2048, from the declared maximum), 4 records per
+//        thread in registers: a fully unrolled bitonic network (in-register,
+//        warp-shuffle and, for strides >= 128, shared-memory exchanges)
 //        in shared memory on (key, original index) -- unique, so the result is
 //        the stable order -- padded to a power of two with (max, max) records;
 //        values gathered by the sorted indices.
@@ -114,62 +116,122 @@ __global__ void __launch_bounds__(kSegSmallBlock)
     }
 }
 
+// (key, index) order: unique, so a sorting network over it yields the stable order
+template <typename K>
+__device__ __forceinline__ bool rec_gt(K a, uint32_t ia, K b, uint32_t ib)
+{
+    return a > b || (a == b && ia > ib);
+}
+
 template <typename K, bool KV, int BLOCK>
 __global__ void __launch_bounds__(BLOCK)
     k_seg_medium(const K *__restrict__ kin, const uint32_t *__restrict__ vin, K *__restrict__ kout,
                  uint32_t *__restrict__ vout, const uint32_t *__restrict__ offsets, uint32_t nseg, uint64_t n, K flip,
                  uint32_t maxlen, uint32_t *__restrict__ bad)
 {
+    // every segment of the launch is padded to P = 4 BLOCK records ((max key, position)
+    // records sort after the real ones); thread t holds positions 4t .. 4t + 3 in registers
+    constexpr int E = 4, P = BLOCK * E;
+    static_assert(P <= kSegMedMax && BLOCK % 32 == 0, "segment capacity");
     pdl_begin();
-    __shared__ K sk[kSegMedMax];
-    __shared__ uint16_t si[kSegMedMax];
-    __shared__ uint32_t sv[KV ? kSegMedMax : 1];  // values staged too: in place is safe
+    __shared__ K sk[P];
+    __shared__ uint32_t si[P];
+    __shared__ uint32_t sv[KV ? P : 1];  // values staged too: in place is safe
     const uint32_t seg = blockIdx.x;
     if (seg >= nseg) return;
     const uint32_t lo = __ldg(&offsets[seg]), hi = __ldg(&offsets[seg + 1]);
-    if (hi < lo || (uint64_t)hi > n || hi - lo > maxlen) {  // maxlen <= kSegMedMax
+    if (hi < lo || (uint64_t)hi > n || hi - lo > maxlen || hi - lo > (uint32_t)P) {
         if (threadIdx.x == 0) atomicAdd(bad, 1u);
         return;
     }
-    const uint32_t len = hi - lo;
+    const uint32_t len = hi - lo, t = threadIdx.x;
     if (len < 2) {
-        if (len == 1 && threadIdx.x == 0) {
+        if (len == 1 && t == 0) {
             kout[lo] = kin[lo];
             if constexpr (KV) vout[lo] = vin[lo];
         }
         return;
     }
-    uint32_t P = 2;
-    while (P < len) P <<= 1;
-    const K kmax = ~K(0);
-    for (uint32_t i = threadIdx.x; i < P; i += BLOCK) {
-        sk[i] = i < len ? (kin[lo + i] ^ flip) : kmax;
-        si[i] = (uint16_t)i;  // padding sorts after every real record: (max, index >= len)
+    for (uint32_t i = t; i < (uint32_t)P; i += BLOCK) {  // coalesced staging
+        sk[i] = i < len ? (kin[lo + i] ^ flip) : ~K(0);
         if constexpr (KV)
             if (i < len) sv[i] = vin[lo + i];
     }
     __syncthreads();
-    // bitonic network over (key, index): compare-exchange pairs (i, i ^ j)
-    for (uint32_t k = 2; k <= P; k <<= 1) {
-        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-            for (uint32_t t = threadIdx.x; t < P / 2; t += BLOCK) {
-                const uint32_t i = ((t & ~(j - 1)) << 1) | (t & (j - 1));  // lower index of the pair (j = 2^m)
-                const uint32_t l = i + j;
-                const bool up = (i & k) == 0;
-                const K a = sk[i], b = sk[l];
-                const uint16_t ia = si[i], ib = si[l];
-                const bool gt = a > b || (a == b && ia > ib);
-                if (gt == up) {
-                    sk[i] = b;
-                    sk[l] = a;
-                    si[i] = ib;
-                    si[l] = ia;
+    K key[E];
+    uint32_t idx[E];
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+        key[e] = sk[t * E + e];
+        idx[e] = t * E + e;
+    }
+    // bitonic network, fully unrolled: stride j < E in registers, j < 32 E by warp
+    // shuffles (partner lane t ^ j / E), larger strides through shared memory
+#pragma unroll
+    for (int k = 2; k <= P; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j < E) {
+#pragma unroll
+                for (int e = 0; e < E; e++) {
+                    const int pe = e ^ j;
+                    if (pe > e) {
+                        const bool up = ((t * E + e) & k) == 0;
+                        if (rec_gt(key[e], idx[e], key[pe], idx[pe]) == up) {
+                            const K tk = key[e];
+                            key[e] = key[pe];
+                            key[pe] = tk;
+                            const uint32_t ti = idx[e];
+                            idx[e] = idx[pe];
+                            idx[pe] = ti;
+                        }
+                    }
+                }
+            } else {
+                K ok[E];
+                uint32_t oi[E];
+                if (j < E * 32) {
+#pragma unroll
+                    for (int e = 0; e < E; e++) {
+                        ok[e] = __shfl_xor_sync(kFull, key[e], j / E);
+                        oi[e] = __shfl_xor_sync(kFull, idx[e], j / E);
+                    }
+                } else {
+                    __syncthreads();  // the previous exchange's reads are done
+#pragma unroll
+                    for (int e = 0; e < E; e++) {
+                        sk[t * E + e] = key[e];
+                        si[t * E + e] = idx[e];
+                    }
+                    __syncthreads();
+#pragma unroll
+                    for (int e = 0; e < E; e++) {
+                        ok[e] = sk[(t * E + e) ^ j];
+                        oi[e] = si[(t * E + e) ^ j];
+                    }
+                }
+#pragma unroll
+                for (int e = 0; e < E; e++) {
+                    const uint32_t p = t * E + e;
+                    const bool up = (p & k) == 0, lower = (p & j) == 0;
+                    // ascending: the lower position keeps the smaller record
+                    const bool take = rec_gt(key[e], idx[e], ok[e], oi[e]) == (lower == up);
+                    if (take) {
+                        key[e] = ok[e];
+                        idx[e] = oi[e];
+                    }
                 }
             }
-            __syncthreads();
         }
     }
-    for (uint32_t i = threadIdx.x; i < len; i += BLOCK) {
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+        sk[t * E + e] = key[e];
+        si[t * E + e] = idx[e];
+    }
+    __syncthreads();
+    for (uint32_t i = t; i < len; i += BLOCK) {  // coalesced store; values by the sorted indices
         kout[lo + i] = sk[i] ^ flip;
         if constexpr (KV) vout[lo + i] = sv[si[i]];
     }

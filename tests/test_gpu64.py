@@ -222,3 +222,17 @@ def test_dirty_workspace(dt):
             assert np.array_equal(to_host(ko, keys.dtype), want_k), (dt, kv, rep)
             if kv:
                 assert np.array_equal(to_host(vo, np.uint32), want_v), (dt, kv, rep)
+
+
+@pytest.mark.parametrize("family", ["full_u64", "i64_small", "u64_top_bits", "i64_extremes", "kmers30"])
+def test_entropy_sorted_64(family):
+    """NEXT-2 on 64-bit keys: K8 over the sorted output vs the oracle's H_exact (1e-9)."""
+    for n in (1, 2, 17, 4097, 100_003, 1_000_003):
+        keys = FAMILIES[family](n)
+        ok = np.sort(keys, kind="stable")
+        want = oracle.h_exact_sorted(ok)
+        ws = ahs.Workspace(n, False, key_dtype=keys.dtype)
+        got = ahs.ahs_entropy_sorted(to_dev(ok), ws)
+        assert abs(got - want) <= H_TOL, (family, n, got, want)
+        got = ahs.ahs_entropy_sorted(to_dev(ok, misalign=1), ws)
+        assert abs(got - want) <= H_TOL, (family, n, got, want)
