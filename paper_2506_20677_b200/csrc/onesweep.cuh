@@ -406,9 +406,15 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(const PassArgsT<K> a)
                         n_rounds++;
 #endif
                         uint32_t st[kLookback];
+                        if (jt >= kLookback - 1) {  // the whole window exists: one base, immediate offsets
+                            const uint32_t *ps = status + (size_t)jt * kBins + d;
     #pragma unroll
-                        for (int q = 0; q < kLookback; q++)
-                            st[q] = (jt - q >= 0) ? ld_relaxed(&status[(size_t)(jt - q) * kBins + d]) : kFlagIncl;
+                            for (int q = 0; q < kLookback; q++) st[q] = ld_relaxed(ps - q * kBins);
+                        } else {
+    #pragma unroll
+                            for (int q = 0; q < kLookback; q++)
+                                st[q] = (jt - q >= 0) ? ld_relaxed(&status[(size_t)(jt - q) * kBins + d]) : kFlagIncl;
+                        }
                         int used = 0;
                         bool fin = false, stop = false;
     #pragma unroll
