@@ -301,31 +301,48 @@ def segments_report(torch, ahs, device, reps=10):
 
 
 def time_e2e(torch, ahs, keys_np, vals_np, steps, warmup, device):
-    """Same metric through the C-ABI host entry point: pinned host buffers, H2D and D2H
-    inside the timed region every step."""
+    """Same metric through the C-ABI host entry point: pinned host buffers, every step's H2D
+    and D2H inside the timed region.  Steps alternate between two streams (each with its own
+    device scratch and pinned output buffers) through ahs_sort_host_async, so one step's D2H
+    overlaps the next step's H2D and compute (PCIe is full duplex); a stream is synchronized
+    before its buffers are reused.  Device time: events on both streams, from a start event
+    both wait on to the later of the two end events."""
     n = keys_np.size
-    hk = torch.from_numpy(keys_np.view(np.int32)).pin_memory()
-    hko = torch.empty_like(hk).pin_memory()
+    w = np.int64 if keys_np.itemsize == 8 else np.int32
+    hk = torch.from_numpy(keys_np.view(w)).pin_memory()
     hv = torch.from_numpy(vals_np.view(np.int32)).pin_memory() if vals_np is not None else None
-    hvo = torch.empty_like(hv).pin_memory() if hv is not None else None
-    if keys_np.dtype == np.uint32:
-        hk, hko = hk.view(torch.uint32), hko.view(torch.uint32)
+    hko = [torch.empty_like(hk).pin_memory() for _ in range(2)]
+    hvo = [torch.empty_like(hv).pin_memory() if hv is not None else None for _ in range(2)]
+    udt = {np.dtype(np.uint32): torch.uint32, np.dtype(np.uint64): torch.uint64}.get(keys_np.dtype)
+    if udt is not None:
+        hk, hko = hk.view(udt), [t.view(udt) for t in hko]
     if hv is not None:
-        hv, hvo = hv.view(torch.uint32), hvo.view(torch.uint32)
-    scratch = torch.empty(ahs.ahs_host_scratch_bytes(n, hv is not None), dtype=torch.uint8, device=device)
-    stream = torch.cuda.current_stream(device)
-    for _ in range(warmup):
-        ahs.ahs_sort_host(hk, hv, hko, hvo, scratch, stream=stream)
+        hv, hvo = hv.view(torch.uint32), [t.view(torch.uint32) for t in hvo]
+    nb = ahs.ahs_host_scratch_bytes(n, hv is not None, keys_np.dtype)
+    scratch = [torch.empty(nb, dtype=torch.uint8, device=device) for _ in range(2)]
+    streams = [torch.cuda.Stream(device), torch.cuda.Stream(device)]
+    for i in range(warmup):
+        ahs.ahs_sort_host(hk, hv, hko[i % 2], hvo[i % 2], scratch[i % 2], stream=streams[i % 2])
     torch.cuda.synchronize(device)
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(stream)
-    for _ in range(steps):
-        ahs.ahs_sort_host(hk, hv, hko, hvo, scratch, stream=stream)
-    b.record(stream)
+    start = torch.cuda.Event(enable_timing=True)
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    start.record(streams[0])
+    streams[1].wait_event(start)
+    for i in range(steps):
+        b = i % 2
+        if i >= 2:
+            streams[b].synchronize()  # step i - 2 used these buffers
+        ahs.ahs_sort_host(hk, hv, hko[b], hvo[b], scratch[b], stream=streams[b], sync=False)
+    for b in range(2):
+        ends[b].record(streams[b])
     torch.cuda.synchronize(device)
-    ms = a.elapsed_time(b)
-    nb = n * 4 * (2 if hv is not None else 1)
-    return ms, nb, nb
+    ms = max(start.elapsed_time(e) for e in ends)
+    last = hko[(steps - 1) % 2].view(torch.int64 if keys_np.itemsize == 8 else torch.int32).numpy().view(keys_np.dtype)
+    if not bool((last[1:] >= last[:-1]).all()):  # the host output of the last step is sorted
+        raise RuntimeError("e2e: ahs_sort_host_async produced unsorted output")
+    kb = keys_np.itemsize
+    nbi = n * kb + (n * 4 if hv is not None else 0)
+    return ms, nbi, nbi
 
 
 def sort_bytes(strategy: int, passes: int, n: int, kv: bool, shift: int = 1, kb: int = 4) -> int:

@@ -199,6 +199,16 @@ AHS_API int ahs_sort_host(const void *h_keys_in, const uint32_t *h_vals_in, void
                   uint32_t *h_vals_out, uint64_t n, int32_t dtype, const ahs_thresholds_t *th,
                   void *d_scratch, size_t scratch_bytes, ahs_features_t *feat,
                   int32_t *strategy, int32_t *rule, void *stream);
+/* The same without the final stream sync: returns once the sort and the D2H
+ * copies are enqueued on `stream` (the features round trip inside is the only
+ * wait).  h_keys_out / h_vals_out are valid, and the host inputs and d_scratch
+ * reusable, after `stream` completes.  Two streams with two scratch buffers
+ * overlap one sort's D2H with the next one's H2D and compute (PCIe is full
+ * duplex). */
+AHS_API int ahs_sort_host_async(const void *h_keys_in, const uint32_t *h_vals_in, void *h_keys_out,
+                                uint32_t *h_vals_out, uint64_t n, int32_t dtype, const ahs_thresholds_t *th,
+                                void *d_scratch, size_t scratch_bytes, ahs_features_t *feat, int32_t *strategy,
+                                int32_t *rule, void *stream);
 
 /* ------------------------------------------ paper-literal entropy (NEXT-2) */
 /* H over the DISTINCT key values (§III.A line 96, H = -sum_v p_v

@@ -89,6 +89,8 @@ def lib():
             "ahs_host_scratch_bytes": ([u64, C.c_int], sz),
             "ahs_sort_host": ([vp, vp, vp, vp, u64, i32, C.POINTER(Thresholds), vp, sz,
                                C.POINTER(Features), p_i32, p_i32, vp], C.c_int),
+            "ahs_sort_host_async": ([vp, vp, vp, vp, u64, i32, C.POINTER(Thresholds), vp, sz,
+                                     C.POINTER(Features), p_i32, p_i32, vp], C.c_int),
             "ahs_launch_count": ([], C.c_uint64),
             "ahs_rank_mode": ([C.c_int], C.c_int),
             "ahs_set_skip_trivial": ([C.c_int], C.c_int),
@@ -314,8 +316,10 @@ def sort(keys, vals=None, th: Thresholds | None = None, ws: Workspace | None = N
 
 
 def ahs_sort_host(keys: np.ndarray, vals: np.ndarray | None, keys_out: np.ndarray,
-                  vals_out: np.ndarray | None, scratch, th: Thresholds | None = None, stream=None):
-    """End to end from host arrays (numpy or pinned torch CPU tensors) through the C ABI."""
+                  vals_out: np.ndarray | None, scratch, th: Thresholds | None = None, stream=None,
+                  sync: bool = True):
+    """End to end from host arrays (numpy or pinned torch CPU tensors) through the C ABI.
+    sync=False: ahs_sort_host_async (outputs valid once `stream` completes)."""
     def hptr(a):
         if a is None:
             return None
@@ -330,9 +334,10 @@ def ahs_sort_host(keys: np.ndarray, vals: np.ndarray | None, keys_out: np.ndarra
     f = Features()
     s, r = C.c_int32(), C.c_int32()
     nbytes = scratch.numel() * scratch.element_size()
-    rc = lib().ahs_sort_host(hptr(keys), hptr(vals), hptr(keys_out), hptr(vals_out), n, code(keys),
-                             None if th is None else C.byref(th), _dev_ptr(scratch), nbytes, C.byref(f),
-                             C.byref(s), C.byref(r), _stream(stream))
+    fn = lib().ahs_sort_host if sync else lib().ahs_sort_host_async
+    rc = fn(hptr(keys), hptr(vals), hptr(keys_out), hptr(vals_out), n, code(keys),
+            None if th is None else C.byref(th), _dev_ptr(scratch), nbytes, C.byref(f),
+            C.byref(s), C.byref(r), _stream(stream))
     _check(rc, "ahs_sort_host")
     return f, s.value, r.value
 

@@ -974,6 +974,16 @@ int ahs_sort_host(const void *h_keys_in, const uint32_t *h_vals_in, void *h_keys
                   uint64_t n, int32_t dtype, const ahs_thresholds_t *th, void *d_scratch, size_t scratch_bytes,
                   ahs_features_t *feat, int32_t *strategy, int32_t *rule, void *stream)
 {
+    const int rc = ahs_sort_host_async(h_keys_in, h_vals_in, h_keys_out, h_vals_out, n, dtype, th, d_scratch,
+                                       scratch_bytes, feat, strategy, rule, stream);
+    if (rc) return rc;
+    return cudaStreamSynchronize((cudaStream_t)stream) == cudaSuccess ? AHS_OK : AHS_ECUDA;
+}
+
+int ahs_sort_host_async(const void *h_keys_in, const uint32_t *h_vals_in, void *h_keys_out, uint32_t *h_vals_out,
+                        uint64_t n, int32_t dtype, const ahs_thresholds_t *th, void *d_scratch, size_t scratch_bytes,
+                        ahs_features_t *feat, int32_t *strategy, int32_t *rule, void *stream)
+{
     if (!dtype_valid(dtype)) return AHS_EINVAL;
     const bool kv = h_vals_in != nullptr;
     if (n > 0 && (!h_keys_in || !h_keys_out || (kv && !h_vals_out) || !d_scratch)) return AHS_EINVAL;
@@ -1021,7 +1031,6 @@ int ahs_sort_host(const void *h_keys_in, const uint32_t *h_vals_in, void *h_keys
             return AHS_ECUDA;
         if (kv && cudaMemcpyAsync(h_vals_out, dv_out, n * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess)
             return AHS_ECUDA;
-        if (cudaStreamSynchronize(s) != cudaSuccess) return AHS_ECUDA;
     }
     if (feat) *feat = f;
     if (strategy) *strategy = st;

@@ -301,6 +301,33 @@ def test_host_entry_point():
     assert np.array_equal(ko, ref["keys"]) and np.array_equal(vo, ref["vals"])
 
 
+def test_host_entry_point_async_two_streams():
+    """ahs_sort_host_async on alternating streams / scratch buffers (pinned host memory), as the
+    bench's e2e leg runs it: every output equals the oracle's."""
+    inputs = [synth.cfg2(300_007), synth.uniform_range(71, 300_007, -50, 50), synth.cfg3(300_007, seed=72),
+              synth.cfg2(123_457)]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    nmax = max(k.size for k in inputs)
+    scratch = [torch.empty(ahs.ahs_host_scratch_bytes(nmax, True), dtype=torch.uint8, device="cuda")
+               for _ in range(2)]
+    outs = []
+    for i, keys in enumerate(inputs):
+        hk = torch.from_numpy(keys.view(np.int32)).pin_memory()
+        hv = torch.arange(keys.size, dtype=torch.int32).pin_memory().view(torch.uint32)
+        ko, vo = torch.empty_like(hk).pin_memory(), torch.empty_like(hv).pin_memory()
+        if keys.dtype == np.uint32:
+            hk, ko = hk.view(torch.uint32), ko.view(torch.uint32)
+        if i >= 2:
+            streams[i % 2].synchronize()
+        ahs.ahs_sort_host(hk, hv, ko, vo, scratch[i % 2], stream=streams[i % 2], sync=False)
+        outs.append((keys, hk, hv, ko, vo))
+    torch.cuda.synchronize()
+    for keys, hk, hv, ko, vo in outs:
+        ref = oracle.ahs(keys, np.arange(keys.size, dtype=np.uint32))
+        assert np.array_equal(ko.view(torch.int32).numpy().view(keys.dtype), ref["keys"])
+        assert np.array_equal(vo.view(torch.int32).numpy().view(np.uint32), ref["vals"])
+
+
 def test_launch_count_and_profile():
     keys = synth.cfg2(1 << 16)
     c0 = ahs.ahs_launch_count()
