@@ -302,11 +302,12 @@ def segments_report(torch, ahs, device, reps=10):
 
 def time_e2e(torch, ahs, keys_np, vals_np, steps, warmup, device):
     """Same metric through the C-ABI host entry point: pinned host buffers, every step's H2D
-    and D2H inside the timed region.  Steps alternate between two streams (each with its own
-    device scratch and pinned output buffers) through ahs_sort_host_async, so one step's D2H
-    overlaps the next step's H2D and compute (PCIe is full duplex); a stream is synchronized
-    before its buffers are reused.  Device time: events on both streams, from a start event
-    both wait on to the later of the two end events."""
+    and D2H inside the timed region.  Steps alternate between two streams, each with its own
+    device scratch, pinned output buffers and host thread, through ahs_sort_host_async: one
+    step's D2H overlaps the next step's H2D and compute (PCIe is full duplex), and a thread
+    waiting in its step's features round trip does not hold back the other's uploads; a
+    stream is synchronized before its buffers are reused.  Device time: events on both
+    streams, from a start event both wait on to the later of the two end events."""
     n = keys_np.size
     w = np.int64 if keys_np.itemsize == 8 else np.int32
     hk = torch.from_numpy(keys_np.view(w)).pin_memory()
@@ -328,13 +329,26 @@ def time_e2e(torch, ahs, keys_np, vals_np, steps, warmup, device):
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     start.record(streams[0])
     streams[1].wait_event(start)
-    for i in range(steps):
-        b = i % 2
-        if i >= 2:
-            streams[b].synchronize()  # step i - 2 used these buffers
-        ahs.ahs_sort_host(hk, hv, hko[b], hvo[b], scratch[b], stream=streams[b], sync=False)
-    for b in range(2):
-        ends[b].record(streams[b])
+    errors = []
+
+    def worker(b):  # one host thread per stream: it blocks in its step's features round trip
+        try:  # while the other thread's step keeps the copy engines busy
+            torch.cuda.set_device(device)
+            for i in range(b, steps, 2):
+                if i >= 2:
+                    streams[b].synchronize()  # step i - 2 used these buffers
+                ahs.ahs_sort_host(hk, hv, hko[b], hvo[b], scratch[b], stream=streams[b], sync=False)
+            ends[b].record(streams[b])
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(e)
+
+    threads = [threading.Thread(target=worker, args=(b,)) for b in range(2)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if errors:
+        raise errors[0]
     torch.cuda.synchronize(device)
     ms = max(start.elapsed_time(e) for e in ends)
     last = hko[(steps - 1) % 2].view(torch.int64 if keys_np.itemsize == 8 else torch.int32).numpy().view(keys_np.dtype)
