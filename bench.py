@@ -302,56 +302,67 @@ def segments_report(torch, ahs, device, reps=10):
 
 def time_e2e(torch, ahs, keys_np, vals_np, steps, warmup, device):
     """Same metric through the C-ABI host entry point: pinned host buffers, every step's H2D
-    and D2H inside the timed region.  Steps alternate between two streams, each with its own
+    and D2H inside the timed region.  Steps rotate over three streams, each with its own
     device scratch, pinned output buffers and host thread, through ahs_sort_host_async: one
-    step's D2H overlaps the next step's H2D and compute (PCIe is full duplex), and a thread
-    waiting in its step's features round trip does not hold back the other's uploads; a
-    stream is synchronized before its buffers are reused.  Device time: events on both
-    streams, from a start event both wait on to the later of the two end events."""
+    step's D2H overlaps the next steps' H2D and compute (PCIe is full duplex), and a thread
+    waiting in its step's features round trip does not hold back the others' uploads; a
+    stream is synchronized before its buffers are reused, three steps later, so the upload
+    engine never waits for a download.  Device time: events on every stream, from a start
+    event all wait on to the latest end event."""
     n = keys_np.size
     w = np.int64 if keys_np.itemsize == 8 else np.int32
     hk = torch.from_numpy(keys_np.view(w)).pin_memory()
     hv = torch.from_numpy(vals_np.view(np.int32)).pin_memory() if vals_np is not None else None
-    hko = [torch.empty_like(hk).pin_memory() for _ in range(2)]
-    hvo = [torch.empty_like(hv).pin_memory() if hv is not None else None for _ in range(2)]
+    NB = 3  # streams / buffers / host threads in flight
+    hko = [torch.empty_like(hk).pin_memory() for _ in range(NB)]
+    hvo = [torch.empty_like(hv).pin_memory() if hv is not None else None for _ in range(NB)]
     udt = {np.dtype(np.uint32): torch.uint32, np.dtype(np.uint64): torch.uint64}.get(keys_np.dtype)
     if udt is not None:
         hk, hko = hk.view(udt), [t.view(udt) for t in hko]
     if hv is not None:
         hv, hvo = hv.view(torch.uint32), [t.view(torch.uint32) for t in hvo]
     nb = ahs.ahs_host_scratch_bytes(n, hv is not None, keys_np.dtype)
-    scratch = [torch.empty(nb, dtype=torch.uint8, device=device) for _ in range(2)]
-    streams = [torch.cuda.Stream(device), torch.cuda.Stream(device)]
-    for i in range(warmup):
-        ahs.ahs_sort_host(hk, hv, hko[i % 2], hvo[i % 2], scratch[i % 2], stream=streams[i % 2])
-    torch.cuda.synchronize(device)
+    scratch = [torch.empty(nb, dtype=torch.uint8, device=device) for _ in range(NB)]
+    streams = [torch.cuda.Stream(device) for _ in range(NB)]
     start = torch.cuda.Event(enable_timing=True)
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-    start.record(streams[0])
-    streams[1].wait_event(start)
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(NB)]
     errors = []
+    ready, go = threading.Barrier(NB + 1), threading.Barrier(NB + 1)
 
     def worker(b):  # one host thread per stream: it blocks in its step's features round trip
-        try:  # while the other thread's step keeps the copy engines busy
+        try:  # while the other threads' steps keep the copy engines busy
             torch.cuda.set_device(device)
-            for i in range(b, steps, 2):
-                if i >= 2:
-                    streams[b].synchronize()  # step i - 2 used these buffers
+            for _ in range(max(1, warmup // NB)):  # per-thread warm-up (the library's per-thread
+                ahs.ahs_sort_host(hk, hv, hko[b], hvo[b], scratch[b], stream=streams[b])  # host buffer)
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(e)
+        ready.wait()
+        go.wait()
+        try:
+            for i in range(b, steps, NB):
+                if i >= NB:
+                    streams[b].synchronize()  # step i - NB used these buffers
                 ahs.ahs_sort_host(hk, hv, hko[b], hvo[b], scratch[b], stream=streams[b], sync=False)
             ends[b].record(streams[b])
         except Exception as e:  # pragma: no cover - reported below
             errors.append(e)
 
-    threads = [threading.Thread(target=worker, args=(b,)) for b in range(2)]
+    threads = [threading.Thread(target=worker, args=(b,)) for b in range(NB)]
     for t in threads:
         t.start()
+    ready.wait()
+    torch.cuda.synchronize(device)
+    start.record(streams[0])
+    for b in range(1, NB):
+        streams[b].wait_event(start)
+    go.wait()
     for t in threads:
         t.join()
     if errors:
         raise errors[0]
     torch.cuda.synchronize(device)
     ms = max(start.elapsed_time(e) for e in ends)
-    last = hko[(steps - 1) % 2].view(torch.int64 if keys_np.itemsize == 8 else torch.int32).numpy().view(keys_np.dtype)
+    last = hko[(steps - 1) % NB].view(torch.int64 if keys_np.itemsize == 8 else torch.int32).numpy().view(keys_np.dtype)
     if not bool((last[1:] >= last[:-1]).all()):  # the host output of the last step is sorted
         raise RuntimeError("e2e: ahs_sort_host_async produced unsorted output")
     kb = keys_np.itemsize
