@@ -145,6 +145,8 @@ AHS_API size_t ahs_workspace_bytes(uint64_t n);
  * key type (0 for an invalid dtype). */
 AHS_API size_t ahs_sort_tmp_bytes(uint64_t n, int has_vals);
 AHS_API size_t ahs_sort_tmp_bytes_dtype(uint64_t n, int has_vals, int32_t dtype);
+/* value_bytes: 0 (keys only), 4 or 8 (64-bit payloads, NEXT-3); 0 for invalid arguments. */
+AHS_API size_t ahs_sort_tmp_bytes_ex(uint64_t n, uint32_t value_bytes, int32_t dtype);
 
 /* Number of 8-bit digit passes ahs_sort will run for this strategy
  * (RADIX: ceil(bits/8) per Eq. 4; GENERAL: 4; COUNTING: 0 keys-only or 1 KV). */
@@ -188,6 +190,13 @@ AHS_API int ahs_select(const ahs_features_t *feat, const ahs_thresholds_t *th, i
 AHS_API int ahs_sort(const void *d_keys_in, const uint32_t *d_vals_in, void *d_keys_out,
              uint32_t *d_vals_out, uint64_t n, int32_t strategy, const ahs_features_t *feat,
              void *d_ws, size_t ws_bytes, void *d_tmp, size_t tmp_bytes, void *stream);
+/* ahs_sort with 4- or 8-byte values (value_bytes; ignored when d_vals_in is
+ * NULL): 64-bit payloads (NEXT-3).  The values are moved bit-exactly; d_tmp >=
+ * ahs_sort_tmp_bytes_ex(n, value_bytes, dtype).  EINVAL for another value_bytes
+ * or value pointers not aligned to it. */
+AHS_API int ahs_sort_ex(const void *d_keys_in, const void *d_vals_in, void *d_keys_out, void *d_vals_out,
+                        uint64_t n, uint32_t value_bytes, int32_t strategy, const ahs_features_t *feat,
+                        void *d_ws, size_t ws_bytes, void *d_tmp, size_t tmp_bytes, void *stream);
 
 /* End to end from HOST buffers: H2D copy, ahs_features, ahs_select, ahs_sort,
  * D2H copy, stream sync.  h_* are host pointers (pinned for full speed);

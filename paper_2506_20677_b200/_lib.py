@@ -73,6 +73,9 @@ def lib():
             "ahs_workspace_bytes": ([u64], sz),
             "ahs_sort_tmp_bytes": ([u64, C.c_int], sz),
             "ahs_sort_tmp_bytes_dtype": ([u64, C.c_int, i32], sz),
+            "ahs_sort_tmp_bytes_ex": ([u64, C.c_uint32, i32], sz),
+            "ahs_sort_ex": ([vp, vp, vp, vp, u64, C.c_uint32, i32, C.POINTER(Features), vp, sz, vp, sz, vp],
+                            C.c_int),
             "ahs_entropy_sorted_dtype": ([vp, u64, i32, vp, sz, C.POINTER(C.c_double), vp], C.c_int),
             "ahs_model_load": ([C.c_char_p, sz, C.POINTER(vp), C.c_char_p, sz], C.c_int),
             "ahs_sort_segments": ([vp, vp, vp, vp, u64, vp, C.c_uint32, C.c_uint32, i32, vp, vp], C.c_int),
@@ -259,14 +262,15 @@ def _stream(stream):
 class Workspace:
     """Device buffers for one n: ws (features) and tmp (sort), owned by torch."""
 
-    def __init__(self, n: int, has_vals: bool, device=None, key_dtype=None):
+    def __init__(self, n: int, has_vals: bool, device=None, key_dtype=None, val_bytes: int = 4):
         torch = _torch()
         device = device or torch.device("cuda", torch.cuda.current_device())
         self.n, self.has_vals = n, has_vals
         self.ws_bytes = ahs_workspace_bytes(n)
-        # key_dtype: None = 32-bit keys; else a torch / numpy dtype or ahs code (64-bit keys need more)
-        self.tmp_bytes = (ahs_sort_tmp_bytes(n, has_vals) if key_dtype is None
-                          else ahs_sort_tmp_bytes_dtype(n, has_vals, key_dtype))
+        # key_dtype: None = 32-bit keys; else a torch / numpy dtype or ahs code (64-bit keys need more);
+        # val_bytes: 4 or 8 (64-bit payloads)
+        self.tmp_bytes = lib().ahs_sort_tmp_bytes_ex(n, val_bytes if has_vals else 0,
+                                                     AHS_U32 if key_dtype is None else _code_of(key_dtype))
         self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=device)
         self.tmp = torch.empty(self.tmp_bytes, dtype=torch.uint8, device=device)
 
@@ -289,9 +293,11 @@ def ahs_select(feat: Features, th: Thresholds | None = None) -> tuple[int, int]:
 
 def ahs_sort(keys_in, vals_in, keys_out, vals_out, strategy: int, feat: Features, ws: Workspace,
              stream=None):
-    rc = lib().ahs_sort(_dev_ptr(keys_in), _dev_ptr(vals_in), _dev_ptr(keys_out), _dev_ptr(vals_out),
-                        keys_in.numel(), strategy, C.byref(feat), _dev_ptr(ws.ws), ws.ws_bytes,
-                        _dev_ptr(ws.tmp), ws.tmp_bytes, _stream(stream))
+    """Values: 4-byte (int32 / uint32 / float32 ...) or 8-byte tensors (64-bit payloads: ahs_sort_ex)."""
+    vb = vals_in.element_size() if vals_in is not None else 4
+    rc = lib().ahs_sort_ex(_dev_ptr(keys_in), _dev_ptr(vals_in), _dev_ptr(keys_out), _dev_ptr(vals_out),
+                           keys_in.numel(), vb, strategy, C.byref(feat), _dev_ptr(ws.ws), ws.ws_bytes,
+                           _dev_ptr(ws.tmp), ws.tmp_bytes, _stream(stream))
     _check(rc, "ahs_sort")
 
 
@@ -303,7 +309,8 @@ def sort(keys, vals=None, th: Thresholds | None = None, ws: Workspace | None = N
     torch = _torch()
     n = keys.numel()
     if ws is None:
-        ws = Workspace(n, vals is not None, keys.device, key_dtype=keys.dtype)
+        ws = Workspace(n, vals is not None, keys.device, key_dtype=keys.dtype,
+                       val_bytes=vals.element_size() if vals is not None else 4)
     feat = ahs_features(keys, ws, stream)
     strategy, rule = ahs_select(feat, th)
     if out is None:

@@ -30,12 +30,12 @@ struct DevInfo {
     int sms = 0;
     int hist_clusters = 0;  // co-resident K2 clusters
     // K6 variants: [kv][rank mode]
-    // K6 variants [key width: 0 = 32-bit, 1 = 64-bit][kv][rank mode]
-    const void *os_fn[2][2][2] = {};
-    size_t os_smem[2][2][2] = {};
-    int os_tile[2][2][2] = {};
-    int os_per_sm[2][2][2] = {};  // co-resident CTAs per SM
-    int os_block[2][2][2] = {};
+    // K6 variants [key width: 0 = 32-bit, 1 = 64-bit][values: 0 none, 1 32-bit, 2 64-bit][rank mode]
+    const void *os_fn[2][3][2] = {};
+    size_t os_smem[2][3][2] = {};
+    int os_tile[2][3][2] = {};
+    int os_per_sm[2][3][2] = {};  // co-resident CTAs per SM
+    int os_block[2][3][2] = {};
     bool lane_order_ok = false;              // self-test of the ordered ranking passed
     int ent_grid = 0;                        // K8 cooperative grid
     int rank_mode = kRankMasked;
@@ -132,8 +132,14 @@ int device_info(int *sms, int *hist_clusters = nullptr, DevInfo **info = nullptr
             set_k6(1, 0, kRankOrdered, (const void *)K6W_KEYS_O, OsKeys64O::kSmem, OsKeys64O::kTile, kSortBlock);
             set_k6(1, 1, kRankOrdered, (const void *)K6W_PAIRS_O, OsPairs64O::kSmem, OsPairs64O::kTile,
                    kSortBlockPairsO);
+            set_k6(0, 2, kRankMasked, (const void *)K6V_PAIRS_M, OsPairsV64M::kSmem, OsPairsV64M::kTile, kSortBlock);
+            set_k6(0, 2, kRankOrdered, (const void *)K6V_PAIRS_O, OsPairsV64O::kSmem, OsPairsV64O::kTile,
+                   kSortBlockPairsO);
+            set_k6(1, 2, kRankMasked, (const void *)K6WV_PAIRS_M, OsPairs64V64M::kSmem, OsPairs64V64M::kTile, 256);
+            set_k6(1, 2, kRankOrdered, (const void *)K6WV_PAIRS_O, OsPairs64V64O::kSmem, OsPairs64V64O::kTile,
+                   kSortBlockPairsO);
             for (int w = 0; w < 2; w++)
-                for (int kv = 0; kv < 2; kv++)
+                for (int kv = 0; kv < 3; kv++)
                     for (int m = 0; m < 2; m++) {
                         // persistent K6 grids: co-resident CTAs per SM
                         good &= cudaFuncSetAttribute(d.os_fn[w][kv][m], cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -311,7 +317,7 @@ struct TmpLayout {
     size_t ctrl, dhist, bucket, ticket, status, status_region_bytes, keys, vals, total;
 };
 constexpr int kTicketPlan = 16;  // plan offset in the ticket block (words)
-TmpLayout tmp_layout(uint64_t n, int has_vals, size_t key_bytes = 4)
+TmpLayout tmp_layout(uint64_t n, int has_vals, size_t key_bytes = 4, size_t val_bytes = 4)
 {
     TmpLayout L;
     size_t o = 0;
@@ -327,7 +333,7 @@ TmpLayout tmp_layout(uint64_t n, int has_vals, size_t key_bytes = 4)
     L.keys = o;
     o += align_up(n * key_bytes, 256);
     L.vals = o;
-    if (has_vals) o += align_up(n * 4, 256);
+    if (has_vals) o += align_up(n * val_bytes, 256);
     L.total = o;
     return L;
 }
@@ -398,6 +404,12 @@ size_t ahs_sort_tmp_bytes(uint64_t n, int has_vals) { return tmp_layout(n, has_v
 size_t ahs_sort_tmp_bytes_dtype(uint64_t n, int has_vals, int32_t dtype)
 {
     return dtype_valid(dtype) ? tmp_layout(n, has_vals, key_bytes_of(dtype)).total : 0;
+}
+
+size_t ahs_sort_tmp_bytes_ex(uint64_t n, uint32_t value_bytes, int32_t dtype)
+{
+    if (!dtype_valid(dtype) || (value_bytes != 0 && value_bytes != 4 && value_bytes != 8)) return 0;
+    return tmp_layout(n, value_bytes != 0, key_bytes_of(dtype), value_bytes ? value_bytes : 4).total;
 }
 
 int ahs_sort_passes(const ahs_features_t *f, int32_t strategy, int has_vals)
@@ -716,8 +728,8 @@ int ahs_select(const ahs_features_t *f, const ahs_thresholds_t *th, int32_t *str
 
 namespace {
 // The digit passes of ahs_sort for key type K (uint32_t, or uint64_t: NEXT-3).
-template <typename K>
-int sort_impl(const K *kin, const uint32_t *d_vals_in, K *kout, uint32_t *d_vals_out, uint64_t n, int32_t strategy,
+template <typename K, typename V>
+int sort_impl(const K *kin, const V *d_vals_in, K *kout, V *d_vals_out, uint64_t n, int32_t strategy,
               const ahs_features_t *feat, void *d_ws, size_t ws_bytes, void *d_tmp, size_t tmp_bytes,
               cudaStream_t s)
 {
@@ -725,6 +737,7 @@ int sort_impl(const K *kin, const uint32_t *d_vals_in, K *kout, uint32_t *d_vals
     constexpr int W = kWide ? 1 : 0;
     const int32_t dtype = (int32_t)feat->dtype;
     const bool kv = d_vals_in != nullptr;
+    const int VK = kv ? (sizeof(V) == 8 ? 2 : 1) : 0;  // K6 variant: no values / 32-bit / 64-bit
     int sms = 0;
     DevInfo *di = nullptr;
     int rc = device_info(&sms, nullptr, &di);
@@ -738,7 +751,7 @@ int sort_impl(const K *kin, const uint32_t *d_vals_in, K *kout, uint32_t *d_vals
         if (kout != kin && cudaMemcpyAsync(kout, kin, n * sizeof(K), cudaMemcpyDeviceToDevice, s) != cudaSuccess)
             return AHS_ECUDA;
         if (kv && d_vals_out != d_vals_in &&
-            cudaMemcpyAsync(d_vals_out, d_vals_in, n * 4, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+            cudaMemcpyAsync(d_vals_out, d_vals_in, n * sizeof(V), cudaMemcpyDeviceToDevice, s) != cudaSuccess)
             return AHS_ECUDA;
         return AHS_OK;
     }
@@ -771,11 +784,11 @@ int sort_impl(const K *kin, const uint32_t *d_vals_in, K *kout, uint32_t *d_vals
     }
 
     // ---- digit passes: plan
-    const TmpLayout TL = tmp_layout(n, kv, sizeof(K));
+    const TmpLayout TL = tmp_layout(n, kv, sizeof(K), sizeof(V));
     if (!d_tmp || tmp_bytes < TL.total || ((uintptr_t)d_tmp & 255u)) return AHS_ENOSPACE;
     char *tmp = (char *)d_tmp;
     K *tkeys = (K *)(tmp + TL.keys);
-    uint32_t *tvals = kv ? (uint32_t *)(tmp + TL.vals) : nullptr;
+    V *tvals = kv ? (V *)(tmp + TL.vals) : nullptr;
     uint32_t *dhist = (uint32_t *)(tmp + TL.dhist);
     uint32_t *bucket = (uint32_t *)(tmp + TL.bucket);
     uint32_t *tickets = (uint32_t *)(tmp + TL.ticket);
@@ -790,11 +803,11 @@ int sort_impl(const K *kin, const uint32_t *d_vals_in, K *kout, uint32_t *d_vals
     // zero the control words and both status regions (one memset); passes
     // alternate between the regions, each clearing the previous pass's
     const int mode = di->rank_mode;
-    const uint64_t tile = (uint64_t)di->os_tile[W][kv][mode];
+    const uint64_t tile = (uint64_t)di->os_tile[W][VK][mode];
     const uint64_t tiles = (n + tile - 1) / tile;
-    const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)sms * di->os_per_sm[W][kv][mode]);
-    const void *k6 = di->os_fn[W][kv][mode];
-    const size_t k6_smem = di->os_smem[W][kv][mode];
+    const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)sms * di->os_per_sm[W][VK][mode]);
+    const void *k6 = di->os_fn[W][VK][mode];
+    const size_t k6_smem = di->os_smem[W][VK][mode];
     const size_t status_words_per_pass = (size_t)tiles * kBins;
     const size_t zero_bytes = (TL.status - TL.ctrl) + status_words_per_pass * 4 * (passes > 1 ? 2 : 1);
     if (cudaMemsetAsync(tmp + TL.ctrl, 0, zero_bytes, s) != cudaSuccess) return AHS_ECUDA;
@@ -802,13 +815,13 @@ int sort_impl(const K *kin, const uint32_t *d_vals_in, K *kout, uint32_t *d_vals
     // in place with an odd pass count: stream the input to tmp first.  In place,
     // the pass count (and so the buffer parity) must be known here: no skipping.
     const K *src_k = kin;
-    const uint32_t *src_v = d_vals_in;
+    const V *src_v = d_vals_in;
     const bool inplace = kout == kin || (kv && d_vals_out == d_vals_in);
     const bool skip = !inplace && g_skip_trivial.load() && !count_kv;
     if (inplace && (passes & 1)) {
         if (cudaMemcpyAsync(tkeys, kin, n * sizeof(K), cudaMemcpyDeviceToDevice, s) != cudaSuccess)
             return AHS_ECUDA;
-        if (kv && cudaMemcpyAsync(tvals, d_vals_in, n * 4, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+        if (kv && cudaMemcpyAsync(tvals, d_vals_in, n * sizeof(V), cudaMemcpyDeviceToDevice, s) != cudaSuccess)
             return AHS_ECUDA;
         src_k = tkeys;
         src_v = tvals;
@@ -849,7 +862,7 @@ int sort_impl(const K *kin, const uint32_t *d_vals_in, K *kout, uint32_t *d_vals
     }
 
     for (int p = 0; p < passes; p++) {
-        PassArgsT<K> pa;
+        PassArgsT<K, V> pa;
         pa.keys_in = src_k;
         pa.vals_in = kv ? src_v : nullptr;
         pa.keys_out = kout;
@@ -873,7 +886,7 @@ int sort_impl(const K *kin, const uint32_t *d_vals_in, K *kout, uint32_t *d_vals
         const cudaError_t e = launch(kv ? (count_kv ? KID_COUNT_SCATTER_KV : KID_ONESWEEP_KV) : KID_ONESWEEP, s, [&] {
             cudaLaunchConfig_t cfg;
             cudaLaunchAttribute attr[1];
-            pdl_config(cfg, attr, dim3(grid), dim3(di->os_block[W][kv][mode]), k6_smem, s);
+            pdl_config(cfg, attr, dim3(grid), dim3(di->os_block[W][VK][mode]), k6_smem, s);
             cudaLaunchKernelExC(&cfg, k6, args);
         });
         if (e != cudaSuccess) return AHS_ECUDA;
@@ -887,25 +900,36 @@ int ahs_sort(const void *d_keys_in, const uint32_t *d_vals_in, void *d_keys_out,
              uint64_t n, int32_t strategy, const ahs_features_t *feat, void *d_ws, size_t ws_bytes,
              void *d_tmp, size_t tmp_bytes, void *stream)
 {
+    return ahs_sort_ex(d_keys_in, d_vals_in, d_keys_out, d_vals_out, n, 4, strategy, feat, d_ws, ws_bytes, d_tmp,
+                       tmp_bytes, stream);
+}
+
+int ahs_sort_ex(const void *d_keys_in, const void *d_vals_in, void *d_keys_out, void *d_vals_out, uint64_t n,
+                uint32_t value_bytes, int32_t strategy, const ahs_features_t *feat, void *d_ws, size_t ws_bytes,
+                void *d_tmp, size_t tmp_bytes, void *stream)
+{
     if (!feat) return AHS_EINVAL;
     if (strategy != AHS_COUNTING && strategy != AHS_RADIX && strategy != AHS_GENERAL) return AHS_EINVAL;
+    const bool kv = d_vals_in != nullptr;
+    if (kv && value_bytes != 4 && value_bytes != 8) return AHS_EINVAL;
     if (feat->n != n) return AHS_EFEAT;
     if (n == 0) return AHS_OK;
     if (n > AHS_MAX_N) return AHS_ERANGE;
     const int32_t dtype = (int32_t)feat->dtype;
     if (!dtype_valid(dtype)) return AHS_EFEAT;
-    const bool kv = d_vals_in != nullptr;
-    const uintptr_t kal = key_bytes_of(dtype) - 1;
+    const uintptr_t kal = key_bytes_of(dtype) - 1, val = (kv ? value_bytes : 4) - 1;
     if (!d_keys_in || !d_keys_out || (kv && !d_vals_out) || ((uintptr_t)d_keys_in & kal) ||
-        ((uintptr_t)d_keys_out & kal) || (kv && (((uintptr_t)d_vals_in & 3u) || ((uintptr_t)d_vals_out & 3u))))
+        ((uintptr_t)d_keys_out & kal) || (kv && (((uintptr_t)d_vals_in & val) || ((uintptr_t)d_vals_out & val))))
         return AHS_EINVAL;
     if (feat->k == 0 || feat->nbins == 0 || (!dtype_wide(dtype) && feat->k > (1ull << 32))) return AHS_EFEAT;
     cudaStream_t s = (cudaStream_t)stream;
-    if (dtype_wide(dtype))
-        return sort_impl<uint64_t>((const uint64_t *)d_keys_in, d_vals_in, (uint64_t *)d_keys_out, d_vals_out, n,
-                                   strategy, feat, d_ws, ws_bytes, d_tmp, tmp_bytes, s);
-    return sort_impl<uint32_t>((const uint32_t *)d_keys_in, d_vals_in, (uint32_t *)d_keys_out, d_vals_out, n,
-                               strategy, feat, d_ws, ws_bytes, d_tmp, tmp_bytes, s);
+    const bool v64 = kv && value_bytes == 8;
+#define AHS_SORT_CALL(K, V)                                                                                   \
+    sort_impl<K, V>((const K *)d_keys_in, (const V *)d_vals_in, (K *)d_keys_out, (V *)d_vals_out, n, strategy, \
+                    feat, d_ws, ws_bytes, d_tmp, tmp_bytes, s)
+    if (dtype_wide(dtype)) return v64 ? AHS_SORT_CALL(uint64_t, uint64_t) : AHS_SORT_CALL(uint64_t, uint32_t);
+    return v64 ? AHS_SORT_CALL(uint32_t, uint64_t) : AHS_SORT_CALL(uint32_t, uint32_t);
+#undef AHS_SORT_CALL
 }
 
 // ------------------------------------------------------------ NEXT-2

@@ -101,7 +101,7 @@ __device__ __forceinline__ uint32_t swz(uint32_t i) { return i ^ ((i >> 5) & 31u
 constexpr int kRankMasked = 0;
 constexpr int kRankOrdered = 1;
 
-template <bool KV, int BLOCK, int ITEMS, int RANK = kRankMasked, typename K = uint32_t>
+template <bool KV, int BLOCK, int ITEMS, int RANK = kRankMasked, typename K = uint32_t, typename V = uint32_t>
 struct Onesweep {
     static constexpr int kWarps = BLOCK / 32;
     static constexpr int kGroupLanes = RANK == kRankOrdered ? 32 : 16;  // lanes sharing one digit table
@@ -115,7 +115,7 @@ struct Onesweep {
     static_assert(BLOCK >= 256 && BLOCK <= 512 && BLOCK % 128 == 0, "256, 384 or 512 threads");
     static_assert((kTile * 4) % 16 == 0, "TMA tile size");
     static constexpr size_t kBufK = (size_t)kTile * sizeof(K);           // keys: 4 or 8 bytes
-    static constexpr size_t kBuf = (size_t)kTile * 4;                    // values: 4 bytes
+    static constexpr size_t kBuf = (size_t)kTile * sizeof(V);            // values: 4 or 8 bytes
     static constexpr size_t kOffK = 0;                                   // keys   [2][TILE]
     static constexpr size_t kOffV = kOffK + 2 * kBufK;                   // values [2][TILE]
     static constexpr size_t kOffCnt = kOffV + (KV ? 2 * kBuf : 0);       // digit tables [SUB][256]
@@ -133,14 +133,14 @@ struct Onesweep {
 // and the executed passes are renumbered 0 .. m-1 (plan word: exec index << 8
 // | m, or kPassSkip).  Without a plan, pass p is executed pass p of npasses.
 constexpr uint32_t kPassSkip = 0xffffffffu;
-template <typename K>
+template <typename K, typename V = uint32_t>
 struct PassArgsT {
     const K *keys_in;
-    const uint32_t *vals_in;
+    const V *vals_in;
     K *keys_out;
-    uint32_t *vals_out;
+    V *vals_out;
     K *keys_tmp;
-    uint32_t *vals_tmp;
+    V *vals_tmp;
     uint32_t n, pass, npasses, shift;
     K flip, sub;
     const uint32_t *bucket_base;  // this pass's 256 digit bases
@@ -151,9 +151,11 @@ struct PassArgsT {
 };
 using PassArgs = PassArgsT<uint32_t>;
 
-// K: uint32_t (32-bit keys) or uint64_t (64-bit keys, NEXT-3); values are 32-bit
-template <bool KV, int BLOCK, int ITEMS, int MINB, int RANK = kRankMasked, typename K = uint32_t>
-__global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(const PassArgsT<K> a)
+// K: uint32_t (32-bit keys) or uint64_t (64-bit keys, NEXT-3); V: the value type (uint32_t,
+// or uint64_t for 64-bit payloads, NEXT-3)
+template <bool KV, int BLOCK, int ITEMS, int MINB, int RANK = kRankMasked, typename K = uint32_t,
+          typename V = uint32_t>
+__global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(const PassArgsT<K, V> a)
 {
     pdl_begin();
     // the previous pass is complete (pdl_begin): its status region is free and
@@ -172,9 +174,9 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(const PassArgsT<K> a)
     const bool to_out = ((m - 1 - e) & 1u) == 0;        // destination parity: the last lands in out
     const bool from_out = !first && !to_out;             // source = the previous pass's destination
     const K *__restrict__ keys_in = first ? a.keys_in : (from_out ? a.keys_out : a.keys_tmp);
-    const uint32_t *__restrict__ vals_in = first ? a.vals_in : (from_out ? a.vals_out : a.vals_tmp);
+    const V *__restrict__ vals_in = first ? a.vals_in : (from_out ? a.vals_out : a.vals_tmp);
     K *__restrict__ keys_out = to_out ? a.keys_out : a.keys_tmp;
-    uint32_t *__restrict__ vals_out = to_out ? a.vals_out : a.vals_tmp;
+    V *__restrict__ vals_out = to_out ? a.vals_out : a.vals_tmp;
     const uint32_t n = a.n, shift = a.shift;
     const K in_flip = first ? a.flip : K(0), in_sub = first ? a.sub : K(0);
     const K out_flip = last ? a.flip : K(0), out_add = last ? a.sub : K(0);
@@ -183,12 +185,12 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(const PassArgsT<K> a)
     uint32_t *__restrict__ tile_ticket = a.ticket;
     const uint32_t tma_ok = (((uintptr_t)keys_in & 15u) == 0) && (!KV || ((uintptr_t)vals_in & 15u) == 0);
 
-    using C = Onesweep<KV, BLOCK, ITEMS, RANK, K>;
+    using C = Onesweep<KV, BLOCK, ITEMS, RANK, K, V>;
     constexpr int TILE = C::kTile, SEG = C::kSeg, GL = C::kGroupLanes;
     constexpr bool ORDERED = RANK == kRankOrdered;
     extern __shared__ __align__(128) uint8_t smem[];
     K *s_kb = reinterpret_cast<K *>(smem + C::kOffK);
-    uint32_t *s_vb = reinterpret_cast<uint32_t *>(smem + C::kOffV);
+    V *s_vb = reinterpret_cast<V *>(smem + C::kOffV);
     uint32_t *s_cnt = reinterpret_cast<uint32_t *>(smem + C::kOffCnt);
     uint32_t *s_part = reinterpret_cast<uint32_t *>(smem + C::kOffAux);
     uint32_t *s_start = s_part + 2 * kBins;
@@ -205,7 +207,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(const PassArgsT<K> a)
 
     auto tile_full = [&](uint32_t t) { return (uint64_t)(t + 1) * TILE <= n; };
     auto issue = [&](uint32_t t, uint32_t b) {  // thread 0
-        const uint32_t kbytes = (uint32_t)(TILE * sizeof(K)), vbytes = (uint32_t)TILE * 4u;
+        const uint32_t kbytes = (uint32_t)(TILE * sizeof(K)), vbytes = (uint32_t)(TILE * sizeof(V));
         mbar_expect_tx(&s_bar[b], kbytes + (KV ? vbytes : 0u));
         tma_load_1d(s_kb + b * TILE, keys_in + (size_t)t * TILE, kbytes, &s_bar[b]);
         if constexpr (KV) tma_load_1d(s_vb + b * TILE, vals_in + (size_t)t * TILE, vbytes, &s_bar[b]);
@@ -245,7 +247,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(const PassArgsT<K> a)
         const uint32_t tile_n = min((uint32_t)TILE, n - tile_base);
         const bool full = tile_n == (uint32_t)TILE;
         K *sk = s_kb + b * TILE;
-        uint32_t *sv = s_vb + b * TILE;
+        V *sv = s_vb + b * TILE;
         if (tma_ok && full) {
             mbar_wait(&s_bar[b], (phase >> b) & 1u);
             PHASE_MARK(0);
@@ -267,7 +269,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(const PassArgsT<K> a)
             // --------------------------------------------- early counts
             // keys (and values) into registers; per sub-warp digit counts
             K v[ITEMS];
-            [[maybe_unused]] uint32_t pv[KV ? ITEMS : 1];
+            [[maybe_unused]] V pv[KV ? ITEMS : 1];
             uint32_t *cw = s_cnt + sub * kBins;
             const uint32_t sbase = sub * SEG + j;
     #pragma unroll
@@ -275,7 +277,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(const PassArgsT<K> a)
                 const uint32_t idx = sbase + it * GL;
                 const bool valid = FULL || idx < tile_n;
                 v[it] = ((valid ? sk[idx] : K(0)) ^ in_flip) - in_sub;
-                if constexpr (KV) pv[it] = valid ? sv[idx] : 0u;
+                if constexpr (KV) pv[it] = valid ? sv[idx] : V(0);
                 const uint32_t d = digit8(v[it], shift);
                 if (it == 0 && !wskew) wskew = __all_sync(kFull, d == __shfl_sync(kFull, d, 0));
                 if (wskew) {

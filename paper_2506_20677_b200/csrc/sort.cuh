@@ -50,10 +50,22 @@ using OsPairs64O = Onesweep<true, kSortBlockPairsO, 8, kRankOrdered, uint64_t>;
 #define K6W_PAIRS_M k_onesweep<true, kSortBlock, 5, 2, kRankMasked, uint64_t>
 #define K6W_KEYS_O k_onesweep<false, kSortBlock, 9, 2, kRankOrdered, uint64_t>
 #define K6W_PAIRS_O k_onesweep<true, kSortBlockPairsO, 8, 2, kRankOrdered, uint64_t>
+// 64-bit values (NEXT-3 payloads), 2 CTAs/SM: 32-bit keys ordered 384 x 9 (3456), masked 512 x 5
+// (2560); 64-bit keys ordered 384 x 7 (2688), masked 256 x 11 (2816).
+using OsPairsV64O = Onesweep<true, kSortBlockPairsO, 9, kRankOrdered, uint32_t, uint64_t>;
+using OsPairsV64M = Onesweep<true, kSortBlock, 5, kRankMasked, uint32_t, uint64_t>;
+using OsPairs64V64O = Onesweep<true, kSortBlockPairsO, 7, kRankOrdered, uint64_t, uint64_t>;
+using OsPairs64V64M = Onesweep<true, 256, 11, kRankMasked, uint64_t, uint64_t>;
+#define K6V_PAIRS_O k_onesweep<true, kSortBlockPairsO, 9, 2, kRankOrdered, uint32_t, uint64_t>
+#define K6V_PAIRS_M k_onesweep<true, kSortBlock, 5, 2, kRankMasked, uint32_t, uint64_t>
+#define K6WV_PAIRS_O k_onesweep<true, kSortBlockPairsO, 7, 2, kRankOrdered, uint64_t, uint64_t>
+#define K6WV_PAIRS_M k_onesweep<true, 256, 11, 2, kRankMasked, uint64_t, uint64_t>
 constexpr int kMinTile = 2560;  // smallest K6 tile: sizes the look-back status regions
 static_assert(kMinTile <= OsKeysM::kTile && kMinTile <= OsPairsM::kTile && kMinTile <= OsKeysO::kTile &&
                   kMinTile <= OsPairsO::kTile && kMinTile <= OsKeys64M::kTile &&
-                  kMinTile <= OsPairs64M::kTile && kMinTile <= OsKeys64O::kTile && kMinTile <= OsPairs64O::kTile,
+                  kMinTile <= OsPairs64M::kTile && kMinTile <= OsKeys64O::kTile && kMinTile <= OsPairs64O::kTile &&
+                  kMinTile <= OsPairsV64O::kTile && kMinTile <= OsPairsV64M::kTile &&
+                  kMinTile <= OsPairs64V64O::kTile && kMinTile <= OsPairs64V64M::kTile,
               "kMinTile");
 
 // ------------------------------------------------------------------ K5 ----

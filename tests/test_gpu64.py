@@ -236,3 +236,26 @@ def test_entropy_sorted_64(family):
         assert abs(got - want) <= H_TOL, (family, n, got, want)
         got = ahs.ahs_entropy_sorted(to_dev(ok, misalign=1), ws)
         assert abs(got - want) <= H_TOL, (family, n, got, want)
+
+
+@pytest.mark.parametrize("kdt", ["u32", "i32", "u64", "i64"])
+def test_64bit_payloads(kdt):
+    """NEXT-3 payloads: 8-byte values travel bit-exactly with their keys (ahs_sort_ex), every strategy."""
+    fams = {"u32": lambda n: synth.cfg2(n), "i32": lambda n: synth.uniform_range(81, n, -200, 200),
+            "u64": lambda n: synth.kmers(82, n), "i64": lambda n: synth.uniform_range64(83, n, -3, 3)}
+    for n in (1, 17, 3071, 3457, 100_003, 1_500_007):
+        keys = fams[kdt](n)
+        vals = synth.stream(84, n)  # full 64-bit payloads
+        ref_k, order = oracle.sort(keys, np.arange(n, dtype=np.uint32), oracle.QUICK)
+        for strategy in (None, 0, 1, 2):
+            dk = to_dev(keys)
+            dv = torch.from_numpy(vals.view(np.int64)).cuda()
+            ws = ahs.Workspace(n, True, key_dtype=keys.dtype, val_bytes=8)
+            f = ahs.ahs_features(dk, ws)
+            s, r = ahs.ahs_select(f)
+            s = s if strategy is None else strategy
+            ko, vo = to_dev(np.zeros_like(keys)), torch.empty_like(dv)
+            ahs.ahs_sort(dk, dv, ko, vo, s, f, ws)
+            torch.cuda.synchronize()
+            assert np.array_equal(to_host(ko, keys.dtype), ref_k), (kdt, n, strategy)
+            assert np.array_equal(vo.cpu().numpy().view(np.uint64), vals[order]), (kdt, n, strategy)
