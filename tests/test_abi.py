@@ -153,6 +153,36 @@ def test_entropy_sorted_arguments():
     assert L.ahs_entropy_sorted(C.c_void_p(4096), 10, C.c_void_p(4096), 1 << 30, None, None) == -1
 
 
+def test_new_entry_points_check_arguments():
+    """NEXT-3 / NEXT-4 entry points reject bad arguments before touching a device."""
+    L = ahs.lib()
+    f = ahs.Features()
+    f.n, f.dtype = 5, ahs.AHS_U32
+    # ahs_sort_ex: values of 3 bytes, misaligned 8-byte values
+    assert L.ahs_sort_ex(C.c_void_p(4096), C.c_void_p(8192), C.c_void_p(12288), C.c_void_p(16384), 5, 3, 2,
+                         C.byref(f), None, 0, None, 0, None) == -1
+    assert L.ahs_sort_ex(C.c_void_p(4096), C.c_void_p(8196), C.c_void_p(12288), C.c_void_p(16384), 5, 8, 2,
+                         C.byref(f), None, 0, None, 0, None) == -1
+    assert L.ahs_sort_tmp_bytes_ex(100, 3, 0) == 0 and L.ahs_sort_tmp_bytes_ex(100, 8, 9) == 0
+    assert L.ahs_sort_tmp_bytes_ex(1 << 20, 8, 3) > L.ahs_sort_tmp_bytes_ex(1 << 20, 4, 3) > \
+        L.ahs_sort_tmp_bytes_ex(1 << 20, 0, 3) > L.ahs_sort_tmp_bytes_ex(1 << 20, 0, 1)
+    # 64-bit keys must be 8-byte aligned
+    assert L.ahs_features(C.c_void_p(4100), 10, ahs.AHS_U64, C.c_void_p(4096), 1 << 30, C.byref(f), None) == -1
+    # segment sort: above the 2048-key limit, bad dtype, missing counter
+    bad = C.c_void_p(4096)
+    assert L.ahs_sort_segments(C.c_void_p(4096), None, C.c_void_p(8192), None, 10, C.c_void_p(12288), 2, 4096,
+                               0, bad, None) == -3
+    assert L.ahs_sort_segments(C.c_void_p(4096), None, C.c_void_p(8192), None, 10, C.c_void_p(12288), 2, 32,
+                               7, bad, None) == -1
+    assert L.ahs_sort_segments(C.c_void_p(4096), None, C.c_void_p(8192), None, 10, C.c_void_p(12288), 2, 32,
+                               0, None, None) == -1
+    # classifier: NULL inputs
+    h = C.c_void_p()
+    assert L.ahs_model_load(None, 0, C.byref(h), None, 0) == -1
+    a = C.c_int32()
+    assert L.ahs_model_predict(None, 1.0, 1.0, 1.0, C.byref(a), None) == -1
+
+
 @pytest.mark.skipif(os.path.exists("/dev/nvidia0"), reason="checks the no-GPU path")
 def test_no_device_is_an_error_not_a_fallback():
     L = ahs.lib()

@@ -451,3 +451,40 @@ def test_entropy_sorted_on_pipeline_output_and_paper_branch():
 def test_entropy_sorted_empty():
     ws = ahs.Workspace(1, False)
     assert ahs.ahs_entropy_sorted(torch.empty(0, dtype=torch.int32, device="cuda"), ws) == 0.0
+
+
+def test_maximum_n():
+    """n = AHS_MAX_N = 2^30 - 1 (the 30-bit look-back counts), GENERAL pairs with values = input index:
+    the oracle cannot sort 2^30 keys in test time, so properties that hold at any size: the output is
+    non-decreasing; it is a permutation of the input (the values are a permutation of the indices and
+    gather the output; sums of keys and squares agree); equal keys keep their input order; sampled
+    positions hold the order statistic (counted on the host)."""
+    n = (1 << 30) - 1
+    g = torch.Generator(device="cuda").manual_seed(2506)
+    dk = torch.randint(-(2 ** 31), 2 ** 31, (n,), dtype=torch.int64, device="cuda", generator=g).to(torch.int32)
+    ws = ahs.Workspace(n, True)
+    f = ahs.ahs_features(dk, ws)
+    s, r = ahs.ahs_select(f)
+    assert ahs.STRATEGY_NAMES[s] == "GENERAL"
+    dv = torch.arange(n, dtype=torch.int32, device="cuda").view(torch.uint32)
+    ko, vo = torch.empty_like(dk), torch.empty_like(dv)
+    ahs.ahs_sort(dk, dv, ko, vo, s, f, ws)
+    torch.cuda.synchronize()
+    k64, o64 = dk.to(torch.int64), ko.to(torch.int64)
+    assert bool((ko[1:] >= ko[:-1]).all())
+    assert int(k64.sum()) == int(o64.sum()) and int((k64 * k64).sum()) == int((o64 * o64).sum())
+    # values: the original index of each output key; every index exactly once, and gathering the
+    # input by them reproduces the output (so the output is a permutation of the input)
+    vi64 = vo.view(torch.int32).to(torch.int64)
+    assert bool((torch.bincount(vi64, minlength=n) == 1).all())
+    assert bool((dk[vi64] == ko).all())
+    # stability: equal neighbours keep their input order
+    same = ko[1:] == ko[:-1]
+    vi = vo.view(torch.int32)
+    assert bool((vi[1:][same] > vi[:-1][same]).all())
+    hk = dk.cpu().numpy()
+    for pos in (0, n // 3, n - 1):
+        x = int(ko[pos])
+        below, upto = int((hk < x).sum()), int((hk <= x).sum())
+        assert below <= pos < upto
+    assert f.n == n and f.min == int(dk.min()) and f.max == int(dk.max())
