@@ -114,13 +114,13 @@ __global__ void __launch_bounds__(BLOCK)
         if (lane == 0) prev = edge;
         if (lane == 31) next = edge;
         // a start at local 0 of chunk 0 is real; elsewhere starts compare with the previous key
-        uint32_t mine = 0;  // last local start among my keys (0: none; neutral, carry >= 0)
+        // bit q: key q equals its predecessor; starts = the other valid keys
+        uint32_t eqm = 0;
 #pragma unroll
-        for (int q = 0; q < kEntItems; q++) {
-            const uint32_t i = i0 + q;
-            const bool st = i < len && k[q] != (q ? k[q - 1] : prev);
-            if (st) mine = i;
-        }
+        for (int q = 0; q < kEntItems; q++) eqm |= (uint32_t)(k[q] == (q ? k[q - 1] : prev)) << q;
+        const uint32_t valid = i0 >= len ? 0u : (len - i0 >= (uint32_t)kEntItems ? 0xffffu : (1u << (len - i0)) - 1u);
+        const uint32_t stm = ~eqm & valid;
+        uint32_t mine = stm ? i0 + 31u - (uint32_t)__clz(stm) : 0u;  // last local start (0: none; neutral)
         // exclusive max-scan over the block (thread order = key order)
         uint32_t incl = mine;
 #pragma unroll
@@ -137,6 +137,13 @@ __global__ void __launch_bounds__(BLOCK)
         }
         const uint32_t up = __shfl_up_sync(kFull, incl, 1);
         uint32_t cur = lane ? max(before, up) : before;
+        // fast paths (no contribution, no boundary piece): every run of my keys is a single key
+        // that ends here, or all my keys sit inside one run that goes on past them; keys at the
+        // chunk's edges and partial tiles take the loop
+        const bool inner = valid == 0xffffu && i0 != 0u && i0 + kEntItems < len;
+        const bool singles = inner && eqm == 0u && next != k[kEntItems - 1];
+        const bool interior = inner && eqm == 0xffffu && next == k[kEntItems - 1];
+        if (!singles && !interior)
 #pragma unroll
         for (int q = 0; q < kEntItems; q++) {
             const uint32_t i = i0 + q;
