@@ -37,7 +37,7 @@ struct DevInfo {
     int os_per_sm[2][3][2] = {};  // co-resident CTAs per SM
     int os_block[2][3][2] = {};
     bool lane_order_ok = false;              // self-test of the ordered ranking passed
-    int ent_grid = 0;                        // K8 cooperative grid
+    int ent_grid[2] = {0, 0};                // K8 cooperative grid per key width (32 / 64-bit)
     int rank_mode = kRankMasked;
 };
 std::mutex g_dev_mu;
@@ -166,9 +166,9 @@ int device_info(int *sms, int *hist_clusters = nullptr, DevInfo **info = nullptr
                                                                       kEntBlock, 0) == cudaSuccess;
                 good &= cudaOccupancyMaxActiveBlocksPerMultiprocessor(
                             &per64, k_entropy_sorted<kEntBlock, uint64_t>, kEntBlock, 0) == cudaSuccess;
-                per = std::min(per, per64);  // one cooperative grid size for both key widths
-                d.ent_grid = std::min(kEntMaxGrid, per * d.sms);
-                good &= d.ent_grid > 0;
+                d.ent_grid[0] = std::min(kEntMaxGrid, per * d.sms);
+                d.ent_grid[1] = std::min(kEntMaxGrid, per64 * d.sms);
+                good &= d.ent_grid[0] > 0 && d.ent_grid[1] > 0;
             }
             if (!good) {
                 cudaGetLastError();
@@ -956,7 +956,7 @@ int ahs_entropy_sorted_dtype(const void *d_keys, uint64_t n, int32_t dtype, void
     int rc = device_info(&sms, nullptr, &di);
     if (rc) return rc;
     constexpr uint64_t kTileKeys = (uint64_t)kEntBlock * kEntItems;
-    uint64_t grid = std::min<uint64_t>((n + kTileKeys - 1) / kTileKeys, (uint64_t)di->ent_grid);
+    uint64_t grid = std::min<uint64_t>((n + kTileKeys - 1) / kTileKeys, (uint64_t)di->ent_grid[wide ? 1 : 0]);
     grid = std::max<uint64_t>(1, grid);
     uint64_t chunk = (n + grid - 1) / grid;
     chunk = (chunk + kEntItems - 1) / kEntItems * kEntItems;  // chunk starts stay 16-key aligned
