@@ -488,3 +488,42 @@ def test_maximum_n():
         below, upto = int((hk < x).sum()), int((hk <= x).sum())
         assert below <= pos < upto
     assert f.n == n and f.min == int(dk.min()) and f.max == int(dk.max())
+
+
+def test_concurrent_host_threads():
+    """Three host threads, each with its own stream and workspace, sort different inputs at once
+    (the library's per-thread state: the mapped features buffer; K6 grids of concurrent sorts share
+    SMs): every result equals the oracle's."""
+    import threading
+
+    cases = [synth.cfg2(400_009), synth.uniform_range(91, 400_009, -600, 600), synth.cfg3(400_009, seed=92),
+             synth.cfg4d(300_007), synth.cfg2(123_457), synth.uniform_range(93, 250_001, 0, 2 ** 20)]
+    results, errors = {}, []
+
+    def worker(t):
+        try:
+            stream = torch.cuda.Stream()
+            for i in range(t, len(cases), 3):
+                keys = cases[i]
+                vals = np.arange(keys.size, dtype=np.uint32)
+                with torch.cuda.stream(stream):
+                    dk, dv = to_dev(keys), to_dev(vals)
+                    ws = ahs.Workspace(keys.size, True)
+                    f = ahs.ahs_features(dk, ws, stream)
+                    s, r = ahs.ahs_select(f)
+                    ko, vo = torch.empty_like(dk), torch.empty_like(dv)
+                    ahs.ahs_sort(dk, dv, ko, vo, s, f, ws, stream)
+                stream.synchronize()
+                results[i] = (to_host(ko), to_host(vo))
+        except Exception as e:  # reported below
+            errors.append(e)
+
+    threads = [threading.Thread(target=worker, args=(t,)) for t in range(3)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert not errors, errors
+    for i, keys in enumerate(cases):
+        ref = oracle.ahs(keys, np.arange(keys.size, dtype=np.uint32))
+        assert np.array_equal(results[i][0], ref["keys"]) and np.array_equal(results[i][1], ref["vals"]), i
