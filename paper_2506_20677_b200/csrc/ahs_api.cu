@@ -310,8 +310,9 @@ WsLayout ws_layout()
 // ------------------------------------------------------------ tmp layout
 // [ctrl: digit histograms, bucket bases (kMaxPasses x 256 u32 each), 256 B of
 //  tickets (passes 0..7, K5 at [8]) and the pass plan (at [16], kMaxPasses + 2
-//  words)] [look-back status: two regions, used by alternate passes]
-// [second key buffer (n x key bytes)] [second value buffer]
+//  words)] [look-back status: room for two regions at the smallest K6 tile;
+//  a sort uses two regions of its own tile count, back to back, alternating
+//  between passes] [second key buffer (n x key bytes)] [second value buffer]
 // The ctrl block sits at offset 0 whatever n and the key width.
 struct TmpLayout {
     size_t ctrl, dhist, bucket, ticket, status, status_region_bytes, keys, vals, total;
