@@ -36,6 +36,10 @@ struct DevInfo {
     int os_tile[2][3][2] = {};
     int os_per_sm[2][3][2] = {};  // co-resident CTAs per SM
     int os_block[2][3][2] = {};
+    // 32-bit keys-only ordered passes for n >= kLargeN (sort.cuh)
+    const void *osl_fn = nullptr;
+    size_t osl_smem = 0;
+    int osl_tile = 0, osl_per_sm = 0;
     bool lane_order_ok = false;              // self-test of the ordered ranking passed
     int ent_grid[2] = {0, 0};                // K8 cooperative grid per key width (32 / 64-bit)
     int rank_mode = kRankMasked;
@@ -138,6 +142,15 @@ int device_info(int *sms, int *hist_clusters = nullptr, DevInfo **info = nullptr
             set_k6(1, 2, kRankMasked, (const void *)K6WV_PAIRS_M, OsPairs64V64M::kSmem, OsPairs64V64M::kTile, 256);
             set_k6(1, 2, kRankOrdered, (const void *)K6WV_PAIRS_O, OsPairs64V64O::kSmem, OsPairs64V64O::kTile,
                    kSortBlockPairsO);
+            d.osl_fn = (const void *)K6_KEYS_OL;
+            d.osl_smem = OsKeysOL::kSmem;
+            d.osl_tile = OsKeysOL::kTile;
+            good &= cudaFuncSetAttribute(d.osl_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d.osl_smem) ==
+                    cudaSuccess;
+            if (good)
+                good &= cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.osl_per_sm, d.osl_fn, kSortBlock,
+                                                                      d.osl_smem) == cudaSuccess;
+            good &= d.osl_per_sm > 0;
             for (int w = 0; w < 2; w++)
                 for (int kv = 0; kv < 3; kv++)
                     for (int m = 0; m < 2; m++) {
@@ -804,11 +817,13 @@ int sort_impl(const K *kin, const V *d_vals_in, K *kout, V *d_vals_out, uint64_t
     // zero the control words and both status regions (one memset); passes
     // alternate between the regions, each clearing the previous pass's
     const int mode = di->rank_mode;
-    const uint64_t tile = (uint64_t)di->os_tile[W][VK][mode];
+    const bool large = W == 0 && VK == 0 && mode == kRankOrdered && n >= kLargeN;
+    const uint64_t tile = large ? (uint64_t)di->osl_tile : (uint64_t)di->os_tile[W][VK][mode];
     const uint64_t tiles = (n + tile - 1) / tile;
-    const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)sms * di->os_per_sm[W][VK][mode]);
-    const void *k6 = di->os_fn[W][VK][mode];
-    const size_t k6_smem = di->os_smem[W][VK][mode];
+    const int per_sm = large ? di->osl_per_sm : di->os_per_sm[W][VK][mode];
+    const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)sms * per_sm);
+    const void *k6 = large ? di->osl_fn : di->os_fn[W][VK][mode];
+    const size_t k6_smem = large ? di->osl_smem : di->os_smem[W][VK][mode];
     const size_t status_words_per_pass = (size_t)tiles * kBins;
     const size_t zero_bytes = (TL.status - TL.ctrl) + status_words_per_pass * 4 * (passes > 1 ? 2 : 1);
     if (cudaMemsetAsync(tmp + TL.ctrl, 0, zero_bytes, s) != cudaSuccess) return AHS_ECUDA;

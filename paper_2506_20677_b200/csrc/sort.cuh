@@ -39,6 +39,11 @@ using OsPairsO = Onesweep<true, kSortBlockPairsO, 12, kRankOrdered>;
 #define K6_PAIRS_M k_onesweep<true, kSortBlock, 9, 2, kRankMasked>
 #define K6_KEYS_O k_onesweep<false, kSortBlock, 16, 2, kRankOrdered>
 #define K6_PAIRS_O k_onesweep<true, kSortBlockPairsO, 12, 2, kRankOrdered>
+// keys-only ordered passes over n >= kLargeN: 512 x 18 (tile 9216; 24 B of register spill at the
+// 64-register cap) is 2.6 % faster per pass at 2^26, 0.6 % slower at 2^24 (profiles/r01_ab_items18.txt)
+constexpr uint64_t kLargeN = 1ull << 25;
+using OsKeysOL = Onesweep<false, kSortBlock, 18, kRankOrdered>;
+#define K6_KEYS_OL k_onesweep<false, kSortBlock, 18, 2, kRankOrdered>
 // 64-bit keys (NEXT-3), 2 CTAs/SM each: ordered keys 512 x 9 (tile 4608, 94 KB
 // of shared memory), ordered pairs 384 x 8 (3072), masked keys 512 x 9 (4608,
 // 111 KB), masked pairs 512 x 5 (2560).
@@ -62,6 +67,7 @@ using OsPairs64V64M = Onesweep<true, 256, 11, kRankMasked, uint64_t, uint64_t>;
 #define K6WV_PAIRS_M k_onesweep<true, 256, 11, 2, kRankMasked, uint64_t, uint64_t>
 constexpr int kMinTile = 2560;  // smallest K6 tile: sizes the look-back status regions
 static_assert(kMinTile <= OsKeysM::kTile && kMinTile <= OsPairsM::kTile && kMinTile <= OsKeysO::kTile &&
+                  kMinTile <= OsKeysOL::kTile &&
                   kMinTile <= OsPairsO::kTile && kMinTile <= OsKeys64M::kTile &&
                   kMinTile <= OsPairs64M::kTile && kMinTile <= OsKeys64O::kTile && kMinTile <= OsPairs64O::kTile &&
                   kMinTile <= OsPairsV64O::kTile && kMinTile <= OsPairsV64M::kTile &&

@@ -269,6 +269,8 @@ int main(int argc, char **argv)
         printf("digit shift %u (max digit share %.3f)\n", shift, (double)mx / n);
         g_idx = 0;
         run_cfg<false, 512, 16, 2, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
+        run_cfg<false, 512, 18, 2, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
+        run_cfg<false, 512, 20, 2, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
         run_cfg<false, 384, 16, 3, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
         run_cfg<false, 384, 14, 3, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
         run_cfg<true, 512, 15, 1, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
