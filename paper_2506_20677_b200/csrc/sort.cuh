@@ -27,18 +27,18 @@ namespace ahs {
 //   masked ranking (no assumption on atomic lane order): keys 512 x 15 (tile
 //     7680, 2 CTAs/SM), pairs 512 x 9 (tile 4608, 2 CTAs/SM);
 //   ordered ranking (after the lane-order self-test): keys 512 x 16 (tile
-//     8192, 2 CTAs/SM), pairs 384 x 12 (tile 4608, 2 CTAs/SM: same speed as
-//     512 x 15 at 1 CTA/SM on uniform keys, 15 % faster on skewed digits).
+//     8192, 2 CTAs/SM), pairs 384 x 16 (tile 6144, 2 CTAs/SM, 112 KB of shared
+//     memory each: 13 % faster than 384 x 12 at 2^26, 10 % at 2^24).
 constexpr int kSortBlock = 512;
 constexpr int kSortBlockPairsO = 384;
 using OsKeysM = Onesweep<false, kSortBlock, 15, kRankMasked>;
 using OsPairsM = Onesweep<true, kSortBlock, 9, kRankMasked>;
 using OsKeysO = Onesweep<false, kSortBlock, 16, kRankOrdered>;
-using OsPairsO = Onesweep<true, kSortBlockPairsO, 12, kRankOrdered>;
+using OsPairsO = Onesweep<true, kSortBlockPairsO, 16, kRankOrdered>;
 #define K6_KEYS_M k_onesweep<false, kSortBlock, 15, 2, kRankMasked>
 #define K6_PAIRS_M k_onesweep<true, kSortBlock, 9, 2, kRankMasked>
 #define K6_KEYS_O k_onesweep<false, kSortBlock, 16, 2, kRankOrdered>
-#define K6_PAIRS_O k_onesweep<true, kSortBlockPairsO, 12, 2, kRankOrdered>
+#define K6_PAIRS_O k_onesweep<true, kSortBlockPairsO, 16, 2, kRankOrdered>
 // keys-only ordered passes over n >= kLargeN: 512 x 18 (tile 9216; 24 B of register spill at the
 // 64-register cap) is 2.6 % faster per pass at 2^26, 0.6 % slower at 2^24 (profiles/r01_ab_items18.txt)
 constexpr uint64_t kLargeN = 1ull << 25;
