@@ -133,7 +133,8 @@ int device_info(int *sms, int *hist_clusters = nullptr, DevInfo **info = nullptr
             set_k6(0, 1, kRankOrdered, (const void *)K6_PAIRS_O, OsPairsO::kSmem, OsPairsO::kTile, kSortBlockPairsO);
             set_k6(1, 0, kRankMasked, (const void *)K6W_KEYS_M, OsKeys64M::kSmem, OsKeys64M::kTile, kSortBlock);
             set_k6(1, 1, kRankMasked, (const void *)K6W_PAIRS_M, OsPairs64M::kSmem, OsPairs64M::kTile, kSortBlock);
-            set_k6(1, 0, kRankOrdered, (const void *)K6W_KEYS_O, OsKeys64O::kSmem, OsKeys64O::kTile, kSortBlock);
+            set_k6(1, 0, kRankOrdered, (const void *)K6W_KEYS_O, OsKeys64O::kSmem, OsKeys64O::kTile,
+                   kSortBlockPairsO);
             set_k6(1, 1, kRankOrdered, (const void *)K6W_PAIRS_O, OsPairs64O::kSmem, OsPairs64O::kTile,
                    kSortBlockPairsO);
             set_k6(0, 2, kRankMasked, (const void *)K6V_PAIRS_M, OsPairsV64M::kSmem, OsPairsV64M::kTile, kSortBlock);

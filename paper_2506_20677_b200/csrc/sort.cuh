@@ -44,24 +44,25 @@ using OsPairsO = Onesweep<true, kSortBlockPairsO, 16, kRankOrdered>;
 constexpr uint64_t kLargeN = 1ull << 25;
 using OsKeysOL = Onesweep<false, kSortBlock, 18, kRankOrdered>;
 #define K6_KEYS_OL k_onesweep<false, kSortBlock, 18, 2, kRankOrdered>
-// 64-bit keys (NEXT-3), 2 CTAs/SM each: ordered keys 512 x 9 (tile 4608, 94 KB
-// of shared memory), ordered pairs 384 x 8 (3072), masked keys 512 x 9 (4608,
-// 111 KB), masked pairs 512 x 5 (2560).
+// 64-bit keys (NEXT-3), 2 CTAs/SM each: ordered keys 384 x 14 (tile 5376, 102 KB
+// of shared memory; 11 % faster than 512 x 9 at cfg6), ordered pairs 384 x 10
+// (3840, 108 KB; 11 % faster than 384 x 8), masked keys 512 x 9 (4608, 111 KB),
+// masked pairs 512 x 5 (2560).
 using OsKeys64M = Onesweep<false, kSortBlock, 9, kRankMasked, uint64_t>;
 using OsPairs64M = Onesweep<true, kSortBlock, 5, kRankMasked, uint64_t>;
-using OsKeys64O = Onesweep<false, kSortBlock, 9, kRankOrdered, uint64_t>;
-using OsPairs64O = Onesweep<true, kSortBlockPairsO, 8, kRankOrdered, uint64_t>;
+using OsKeys64O = Onesweep<false, kSortBlockPairsO, 14, kRankOrdered, uint64_t>;
+using OsPairs64O = Onesweep<true, kSortBlockPairsO, 10, kRankOrdered, uint64_t>;
 #define K6W_KEYS_M k_onesweep<false, kSortBlock, 9, 2, kRankMasked, uint64_t>
 #define K6W_PAIRS_M k_onesweep<true, kSortBlock, 5, 2, kRankMasked, uint64_t>
-#define K6W_KEYS_O k_onesweep<false, kSortBlock, 9, 2, kRankOrdered, uint64_t>
-#define K6W_PAIRS_O k_onesweep<true, kSortBlockPairsO, 8, 2, kRankOrdered, uint64_t>
-// 64-bit values (NEXT-3 payloads), 2 CTAs/SM: 32-bit keys ordered 384 x 9 (3456), masked 512 x 5
+#define K6W_KEYS_O k_onesweep<false, kSortBlockPairsO, 14, 2, kRankOrdered, uint64_t>
+#define K6W_PAIRS_O k_onesweep<true, kSortBlockPairsO, 10, 2, kRankOrdered, uint64_t>
+// 64-bit values (NEXT-3 payloads), 2 CTAs/SM: 32-bit keys ordered 384 x 10 (3840), masked 512 x 5
 // (2560); 64-bit keys ordered 384 x 7 (2688), masked 256 x 11 (2816).
-using OsPairsV64O = Onesweep<true, kSortBlockPairsO, 9, kRankOrdered, uint32_t, uint64_t>;
+using OsPairsV64O = Onesweep<true, kSortBlockPairsO, 10, kRankOrdered, uint32_t, uint64_t>;
 using OsPairsV64M = Onesweep<true, kSortBlock, 5, kRankMasked, uint32_t, uint64_t>;
 using OsPairs64V64O = Onesweep<true, kSortBlockPairsO, 7, kRankOrdered, uint64_t, uint64_t>;
 using OsPairs64V64M = Onesweep<true, 256, 11, kRankMasked, uint64_t, uint64_t>;
-#define K6V_PAIRS_O k_onesweep<true, kSortBlockPairsO, 9, 2, kRankOrdered, uint32_t, uint64_t>
+#define K6V_PAIRS_O k_onesweep<true, kSortBlockPairsO, 10, 2, kRankOrdered, uint32_t, uint64_t>
 #define K6V_PAIRS_M k_onesweep<true, kSortBlock, 5, 2, kRankMasked, uint32_t, uint64_t>
 #define K6WV_PAIRS_O k_onesweep<true, kSortBlockPairsO, 7, 2, kRankOrdered, uint64_t, uint64_t>
 #define K6WV_PAIRS_M k_onesweep<true, 256, 11, 2, kRankMasked, uint64_t, uint64_t>

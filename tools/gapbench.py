@@ -15,13 +15,18 @@ import synth  # noqa: E402
 
 def run(cfg, reps=30):
     keys, vals, _ = synth.make(cfg)
-    dk = torch.from_numpy(keys.view(np.int32)).cuda()
-    if keys.dtype == np.uint32:
-        dk = dk.view(torch.uint32)
+    if keys.itemsize == 8:
+        dk = torch.from_numpy(keys.view(np.int64)).cuda()
+        if keys.dtype == np.uint64:
+            dk = dk.view(torch.uint64)
+    else:
+        dk = torch.from_numpy(keys.view(np.int32)).cuda()
+        if keys.dtype == np.uint32:
+            dk = dk.view(torch.uint32)
     dv = torch.from_numpy(vals.view(np.int32)).cuda().view(torch.uint32) if vals is not None else None
     ko = torch.empty_like(dk)
     vo = torch.empty_like(dv) if dv is not None else None
-    ws = ahs.Workspace(keys.size, dv is not None)
+    ws = ahs.Workspace(keys.size, dv is not None, key_dtype=keys.dtype)
     st = torch.cuda.current_stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     for _ in range(3):
