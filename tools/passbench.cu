@@ -274,7 +274,7 @@ int main(int argc, char **argv)
         run_cfg<false, 384, 16, 3, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
         run_cfg<false, 384, 14, 3, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
         run_cfg<true, 512, 15, 1, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
-        run_cfg<true, 384, 12, 2, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
+        run_cfg<true, 384, 16, 2, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
         run_cfg<true, 384, 9, 3, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
     }
     if (cub) {
