@@ -232,6 +232,11 @@ def _code_of(dt) -> int:
             return dt
         raise TypeError(f"not an ahs dtype code: {dt}")
     name = str(dt).replace("torch.", "")
+    if not name.isidentifier():  # numpy scalar types (np.int64) and dtype objects
+        try:
+            name = np.dtype(dt).name
+        except TypeError:
+            pass
     codes = {"int32": AHS_I32, "uint32": AHS_U32, "int64": AHS_I64, "uint64": AHS_U64}
     if name not in codes:  # PAPER.md P:409 integer keys; 64-bit per S:20 (NEXT-3)
         raise TypeError(f"keys must be int32, uint32, int64 or uint64, got {dt}")

@@ -259,3 +259,18 @@ def test_64bit_payloads(kdt):
             torch.cuda.synchronize()
             assert np.array_equal(to_host(ko, keys.dtype), ref_k), (kdt, n, strategy)
             assert np.array_equal(vo.cpu().numpy().view(np.uint64), vals[order]), (kdt, n, strategy)
+
+
+def test_empty_and_constant_64():
+    """n = 0 (no launch, flags EMPTY | SORTED) and a constant 64-bit input under every strategy."""
+    for dt in (np.int64, np.uint64):
+        keys = np.zeros(0, dtype=dt)
+        ws = ahs.Workspace(1, False, key_dtype=dt)
+        dk = torch.zeros(0, dtype=torch.int64, device="cuda")
+        f = ahs.ahs_features(dk.view(torch.uint64) if dt == np.uint64 else dk, ws)
+        assert f.n == 0 and f.flags & 1
+        keys = np.full(5000, I64_MIN if dt == np.int64 else 2 ** 63 + 5, dtype=dt)
+        vals = np.arange(5000, dtype=np.uint32)
+        for strategy in (None, 0, 1, 2):
+            f, s, r, ko, vo = run_gpu(keys, vals, strategy=strategy)
+            assert f.k == 1 and np.array_equal(ko, keys) and np.array_equal(vo, vals)
