@@ -381,6 +381,16 @@ def sort_bytes(strategy: int, passes: int, n: int, kv: bool, shift: int = 1, kb:
     return hist + passes * (2 * kb + (8 if kv else 0)) * n
 
 
+def contract_bytes(strategy: int, passes_nominal: int, n: int, kv: bool, kb: int = 4) -> int:
+    """BASELINE.json's contract roofline bytes: radix / GENERAL (2p + 1) bytes n with
+    the nominal pass count p and bytes = key bytes (+ 4 per value: BJ counts 8 for 32-bit pairs, which
+    over-counts the histogram read by 4n); counting: a read and a write of the keys (and values)."""
+    bytes_per = kb + (4 if kv else 0)
+    if strategy == 0 and passes_nominal <= 1:
+        return 2 * bytes_per * n
+    return (2 * passes_nominal + 1) * bytes_per * n
+
+
 def traffic_from_profiles(workload: str):
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
@@ -493,6 +503,10 @@ def run_ours(args):
                 "sort_GBps": sb2 / (sort_ms2 * 1e-3) / 1e9 if sort_ms2 > 0 else None,
                 "sort_frac_of_peak": (sb2 / (sort_ms2 * 1e-3) / 1e9) / peak if sort_ms2 > 0 else None,
                 "key_bytes": kb2,
+                "contract_frac_of_8TBps": (contract_bytes(r2["s"], r2["passes"], n2, kv2, kb2) /
+                                           (sort_ms2 * 1e-3) / 8e12) if sort_ms2 > 0 else None,
+                "contract_frac_of_peak": (contract_bytes(r2["s"], r2["passes"], n2, kv2, kb2) /
+                                          (sort_ms2 * 1e-3) / 1e9 / peak) if sort_ms2 > 0 else None,
                 "features_GBps": 2 * kb2 * n2 / (feat_ms2 * 1e-3) / 1e9 if feat_ms2 > 0 else None,
                 "kernels_ms": {k: v["ms"] / v["launches"] for k, v in p2.items() if v["launches"]},
             })
