@@ -269,7 +269,7 @@ def segments_report(torch, ahs, device, reps=10):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
     for name, nseg, lo, hi, kv in (("insertion_1_20", 1 << 20, 1, 20, False),
                                    ("insertion_1_20_kv", 1 << 20, 1, 20, True),
-                                   ("bitonic_1000_2048", 1 << 13, 1000, 2048, False)):
+                                   ("radix_1000_2048", 1 << 13, 1000, 2048, False)):
         lens = np.random.default_rng(7).integers(lo, hi + 1, nseg)
         off = np.zeros(nseg + 1, dtype=np.int64)
         off[1:] = np.cumsum(lens)

@@ -243,8 +243,9 @@ AHS_API int ahs_entropy_sorted_dtype(const void *d_keys, uint64_t n, int32_t dty
  * each sorted ascending and stably, values travelling with their keys; keys
  * outside every segment are not touched.  max_segment: an upper bound on the
  * segment lengths, <= 2048 (ERANGE above); <= 32 runs one thread per segment
- * with Listing 1's insertion sort in shared memory, otherwise one CTA per
- * segment (bitonic network on (key, index): stable).  Out may alias in.
+ * with Listing 1's insertion sort in shared memory, otherwise 32 .. 128
+ * threads per segment (a stable LSD radix sort in shared memory, 8-bit digits,
+ * digits all keys of the segment share skipped).  Out may alias in.
  * d_bad (device uint32, required) receives the number of segments found longer
  * than max_segment or reaching past n: those are left unsorted (never an
  * out-of-bounds access).  Asynchronous.  Errors: EINVAL, ERANGE, ENODEV, ECUDA. */

@@ -1096,20 +1096,24 @@ cudaError_t seg_small(const void *kin, const uint32_t *vin, void *kout, uint32_t
                     vout, offsets, nseg, n, flip, max_segment, bad);
 }
 
-template <typename K, bool KV, int BLOCK>
-cudaError_t seg_medium(const void *kin, const uint32_t *vin, void *kout, uint32_t *vout, uint64_t n,
-                       const uint32_t *offsets, uint32_t nseg, uint32_t max_segment, K flip, uint32_t *bad,
-                       cudaStream_t s)
+template <typename K, bool KV, int GROUP, int CAP, bool ORD, int SPC = 1>
+cudaError_t seg_radix(const void *kin, const uint32_t *vin, void *kout, uint32_t *vout, uint64_t n,
+                      const uint32_t *offsets, uint32_t nseg, uint32_t max_segment, K flip, uint32_t *bad,
+                      cudaStream_t s)
 {
-    return launch_k(k_seg_medium<K, KV, BLOCK>, dim3(nseg), dim3(BLOCK), 0, s, (const K *)kin, vin, (K *)kout, vout,
-                    offsets, nseg, n, flip, max_segment, bad);
+    constexpr size_t smem = SPC * seg_radix_smem<K, KV, GROUP, CAP>();
+    static const bool attr = cudaFuncSetAttribute(k_seg_radix<K, KV, GROUP, CAP, ORD, SPC>,
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess;
+    if (!attr) return cudaErrorInvalidValue;
+    return launch_k(k_seg_radix<K, KV, GROUP, CAP, ORD, SPC>, dim3((nseg + SPC - 1) / SPC), dim3(GROUP * SPC), smem,
+                    s, (const K *)kin, vin, (K *)kout, vout, offsets, nseg, n, flip, max_segment, bad);
 }
 
 // register network length / CTA size from the declared maximum segment
 template <typename K, bool KV>
 cudaError_t seg_launch(const void *kin, const uint32_t *vin, void *kout, uint32_t *vout, uint64_t n,
                        const uint32_t *offsets, uint32_t nseg, uint32_t max_segment, K flip, uint32_t *bad,
-                       cudaStream_t s)
+                       bool ord, cudaStream_t s)
 {
 #define AHS_SEG_ARGS kin, vin, kout, vout, n, offsets, nseg, max_segment, flip, bad, s
     if (max_segment <= 8) return seg_small<K, KV, 8>(AHS_SEG_ARGS);
@@ -1117,10 +1121,18 @@ cudaError_t seg_launch(const void *kin, const uint32_t *vin, void *kout, uint32_
     if (max_segment <= 20) return seg_small<K, KV, 20>(AHS_SEG_ARGS);  // the paper's n <= 20 Insertion branch
     if (max_segment <= 24) return seg_small<K, KV, 24>(AHS_SEG_ARGS);
     if (max_segment <= (uint32_t)kSegSmallMax) return seg_small<K, KV, 32>(AHS_SEG_ARGS);
-    if (max_segment <= 256) return seg_medium<K, KV, 64>(AHS_SEG_ARGS);  // padded length 4 x BLOCK
-    if (max_segment <= 512) return seg_medium<K, KV, 128>(AHS_SEG_ARGS);
-    if (max_segment <= 1024) return seg_medium<K, KV, 256>(AHS_SEG_ARGS);
-    return seg_medium<K, KV, 512>(AHS_SEG_ARGS);
+    // K9r: threads per segment from the declared maximum (16 keys per thread, one
+    // warp up to 512 keys); the ordered ranking when the device passed its self-test
+    if (ord) {
+        if (max_segment <= 256) return seg_radix<K, KV, 32, 256, true>(AHS_SEG_ARGS);
+        if (max_segment <= 512) return seg_radix<K, KV, 32, 512, true>(AHS_SEG_ARGS);
+        if (max_segment <= 1024) return seg_radix<K, KV, 64, 1024, true>(AHS_SEG_ARGS);
+        return seg_radix<K, KV, 128, 2048, true>(AHS_SEG_ARGS);
+    }
+    if (max_segment <= 256) return seg_radix<K, KV, 32, 256, false>(AHS_SEG_ARGS);
+    if (max_segment <= 512) return seg_radix<K, KV, 32, 512, false>(AHS_SEG_ARGS);
+    if (max_segment <= 1024) return seg_radix<K, KV, 64, 1024, false>(AHS_SEG_ARGS);
+    return seg_radix<K, KV, 128, 2048, false>(AHS_SEG_ARGS);
 #undef AHS_SEG_ARGS
 }
 }  // namespace
@@ -1139,8 +1151,10 @@ int ahs_sort_segments(const void *d_keys_in, const uint32_t *d_vals_in, void *d_
         ((uintptr_t)d_keys_in & kal) || ((uintptr_t)d_keys_out & kal))
         return AHS_EINVAL;
     int sms = 0;
-    int rc = device_info(&sms, nullptr);
+    DevInfo *di = nullptr;
+    int rc = device_info(&sms, nullptr, &di);
     if (rc) return rc;
+    const bool ord = di->rank_mode == kRankOrdered;
     cudaStream_t s = (cudaStream_t)stream;
     if (cudaMemsetAsync(d_bad, 0, 4, s) != cudaSuccess) return AHS_ECUDA;
     if (num_segments == 0) return AHS_OK;
@@ -1148,15 +1162,15 @@ int ahs_sort_segments(const void *d_keys_in, const uint32_t *d_vals_in, void *d_
         if (dtype_wide(dtype)) {
             const uint64_t flip = flip64_of(dtype);
             if (kv) seg_launch<uint64_t, true>(d_keys_in, d_vals_in, d_keys_out, d_vals_out, n, d_offsets,
-                                               num_segments, max_segment, flip, d_bad, s);
+                                               num_segments, max_segment, flip, d_bad, ord, s);
             else seg_launch<uint64_t, false>(d_keys_in, nullptr, d_keys_out, nullptr, n, d_offsets, num_segments,
-                                             max_segment, flip, d_bad, s);
+                                             max_segment, flip, d_bad, ord, s);
         } else {
             const uint32_t flip = flip_of(dtype);
             if (kv) seg_launch<uint32_t, true>(d_keys_in, d_vals_in, d_keys_out, d_vals_out, n, d_offsets,
-                                               num_segments, max_segment, flip, d_bad, s);
+                                               num_segments, max_segment, flip, d_bad, ord, s);
             else seg_launch<uint32_t, false>(d_keys_in, nullptr, d_keys_out, nullptr, n, d_offsets, num_segments,
-                                             max_segment, flip, d_bad, s);
+                                             max_segment, flip, d_bad, ord, s);
         }
     });
     return e == cudaSuccess ? AHS_OK : AHS_ECUDA;

@@ -10,13 +10,8 @@
 //        L in {8, 16, 20, 24, 32} with the largest key) and runs Listing 1's
 //        insertion sort as unrolled adjacent swaps (strict > : stable); coalesced
 //        store.
-//   K9m  max segment <= 2048: one CTA per segment, every segment padded to
-//        P = 4 BLOCK (256 .. 2048, from the declared maximum), 4 records per
-//        thread in registers: a fully unrolled bitonic network (in-register,
-//        warp-shuffle and, for strides >= 128, shared-memory exchanges)
-//        in shared memory on (key, original index) -- unique, so the result is
-//        the stable order -- padded to a power of two with (max, max) records;
-//        values gathered by the sorted indices.
+//   K9r  max segment <= 2048: one group of CAP / 16 threads per segment (one
+//        warp up to 512 keys), an LSD radix sort in shared memory (below).
 // Keys compare as unsigned after `flip` (the sign bit for signed types).  A
 // segment longer than the declared maximum (or reaching past n) is left as is
 // and counted in *bad (device word): never an out-of-bounds access.
@@ -28,7 +23,6 @@ namespace ahs {
 
 constexpr int kSegSmallBlock = 256;
 constexpr int kSegSmallMax = 32;
-constexpr int kSegMedBlock = 512;
 constexpr int kSegMedMax = 2048;
 
 template <typename K, bool KV>
@@ -116,35 +110,61 @@ __global__ void __launch_bounds__(kSegSmallBlock)
     }
 }
 
-// (key, index) order: unique, so a sorting network over it yields the stable order
-template <typename K>
-__device__ __forceinline__ bool rec_gt(K a, uint32_t ia, K b, uint32_t ib)
+// K9r: one group per segment of <= CAP keys, staged in shared memory; LSD radix
+// over 8-bit digits, skipping every digit all keys of the segment share (a
+// stable pass over a constant digit is the identity).  Per pass:
+//   count    warp w of the group owns the contiguous keys [w C, (w + 1) C), C = ceil(len / NW),
+//            and counts their digits into its own table cnt[w][256];
+//   scan     offsets in (digit, warp) order: warp w's first slot for digit d is
+//            sum_{d' < d} total(d') + sum_{w' < w} cnt[w'][d];
+//   scatter  warp w walks its keys in order, 32 at a time; peers with equal
+//            digits take consecutive slots in lane order: the old value of a shared
+//            atomicAdd when the device serves one instruction's lanes in lane order
+//            (ORD, self-tested), else a peer mask from 8 ballots (one per digit bit).
+// Keys and values ping-pong between two buffers; every step keeps index order
+// among equal digits, so the sort is stable.
+template <typename K, bool KV, int GROUP, int CAP>
+constexpr size_t seg_radix_smem()  // per segment group
 {
-    return a > b || (a == b && ia > ib);
+    return 2 * (size_t)CAP * sizeof(K) + (KV ? 2 * (size_t)CAP * 4 : 0) + (size_t)(GROUP / 32) * 256 * 4 + 256 * 4;
 }
 
-template <typename K, bool KV, int BLOCK>
-__global__ void __launch_bounds__(BLOCK)
-    k_seg_medium(const K *__restrict__ kin, const uint32_t *__restrict__ vin, K *__restrict__ kout,
-                 uint32_t *__restrict__ vout, const uint32_t *__restrict__ offsets, uint32_t nseg, uint64_t n, K flip,
-                 uint32_t maxlen, uint32_t *__restrict__ bad)
+// GROUP threads sort one segment; a CTA of SPC * GROUP threads holds SPC
+// groups (SPC > 1 only for one-warp groups: their barriers are warp-local)
+template <typename K, bool KV, int GROUP, int CAP, bool ORD, int SPC>
+__global__ void __launch_bounds__(GROUP * SPC)
+    k_seg_radix(const K *__restrict__ kin, const uint32_t *__restrict__ vin, K *__restrict__ kout,
+                uint32_t *__restrict__ vout, const uint32_t *__restrict__ offsets, uint32_t nseg, uint64_t n, K flip,
+                uint32_t maxlen, uint32_t *__restrict__ bad)
 {
-    // every segment of the launch is padded to P = 4 BLOCK records ((max key, position)
-    // records sort after the real ones); thread t holds positions 4t .. 4t + 3 in registers
-    constexpr int E = 4, P = BLOCK * E;
-    static_assert(P <= kSegMedMax && BLOCK % 32 == 0, "segment capacity");
+    constexpr int NW = GROUP / 32;
+    static_assert(CAP <= kSegMedMax && GROUP % 32 == 0 && CAP % 16 == 0, "segment capacity");
+    static_assert(SPC == 1 || GROUP == 32, "several groups per CTA only for one-warp groups");
     pdl_begin();
-    __shared__ K sk[P];
-    __shared__ uint32_t si[P];
-    __shared__ uint32_t sv[KV ? P : 1];  // values staged too: in place is safe
-    const uint32_t seg = blockIdx.x;
-    if (seg >= nseg) return;
+    extern __shared__ __align__(16) uint8_t seg_smem[];  // SPC x seg_radix_smem<K, KV, GROUP, CAP>()
+    const uint32_t g = threadIdx.x / GROUP;
+    uint8_t *const gsm = seg_smem + g * seg_radix_smem<K, KV, GROUP, CAP>();
+    K *const kbuf0 = reinterpret_cast<K *>(gsm);
+    K *const kbuf1 = kbuf0 + CAP;
+    uint32_t *const cnt = reinterpret_cast<uint32_t *>(kbuf1 + CAP);  // [NW][256]
+    uint32_t *const dbase = cnt + NW * 256;                          // [256]
+    [[maybe_unused]] uint32_t *const vbuf0 = dbase + 256;
+    [[maybe_unused]] uint32_t *const vbuf1 = vbuf0 + CAP;
+    __shared__ uint32_t s_diff[SPC][2];
+    __shared__ uint32_t s_idle[NW * SPC];  // ORD: the slot idle lanes' atomics go to
+    auto gsync = [] {
+        if constexpr (NW == 1) __syncwarp();
+        else __syncthreads();
+    };
+    const uint32_t seg = blockIdx.x * SPC + g;
+    if (seg >= nseg) return;  // a whole group: no barrier spans groups
     const uint32_t lo = __ldg(&offsets[seg]), hi = __ldg(&offsets[seg + 1]);
-    if (hi < lo || (uint64_t)hi > n || hi - lo > maxlen || hi - lo > (uint32_t)P) {
-        if (threadIdx.x == 0) atomicAdd(bad, 1u);
+    const uint32_t t = threadIdx.x % GROUP, lane = t & 31u, warp = t >> 5;
+    if (hi < lo || (uint64_t)hi > n || hi - lo > maxlen || hi - lo > (uint32_t)CAP) {
+        if (t == 0) atomicAdd(bad, 1u);
         return;
     }
-    const uint32_t len = hi - lo, t = threadIdx.x;
+    const uint32_t len = hi - lo;
     if (len < 2) {
         if (len == 1 && t == 0) {
             kout[lo] = kin[lo];
@@ -152,88 +172,135 @@ __global__ void __launch_bounds__(BLOCK)
         }
         return;
     }
-    for (uint32_t i = t; i < (uint32_t)P; i += BLOCK) {  // coalesced staging
-        sk[i] = i < len ? (kin[lo + i] ^ flip) : ~K(0);
-        if constexpr (KV)
-            if (i < len) sv[i] = vin[lo + i];
+    // coalesced staging; the bits in which some key differs from the first
+    if (t == 0) s_diff[g][0] = s_diff[g][1] = 0u;
+    gsync();
+    const K first = kin[lo] ^ flip;
+    K dacc = 0;
+    for (uint32_t i = t; i < len; i += GROUP) {
+        const K x = kin[lo + i] ^ flip;
+        kbuf0[i] = x;
+        dacc |= x ^ first;
+        if constexpr (KV) vbuf0[i] = vin[lo + i];
     }
-    __syncthreads();
-    K key[E];
-    uint32_t idx[E];
-#pragma unroll
-    for (int e = 0; e < E; e++) {
-        key[e] = sk[t * E + e];
-        idx[e] = t * E + e;
+    const uint32_t dlo = __reduce_or_sync(kFull, (uint32_t)dacc);
+    const uint32_t dhi = sizeof(K) == 8 ? __reduce_or_sync(kFull, (uint32_t)((uint64_t)dacc >> 32)) : 0u;
+    if (lane == 0) {
+        if (dlo) atomicOr(&s_diff[g][0], dlo);
+        if (dhi) atomicOr(&s_diff[g][1], dhi);
     }
-    // bitonic network, fully unrolled: stride j < E in registers, j < 32 E by warp
-    // shuffles (partner lane t ^ j / E), larger strides through shared memory
+    gsync();
+    const uint64_t diff = ((uint64_t)s_diff[g][1] << 32) | s_diff[g][0];
+    const uint32_t C = (len + NW - 1) / NW;
+    const uint32_t wb = min(len, warp * C), we = min(len, wb + C);
+    uint32_t *const wc = cnt + warp * 256;
+    [[maybe_unused]] const uint32_t lt = (1u << lane) - 1u;
+    int cur = 0;
+    for (int b = 0; b < (int)sizeof(K); b++) {
+        if (((diff >> (8 * b)) & 0xffu) == 0) continue;  // uniform over the group
+        const uint32_t sh = 8u * b;
+        const K *src = cur ? kbuf1 : kbuf0;
+        K *dst = cur ? kbuf0 : kbuf1;
+        for (uint32_t i = t; i < NW * 256u; i += GROUP) cnt[i] = 0u;
+        gsync();
+        for (uint32_t i = wb + lane; i < we; i += 32) atomicAdd(&wc[(uint32_t)(src[i] >> sh) & 0xffu], 1u);
+        gsync();
+        if constexpr (NW > 1) {
+            for (uint32_t d = t; d < 256u; d += GROUP) {  // column prefix over the warps
+                uint32_t run = 0;
 #pragma unroll
-    for (int k = 2; k <= P; k <<= 1) {
-#pragma unroll
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            if (j < E) {
-#pragma unroll
-                for (int e = 0; e < E; e++) {
-                    const int pe = e ^ j;
-                    if (pe > e) {
-                        const bool up = ((t * E + e) & k) == 0;
-                        if (rec_gt(key[e], idx[e], key[pe], idx[pe]) == up) {
-                            const K tk = key[e];
-                            key[e] = key[pe];
-                            key[pe] = tk;
-                            const uint32_t ti = idx[e];
-                            idx[e] = idx[pe];
-                            idx[pe] = ti;
-                        }
-                    }
+                for (int w = 0; w < NW; w++) {
+                    const uint32_t c = cnt[w * 256 + d];
+                    cnt[w * 256 + d] = run;
+                    run += c;
                 }
-            } else {
-                K ok[E];
-                uint32_t oi[E];
-                if (j < E * 32) {
+                dbase[d] = run;
+            }
+            gsync();
+        }
+        if (warp == 0) {  // exclusive scan over the 256 digit totals, 8 per lane
+            const uint32_t *tot = NW > 1 ? dbase : cnt;
+            uint32_t v[8], sum = 0;
 #pragma unroll
-                    for (int e = 0; e < E; e++) {
-                        ok[e] = __shfl_xor_sync(kFull, key[e], j / E);
-                        oi[e] = __shfl_xor_sync(kFull, idx[e], j / E);
-                    }
-                } else {
-                    __syncthreads();  // the previous exchange's reads are done
+            for (int j = 0; j < 8; j++) {
+                v[j] = tot[lane * 8 + j];
+                sum += v[j];
+            }
+            uint32_t incl = sum;
 #pragma unroll
-                    for (int e = 0; e < E; e++) {
-                        sk[t * E + e] = key[e];
-                        si[t * E + e] = idx[e];
-                    }
-                    __syncthreads();
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t x = __shfl_up_sync(kFull, incl, o);
+                if (lane >= (uint32_t)o) incl += x;
+            }
+            uint32_t ex = incl - sum;
+            if constexpr (NW == 1) __syncwarp();  // every lane has read cnt before it is overwritten
 #pragma unroll
-                    for (int e = 0; e < E; e++) {
-                        ok[e] = sk[(t * E + e) ^ j];
-                        oi[e] = si[(t * E + e) ^ j];
-                    }
-                }
-#pragma unroll
-                for (int e = 0; e < E; e++) {
-                    const uint32_t p = t * E + e;
-                    const bool up = (p & k) == 0, lower = (p & j) == 0;
-                    // ascending: the lower position keeps the smaller record
-                    const bool take = rec_gt(key[e], idx[e], ok[e], oi[e]) == (lower == up);
-                    if (take) {
-                        key[e] = ok[e];
-                        idx[e] = oi[e];
-                    }
-                }
+            for (int j = 0; j < 8; j++) {
+                // one warp: its table becomes the absolute slots directly
+                if constexpr (NW == 1) cnt[lane * 8 + j] = ORD ? ex : 0u;
+                dbase[lane * 8 + j] = ex;
+                ex += v[j];
             }
         }
-    }
-    __syncthreads();
+        gsync();
+        if constexpr (ORD) {
+            // the ordered ranking: shared atomics of one warp instruction on one word
+            // return in lane order (self-tested per device, onesweep.cuh), so each
+            // warp's table holds absolute slots and the atomic's old value is the slot
+            if constexpr (NW > 1) {
+                for (uint32_t d = t; d < 256u; d += GROUP) {
+                    const uint32_t base = dbase[d];
 #pragma unroll
-    for (int e = 0; e < E; e++) {
-        sk[t * E + e] = key[e];
-        si[t * E + e] = idx[e];
+                    for (int w = 0; w < NW; w++) cnt[w * 256 + d] += base;
+                }
+                gsync();
+            }
+            for (uint32_t i0 = wb; i0 < we; i0 += 32) {
+                const uint32_t i = i0 + lane;
+                const bool ok = i < we;
+                const K x = ok ? src[i] : K(0);
+                uint32_t *const a = ok ? wc + ((uint32_t)(x >> sh) & 0xffu) : s_idle + g * NW + warp;  // full-warp
+                const uint32_t pos = atomicAdd(a, 1u);
+                if (ok) {
+                    dst[pos] = x;
+                    if constexpr (KV) (cur ? vbuf0 : vbuf1)[pos] = (cur ? vbuf1 : vbuf0)[i];
+                }
+                __syncwarp();
+            }
+        } else {
+            for (uint32_t i0 = wb; i0 < we; i0 += 32) {  // warp-uniform trip count
+                const uint32_t i = i0 + lane;
+                const bool ok = i < we;
+                const K x = ok ? src[i] : K(0);
+                const uint32_t d = (uint32_t)(x >> sh) & 0xffu;
+                uint32_t peers = __ballot_sync(kFull, ok);  // lanes with my digit: one vote per digit bit
+#pragma unroll
+                for (int q = 0; q < 8; q++) {
+                    const uint32_t bq = __ballot_sync(kFull, (d >> q) & 1u);
+                    peers &= ((d >> q) & 1u) ? bq : ~bq;
+                }
+                uint32_t wold = 0, pos = 0;
+                if (ok) {
+                    wold = wc[d];
+                    pos = dbase[d] + wold + __popc(peers & lt);
+                }
+                __syncwarp();
+                if (ok) {
+                    dst[pos] = x;
+                    if constexpr (KV) (cur ? vbuf0 : vbuf1)[pos] = (cur ? vbuf1 : vbuf0)[i];
+                    if (lane == (uint32_t)(__ffs(peers) - 1)) wc[d] = wold + __popc(peers);
+                }
+                __syncwarp();
+            }
+        }
+        gsync();
+        cur ^= 1;
     }
-    __syncthreads();
-    for (uint32_t i = t; i < len; i += BLOCK) {  // coalesced store; values by the sorted indices
-        kout[lo + i] = sk[i] ^ flip;
-        if constexpr (KV) vout[lo + i] = sv[si[i]];
+    const K *fk = cur ? kbuf1 : kbuf0;
+    [[maybe_unused]] const uint32_t *fv = cur ? vbuf1 : vbuf0;
+    for (uint32_t i = t; i < len; i += GROUP) {
+        kout[lo + i] = fk[i] ^ flip;
+        if constexpr (KV) vout[lo + i] = fv[i];
     }
 }
 

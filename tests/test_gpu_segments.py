@@ -100,9 +100,18 @@ def test_small_segments(dt, max_len):
                 assert np.array_equal(vo, ev)
 
 
+@pytest.fixture(params=["ordered", "masked"])
+def rank(request):
+    prev = ahs.ahs_rank_mode()
+    if request.param == "masked":
+        ahs.ahs_rank_mode(ahs.RANK_MASKED)
+    yield request.param
+    ahs.ahs_rank_mode(prev)
+
+
 @pytest.mark.parametrize("dt", list(DT))
-@pytest.mark.parametrize("max_len", [33, 100, 1000, 2048])
-def test_medium_segments(dt, max_len):
+@pytest.mark.parametrize("max_len", [33, 100, 512, 1000, 2048])
+def test_medium_segments(dt, max_len, rank):
     nseg = 300 if max_len <= 100 else 40
     off = make_offsets(nseg, max_len, 17 + max_len)
     n = int(off[-1])
@@ -115,6 +124,32 @@ def test_medium_segments(dt, max_len):
         assert np.array_equal(ko, ek), (dt, max_len)
         if v is not None:
             assert np.array_equal(vo, ev)
+
+
+@pytest.mark.parametrize("pattern", ["byte2", "bytes0_7", "top_bit", "all_equal", "two_values"])
+@pytest.mark.parametrize("max_len", [256, 2048])
+def test_medium_digit_patterns(pattern, max_len, rank):
+    """keys that differ only in some bytes: the radix path skips the shared digits"""
+    nseg = 60
+    off = make_offsets(nseg, max_len, 31 + max_len)
+    n = int(off[-1])
+    x = synth.stream(37, n)
+    base = np.uint64(0x0123456789ABCDEF)
+    k = {"byte2": base ^ ((x & np.uint64(0xff)) << np.uint64(16)),
+         "bytes0_7": base ^ (x & np.uint64(0xff)) ^ ((x >> np.uint64(8)) << np.uint64(56)),
+         "top_bit": base ^ ((x & np.uint64(1)) << np.uint64(63)),
+         "all_equal": np.full(n, base, dtype=np.uint64),
+         "two_values": base ^ ((x & np.uint64(1)) * np.uint64(0x0000010000000100))}[pattern]
+    vals = np.arange(n, dtype=np.uint32)
+    for dt in ("u64", "i64", "u32", "i32"):
+        keys = k.view(np.int64).astype(DT[dt]) if dt == "i64" else (
+            k.astype(DT[dt]) if dt == "u64" else (k & np.uint64(0xffffffff) if pattern != "bytes0_7" else
+                                                   (k & np.uint64(0xff)) | ((k >> np.uint64(32)) & np.uint64(0xff000000))
+                                                   ).astype(np.uint32).view(DT[dt]))
+        ko, vo, bad = run(keys, vals, off, max_len)
+        ek, ev = expected(keys, vals, off, max_len)
+        assert bad == 0
+        assert np.array_equal(ko, ek) and np.array_equal(vo, ev), (pattern, dt)
 
 
 @pytest.mark.parametrize("max_len", [20, 500])

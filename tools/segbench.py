@@ -54,6 +54,10 @@ def bench(name, nseg, lo, hi, max_len, kv, dtype=np.int32, reps=20):
 bench("insertion n<=20", 1 << 20, 1, 20, 20, False)
 bench("insertion n<=20 kv", 1 << 20, 1, 20, 20, True)
 bench("insertion n<=32 u64", 1 << 20, 1, 32, 32, False, np.uint64)
-bench("bitonic 100-200", 1 << 16, 100, 200, 200, False)
-bench("bitonic 1000-2048", 1 << 13, 1000, 2048, 2048, False)
-bench("bitonic 1000-2048 kv", 1 << 13, 1000, 2048, 2048, True)
+bench("radix 100-200", 1 << 16, 100, 200, 200, False)
+bench("radix 1000-2048", 1 << 13, 1000, 2048, 2048, False)
+bench("radix 1000-2048 kv", 1 << 13, 1000, 2048, 2048, True)
+bench("radix 1000-2048 u64", 1 << 13, 1000, 2048, 2048, False, np.uint64)
+bench("radix 33-256", 1 << 16, 33, 256, 256, False)
+bench("radix 300-512", 1 << 15, 300, 512, 512, False)
+bench("radix 600-1024 kv", 1 << 14, 600, 1024, 1024, True)
