@@ -289,7 +289,6 @@ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 // ------------------------------------------------------------ ws layout
 constexpr int kMaxReduceBlocks = 2048;
-constexpr int kMaxHistRows = 80;  // K2 clusters (rows of partial histograms)
 struct WsLayout {
     size_t feat, partials, fctrl, ovf, hist, scan, parts, byte0, digit1, ent, total;
 };
@@ -591,10 +590,10 @@ int ahs_features(const void *d_keys, uint64_t n, int32_t dtype, void *d_ws, size
     e = launch(KID_FEAT_HIST, s, [&] {
         if (wide)
             launch_k(K2_KERNEL64, dim3((unsigned)(rows * kHistCluster)), dim3(kHistBlock), kHistSmemBytes, s, keys64,
-                     n, flip64, (const Partial64 *)partials64, (int)g1, ovf, parts, (uint32_t *)(ws + L.digit1));
+                     n, flip64, (const Partial64 *)partials64, (int)g1, ovf, parts, (uint32_t *)(ws + L.digit1), fctrl);
         else
             launch_k(K2_KERNEL, dim3((unsigned)(rows * kHistCluster)), dim3(kHistBlock), kHistSmemBytes, s, keys, n,
-                     flip, (const Partial *)partials, (int)g1, ovf, parts, (uint32_t *)(ws + L.digit1));
+                     flip, (const Partial *)partials, (int)g1, ovf, parts, (uint32_t *)(ws + L.digit1), fctrl);
     });
     if (e != cudaSuccess) return AHS_ECUDA;
     // the one host sync of the pipeline: K3's last CTA writes the 64-byte
@@ -622,11 +621,11 @@ int ahs_features(const void *d_keys, uint64_t n, int32_t dtype, void *d_ws, size
     e = launch(KID_FEAT_FINALIZE, s, [&] {
         if (wide)
             launch_k(k_feat_finalize<kFinalBlock, kFinalGroups, uint64_t>, dim3(kFinalGrid), dim3(kFinalBlock), 0,
-                     s, n, (const Partial64 *)partials64, (int)g1, (const uint32_t *)parts, (int)rows,
+                     s, n, (int)g1, (const uint32_t *)parts, (int)rows,
                      (const uint32_t *)ovf, hist, fctrl, dfeat, hfb.d, seq);
         else
             launch_k(k_feat_finalize<kFinalBlock, kFinalGroups>, dim3(kFinalGrid), dim3(kFinalBlock), 0, s, n,
-                     (const Partial *)partials, (int)g1, (const uint32_t *)parts, (int)rows, (const uint32_t *)ovf,
+                     (int)g1, (const uint32_t *)parts, (int)rows, (const uint32_t *)ovf,
                      hist, fctrl, dfeat, hfb.d, seq);
     });
     if (e != cudaSuccess) return AHS_ECUDA;

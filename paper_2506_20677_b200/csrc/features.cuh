@@ -39,15 +39,18 @@ constexpr int kHistBins = 128 * 1024;                // bytes: 2^16 packed 16-bi
 constexpr uint32_t kHistWords = kHistBins / 4;       // 32768
 constexpr int kHistSmemBytes = kHistBins + kHistStages * (kHistChunk + 16);
 constexpr int kFinalBins = 256;                      // K3 bins per CTA
-constexpr int kFinalGroups = 4;                      // K3 row groups (threads per bin)
-constexpr int kFinalBlock = kFinalBins * kFinalGroups;
+constexpr int kFinalGroups = 16;                     // K3 row groups (threads per 4-bin quad)
+constexpr int kFinalBlock = kFinalBins / 4 * kFinalGroups;
+constexpr int kMaxHistRows = 80;                     // K2 clusters (rows of partial histograms)
 constexpr uint32_t kMaxBins = 1u << 16;
 constexpr int kFinalGrid = (int)(kMaxBins / kFinalBins);  // 256
 
 // K3 control block in ws (zeroed by K1 where noted)
 struct FinalCtrl {
-    uint32_t barrier;       // K3's finished-CTA count, zeroed by K1
-    uint32_t pad[31];
+    uint32_t barrier;  // K3's finished-CTA count, zeroed by K1
+    uint32_t pad0;
+    alignas(8) unsigned char reduced[24];  // K1's partials reduced (KeyTraits<K>::P), written by K2's CTA 0
+    uint32_t pad[24];
     uint32_t chunk_tot[kFinalGrid];
     double chunk_S[kFinalGrid];
 };
@@ -458,13 +461,16 @@ template <int BLOCK, int CL, typename K = uint32_t>
 __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(BLOCK, 1)
     k_feat_hist(const K *__restrict__ keys, uint64_t n, K flip,
                 const typename KeyTraits<K>::P *__restrict__ partials, int nparts, uint32_t *__restrict__ ovf,
-                uint32_t *__restrict__ parts, uint32_t *__restrict__ digit1_rows)
+                uint32_t *__restrict__ parts, uint32_t *__restrict__ digit1_rows, FinalCtrl *__restrict__ fctrl)
 {
     pdl_begin();
     extern __shared__ __align__(128) uint32_t sh[];
     __shared__ __align__(8) uint64_t bars[kHistStages];
     cg::cluster_group cluster = cg::this_cluster();
     const auto p = KeyTraits<K>::template reduce<BLOCK>(partials, nparts);
+    using P = typename KeyTraits<K>::P;
+    static_assert(sizeof(P) <= sizeof(fctrl->reduced), "reduced partial");
+    if (blockIdx.x == 0 && threadIdx.x == 0) *reinterpret_cast<P *>(fctrl->reduced) = p;  // for K3
     const Range64 rg = KeyTraits<K>::range(p);
     if (rg.nb <= 1u) return;  // k = 1 (uniform for the whole grid): no histogram
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
@@ -609,10 +615,13 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(BLOCK, 1)
 }
 
 // ------------------------------------------------------------------ K3 ----
-// kFinalGrid CTAs x kFinalBlock threads; CTA j owns bins [j * BINS, (j + 1) * BINS),
-// and the GROUPS row groups of its threads sum every GROUPS-th cluster row of
-// them (the row sums are latency bound: GROUPS independent load streams per
-// bin).  CTAs past the last bin (nb < 2^16) return at once; `active` remain.
+// kFinalGrid CTAs x kFinalBlock threads; CTA j owns bins [j * BINS, (j + 1) * BINS).
+// min / max / descents come reduced from K2 (its CTA 0 publishes K1's partials
+// reduced in FinalCtrl), so the row loads start after one dependent read.
+// Thread (g, q) sums 16-byte quads of bins 4q .. 4q + 3 over the cluster rows
+// r = g, g + GROUPS, ... (<= kMaxHistRows / GROUPS loads, all in flight: the row
+// sums are latency bound), then the GROUPS partial sums of a bin meet in shared
+// memory.  CTAs past the last bin (nb < 2^16) return at once; `active` remain.
 //   c_b = sum of the cluster rows + overflow; hist[b] = c_b; per-CTA chunk
 //   total and chunk sum S_j of c_b log2 c_b (fixed tree).
 //   The last active CTA to finish (atomic count, zeroed by K1; no grid
@@ -668,40 +677,54 @@ __device__ __forceinline__ void write_host_features(DevFeatures *hout, const Dev
 
 template <int BLOCK, int GROUPS, typename K = uint32_t>
 __global__ void __launch_bounds__(BLOCK, 2)
-    k_feat_finalize(uint64_t n, const typename KeyTraits<K>::P *__restrict__ partials, int nparts,
+    k_feat_finalize(uint64_t n, int nparts,
                     const uint32_t *__restrict__ parts, int nrows, const uint32_t *__restrict__ ovf,
                     uint32_t *__restrict__ hist, FinalCtrl *__restrict__ fctrl, DevFeatures *__restrict__ out,
                     DevFeatures *__restrict__ hout, uint64_t seq)
 {
     pdl_begin();
-    constexpr uint32_t BINS = BLOCK / GROUPS;
-    const auto p = KeyTraits<K>::template reduce<BLOCK>(partials, nparts);
+    constexpr uint32_t BINS = kFinalBins, QUADS = BINS / 4;
+    constexpr int MAXR = (kMaxHistRows + GROUPS - 1) / GROUPS;
+    static_assert(BLOCK == (int)QUADS * GROUPS && BLOCK >= (int)BINS, "K3 shape");
+    // K1's partials, reduced by K2 (its CTA 0; K2 has completed: griddepcontrol.wait)
+    const auto p = *reinterpret_cast<const typename KeyTraits<K>::P *>(fctrl->reduced);
     const Range64 rg = KeyTraits<K>::range(p);
     const uint32_t active = (rg.nb + BINS - 1u) / BINS;
     if (blockIdx.x >= active) return;  // no bins here (uniform per CTA)
     __shared__ uint32_t s_u[BLOCK / 32];
     __shared__ double s_d[BLOCK / 32];
-    __shared__ uint32_t s_part[GROUPS - 1][BINS];
+    __shared__ __align__(16) uint32_t s_part[GROUPS][BINS];
     __shared__ uint32_t s_last;
-    const uint32_t grp = threadIdx.x / BINS;
-    const uint32_t b = blockIdx.x * BINS + threadIdx.x % BINS;
-
-    uint32_t c = 0;
-    if (b < rg.nb && rg.nb > 1u) {
-#pragma unroll 8
-        for (int r = (int)grp; r < nrows; r += GROUPS) c += __ldcg(&parts[(size_t)r * kMaxBins + b]);
+    const uint32_t b = blockIdx.x * BINS + threadIdx.x;
+    const uint32_t ov = (threadIdx.x < BINS && b < rg.nb && rg.nb > 1u) ? __ldcg(&ovf[b]) : 0u;  // with the rows
+    {
+        const uint32_t grp = threadIdx.x / QUADS, q = threadIdx.x % QUADS;
+        const uint32_t b0 = blockIdx.x * BINS + 4u * q;  // row words past nb are read, never used
+        uint4 acc = make_uint4(0u, 0u, 0u, 0u);
+        if (b0 < rg.nb && rg.nb > 1u) {
+#pragma unroll
+            for (int j = 0; j < MAXR; j++) {
+                const int r = (int)grp + j * GROUPS;
+                if (r < nrows) {
+                    const uint4 v = __ldcg(reinterpret_cast<const uint4 *>(parts + (size_t)r * kMaxBins + b0));
+                    acc.x += v.x;
+                    acc.y += v.y;
+                    acc.z += v.z;
+                    acc.w += v.w;
+                }
+            }
+        }
+        *reinterpret_cast<uint4 *>(&s_part[grp][4u * q]) = acc;
     }
-    if (grp > 0) s_part[grp - 1][threadIdx.x % BINS] = c;
     __syncthreads();
-    if (grp > 0) {
-        c = 0;
-    } else if (b < rg.nb) {  // group 0 holds the bin's count
+    uint32_t c = 0;
+    if (threadIdx.x < BINS && b < rg.nb) {
         if (rg.nb == 1u) {
             c = (uint32_t)n;
         } else {
-            c += __ldcg(&ovf[b]);
+            c = ov;
 #pragma unroll
-            for (int q = 0; q < GROUPS - 1; q++) c += s_part[q][threadIdx.x];
+            for (int g = 0; g < GROUPS; g++) c += s_part[g][threadIdx.x];
         }
         hist[b] = c;
     }
