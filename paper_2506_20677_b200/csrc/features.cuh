@@ -28,9 +28,33 @@ namespace ahs {
 namespace cg = cooperative_groups;
 
 constexpr int kReduceBlock = 256;
-constexpr int kReduceChunk = 32 * 1024;  // bytes per TMA chunk: 8 vectors per thread
+constexpr int kReduceChunk = 24 * 1024;  // bytes per TMA chunk: 6 vectors per thread
 constexpr int kReduceStages = 3;
-constexpr int kReduceSmem = kReduceStages * (kReduceChunk + 16);
+constexpr int kReduceStageBytes = kReduceStages * (kReduceChunk + 16);
+// K1's raw-low-byte histogram, one column per lane: word (byte << 5) | lane.  Lane l
+// always hits bank l, so each atomic instruction is one shared-memory wavefront
+// whatever the bytes (a plain 256-word table costs ~3.6 from bank collisions).
+constexpr int kB0Words = 256 * 32;
+constexpr int kReduceSmem = kReduceStageBytes + kB0Words * 4;
+static_assert(kReduceStageBytes % 16 == 0, "lane table alignment");
+
+// zero / fold the lane-column table (BLOCK threads; the fold rotates the lane
+// per bin so a warp's 32 reads hit 32 banks)
+template <int BLOCK>
+__device__ __forceinline__ void b0_zero(uint32_t *t)
+{
+    for (int i = threadIdx.x; i < kB0Words / 4; i += BLOCK) reinterpret_cast<uint4 *>(t)[i] = make_uint4(0u, 0u, 0u, 0u);
+}
+template <int BLOCK>
+__device__ __forceinline__ void b0_fold(const uint32_t *t, uint32_t *row)
+{
+    for (int b = threadIdx.x; b < 256; b += BLOCK) {
+        uint32_t s = 0;
+#pragma unroll 8
+        for (int l = 0; l < 32; l++) s += t[(b << 5) | ((l + b) & 31)];
+        row[b] = s;
+    }
+}
 constexpr int kHistBlock = 1024;
 constexpr int kHistChunk = 48 * 1024;  // 3 vectors per thread
 constexpr int kHistStages = 2;
@@ -72,8 +96,8 @@ __global__ void __launch_bounds__(BLOCK)
     // histogram of the raw low byte of every key (for the radix sort: digit 0 of
     // key - min is this byte minus min's low byte, mod 256 -- no borrow -- so it
     // is known before min is); one row per CTA, no atomics across CTAs
-    __shared__ uint32_t s_b0[256];
-    for (int i = threadIdx.x; i < 256; i += BLOCK) s_b0[i] = 0u;
+    uint32_t *s_b0 = reinterpret_cast<uint32_t *>(smem_raw + kReduceStageBytes);  // lane columns
+    b0_zero<BLOCK>(s_b0);
     __syncthreads();
     for (uint32_t i = blockIdx.x * BLOCK + threadIdx.x; i < nzero; i += gridDim.x * BLOCK)
         zero_words[i] = 0u;
@@ -98,10 +122,10 @@ __global__ void __launch_bounds__(BLOCK)
                 }
                 mn = min(mn, min(min(a0, a1), min(a2, a3)));
                 mx = max(mx, max(max(a0, a1), max(a2, a3)));
-                atomicAdd(&s_b0[a0 & 255u], 1u);
-                atomicAdd(&s_b0[a1 & 255u], 1u);
-                atomicAdd(&s_b0[a2 & 255u], 1u);
-                atomicAdd(&s_b0[a3 & 255u], 1u);
+                atomicAdd(&s_b0[((a0 & 255u) << 5) | lane], 1u);
+                atomicAdd(&s_b0[((a1 & 255u) << 5) | lane], 1u);
+                atomicAdd(&s_b0[((a2 & 255u) << 5) | lane], 1u);
+                atomicAdd(&s_b0[((a3 & 255u) << 5) | lane], 1u);
                 desc += (uint32_t)(a0 > a1) + (uint32_t)(a1 > a2) + (uint32_t)(a2 > a3) +
                         (uint32_t)(has_next && a3 > nxt);
             }
@@ -114,13 +138,13 @@ __global__ void __launch_bounds__(BLOCK)
             const uint32_t a = keys[i] ^ flip;
             mn = min(mn, a);
             mx = max(mx, a);
-            atomicAdd(&s_b0[a & 255u], 1u);
+            atomicAdd(&s_b0[((a & 255u) << 5) | lane], 1u);
             if (i + 1 < n) desc += (uint32_t)(a > (keys[i + 1] ^ flip));
         }
     }
 
     __syncthreads();
-    for (int i = threadIdx.x; i < 256; i += BLOCK) byte0_rows[(size_t)blockIdx.x * 256 + i] = s_b0[i];
+    b0_fold<BLOCK>(s_b0, byte0_rows + (size_t)blockIdx.x * 256);
     __shared__ uint32_t s_mn[BLOCK / 32], s_mx[BLOCK / 32], s_d[BLOCK / 32];
     mn = __reduce_min_sync(kFull, mn);
     mx = __reduce_max_sync(kFull, mx);
@@ -165,8 +189,9 @@ __global__ void __launch_bounds__(BLOCK)
     pdl_begin();
     extern __shared__ __align__(128) uint8_t smem_raw[];
     __shared__ __align__(8) uint64_t bars[kReduceStages];
-    __shared__ uint32_t s_b0[256];  // raw low byte (digit 0 of key - min up to a rotation), as in K1
-    for (int i = threadIdx.x; i < 256; i += BLOCK) s_b0[i] = 0u;
+    // raw low byte (digit 0 of key - min up to a rotation), lane columns as in K1
+    uint32_t *s_b0 = reinterpret_cast<uint32_t *>(smem_raw + kReduceStageBytes);
+    b0_zero<BLOCK>(s_b0);
     __syncthreads();
     for (uint32_t i = blockIdx.x * BLOCK + threadIdx.x; i < nzero; i += gridDim.x * BLOCK)
         zero_words[i] = 0u;
@@ -193,8 +218,8 @@ __global__ void __launch_bounds__(BLOCK)
                 }
                 mn = min(mn, min(a0, a1));
                 mx = max(mx, max(a0, a1));
-                atomicAdd(&s_b0[x.x & 255u], 1u);
-                atomicAdd(&s_b0[x.z & 255u], 1u);
+                atomicAdd(&s_b0[((x.x & 255u) << 5) | lane], 1u);
+                atomicAdd(&s_b0[((x.z & 255u) << 5) | lane], 1u);
                 desc += (uint32_t)(a0 > a1) + (uint32_t)(has_next && a1 > nxt);
             }
         });
@@ -205,12 +230,12 @@ __global__ void __launch_bounds__(BLOCK)
             const uint64_t a = keys[i] ^ flip;
             mn = min(mn, a);
             mx = max(mx, a);
-            atomicAdd(&s_b0[(uint32_t)a & 255u], 1u);
+            atomicAdd(&s_b0[(((uint32_t)a & 255u) << 5) | lane], 1u);
             if (i + 1 < n) desc += (uint32_t)(a > (keys[i + 1] ^ flip));
         }
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < 256; i += BLOCK) byte0_rows[(size_t)blockIdx.x * 256 + i] = s_b0[i];
+    b0_fold<BLOCK>(s_b0, byte0_rows + (size_t)blockIdx.x * 256);
     __shared__ uint64_t s_mn[BLOCK / 32], s_mx[BLOCK / 32];
     __shared__ uint32_t s_d[BLOCK / 32];
 #pragma unroll
