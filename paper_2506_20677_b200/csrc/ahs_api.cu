@@ -975,7 +975,8 @@ int ahs_entropy_sorted_dtype(const void *d_keys, uint64_t n, int32_t dtype, void
     uint64_t grid = std::min<uint64_t>((n + kTileKeys - 1) / kTileKeys, (uint64_t)di->ent_grid[wide ? 1 : 0]);
     grid = std::max<uint64_t>(1, grid);
     uint64_t chunk = (n + grid - 1) / grid;
-    chunk = (chunk + kEntItems - 1) / kEntItems * kEntItems;  // chunk starts stay 16-key aligned
+    constexpr uint64_t kAlign = (uint64_t)kEntItems * (kEntBlock / 32);  // each warp's sub-chunk: 16-key aligned
+    chunk = (chunk + kAlign - 1) / kAlign * kAlign;
     grid = (n + chunk - 1) / chunk;
     char *ws = (char *)d_ws;
     RunPieces *pieces = (RunPieces *)(ws + L.ent);

@@ -4,15 +4,17 @@
 // (ahs_sort's output):  H = log2 n - (1/n) sum_runs c log2 c.
 //
 // One cooperative launch of G CTAs, CTA c owning the contiguous chunk
-// [c0, c1) = [c * chunk, (c + 1) * chunk), one read of the keys:
-//   per chunk   tiles of BLOCK x 16 keys (next tile prefetched); a run starts at
-//               i when i == 0 or key[i] != key[i-1] and ends at i when i == n-1
-//               or key[i] != key[i+1]; a block max-scan gives every thread the
-//               start of its first run.  Runs that start AND end inside the
-//               chunk add c log2 c (fp64, fixed order) -> S[c].  The chunk's
-//               first run, when it began in an earlier chunk, is only measured
-//               (its length inside the chunk, and whether it ends here); so is
-//               the last run when it continues into the next chunk.
+// [c * chunk, (c + 1) * chunk), one read of the keys:
+//   per warp    the chunk's w-th eighth, in steps of 32 x 16 keys (next step
+//               prefetched); a run starts at i when i == 0 or key[i] != key[i-1]
+//               and ends at i when i == n-1 or key[i] != key[i+1]; a warp
+//               max-scan (carried between steps) gives every lane the start of
+//               its first run.  Runs that start AND end inside the sub-chunk add
+//               c log2 c (fp64, fixed order).  The sub-chunk's first run, when
+//               it began earlier, is only measured (its length inside, and
+//               whether it ends here); so is the last run when it continues.
+//   per CTA     thread 0 stitches the warps' pieces: runs crossing warp
+//               boundaries inside the chunk, and the chunk's own pieces -> S[c].
 //   grid sync
 //   CTA 0       the runs that cross chunk boundaries: the thread of each run's
 //               origin chunk follows it forward to its end; then a fixed tree
@@ -47,31 +49,32 @@ __global__ void __launch_bounds__(BLOCK)
     pdl_begin();
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
-    __shared__ uint32_t s_w[BLOCK / 32];
-    __shared__ double s_d[BLOCK / 32];
-    __shared__ RunPieces s_rp;
+    constexpr int NW = BLOCK / 32;
+    __shared__ double s_d[NW];
+    __shared__ RunPieces s_wp[NW];
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    const uint64_t c0 = (uint64_t)blockIdx.x * chunk;
-    const uint64_t c1 = min(n, c0 + chunk);
-    if (threadIdx.x == 0) s_rp = RunPieces{0ull, 0ull, 0u, 0u};
-    __syncthreads();
-    // a run that began before the chunk enters it unless key[c0] starts a new run
+    // warp w of the CTA owns the contiguous sub-chunk [c0, c1) of the CTA's chunk
+    // (wchunk keys, a multiple of 16): its carry between steps is a warp scan, no
+    // block barrier; the warps' boundary pieces are stitched into the CTA's below
+    const uint64_t wchunk = chunk / NW;
+    const uint64_t c0 = min(n, (uint64_t)blockIdx.x * chunk + warp * wchunk);
+    const uint64_t c1 = min(n, c0 + wchunk);
+    RunPieces rp{0ull, 0ull, 0u, 0u};
+    // a run that began before the sub-chunk enters it unless key[c0] starts a new run
     const bool virt = c0 > 0 && c0 < c1 && keys[c0] == keys[c0 - 1];
 
-    // positions below are chunk-local (32-bit: chunk < 2^32)
+    // positions below are sub-chunk-local (32-bit: chunk < 2^32)
     const uint32_t len = (uint32_t)(c1 - c0);
-    uint32_t carry = 0;  // local start of the run in progress (0 also when it entered the chunk)
+    uint32_t carry = 0;  // local start of the run in progress (0 also when it entered the sub-chunk)
     double S = 0.0;
-    const bool vec = ((uintptr_t)keys & 15u) == 0;  // chunk and tile starts are multiples of 16 keys
-    constexpr uint32_t TILE = (uint32_t)BLOCK * kEntItems;
+    const bool vec = ((uintptr_t)keys & 15u) == 0;  // sub-chunk and step starts are multiples of 16 keys
+    constexpr uint32_t STEP = 32u * kEntItems;
     const K *kc = keys + c0;
-    // keys of tile t0 for this thread (keys past the chunk, up to n, are read
-    // too: a run end looks one key ahead)
-    // keys of tile t0 for this thread, plus the warp's edge neighbours (lane 0:
+    // keys of the step at t0 for this lane, plus the warp's edge neighbours (lane 0:
     // the key before its first, lane 31: the key after its last; keys past the
-    // chunk, up to n, are read too: a run end looks one key ahead)
+    // sub-chunk, up to n, are read too: a run end looks one key ahead)
     auto load = [&](uint32_t t0, K (&k)[kEntItems], K &edge) {
-        const uint32_t i0 = t0 + threadIdx.x * kEntItems;
+        const uint32_t i0 = t0 + lane * kEntItems;
         if (vec && c0 + i0 + kEntItems <= n) {
             const uint4 *p4 = reinterpret_cast<const uint4 *>(kc + i0);
             if constexpr (sizeof(K) == 4) {
@@ -102,44 +105,36 @@ __global__ void __launch_bounds__(BLOCK)
     const bool last_chunk = c1 == n;
     K k[kEntItems], kn[kEntItems], edge = K(0), edge_n = K(0);
     if (len > 0) load(0, kn, edge_n);
-    for (uint32_t t0 = 0; t0 < len; t0 += TILE) {
-        const uint32_t i0 = t0 + threadIdx.x * kEntItems;
+    for (uint32_t t0 = 0; t0 < len; t0 += STEP) {  // warp-uniform trip count
+        const uint32_t i0 = t0 + lane * kEntItems;
 #pragma unroll
         for (int q = 0; q < kEntItems; q++) k[q] = kn[q];
         edge = edge_n;
-        if (t0 + TILE < len) load(t0 + TILE, kn, edge_n);  // next tile in flight while this one is scanned
-        // neighbours: the previous / next thread's keys; the loaded edges at warp edges
+        if (t0 + STEP < len) load(t0 + STEP, kn, edge_n);  // next step in flight while this one is scanned
+        // neighbours: the previous / next lane's keys; the loaded edges at warp edges
         K prev = __shfl_up_sync(kFull, k[kEntItems - 1], 1);
         K next = __shfl_down_sync(kFull, k[0], 1);
         if (lane == 0) prev = edge;
         if (lane == 31) next = edge;
-        // a start at local 0 of chunk 0 is real; elsewhere starts compare with the previous key
         // bit q: key q equals its predecessor; starts = the other valid keys
         uint32_t eqm = 0;
 #pragma unroll
         for (int q = 0; q < kEntItems; q++) eqm |= (uint32_t)(k[q] == (q ? k[q - 1] : prev)) << q;
         const uint32_t valid = i0 >= len ? 0u : (len - i0 >= (uint32_t)kEntItems ? 0xffffu : (1u << (len - i0)) - 1u);
         const uint32_t stm = ~eqm & valid;
-        uint32_t mine = stm ? i0 + 31u - (uint32_t)__clz(stm) : 0u;  // last local start (0: none; neutral)
-        // exclusive max-scan over the block (thread order = key order)
-        uint32_t incl = mine;
+        const uint32_t mine = stm ? i0 + 31u - (uint32_t)__clz(stm) : 0u;  // last local start (0: none; neutral)
+        // exclusive max-scan over the warp (lane order = key order), seeded with the carry
+        uint32_t incl = max(mine, carry);
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t x = __shfl_up_sync(kFull, incl, o);
             if (lane >= (uint32_t)o) incl = max(incl, x);
         }
-        if (lane == 31) s_w[warp] = incl;
-        __syncthreads();
-        uint32_t before = carry, tile_max = carry;
-        for (int w = 0; w < BLOCK / 32; w++) {
-            if (w < (int)warp) before = max(before, (uint32_t)s_w[w]);
-            tile_max = max(tile_max, (uint32_t)s_w[w]);
-        }
         const uint32_t up = __shfl_up_sync(kFull, incl, 1);
-        uint32_t cur = lane ? max(before, up) : before;
+        uint32_t cur = lane ? up : carry;
         // fast paths (no contribution, no boundary piece): every run of my keys is a single key
         // that ends here, or all my keys sit inside one run that goes on past them; keys at the
-        // chunk's edges and partial tiles take the loop
+        // sub-chunk's edges and partial steps take the loop
         const bool inner = valid == 0xffffu && i0 != 0u && i0 + kEntItems < len;
         const bool singles = inner && eqm == 0u && next != k[kEntItems - 1];
         const bool interior = inner && eqm == 0xffffu && next == k[kEntItems - 1];
@@ -152,34 +147,70 @@ __global__ void __launch_bounds__(BLOCK)
                 if (st) cur = i;
                 const bool end = (last_chunk && i + 1 == len) ||
                                  (q + 1 < kEntItems ? k[q + 1] != k[q] : next != k[q]);
-                const bool entered = virt && cur == 0 && !st;  // the run that entered the chunk
+                const bool entered = virt && cur == 0 && !st;  // the run that entered the sub-chunk
                 if (end) {
                     if (entered) {
-                        s_rp.pre = i + 1;
-                        s_rp.pre_ends = 1u;
+                        rp.pre = i + 1;
+                        rp.pre_ends = 1u;
                     } else if (i > cur) {  // runs of one key contribute 1 log2 1 = 0
                         const double c = (double)(i - cur + 1);
                         S += c * log2(c);
                     }
-                } else if (i + 1 == len) {  // the last run continues into the next chunk
-                    if (entered) s_rp.pre = len;  // ... and entered it: it crosses the whole chunk
-                    else s_rp.suf = len - cur;
+                } else if (i + 1 == len) {  // the last run continues into the next sub-chunk
+                    if (entered) rp.pre = len;  // ... and entered it: it crosses the whole sub-chunk
+                    else rp.suf = len - cur;
                 }
             }
         }
-        carry = tile_max;
-        __syncthreads();
+        carry = __shfl_sync(kFull, incl, 31);
     }
-    // fixed-order block sum
+    // the warp's pieces: each is set by at most one lane (the one holding that key)
+    {
+        const uint64_t pre = __reduce_max_sync(kFull, (uint32_t)rp.pre);
+        const uint64_t suf = __reduce_max_sync(kFull, (uint32_t)rp.suf);
+        const uint32_t pe = __reduce_or_sync(kFull, rp.pre_ends);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) S += __shfl_down_sync(kFull, S, o);
-    if (lane == 0) s_d[warp] = S;
+        for (int o = 16; o > 0; o >>= 1) S += __shfl_down_sync(kFull, S, o);  // fixed order
+        if (lane == 0) {
+            s_wp[warp] = RunPieces{pre, suf, pe, 0u};
+            s_d[warp] = S;
+        }
+    }
     __syncthreads();
+    // the CTA's pieces from its warps' (fixed order): runs crossing warp boundaries
+    // inside the chunk end in a later warp (c log2 c) or continue past the chunk (suf);
+    // the run entering the chunk runs through warps while they are crossed whole
     if (threadIdx.x == 0) {
         double t = 0.0;
-        for (int w = 0; w < BLOCK / 32; w++) t += s_d[w];
+        RunPieces cp{0ull, 0ull, 0u, 0u};
+        for (int w = 0; w < NW; w++) t += s_d[w];
+        for (int w = 0; w < NW; w++) {
+            uint64_t run = s_wp[w].suf;
+            if (run == 0) continue;
+            bool ended = false;
+            for (int e = w + 1; e < NW; e++) {
+                run += s_wp[e].pre;
+                if (s_wp[e].pre_ends) {
+                    ended = true;
+                    break;
+                }
+            }
+            if (ended) t += (double)run * log2((double)run);
+            else cp.suf = run;
+        }
+        if (s_wp[0].pre > 0) {
+            uint64_t run = 0;
+            for (int e = 0; e < NW; e++) {
+                run += s_wp[e].pre;
+                if (s_wp[e].pre_ends) {
+                    cp.pre_ends = 1u;
+                    break;
+                }
+            }
+            cp.pre = run;
+        }
         chunk_S[blockIdx.x] = t;
-        pieces[blockIdx.x] = s_rp;
+        pieces[blockIdx.x] = cp;
     }
     grid.sync();
 
