@@ -173,7 +173,7 @@ int device_info(int *sms, int *hist_clusters = nullptr, DevInfo **info = nullptr
                 const bool force_masked = env && std::strcmp(env, "masked") == 0;
                 d.rank_mode = (d.lane_order_ok && !force_masked) ? kRankOrdered : kRankMasked;
             }
-            if (good) {  // K8: co-resident CTAs for its cooperative launch
+            if (good) {  // K8: one wave of resident CTAs
                 int per = 0;
                 int per64 = 0;
                 good &= cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_entropy_sorted<kEntBlock>,
@@ -982,14 +982,16 @@ int ahs_entropy_sorted_dtype(const void *d_keys, uint64_t n, int32_t dtype, void
     RunPieces *pieces = (RunPieces *)(ws + L.ent);
     double *csum = (double *)(ws + L.ent + kEntMaxGrid * sizeof(RunPieces));
     double *dH = csum + kEntMaxGrid;
+    uint32_t *done = (uint32_t *)(dH + 1);  // the CTA ticket
     cudaStream_t s = (cudaStream_t)stream;
-    const void *keys = d_keys;
-    uint64_t nn = n;
-    void *args[] = {&keys, &nn, &chunk, &pieces, &csum, &dH};
+    if (cudaMemsetAsync(done, 0, 4, s) != cudaSuccess) return AHS_ECUDA;
     cudaError_t e = launch(KID_ENTROPY_SORTED, s, [&] {
-        cudaLaunchCooperativeKernel(wide ? (void *)k_entropy_sorted<kEntBlock, uint64_t>
-                                         : (void *)k_entropy_sorted<kEntBlock, uint32_t>,
-                                    dim3((unsigned)grid), dim3(kEntBlock), args, 0, s);
+        if (wide)
+            launch_k(k_entropy_sorted<kEntBlock, uint64_t>, dim3((unsigned)grid), dim3(kEntBlock), 0, s,
+                     (const uint64_t *)d_keys, n, chunk, pieces, csum, dH, done);
+        else
+            launch_k(k_entropy_sorted<kEntBlock, uint32_t>, dim3((unsigned)grid), dim3(kEntBlock), 0, s,
+                     (const uint32_t *)d_keys, n, chunk, pieces, csum, dH, done);
     });
     if (e != cudaSuccess) return AHS_ECUDA;
     if (cudaMemcpyAsync(H, dH, sizeof(double), cudaMemcpyDeviceToHost, s) != cudaSuccess ||

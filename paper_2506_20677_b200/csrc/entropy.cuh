@@ -3,7 +3,7 @@
 // SURVEY Appendix A) from a key array in which equal keys are contiguous
 // (ahs_sort's output):  H = log2 n - (1/n) sum_runs c log2 c.
 //
-// One cooperative launch of G CTAs, CTA c owning the contiguous chunk
+// One launch of G <= kEntMaxGrid CTAs, CTA c owning the contiguous chunk
 // [c * chunk, (c + 1) * chunk), one read of the keys:
 //   per warp    the chunk's w-th eighth, in steps of 32 x 16 keys (next step
 //               prefetched); a run starts at i when i == 0 or key[i] != key[i-1]
@@ -14,15 +14,13 @@
 //               it began earlier, is only measured (its length inside, and
 //               whether it ends here); so is the last run when it continues.
 //   per CTA     thread 0 stitches the warps' pieces: runs crossing warp
-//               boundaries inside the chunk, and the chunk's own pieces -> S[c].
-//   grid sync
-//   CTA 0       the runs that cross chunk boundaries: the thread of each run's
+//               boundaries inside the chunk, and the chunk's own pieces -> S[c];
+//               then takes a ticket (no grid barrier, no co-residency needed)
+//   last CTA    the runs that cross chunk boundaries: the thread of each run's
 //               origin chunk follows it forward to its end; then a fixed tree
 //               over the chunk sums and those runs: H = log2 n - S / n, >= 0.
 // Deterministic for a given G.  Work is independent of the run lengths.
 #pragma once
-
-#include <cooperative_groups.h>
 
 #include "common.cuh"
 
@@ -44,12 +42,12 @@ struct RunPieces {
 template <int BLOCK, typename K = uint32_t>
 __global__ void __launch_bounds__(BLOCK)
     k_entropy_sorted(const K *__restrict__ keys, uint64_t n, uint64_t chunk,
-                     RunPieces *__restrict__ pieces, double *__restrict__ chunk_S, double *__restrict__ out_H)
+                     RunPieces *__restrict__ pieces, double *__restrict__ chunk_S, double *__restrict__ out_H,
+                     uint32_t *__restrict__ done)
 {
     pdl_begin();
-    namespace cg = cooperative_groups;
-    cg::grid_group grid = cg::this_grid();
     constexpr int NW = BLOCK / 32;
+    __shared__ uint32_t s_last;
     __shared__ double s_d[NW];
     __shared__ RunPieces s_wp[NW];
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
@@ -211,14 +209,18 @@ __global__ void __launch_bounds__(BLOCK)
         }
         chunk_S[blockIdx.x] = t;
         pieces[blockIdx.x] = cp;
+        __threadfence();
+        s_last = atomicAdd(done, 1u) == gridDim.x - 1u;  // *done is zeroed before the launch
     }
-    grid.sync();
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
 
-    // ---- CTA 0: the runs crossing chunk boundaries, then a fixed tree over the
-    // chunk sums.  A crossing run has exactly one origin chunk (suf > 0, where
+    // ---- the last CTA to finish: the runs crossing chunk boundaries, then a fixed
+    // tree over the chunk sums (the same for whichever CTA is last).  A crossing run has exactly one origin chunk (suf > 0, where
     // it starts); the thread of that chunk follows it forward through chunks it
     // crosses whole (pre > 0, !pre_ends) to the one it ends in.
-    if (blockIdx.x == 0) {
+    {
         __shared__ RunPieces s_pieces[kEntMaxGrid];
         for (uint32_t c = threadIdx.x; c < gridDim.x; c += BLOCK) {
             RunPieces rp;
