@@ -41,7 +41,7 @@ struct DevInfo {
     size_t osl_smem = 0;
     int osl_tile = 0, osl_per_sm = 0;
     bool lane_order_ok = false;              // self-test of the ordered ranking passed
-    int ent_grid[2] = {0, 0};                // K8 cooperative grid per key width (32 / 64-bit)
+    int ent_grid[2] = {0, 0};                // K8 grid per key width (32 / 64-bit): one resident wave
     int rank_mode = kRankMasked;
 };
 std::mutex g_dev_mu;
