@@ -1098,16 +1098,16 @@ cudaError_t seg_small(const void *kin, const uint32_t *vin, void *kout, uint32_t
                     vout, offsets, nseg, n, flip, max_segment, bad);
 }
 
-template <typename K, bool KV, int GROUP, int CAP, bool ORD, int SPC = 1>
+template <typename K, bool KV, int GROUP, int CAP, bool ORD>
 cudaError_t seg_radix(const void *kin, const uint32_t *vin, void *kout, uint32_t *vout, uint64_t n,
                       const uint32_t *offsets, uint32_t nseg, uint32_t max_segment, K flip, uint32_t *bad,
                       cudaStream_t s)
 {
-    constexpr size_t smem = SPC * seg_radix_smem<K, KV, GROUP, CAP>();
-    static const bool attr = cudaFuncSetAttribute(k_seg_radix<K, KV, GROUP, CAP, ORD, SPC>,
+    constexpr size_t smem = seg_radix_smem<K, KV, GROUP, CAP>();
+    static const bool attr = cudaFuncSetAttribute(k_seg_radix<K, KV, GROUP, CAP, ORD>,
                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess;
     if (!attr) return cudaErrorInvalidValue;
-    return launch_k(k_seg_radix<K, KV, GROUP, CAP, ORD, SPC>, dim3((nseg + SPC - 1) / SPC), dim3(GROUP * SPC), smem,
+    return launch_k(k_seg_radix<K, KV, GROUP, CAP, ORD>, dim3(nseg), dim3(GROUP), smem,
                     s, (const K *)kin, vin, (K *)kout, vout, offsets, nseg, n, flip, max_segment, bad);
 }
 

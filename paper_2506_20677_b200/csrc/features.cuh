@@ -7,16 +7,19 @@
 // §I line 25 / north_star) = #{i : key[i] > key[i+1]}.
 //
 // Data flow (no host sync until the end):
-//   K1 reads the keys once: per-block (min, max, descents) -> ws partials;
-//      zeroes the overflow bins and K3's barrier word.
+//   K1 reads the keys once: per-block (min, max, descents) -> ws partials, and
+//      per-block histograms of the raw low byte (radix digit 0); zeroes the
+//      overflow bins and K3's ticket word.
 //   K2 reads the keys again.  Every CTA re-reduces the K1 partials (min and
-//      the bucket shift), privatises the histogram in shared memory, and each
-//      cluster of kHistCluster CTAs merges its shared-memory histograms over
-//      DSMEM into ONE partial row in global memory (plain coalesced stores, no
-//      global atomics).
-//   K3 (cooperative, one CTA per 1024 bins) sums the cluster rows, computes
-//      H in fp64 in a fixed order (deterministic), and the exclusive scan of
-//      the histogram that COUNTING reuses.
+//      the bucket shift; CTA 0 publishes the reduced record for K3),
+//      privatises the histogram in shared memory, and each cluster of
+//      kHistCluster CTAs merges its shared-memory histograms over DSMEM into
+//      ONE partial row in global memory (plain coalesced stores, no global
+//      atomics).
+//   K3 (one CTA per 256 bins, no grid barrier) sums the cluster rows and
+//      computes H in fp64 in a fixed order (deterministic); the last CTA
+//      writes the features.  The exclusive scan of the histogram that
+//      COUNTING reuses is K3s, run by ahs_sort only for COUNTING.
 #pragma once
 
 #include <cooperative_groups.h>

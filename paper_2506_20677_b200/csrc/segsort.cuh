@@ -129,37 +129,34 @@ constexpr size_t seg_radix_smem()  // per segment group
     return 2 * (size_t)CAP * sizeof(K) + (KV ? 2 * (size_t)CAP * 4 : 0) + (size_t)(GROUP / 32) * 256 * 4 + 256 * 4;
 }
 
-// GROUP threads sort one segment; a CTA of SPC * GROUP threads holds SPC
-// groups (SPC > 1 only for one-warp groups: their barriers are warp-local)
-template <typename K, bool KV, int GROUP, int CAP, bool ORD, int SPC>
-__global__ void __launch_bounds__(GROUP * SPC)
+// a CTA of GROUP threads sorts one segment (one-warp groups use warp barriers;
+// packing several one-warp segments per CTA measured no faster)
+template <typename K, bool KV, int GROUP, int CAP, bool ORD>
+__global__ void __launch_bounds__(GROUP)
     k_seg_radix(const K *__restrict__ kin, const uint32_t *__restrict__ vin, K *__restrict__ kout,
                 uint32_t *__restrict__ vout, const uint32_t *__restrict__ offsets, uint32_t nseg, uint64_t n, K flip,
                 uint32_t maxlen, uint32_t *__restrict__ bad)
 {
     constexpr int NW = GROUP / 32;
     static_assert(CAP <= kSegMedMax && GROUP % 32 == 0 && CAP % 16 == 0, "segment capacity");
-    static_assert(SPC == 1 || GROUP == 32, "several groups per CTA only for one-warp groups");
     pdl_begin();
-    extern __shared__ __align__(16) uint8_t seg_smem[];  // SPC x seg_radix_smem<K, KV, GROUP, CAP>()
-    const uint32_t g = threadIdx.x / GROUP;
-    uint8_t *const gsm = seg_smem + g * seg_radix_smem<K, KV, GROUP, CAP>();
-    K *const kbuf0 = reinterpret_cast<K *>(gsm);
+    extern __shared__ __align__(16) uint8_t seg_smem[];  // seg_radix_smem<K, KV, GROUP, CAP>()
+    K *const kbuf0 = reinterpret_cast<K *>(seg_smem);
     K *const kbuf1 = kbuf0 + CAP;
     uint32_t *const cnt = reinterpret_cast<uint32_t *>(kbuf1 + CAP);  // [NW][256]
     uint32_t *const dbase = cnt + NW * 256;                          // [256]
     [[maybe_unused]] uint32_t *const vbuf0 = dbase + 256;
     [[maybe_unused]] uint32_t *const vbuf1 = vbuf0 + CAP;
-    __shared__ uint32_t s_diff[SPC][2];
-    __shared__ uint32_t s_idle[NW * SPC];  // ORD: the slot idle lanes' atomics go to
+    __shared__ uint32_t s_diff[2];
+    __shared__ uint32_t s_idle[NW];  // ORD: the slot idle lanes' atomics go to
     auto gsync = [] {
         if constexpr (NW == 1) __syncwarp();
         else __syncthreads();
     };
-    const uint32_t seg = blockIdx.x * SPC + g;
-    if (seg >= nseg) return;  // a whole group: no barrier spans groups
+    const uint32_t seg = blockIdx.x;
+    if (seg >= nseg) return;
     const uint32_t lo = __ldg(&offsets[seg]), hi = __ldg(&offsets[seg + 1]);
-    const uint32_t t = threadIdx.x % GROUP, lane = t & 31u, warp = t >> 5;
+    const uint32_t t = threadIdx.x, lane = t & 31u, warp = t >> 5;
     if (hi < lo || (uint64_t)hi > n || hi - lo > maxlen || hi - lo > (uint32_t)CAP) {
         if (t == 0) atomicAdd(bad, 1u);
         return;
@@ -173,7 +170,7 @@ __global__ void __launch_bounds__(GROUP * SPC)
         return;
     }
     // coalesced staging; the bits in which some key differs from the first
-    if (t == 0) s_diff[g][0] = s_diff[g][1] = 0u;
+    if (t == 0) s_diff[0] = s_diff[1] = 0u;
     gsync();
     const K first = kin[lo] ^ flip;
     K dacc = 0;
@@ -186,11 +183,11 @@ __global__ void __launch_bounds__(GROUP * SPC)
     const uint32_t dlo = __reduce_or_sync(kFull, (uint32_t)dacc);
     const uint32_t dhi = sizeof(K) == 8 ? __reduce_or_sync(kFull, (uint32_t)((uint64_t)dacc >> 32)) : 0u;
     if (lane == 0) {
-        if (dlo) atomicOr(&s_diff[g][0], dlo);
-        if (dhi) atomicOr(&s_diff[g][1], dhi);
+        if (dlo) atomicOr(&s_diff[0], dlo);
+        if (dhi) atomicOr(&s_diff[1], dhi);
     }
     gsync();
-    const uint64_t diff = ((uint64_t)s_diff[g][1] << 32) | s_diff[g][0];
+    const uint64_t diff = ((uint64_t)s_diff[1] << 32) | s_diff[0];
     const uint32_t C = (len + NW - 1) / NW;
     const uint32_t wb = min(len, warp * C), we = min(len, wb + C);
     uint32_t *const wc = cnt + warp * 256;
@@ -259,7 +256,7 @@ __global__ void __launch_bounds__(GROUP * SPC)
                 const uint32_t i = i0 + lane;
                 const bool ok = i < we;
                 const K x = ok ? src[i] : K(0);
-                uint32_t *const a = ok ? wc + ((uint32_t)(x >> sh) & 0xffu) : s_idle + g * NW + warp;  // full-warp
+                uint32_t *const a = ok ? wc + ((uint32_t)(x >> sh) & 0xffu) : s_idle + warp;  // full-warp
                 const uint32_t pos = atomicAdd(a, 1u);
                 if (ok) {
                     dst[pos] = x;
