@@ -313,7 +313,7 @@ def time_e2e(torch, ahs, keys_np, vals_np, steps, warmup, device):
     w = np.int64 if keys_np.itemsize == 8 else np.int32
     hk = torch.from_numpy(keys_np.view(w)).pin_memory()
     hv = torch.from_numpy(vals_np.view(np.int32)).pin_memory() if vals_np is not None else None
-    NB = 3  # streams / buffers / host threads in flight
+    NB = 3  # streams / buffers / host threads in flight (4 or 6: no faster, r01_summary.md)
     hko = [torch.empty_like(hk).pin_memory() for _ in range(NB)]
     hvo = [torch.empty_like(hv).pin_memory() if hv is not None else None for _ in range(NB)]
     udt = {np.dtype(np.uint32): torch.uint32, np.dtype(np.uint64): torch.uint64}.get(keys_np.dtype)
