@@ -428,10 +428,23 @@ struct HistAdd {
         const uint32_t o1 = atomicAdd(&sh[b1 >> 1], 1u << ((b1 & 1u) << 4));
         const uint32_t o2 = atomicAdd(&sh[b2 >> 1], 1u << ((b2 & 1u) << 4));
         const uint32_t o3 = atomicAdd(&sh[b3 >> 1], 1u << ((b3 & 1u) << 4));
-        fix(o0, b0, 1u);
-        fix(o1, b1, 1u);
-        fix(o2, b2, 1u);
-        fix(o3, b3, 1u);
+        // a +1 crosses 0x8000 only from 0x7fff: one combined test, the rare fix-ups behind it
+        const bool f0 = ((o0 >> ((b0 & 1u) << 4)) & 0xffffu) == 0x7fffu;
+        const bool f1 = ((o1 >> ((b1 & 1u) << 4)) & 0xffffu) == 0x7fffu;
+        const bool f2 = ((o2 >> ((b2 & 1u) << 4)) & 0xffffu) == 0x7fffu;
+        const bool f3 = ((o3 >> ((b3 & 1u) << 4)) & 0xffffu) == 0x7fffu;
+        if (f0 | f1 | f2 | f3) {
+            if (f0) carry(b0);
+            if (f1) carry(b1);
+            if (f2) carry(b2);
+            if (f3) carry(b3);
+        }
+    }
+    // move 0x8000 of bin b's packed counter into its overflow word
+    __device__ __forceinline__ void carry(uint32_t b) const
+    {
+        atomicSub(&sh[b >> 1], 0x8000u << ((b & 1u) << 4));
+        atomicAdd(&ovf[b], 0x8000u);
     }
 };
 
