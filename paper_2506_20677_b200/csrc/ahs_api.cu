@@ -6,7 +6,9 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <chrono>
 #include <cstdlib>
+#include <thread>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -633,9 +635,16 @@ int ahs_features(const void *d_keys, uint64_t n, int32_t dtype, void *d_ws, size
     DevFeatures hf;
     if (hfb.h) {
         volatile uint64_t *flag = &hfb.h->seq;
+        // spin while the record is close (the device-resident case: tens of us); once
+        // the wait is long (an upload ahead of it on the stream), yield between polls
+        // so concurrent callers' threads are not starved of cores
+        const auto t0 = std::chrono::steady_clock::now();
+        bool polite = false;
         for (uint32_t spin = 0;; spin++) {
             if (*flag == seq) break;
+            if (polite) std::this_thread::yield();
             if ((spin & 255u) == 255u) {  // the kernel may have failed: stream state
+                if (!polite && std::chrono::steady_clock::now() - t0 > std::chrono::microseconds(100)) polite = true;
                 const cudaError_t q = cudaStreamQuery(s);
                 if (q == cudaSuccess) {
                     if (*flag == seq) break;
