@@ -158,8 +158,9 @@ AHS_API int ahs_sort_passes(const ahs_features_t *feat, int32_t strategy, int ha
  * histogram of (key - min) >> shift), computes H in fp64 on the device, and
  * WAITS for the result on the host (the one host sync of the pipeline: the FSM
  * runs on the host): the last kernel writes the 64-byte record into a mapped
- * pinned per-thread buffer that the call polls (falling back to a copy + stream
- * sync when mapped memory is unavailable).  On return every read of d_keys is
+ * pinned per-thread buffer that the call polls (spinning for ~100 us, then
+ * yielding the core between polls; falling back to a copy + stream sync when
+ * mapped memory is unavailable).  On return every read of d_keys is
  * complete; later work on `stream` is ordered after the kernels as usual.
  * d_ws (>= ahs_workspace_bytes) keeps the histogram and the digit rows for a
  * following ahs_sort on the same keys.
