@@ -274,3 +274,12 @@ def test_empty_and_constant_64():
         for strategy in (None, 0, 1, 2):
             f, s, r, ko, vo = run_gpu(keys, vals, strategy=strategy)
             assert f.k == 1 and np.array_equal(ko, keys) and np.array_equal(vo, vals)
+
+
+@pytest.mark.parametrize("cfg", ["cfg6", "cfg6kv"])
+def test_config_full_size_64(cfg):
+    """NEXT-3 at BASELINE size: 2^26 uint64 30-mer codes (k = 4^30), keys and
+    (cfg6kv) values = input index, in the bench's launch configuration: features, strategy, rule,
+    keys and values bit-exact against the oracle."""
+    keys, vals, _ = synth.make(cfg)
+    check_pipeline(keys, vals)
