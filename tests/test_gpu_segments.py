@@ -194,3 +194,30 @@ def test_no_segments_and_errors():
     assert int(bad.item()) == 0
     with pytest.raises(ahs.AhsError):
         ahs.ahs_sort_segments(keys, None, keys, None, off, 4096)  # ERANGE: above the 2048-key limit
+
+
+@pytest.mark.parametrize("lo,hi,nseg", [(1, 20, 1 << 20), (1000, 2048, 1 << 13)])
+def test_bench_size_properties(lo, hi, nseg, rank):
+    """The bench's segment workloads at full size (2^20 segments of 1..20 keys: Listing 1's path;
+    2^13 of 1000..2048: the radix path), values = input index.  The per-segment oracle is too slow
+    here, so properties that hold at any size: every segment is non-decreasing, the values are a
+    permutation of the indices inside each segment that gathers the output from the input, and
+    equal keys keep their input order (stability)."""
+    rng = np.random.default_rng(7)
+    lens = rng.integers(lo, hi + 1, nseg)
+    off = np.zeros(nseg + 1, dtype=np.int64)
+    off[1:] = np.cumsum(lens)
+    n = int(off[-1])
+    keys = (synth.stream(5, n) >> np.uint64(40)).astype(np.uint32).view(np.int32)  # 24-bit: duplicates
+    vals = np.arange(n, dtype=np.uint32)
+    ko, vo, bad = run(keys, vals, off.astype(np.uint32), hi)
+    assert bad == 0
+    seg = np.repeat(np.arange(nseg), lens)
+    inner = seg[1:] == seg[:-1]  # adjacent pairs inside one segment
+    assert (ko[1:][inner] >= ko[:-1][inner]).all()
+    vi = vo.astype(np.int64)
+    assert (seg[vi] == seg).all()  # values stay in their segment
+    assert np.array_equal(np.sort(vi), np.arange(n))
+    assert np.array_equal(keys[vi], ko)  # the values gather the output
+    eq = inner & (ko[1:] == ko[:-1])
+    assert (vi[1:][eq] > vi[:-1][eq]).all()  # stable
