@@ -283,3 +283,15 @@ def test_config_full_size_64(cfg):
     keys and values bit-exact against the oracle."""
     keys, vals, _ = synth.make(cfg)
     check_pipeline(keys, vals)
+
+
+@pytest.mark.parametrize("cfg", ["cfg3", "cfg4d", "cfg6"])
+def test_entropy_sorted_full_size(cfg):
+    """NEXT-2 (K8) at BASELINE sizes (2^26 keys: Zipf-like cfg3, 16 long runs in cfg4d, 64-bit cfg6)
+    against the oracle's H_exact over the same sorted array (1e-9)."""
+    keys, _, _ = synth.make(cfg)
+    ok = np.sort(keys, kind="stable")  # K8's input: equal keys contiguous (any sort)
+    want = oracle.h_exact_sorted(ok)
+    ws = ahs.Workspace(keys.size, False, key_dtype=keys.dtype)
+    got = ahs.ahs_entropy_sorted(to_dev(ok), ws)
+    assert abs(got - want) <= H_TOL, (cfg, got, want)
