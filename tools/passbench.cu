@@ -12,7 +12,8 @@
 #include <cstring>
 #include <vector>
 
-#include "../paper_2506_20677_b200/csrc/onesweep.cuh"
+#include "onesweep_p.cuh"
+#include "../paper_2506_20677_b200/csrc/onesweep2.cuh"
 
 using namespace ahs;
 
@@ -79,18 +80,19 @@ struct Bufs {
 
 static int g_only = -1, g_idx = 0;
 static bool g_noflush = false;  // env PB_NOFLUSH=1: the pass input stays L2-warm (as inside a sort)
+static bool g_mid = false;      // env PB_MID=1: run as a middle pass of a chain (no key transforms)
 
-template <bool KV, int BLOCK, int ITEMS, int MINB, int RANK = kRankMasked>
-float run_cfg(const Bufs &B, uint32_t n, uint32_t shift, int sms, int reps, bool check,
-              const std::vector<uint32_t> &hk, const std::vector<uint32_t> &hbase)
+template <bool KV>
+float run_kern(const Bufs &B, uint32_t n, uint32_t shift, int sms, int reps, bool check,
+               const std::vector<uint32_t> &hk, const std::vector<uint32_t> &hbase, const void *kern, size_t smem,
+               int tile, int block, const char *name)
 {
     if (g_only >= 0 && g_idx++ != g_only) return 0.f;
-    using C = Onesweep<KV, BLOCK, ITEMS, RANK>;
-    auto kern = k_onesweep<KV, BLOCK, ITEMS, MINB, RANK>;
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmem));
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, BLOCK, C::kSmem));
-    const uint32_t tiles = (n + C::kTile - 1) / C::kTile;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, block, smem));
+    const uint32_t tiles = (n + tile - 1) / tile;
+    if (getenv("PB_OCC")) occ = std::min(occ, atoi(getenv("PB_OCC")));  // fewer CTAs per SM
     const uint32_t grid = std::min<uint32_t>(tiles, (uint32_t)(occ * sms));
     cudaEvent_t a, b;
     CK(cudaEventCreate(&a));
@@ -111,12 +113,18 @@ float run_cfg(const Bufs &B, uint32_t n, uint32_t shift, int sms, int reps, bool
         pa.n = n;
         pa.pass = 0;
         pa.npasses = 1;
+        if (g_mid) {  // executed pass 1 of 3: reads keys_out, writes keys_tmp, no transforms
+            pa.pass = 1;
+            pa.npasses = 3;
+            pa.keys_out = B.k;
+            pa.vals_out = B.v;
+        }
         pa.shift = shift;
         pa.bucket_base = B.bb;
         pa.status = B.status;
         pa.ticket = B.ticket;
         pa.plan = nullptr;
-        kern<<<grid, BLOCK, C::kSmem>>>(pa);
+        { void *args[] = {&pa}; CK(cudaLaunchKernel(kern, dim3(grid), dim3(block), args, smem, 0)); }
         CK(cudaEventRecord(b));
         CK(cudaEventSynchronize(b));
         CK(cudaGetLastError());
@@ -172,11 +180,45 @@ float run_cfg(const Bufs &B, uint32_t n, uint32_t shift, int sms, int reps, bool
         }
     }
     const double bytes = (KV ? 16.0 : 8.0) * n;
-    printf("  %s<%s,B%d,I%d,minb%d> tile %5d occ %d grid %4u: %8.1f us  %7.1f GB/s  %6.1f Gkeys/s  "
+    printf("  %-32s tile %5d occ %d grid %4u: %8.1f us  %7.1f GB/s  %6.1f Gkeys/s  "
            "%.2f keys/clk/SM@1.9 max %.1f us %s\n",
-           RANK == kRankOrdered ? "ordered " : "masked  ", KV ? "kv" : "k", BLOCK, ITEMS, MINB, C::kTile, occ, grid, med * 1e3, bytes / med / 1e6,
+           name, tile, occ, grid, med * 1e3, bytes / med / 1e6,
            n / med / 1e6, n / med / 1e6 / sms / 1.9, ts.back() * 1e3, check ? (ok ? "ok" : "FAIL") : "");
     return med;
+}
+
+template <bool KV, int BLOCK, int ITEMS, int MINB, int RANK = kRankMasked>
+float run_cfg(const Bufs &B, uint32_t n, uint32_t shift, int sms, int reps, bool check,
+              const std::vector<uint32_t> &hk, const std::vector<uint32_t> &hbase)
+{
+    using C = Onesweep<KV, BLOCK, ITEMS, RANK>;
+    char nm[96];
+    snprintf(nm, sizeof nm, "%s<%s,B%d,I%d,minb%d>", RANK == kRankOrdered ? "ordered" : "masked", KV ? "kv" : "k",
+             BLOCK, ITEMS, MINB);
+    return run_kern<KV>(B, n, shift, sms, reps, check, hk, hbase,
+                        (const void *)k_onesweep<KV, BLOCK, ITEMS, MINB, RANK>, C::kSmem, C::kTile, BLOCK, nm);
+}
+
+template <bool KV, int NW, int ITEMS, int LBW, int W = 8>
+float run_p(const Bufs &B, uint32_t n, uint32_t shift, int sms, int reps, bool check,
+            const std::vector<uint32_t> &hk, const std::vector<uint32_t> &hbase)
+{
+    using C = OnesweepP<KV, NW, ITEMS, LBW>;
+    char nm[96];
+    snprintf(nm, sizeof nm, "P<%s,NW%d,I%d,LB%d,W%d>", KV ? "kv" : "k", NW, ITEMS, LBW, W);
+    return run_kern<KV>(B, n, shift, sms, reps, check, hk, hbase,
+                        (const void *)k_onesweep_p<KV, NW, ITEMS, LBW, W>, C::kSmem, C::kTile, C::kBlock, nm);
+}
+
+template <bool KV, int BLOCK, int ITEMS>
+float run2(const Bufs &B, uint32_t n, uint32_t shift, int sms, int reps, bool check,
+           const std::vector<uint32_t> &hk, const std::vector<uint32_t> &hbase)
+{
+    using C = Onesweep2<KV, BLOCK, ITEMS>;
+    char nm[96];
+    snprintf(nm, sizeof nm, "v2<%s,B%d,I%d>", KV ? "kv" : "k", BLOCK, ITEMS);
+    return run_kern<KV>(B, n, shift, sms, reps, check, hk, hbase, (const void *)k_onesweep2<KV, BLOCK, ITEMS, (BLOCK == 256 ? 4 : 2)>,
+                        C::kSmem, C::kTile, BLOCK, nm);
 }
 
 template <bool KV>
@@ -223,6 +265,7 @@ int main(int argc, char **argv)
     const bool cub = argc > 4 ? atoi(argv[4]) != 0 : true;
     g_only = argc > 5 ? atoi(argv[5]) : -1;
     g_noflush = getenv("PB_NOFLUSH") && getenv("PB_NOFLUSH")[0] == '1';
+    g_mid = getenv("PB_MID") && getenv("PB_MID")[0] == '1';
     int sms;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
     Bufs B;
@@ -268,14 +311,15 @@ int main(int argc, char **argv)
         CK(cudaMemcpy(B.bb, base.data(), 1024, cudaMemcpyHostToDevice));
         printf("digit shift %u (max digit share %.3f)\n", shift, (double)mx / n);
         g_idx = 0;
-        run_cfg<false, 512, 16, 2, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
         run_cfg<false, 512, 18, 2, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
-        run_cfg<false, 512, 20, 2, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
-        run_cfg<false, 384, 16, 3, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
-        run_cfg<false, 384, 14, 3, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
-        run_cfg<true, 512, 15, 1, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
+        run2<false, 512, 18>(B, n, shift, sms, reps, true, hk, base);
+        run2<false, 512, 20>(B, n, shift, sms, reps, true, hk, base);
+        run2<false, 256, 16>(B, n, shift, sms, reps, true, hk, base);
+        run2<false, 256, 20>(B, n, shift, sms, reps, true, hk, base);
+        run2<false, 384, 16>(B, n, shift, sms, reps, true, hk, base);
         run_cfg<true, 384, 16, 2, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
-        run_cfg<true, 384, 9, 3, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
+        run2<true, 384, 16>(B, n, shift, sms, reps, true, hk, base);
+        run2<true, 256, 16>(B, n, shift, sms, reps, true, hk, base);
     }
     if (cub) {
         run_cub<false>(B, n, 0, 32, sms, reps);
