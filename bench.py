@@ -1,13 +1,15 @@
 #!/usr/bin/env python3
 """Benchmark of the AHS hot path on B200: features -> select -> sort.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg5_r32] [--impl ours|reference]
 
 One step = one pass of the whole hot path (ahs_features, ahs_select, ahs_sort)
-over the workload's keys, resident in HBM.  The default workload is
-BASELINE.json configs[1] (cfg2: 2^24 uint32 keys uniform over 32 bits,
-GENERAL branch).  L2 is flushed (256 MiB write) before every timed step
-because the 64 MiB input would otherwise stay L2-resident.  Timing: CUDA
+over the workload's keys, resident in HBM.  The default workload is the
+largest BASELINE.json config (cfg5 r=32: 2^28 (uint32 key, uint32 value)
+pairs, keys uniform over 32 bits, GENERAL branch, 2 GiB), above BASELINE's
+n >= 2^26 gate; a second headline block (`headline_keys`) times the
+keys-only GENERAL config cfg4a (2^26 int32).  L2 is flushed (256 MiB write)
+before every timed step.  Timing: CUDA
 events on the launching stream around each step, barrier + synchronize around
 the timed region, max over ranks.  N > 1 runs independent replicas (one per
 GPU, weak scaling; the method has no cross-GPU exchange: DESIGN.md §7).
@@ -138,21 +140,50 @@ def barrier(pg):
 
 
 # --------------------------------------------------------- oracle (CPU)
+def host_info():
+    """CPU model, logical CPU count and the affinity the process started with."""
+    model = None
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    try:
+        aff = sorted(os.sched_getaffinity(0))
+    except (AttributeError, OSError):
+        aff = None
+    return {"cpu_model": model, "os_cpu_count": os.cpu_count(), "affinity_cpus": len(aff) if aff else None}
+
+
 def cpu_oracle_rate(keys, vals, budget_s: float, max_n: int):
-    """Time the oracle pipeline (features -> FSM -> sort) on a bounded prefix."""
+    """Time the oracle pipeline (features -> FSM -> sort) on a bounded prefix, pinned to one
+    core (sched_setaffinity) for the duration: the oracle is single-threaded C."""
     import oracle
     n = min(keys.size, max_n)
     k, v = keys[:n].copy(), (vals[:n].copy() if vals is not None else None)
+    pinned = None
+    try:
+        old = os.sched_getaffinity(0)
+        pinned = min(old)
+        os.sched_setaffinity(0, {pinned})
+    except (AttributeError, OSError):
+        old = None
     times = []
-    t_end = time.perf_counter() + budget_s
-    while True:
-        t0 = time.perf_counter()
-        oracle.ahs(k, v)
-        times.append(time.perf_counter() - t0)
-        if time.perf_counter() > t_end or len(times) >= 10:
-            break
+    try:
+        t_end = time.perf_counter() + budget_s
+        while True:
+            t0 = time.perf_counter()
+            oracle.ahs(k, v)
+            times.append(time.perf_counter() - t0)
+            if time.perf_counter() > t_end or len(times) >= 10:
+                break
+    finally:
+        if old is not None:
+            os.sched_setaffinity(0, old)
     med = statistics.median(times)
-    return n / med / 1e9, n, len(times), med
+    return n / med / 1e9, n, len(times), med, pinned
 
 
 # ------------------------------------------------------------ GPU timing
@@ -392,12 +423,78 @@ def contract_bytes(strategy: int, passes_nominal: int, n: int, kv: bool, kb: int
 
 
 def traffic_from_profiles(workload: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant kernel, from the
+    committed `ncu --set full` capture of that workload (profiles/ncu_traffic.json)."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         d = json.load(open(p))
         return d.get(workload, {}).get("onesweep_dram_bytes_per_launch")
     except Exception:
         return None
+
+
+PER_LAUNCH_BYTES = {"onesweep": 8, "onesweep_kv": 16, "count_fill": 4, "count_scatter_kv": 16,
+                    "radix_hist": 4, "feat_reduce": 4, "feat_hist": 4}
+
+
+def dominant_roofline(res, n, kv, kb, workload, peak, peak_kind):
+    """Roofline of the step's dominant kernel (the onesweep digit pass): algorithmic bytes per
+    launch (read + write of every key and value) / its mean CUDA-event launch time."""
+    prof = res["prof"]
+    kname = "onesweep_kv" if kv else "onesweep"
+    if prof.get(kname, {}).get("launches", 0) == 0:
+        kname = max(prof, key=lambda k: prof[k]["ms"])
+    kl = prof[kname]["launches"]
+    if kname.startswith("onesweep") and res["executed"] < res["passes"]:
+        kl = kl * res["executed"] // res["passes"]  # NEXT-1 skipped launches return at once
+    kms = prof[kname]["ms"] / max(1, kl)
+    per = PER_LAUNCH_BYTES.get(kname, 4) * n
+    if kname.startswith("onesweep") and kb == 8:
+        per = (16 + (8 if kv else 0)) * n
+    achieved = per / (kms * 1e-3) / 1e9
+    return {"bound": "hbm", "kernel": kname, "achieved": round(achieved, 1), "peak": peak,
+            "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
+            "traffic": traffic_from_profiles(workload), "algorithmic_bytes_per_launch": per,
+            "ms_per_launch": kms,
+            "timing": "CUDA events around every launch on the launching stream, second timed pass of the "
+                      "same K steps (the headline value is timed without them)"}
+
+
+def table_row(torch, ahs, cfg, k2, v2, steps, device, flush, peak, skip=True):
+    """One per-strategy row: pipeline and sort throughput, fractions of the roofline.  With
+    skip=False the NEXT-1 trivial-pass skipping is off: every nominal pass executes (the
+    contract row of SURVEY §8(d)); with skip=True the row is the NEXT-1 row."""
+    prev = ahs.ahs_set_skip_trivial(1 if skip else 0)
+    try:
+        r2 = time_pipeline(torch, ahs, k2, v2, steps, 2, device, flush, profile=True)
+    finally:
+        ahs.ahs_set_skip_trivial(prev)
+    p2 = r2["prof"]
+    n2 = k2.size
+    kv2 = v2 is not None
+    sort_ms2 = sum(v["ms"] for k, v in p2.items() if not k.startswith("feat")) / steps
+    feat_ms2 = sum(v["ms"] for k, v in p2.items() if k.startswith("feat")) / steps
+    kb2 = k2.dtype.itemsize
+    sb2 = sort_bytes(r2["s"], r2["executed"], n2, kv2, r2["f"].shift, kb2)
+    row = {
+        "workload": cfg, "n": n2, "kv": kv2, "strategy": ahs.STRATEGY_NAMES[r2["s"]],
+        "rule": ahs.RULE_NAMES[r2["r"]], "skip_trivial": skip, "passes": r2["passes"],
+        "passes_executed": r2["executed"],
+        "pipeline_Gkeys_s": n2 * steps / (r2["total_ms"] * 1e-3) / 1e9,
+        "sort_Gkeys_s": n2 / (sort_ms2 * 1e-3) / 1e9 if sort_ms2 > 0 else None,
+        "sort_GBps": sb2 / (sort_ms2 * 1e-3) / 1e9 if sort_ms2 > 0 else None,
+        "sort_frac_of_peak": (sb2 / (sort_ms2 * 1e-3) / 1e9) / peak if sort_ms2 > 0 else None,
+        "key_bytes": kb2,
+        "features_GBps": 2 * kb2 * n2 / (feat_ms2 * 1e-3) / 1e9 if feat_ms2 > 0 else None,
+        "kernels_ms": {k: v["ms"] / v["launches"] for k, v in p2.items() if v["launches"]},
+    }
+    # BASELINE's contract roofline ((2p + 1) bytes n, p nominal) is only meaningful when the
+    # nominal passes all ran: skip-on rows that skipped a pass report it as null (SURVEY §8(d))
+    contract_ok = sort_ms2 > 0 and r2["executed"] == r2["passes"]
+    cb = contract_bytes(r2["s"], r2["passes"], n2, kv2, kb2)
+    row["contract_frac_of_8TBps"] = cb / (sort_ms2 * 1e-3) / 8e12 if contract_ok else None
+    row["contract_frac_of_peak"] = cb / (sort_ms2 * 1e-3) / 1e9 / peak if contract_ok else None
+    return row, r2
 
 
 def run_ours(args):
@@ -418,26 +515,14 @@ def run_ours(args):
     value = ws * n * args.steps / (tmax * 1e-3) / 1e9
     f, s, r, prof = res["f"], res["s"], res["r"], res["prof"]
     kv = vals is not None
-    # dominant kernel: the onesweep digit pass (read + write of every key (and value))
-    kname = "onesweep_kv" if kv else "onesweep"
-    if prof[kname]["launches"] == 0:
-        kname = max(prof, key=lambda k: prof[k]["ms"])
-    kl = prof[kname]["launches"]
-    if kname.startswith("onesweep") and res["executed"] < res["passes"]:
-        # NEXT-1 skipped launches return at once: average over the executed ones
-        kl = kl * res["executed"] // res["passes"]
-    kms = prof[kname]["ms"] / max(1, kl)
-    per_launch_bytes = {"onesweep": 8 * n, "onesweep_kv": 16 * n, "count_fill": 4 * n,
-                        "count_scatter_kv": 16 * n, "radix_hist": 4 * n, "feat_reduce": 4 * n,
-                        "feat_hist": 4 * n}.get(kname, 4 * n)
-    achieved = per_launch_bytes / (kms * 1e-3) / 1e9
-    traffic = traffic_from_profiles(args.workload)
+    kb = keys.dtype.itemsize
+    roof = dominant_roofline(res, n, kv, kb, args.workload, peak, peak_kind)
     step_total = sum(v["ms"] for v in prof.values())
     # per-kernel numbers come from the profiled pass (steps with per-launch events)
     kernels = {k: {"ms_per_launch": v["ms"] / v["launches"], "launches": v["launches"],
                    "share_of_kernel_time": v["ms"] / step_total}
                for k, v in prof.items() if v["launches"]}
-    sb = sort_bytes(s, res["executed"], n, kv, f.shift)
+    sb = sort_bytes(s, res["executed"], n, kv, f.shift, kb)
     sort_ms = sum(v["ms"] for k, v in prof.items() if not k.startswith("feat")) / args.steps
     feat_ms = sum(v["ms"] for k, v in prof.items() if k.startswith("feat")) / args.steps
 
@@ -449,25 +534,34 @@ def run_ours(args):
         "config": {"workload": args.workload, "n": n, "key_dtype": dt, "kv": kv,
                    "strategy": ahs.STRATEGY_NAMES[s], "rule": ahs.RULE_NAMES[r], "passes": res["passes"],
                    "passes_executed": res["executed"],
-                   "l2": "flushed before every timed step (256 MiB write)",
+                   "l2": "flushed before every timed step (256 MiB write); the inputs are also larger than L2",
                    "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU"},
-        "roofline": {"bound": "hbm", "kernel": kname, "achieved": round(achieved, 1), "peak": peak,
-                     "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                     "traffic": traffic, "algorithmic_bytes_per_launch": per_launch_bytes,
-                     "ms_per_launch": kms,
-                     "timing": "CUDA events around every launch on the launching stream, second timed pass "
-                               "of the same K steps (the headline value is timed without them)"},
+        "roofline": roof,
         "stages": {"features_ms": feat_ms, "sort_kernels_ms": sort_ms,
                    "sort_algorithmic_bytes": sb,
                    "sort_GBps": sb / (sort_ms * 1e-3) / 1e9 if sort_ms > 0 else None,
+                   "sort_frac_of_peak": (sb / (sort_ms * 1e-3) / 1e9) / peak if sort_ms > 0 else None,
                    "step_ms_median": statistics.median(res["step_ms"])},
         "kernels": kernels,
         "gpu_launches": res["launches"],
         "clocks": res["clocks"],
         "features": {"k": f.k, "nbins": f.nbins, "H": f.entropy, "descents": f.descents},
     }
+    # second headline: keys-only GENERAL at 2^26 (cfg4a), same protocol, its own roofline
+    if args.keys_workload and args.keys_workload != args.workload:
+        k4, v4, dt4 = synth.make(args.keys_workload)
+        r4 = time_pipeline(torch, ahs, k4, v4, args.steps, args.warmup, device, flush, profile=True, pg=pg)
+        t4 = dist_max(pg, r4["total_ms"], device)
+        out["headline_keys"] = {
+            "workload": args.keys_workload, "n": k4.size, "dtype": dt4, "kv": v4 is not None,
+            "strategy": ahs.STRATEGY_NAMES[r4["s"]], "passes_executed": r4["executed"],
+            "value": round(ws * k4.size * args.steps / (t4 * 1e-3) / 1e9, 4), "unit": "Gkeys/s",
+            "ms_per_step": t4 / args.steps, "gpu_launches": r4["launches"],
+            "roofline": dominant_roofline(r4, k4.size, v4 is not None, k4.dtype.itemsize, args.keys_workload,
+                                          peak, peak_kind)}
+        del k4, v4
     # NEXT-2: paper-literal entropy of the output and the branch it implies
-    if rank == 0:
+    if rank == 0 and kb == 4:
         out["entropy_exact"] = entropy_exact_report(torch, ahs, keys, vals, device)
     # NEXT-4: batched small-n segment sorts
     if rank == 0 and args.configs:
@@ -476,54 +570,39 @@ def run_ours(args):
             r["frac_of_peak"] = r["GBps"] / peak
     # end to end through the C ABI with host buffers
     if not args.no_e2e:
-        e_ms, bi, bo = time_e2e(torch, ahs, keys, vals, max(3, args.steps // 2), 2, device)
         e_steps = max(3, args.steps // 2)
+        e_ms, bi, bo = time_e2e(torch, ahs, keys, vals, e_steps, 2, device)
         e_max = dist_max(pg, e_ms, device)
         out["e2e"] = {"value": round(ws * n * e_steps / (e_max * 1e-3) / 1e9, 4), "unit": "Gkeys/s",
                       "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo,
                       "ms_per_step": e_max / e_steps, "api": "ahs_sort_host (pinned host buffers)"}
-    # per-strategy table (BASELINE.json metric is per strategy)
+    # per-strategy table (BASELINE.json metric is per strategy).  Every radix row whose NEXT-1
+    # plan skips passes gets a second, contract row with skipping off.
     if args.configs and ws == 1:
         rows = []
         for cfg in [c for c in args.configs.split(",") if c]:
             k2, v2, dt2 = synth.make(cfg)
-            r2 = time_pipeline(torch, ahs, k2, v2, args.table_steps, 2, device, flush, profile=True)
-            p2 = r2["prof"]
-            n2 = k2.size
-            kv2 = v2 is not None
-            sort_ms2 = sum(v["ms"] for k, v in p2.items() if not k.startswith("feat")) / args.table_steps
-            feat_ms2 = sum(v["ms"] for k, v in p2.items() if k.startswith("feat")) / args.table_steps
-            kb2 = k2.dtype.itemsize
-            sb2 = sort_bytes(r2["s"], r2["executed"], n2, kv2, r2["f"].shift, kb2)
-            rows.append({
-                "workload": cfg, "n": n2, "kv": kv2, "strategy": ahs.STRATEGY_NAMES[r2["s"]],
-                "rule": ahs.RULE_NAMES[r2["r"]], "passes": r2["passes"], "passes_executed": r2["executed"],
-                "pipeline_Gkeys_s": n2 * args.table_steps / (r2["total_ms"] * 1e-3) / 1e9,
-                "sort_Gkeys_s": n2 / (sort_ms2 * 1e-3) / 1e9 if sort_ms2 > 0 else None,
-                "sort_GBps": sb2 / (sort_ms2 * 1e-3) / 1e9 if sort_ms2 > 0 else None,
-                "sort_frac_of_peak": (sb2 / (sort_ms2 * 1e-3) / 1e9) / peak if sort_ms2 > 0 else None,
-                "key_bytes": kb2,
-                "contract_frac_of_8TBps": (contract_bytes(r2["s"], r2["passes"], n2, kv2, kb2) /
-                                           (sort_ms2 * 1e-3) / 8e12) if sort_ms2 > 0 else None,
-                "contract_frac_of_peak": (contract_bytes(r2["s"], r2["passes"], n2, kv2, kb2) /
-                                          (sort_ms2 * 1e-3) / 1e9 / peak) if sort_ms2 > 0 else None,
-                "features_GBps": 2 * kb2 * n2 / (feat_ms2 * 1e-3) / 1e9 if feat_ms2 > 0 else None,
-                "kernels_ms": {k: v["ms"] / v["launches"] for k, v in p2.items() if v["launches"]},
-            })
-            if kb2 == 4:  # K8 (NEXT-2) is built for 32-bit keys
+            row, r2 = table_row(torch, ahs, cfg, k2, v2, args.table_steps, device, flush, peak, skip=True)
+            if k2.dtype.itemsize == 4:  # K8 (NEXT-2) is built for 32-bit keys
                 ee = entropy_exact_report(torch, ahs, k2, v2, device, reps=2)
-                rows[-1].update({"H16": ee["H16"], "H_exact": ee["H_exact"],
-                                 "branch_paper_literal": ee["branch_paper_literal"], "branch_agree": ee["agree"]})
+                row.update({"H16": ee["H16"], "H_exact": ee["H_exact"],
+                            "branch_paper_literal": ee["branch_paper_literal"], "branch_agree": ee["agree"]})
             else:
-                rows[-1].update({"H16": r2["f"].entropy})
+                row.update({"H16": r2["f"].entropy})
+            rows.append(row)
+            if r2["executed"] < r2["passes"]:
+                row_c, _ = table_row(torch, ahs, cfg, k2, v2, args.table_steps, device, flush, peak, skip=False)
+                rows.append(row_c)
             del k2, v2
         out["strategies"] = rows
     # CPU oracle baseline (rank 0, N = 1 only)
     if rank == 0 and ws == 1 and not args.no_cpu:
-        rate, ns, reps, med = cpu_oracle_rate(keys, vals, args.cpu_budget, n)
+        rate, ns, reps, med, core = cpu_oracle_rate(keys, vals, args.cpu_budget, args.cpu_sample)
         out["cpu_baseline"] = {"value": round(rate, 6), "unit": "Gkeys/s", "cores": 1, "kind": "oracle",
-                               "sample": f"full {args.workload} ({ns} keys), oracle features+FSM+sort, "
-                                         f"median of {reps} runs ({med:.2f} s each), one thread"}
+                               "sample": f"first {ns} keys of {args.workload} ({'pairs' if kv else 'keys'}), "
+                                         f"oracle features+FSM+sort, median of {reps} runs ({med:.2f} s each), "
+                                         f"one thread pinned to CPU {core}",
+                               "host": host_info()}
     if rank == 0:
         print(json.dumps(out))
     if pg is not None:
@@ -567,12 +646,15 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="cfg2", choices=sorted(synth.CONFIGS))
-    ap.add_argument("--configs", default="cfg1,cfg2kv,cfg3,cfg4a,cfg4b,cfg4d,cfg5_r8,cfg5_r16,cfg5_r24,cfg5_r32,cfg6,cfg6kv",
+    ap.add_argument("--workload", default="cfg5_r32", choices=sorted(synth.CONFIGS))
+    ap.add_argument("--keys-workload", default="cfg4a", help="second (keys-only) headline block; '' to skip")
+    ap.add_argument("--configs", default="cfg1,cfg2,cfg2kv,cfg3,cfg4a,cfg4b,cfg4c,cfg4d,cfg5_r8,cfg5_r16,cfg5_r20,"
+                                         "cfg5_r24,cfg5_r28,cfg5_r32,cfg6,cfg6kv",
                     help="per-strategy table rows (single GPU only); '' to skip")
     ap.add_argument("--table-steps", type=int, default=5)
     ap.add_argument("--soak", type=float, default=2.0, help="untimed seconds of load before timing")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--cpu-sample", type=int, default=1 << 24, help="oracle baseline: first N keys")
     ap.add_argument("--ref-sample", type=int, default=1 << 22)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")

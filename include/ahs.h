@@ -312,7 +312,11 @@ AHS_API int ahs_lane_order_ok(void);
  * ahs_set_skip_trivial(0/1) sets it (any other value queries); returns the
  * setting.  ahs_sort_executed_passes() reads the plan of the last ahs_sort on
  * that d_tmp (synchronizes `stream`): the number of executed digit passes, or
- * -1 if that sort wrote no plan (COUNTING paths). */
+ * -1 if that sort wrote no plan (COUNTING paths), or AHS_ECUDA if one of its
+ * digit passes gave up waiting for a predecessor tile's look-back status (more
+ * than 2^28 empty polls, > 17 s: a stalled or preempted CTA; the output is then
+ * invalid, and the pass finished instead of trapping the context).
+ * ahs_sort_host() performs the same check after its final synchronisation. */
 AHS_API int ahs_set_skip_trivial(int on);
 AHS_API int ahs_sort_executed_passes(const void *d_tmp, size_t tmp_bytes, uint64_t n, int has_vals,
                                      void *stream);

@@ -296,9 +296,27 @@ def ahs_select(feat: Features, th: Thresholds | None = None) -> tuple[int, int]:
     return s.value, r.value
 
 
+def _check_outputs(keys_in, vals_in, keys_out, vals_out):
+    """The C ABI writes n keys (and n values of vals_in's width) through the output pointers:
+    refuse outputs that are smaller or of another width before any pointer crosses it."""
+    if keys_out is None or keys_out.numel() != keys_in.numel() or keys_out.element_size() != keys_in.element_size():
+        raise ValueError("keys_out must have the numel and element size of keys_in")
+    if _dtype_code(keys_out) != _dtype_code(keys_in):
+        raise ValueError(f"keys_out dtype {keys_out.dtype} differs from keys_in dtype {keys_in.dtype}")
+    if vals_in is not None:
+        if vals_in.numel() != keys_in.numel():
+            raise ValueError("vals_in must have one value per key")
+        if (vals_out is None or vals_out.numel() != vals_in.numel()
+                or vals_out.element_size() != vals_in.element_size()):
+            raise ValueError("vals_out must have the numel and element size of vals_in")
+    elif vals_out is not None:
+        raise ValueError("vals_out given without vals_in")
+
+
 def ahs_sort(keys_in, vals_in, keys_out, vals_out, strategy: int, feat: Features, ws: Workspace,
              stream=None):
     """Values: 4-byte (int32 / uint32 / float32 ...) or 8-byte tensors (64-bit payloads: ahs_sort_ex)."""
+    _check_outputs(keys_in, vals_in, keys_out, vals_out)
     vb = vals_in.element_size() if vals_in is not None else 4
     rc = lib().ahs_sort_ex(_dev_ptr(keys_in), _dev_ptr(vals_in), _dev_ptr(keys_out), _dev_ptr(vals_out),
                            keys_in.numel(), vb, strategy, C.byref(feat), _dev_ptr(ws.ws), ws.ws_bytes,
@@ -342,7 +360,25 @@ def ahs_sort_host(keys: np.ndarray, vals: np.ndarray | None, keys_out: np.ndarra
     def code(a):
         return _code_of(a.dtype)
 
-    n = keys.size if isinstance(keys, np.ndarray) else keys.numel()
+    def size(a):
+        return a.size if isinstance(a, np.ndarray) else a.numel()
+
+    def width(a):
+        return a.itemsize if isinstance(a, np.ndarray) else a.element_size()
+
+    def contiguous(a):
+        return a.flags["C_CONTIGUOUS"] if isinstance(a, np.ndarray) else a.is_contiguous()
+
+    n = size(keys)
+    for nm, a in (("keys", keys), ("keys_out", keys_out), ("vals", vals), ("vals_out", vals_out)):
+        if a is not None and not contiguous(a):
+            raise ValueError(f"{nm} must be C-contiguous")
+    if size(keys_out) != n or width(keys_out) != width(keys):
+        raise ValueError("keys_out must have the size and element width of keys")
+    if (vals is None) != (vals_out is None):
+        raise ValueError("vals and vals_out go together")
+    if vals is not None and (size(vals) != n or size(vals_out) != n or width(vals) != 4 or width(vals_out) != 4):
+        raise ValueError("host values are 4 bytes wide, one per key (vals and vals_out)")
     f = Features()
     s, r = C.c_int32(), C.c_int32()
     nbytes = scratch.numel() * scratch.element_size()

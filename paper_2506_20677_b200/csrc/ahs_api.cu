@@ -11,6 +11,8 @@
 #include <thread>
 #include <cstring>
 #include <mutex>
+#include <set>
+#include <utility>
 #include <vector>
 
 #include "../../include/ahs.h"
@@ -332,7 +334,8 @@ WsLayout ws_layout()
 struct TmpLayout {
     size_t ctrl, dhist, bucket, ticket, status, status_region_bytes, keys, vals, total;
 };
-constexpr int kTicketPlan = 16;  // plan offset in the ticket block (words)
+constexpr int kTicketPlan = 16;   // plan offset in the ticket block (words)
+constexpr int kTicketFault = 32;  // K6 look-back gave up (onesweep.cuh kLookbackSpinLimit): AHS_ECUDA
 TmpLayout tmp_layout(uint64_t n, int has_vals, size_t key_bytes = 4, size_t val_bytes = 4)
 {
     TmpLayout L;
@@ -484,6 +487,14 @@ int ahs_sort_executed_passes(const void *d_tmp, size_t tmp_bytes, uint64_t n, in
         cudaGetLastError();
         return AHS_ECUDA;
     }
+    uint32_t fault = 0;
+    if (cudaMemcpyAsync(&fault, (const char *)d_tmp + TL.ticket + kTicketFault * 4, 4, cudaMemcpyDeviceToHost, s) !=
+            cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess) {
+        cudaGetLastError();
+        return AHS_ECUDA;
+    }
+    if (fault) return AHS_ECUDA;
     return w[kMaxPasses + 1] == kPlanMagic ? (int)w[kMaxPasses] : -1;
 }
 
@@ -769,8 +780,16 @@ int sort_impl(const K *kin, const V *d_vals_in, K *kout, V *d_vals_out, uint64_t
     const K umin = kWide ? (K)umin64_of(feat) : (K)umin_of(feat);
     const uint32_t n32 = (uint32_t)n;
 
+    // paths without digit passes still clear the look-back fault word of a reused d_tmp
+    // (the digit-pass path clears the whole control block below)
+    auto clear_fault = [&]() -> bool {
+        const TmpLayout T0 = tmp_layout(0, 0);
+        if (!d_tmp || tmp_bytes < T0.status) return true;
+        return cudaMemsetAsync((char *)d_tmp + T0.ticket + kTicketFault * 4, 0, 4, s) == cudaSuccess;
+    };
     // constant input: stable identity
     if (feat->k == 1) {
+        if (!clear_fault()) return AHS_ECUDA;
         if (kout != kin && cudaMemcpyAsync(kout, kin, n * sizeof(K), cudaMemcpyDeviceToDevice, s) != cudaSuccess)
             return AHS_ECUDA;
         if (kv && d_vals_out != d_vals_in &&
@@ -784,6 +803,7 @@ int sort_impl(const K *kin, const V *d_vals_in, K *kout, V *d_vals_out, uint64_t
     // ---- keys-only COUNTING from the feature histogram (Listing 2)
     if (strategy == AHS_COUNTING && exact_hist && !kv) {
         if (!d_ws || ws_bytes < WL.total) return AHS_ENOSPACE;
+        if (!clear_fault()) return AHS_ECUDA;
         const uint32_t *scan = hist_scan(d_ws, feat, s);
         if (!scan) return AHS_ECUDA;
         cudaError_t e;
@@ -907,6 +927,7 @@ int sort_impl(const K *kin, const V *d_vals_in, K *kout, V *d_vals_out, uint64_t
         pa.plan = count_kv ? nullptr : plan;  // K5's plan (no skipping when not enabled)
         pa.status_clear = p > 0 ? status + (size_t)((p - 1) & 1) * status_words_per_pass : nullptr;
         pa.clear_words = p > 0 && p + 1 < passes ? (uint32_t)status_words_per_pass : 0u;
+        pa.fault = tickets + kTicketFault;
         void *args[] = {&pa};
         const cudaError_t e = launch(kv ? (count_kv ? KID_COUNT_SCATTER_KV : KID_ONESWEEP_KV) : KID_ONESWEEP, s, [&] {
             cudaLaunchConfig_t cfg;
@@ -1029,7 +1050,17 @@ int ahs_sort_host(const void *h_keys_in, const uint32_t *h_vals_in, void *h_keys
     const int rc = ahs_sort_host_async(h_keys_in, h_vals_in, h_keys_out, h_vals_out, n, dtype, th, d_scratch,
                                        scratch_bytes, feat, strategy, rule, stream);
     if (rc) return rc;
-    return cudaStreamSynchronize((cudaStream_t)stream) == cudaSuccess ? AHS_OK : AHS_ECUDA;
+    if (cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) return AHS_ECUDA;
+    if (n == 0) return AHS_OK;
+    // a look-back that gave up (kTicketFault in the sort's tmp block, same layout as the async call)
+    const bool kv = h_vals_in != nullptr;
+    const size_t kb = align_up(n * key_bytes_of(dtype), 256), vb = align_up(n * 4, 256);
+    const char *tmp = (const char *)d_scratch + 2 * kb + (kv ? 2 * vb : 0) + ws_layout().total;
+    uint32_t fault = 0;
+    if (cudaMemcpy(&fault, tmp + tmp_layout(0, 0).ticket + kTicketFault * 4, 4, cudaMemcpyDeviceToHost) !=
+        cudaSuccess)
+        return AHS_ECUDA;
+    return fault ? AHS_ECUDA : AHS_OK;
 }
 
 int ahs_sort_host_async(const void *h_keys_in, const uint32_t *h_vals_in, void *h_keys_out, uint32_t *h_vals_out,
@@ -1093,15 +1124,32 @@ int ahs_sort_host_async(const void *h_keys_in, const uint32_t *h_vals_in, void *
 // --------------------------------------------------- segment sort (NEXT-4)
 }  // extern "C"
 namespace {
+// Opt-in dynamic shared memory above 48 KiB is a per-device function attribute: set it once per
+// (kernel, device) pair.  A failure is returned (and not cached), so the caller reports it.
+cudaError_t opt_in_smem(const void *fn, size_t smem)
+{
+    if (smem <= 48u * 1024u) return cudaSuccess;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    static std::mutex mu;
+    static std::set<std::pair<const void *, int>> done;
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.count({fn, dev})) return cudaSuccess;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    done.insert({fn, dev});
+    return cudaSuccess;
+}
+
 template <typename K, bool KV, int L>
 cudaError_t seg_small(const void *kin, const uint32_t *vin, void *kout, uint32_t *vout, uint64_t n,
                       const uint32_t *offsets, uint32_t nseg, uint32_t max_segment, K flip, uint32_t *bad,
                       cudaStream_t s)
 {
     constexpr size_t smem = seg_small_smem<K, KV>();
-    static const bool attr = cudaFuncSetAttribute(k_seg_small<K, KV, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                  (int)smem) == cudaSuccess;
-    if (!attr) return cudaErrorInvalidValue;
+    const cudaError_t ae = opt_in_smem((const void *)k_seg_small<K, KV, L>, smem);
+    if (ae != cudaSuccess) return ae;
     const unsigned g = (nseg + kSegSmallBlock - 1) / kSegSmallBlock;
     return launch_k(k_seg_small<K, KV, L>, dim3(g), dim3(kSegSmallBlock), smem, s, (const K *)kin, vin, (K *)kout,
                     vout, offsets, nseg, n, flip, max_segment, bad);
@@ -1113,9 +1161,8 @@ cudaError_t seg_radix(const void *kin, const uint32_t *vin, void *kout, uint32_t
                       cudaStream_t s)
 {
     constexpr size_t smem = seg_radix_smem<K, KV, GROUP, CAP>();
-    static const bool attr = cudaFuncSetAttribute(k_seg_radix<K, KV, GROUP, CAP, ORD>,
-                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess;
-    if (!attr) return cudaErrorInvalidValue;
+    const cudaError_t ae = opt_in_smem((const void *)k_seg_radix<K, KV, GROUP, CAP, ORD>, smem);
+    if (ae != cudaSuccess) return ae;
     return launch_k(k_seg_radix<K, KV, GROUP, CAP, ORD>, dim3(nseg), dim3(GROUP), smem,
                     s, (const K *)kin, vin, (K *)kout, vout, offsets, nseg, n, flip, max_segment, bad);
 }
@@ -1169,22 +1216,23 @@ int ahs_sort_segments(const void *d_keys_in, const uint32_t *d_vals_in, void *d_
     cudaStream_t s = (cudaStream_t)stream;
     if (cudaMemsetAsync(d_bad, 0, 4, s) != cudaSuccess) return AHS_ECUDA;
     if (num_segments == 0) return AHS_OK;
+    cudaError_t le = cudaSuccess;  // seg_launch's own status (attribute set-up, launch)
     const cudaError_t e = launch(KID_SEG_SORT, s, [&] {
         if (dtype_wide(dtype)) {
             const uint64_t flip = flip64_of(dtype);
-            if (kv) seg_launch<uint64_t, true>(d_keys_in, d_vals_in, d_keys_out, d_vals_out, n, d_offsets,
-                                               num_segments, max_segment, flip, d_bad, ord, s);
-            else seg_launch<uint64_t, false>(d_keys_in, nullptr, d_keys_out, nullptr, n, d_offsets, num_segments,
-                                             max_segment, flip, d_bad, ord, s);
+            if (kv) le = seg_launch<uint64_t, true>(d_keys_in, d_vals_in, d_keys_out, d_vals_out, n, d_offsets,
+                                                    num_segments, max_segment, flip, d_bad, ord, s);
+            else le = seg_launch<uint64_t, false>(d_keys_in, nullptr, d_keys_out, nullptr, n, d_offsets,
+                                                  num_segments, max_segment, flip, d_bad, ord, s);
         } else {
             const uint32_t flip = flip_of(dtype);
-            if (kv) seg_launch<uint32_t, true>(d_keys_in, d_vals_in, d_keys_out, d_vals_out, n, d_offsets,
-                                               num_segments, max_segment, flip, d_bad, ord, s);
-            else seg_launch<uint32_t, false>(d_keys_in, nullptr, d_keys_out, nullptr, n, d_offsets, num_segments,
-                                             max_segment, flip, d_bad, ord, s);
+            if (kv) le = seg_launch<uint32_t, true>(d_keys_in, d_vals_in, d_keys_out, d_vals_out, n, d_offsets,
+                                                    num_segments, max_segment, flip, d_bad, ord, s);
+            else le = seg_launch<uint32_t, false>(d_keys_in, nullptr, d_keys_out, nullptr, n, d_offsets,
+                                                  num_segments, max_segment, flip, d_bad, ord, s);
         }
     });
-    return e == cudaSuccess ? AHS_OK : AHS_ECUDA;
+    return (e == cudaSuccess && le == cudaSuccess) ? AHS_OK : AHS_ECUDA;
 }
 
 // ------------------------------------------------------ classifier (NEXT-4)

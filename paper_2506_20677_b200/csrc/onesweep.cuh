@@ -148,7 +148,15 @@ struct PassArgsT {
     const uint32_t *plan;         // nullptr: no skipping
     uint32_t *status_clear;       // the previous pass's status region: zeroed here for the next pass
     uint32_t clear_words;         //   (passes alternate between two regions; 0: nothing to clear)
+    uint32_t *fault;              // set to 1 when a look-back gives up (nullptr: __trap instead)
 };
+
+// Look-back polls before a pass gives up on an unpublished predecessor (each empty round
+// sleeps >= 64 ns: > 17 s).  A predecessor CTA can be descheduled for a long time (time
+// slicing, MPS, a debugger), so the bound is far above any legitimate wait; when it is hit
+// the pass sets *fault (the host reports AHS_ECUDA) and finishes instead of trapping, which
+// would kill the context for every stream of the process.
+constexpr uint32_t kLookbackSpinLimit = 1u << 28;
 using PassArgs = PassArgsT<uint32_t>;
 
 // K: uint32_t (32-bit keys) or uint64_t (64-bit keys, NEXT-3); V: the value type (uint32_t,
@@ -444,7 +452,11 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(const PassArgsT<K, V> 
 #endif
                         if (used == 0) {
                             // predecessors hold earlier tickets and publish before they wait
-                            if (++spins > (1u << 24)) __trap();
+                            if (++spins > kLookbackSpinLimit) {
+                                if (!a.fault) __trap();
+                                atomicExch(a.fault, 1u);
+                                break;
+                            }
                             __nanosleep(64);
                         }
                     }
@@ -508,10 +520,15 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(const PassArgsT<K, V> 
 // Self-test of the hardware property kRankOrdered relies on: the lanes of one
 // shared-memory atomicAdd instruction that hit the same address are served in
 // ascending lane order, so the returned old values are lane-ordered ranks.
-// Same source pattern as the ranking loop (per-warp 256-word tables, items in
-// sequence separated by __syncwarp), with digit collision rates from "all 32
-// lanes on one word" to "spread over 256 words".  Expected ranks come from
-// match.any (slow but independent).  *bad counts violations.
+// Same source pattern as the ranking loops (per-warp 256-word tables, items in
+// sequence separated by __syncwarp, the atomic's return value used), with digit
+// collision rates from "all 32 lanes on one word" to "spread over 256 words",
+// and with the active-lane masks the kernels issue: the full warp (K6 full
+// tiles, K9r, whose idle lanes hit a dummy word), a prefix of the lanes (K6's
+// partial last tile: `if (valid) atomicAdd`), a suffix and scattered lanes.
+// Expected ranks come from match.any (slow but independent).  *bad counts
+// violations.  (tests/test_sass_rank.py checks that this kernel and the ranking
+// kernels compile the rank site to the same ATOMS.ADD-with-return form.)
 __device__ __forceinline__ uint32_t selftest_hash(uint32_t x)
 {
     x ^= x >> 16;
@@ -535,10 +552,20 @@ __global__ void __launch_bounds__(512)
         const uint32_t r = selftest_hash((blockIdx.x * blockDim.x + threadIdx.x) * 977u + it * 0x9e3779b9u);
         const uint32_t mask = (1u << (it % 9)) - 1u;  // 1 .. 256 distinct words
         const uint32_t dd = (r & mask) * (kBins / (mask + 1u));
-        const uint32_t pos = atomicAdd(&tab[warp][dd], 1u);
-        const uint32_t peers = __match_any_sync(kFull, dd);
-        const uint32_t base = __shfl_sync(kFull, pos, __ffs(peers) - 1);
-        nbad += pos != base + __popc(peers & lt);
+        // active lanes of this item (warp-uniform): full, prefix, suffix, scattered
+        const uint32_t h = selftest_hash(blockIdx.x * 7919u + warp * 104729u + (uint32_t)it);
+        const uint32_t m = 1u + h % 31u;  // 1 .. 31
+        const uint32_t kind = (uint32_t)(it / 9) % 4u;
+        const uint32_t act = kind == 0 ? kFull
+                           : kind == 1 ? (1u << m) - 1u                   // lanes < m
+                           : kind == 2 ? ~((1u << m) - 1u)                // lanes >= m
+                                       : (selftest_hash(h) | 1u);         // scattered, lane 0 active
+        if ((act >> lane) & 1u) {
+            const uint32_t pos = atomicAdd(&tab[warp][dd], 1u);
+            const uint32_t peers = __match_any_sync(act, dd);
+            const uint32_t base = __shfl_sync(act, pos, __ffs(peers) - 1);
+            nbad += pos != base + __popc(peers & lt);
+        }
         __syncwarp();
     }
     nbad = __reduce_add_sync(kFull, nbad);

@@ -309,7 +309,11 @@ __device__ __forceinline__ void onesweep2_body(const PassArgsT<K, V> &a, const K
                         if (fin) break;
                         jt -= used;
                         if (used == 0) {
-                            if (++spins > (1u << 26)) __trap();
+                            if (++spins > kLookbackSpinLimit) {
+                                if (!a.fault) __trap();
+                                atomicExch(a.fault, 1u);
+                                break;
+                            }
                             __nanosleep(64);
                         }
                     }

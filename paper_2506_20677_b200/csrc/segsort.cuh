@@ -46,41 +46,22 @@ __global__ void __launch_bounds__(kSegSmallBlock)
     __shared__ uint32_t s_ok;
     const uint32_t s0 = blockIdx.x * kSegSmallBlock, s1 = min(nseg, s0 + kSegSmallBlock);
     const uint32_t base = __ldg(&offsets[s0]), end = __ldg(&offsets[s1]);
-    // the range must hold the CTA's segments (each <= L keys, inside [0, n))
+    // staged path: the CTA's range [base, end) holds all its segments and fits the buffer
     if (threadIdx.x == 0) s_ok = (end >= base && (uint64_t)end <= n && end - base <= CAP) ? 1u : 0u;
     const uint32_t my = s0 + threadIdx.x;
     uint32_t lo = 0, hi = 0;
-    bool mine = my < s1;
+    bool mine = my < s1, inb = false;
     if (mine) {
         lo = __ldg(&offsets[my]);
         hi = __ldg(&offsets[my + 1]);
-        if (hi < lo || hi - lo > maxlen || lo < base || hi > end) mine = false;  // maxlen <= L
+        inb = hi >= lo && (uint64_t)hi <= n;  // a real segment inside the keys
+        if (!inb || hi - lo > maxlen) mine = false;  // maxlen <= L
     }
     __syncthreads();
-    if (!s_ok) {
-        if (my < s1) atomicAdd(bad, 1u);
-        return;
-    }
-    if (my < s1 && !mine) atomicAdd(bad, 1u);
-    const uint32_t len = end - base;
-    for (uint32_t i = threadIdx.x; i < len; i += kSegSmallBlock) {
-        sk[i] = kin[base + i] ^ flip;
-        if constexpr (KV) sv[i] = vin[base + i];
-    }
-    __syncthreads();
-    if (mine) {
-        // the segment into registers, padded with the largest key (padding stays
-        // last: the network only moves a key past a strictly greater one)
-        const uint32_t a = lo - base, m = hi - lo;
-        K r[L];
-        [[maybe_unused]] uint32_t q[KV ? L : 1];
-#pragma unroll
-        for (int i = 0; i < L; i++) {
-            r[i] = (uint32_t)i < m ? sk[a + i] : ~K(0);
-            if constexpr (KV) q[i] = (uint32_t)i < m ? sv[a + i] : 0u;
-        }
-        // Listing 1 as adjacent swaps: key i moves left past every
-        // strictly greater key (stable); unrolled so the array stays in registers
+    if (my < s1 && !mine) atomicAdd(bad, 1u);  // only the segments that are themselves bad
+    // the segment sort of one thread, Listing 1 as adjacent swaps: key i moves
+    // left past every strictly greater key (stable); unrolled so the array stays in registers
+    auto sort_regs = [&](K(&r)[L], uint32_t(&q)[KV ? L : 1]) {
 #pragma unroll
         for (int i = 1; i < L; i++) {
 #pragma unroll
@@ -96,6 +77,56 @@ __global__ void __launch_bounds__(kSegSmallBlock)
                 }
             }
         }
+    };
+    if (!s_ok) {
+        // a bad segment (or non-monotone offsets) spoils the CTA's range: every good segment is
+        // sorted straight from global memory; a too-long segment inside the keys is copied as is
+        if (mine) {
+            const uint32_t m = hi - lo;
+            K r[L];
+            uint32_t q[KV ? L : 1];
+#pragma unroll
+            for (int i = 0; i < L; i++) {
+                r[i] = (uint32_t)i < m ? (K)(kin[lo + i] ^ flip) : ~K(0);
+                if constexpr (KV) q[i] = (uint32_t)i < m ? vin[lo + i] : 0u;
+            }
+            sort_regs(r, q);
+#pragma unroll
+            for (int i = 0; i < L; i++)
+                if ((uint32_t)i < m) {
+                    kout[lo + i] = r[i] ^ flip;
+                    if constexpr (KV) vout[lo + i] = q[i];
+                }
+        } else if (my < s1 && inb && kout != kin) {
+            for (uint32_t i = lo; i < hi; i++) {
+                kout[i] = kin[i];
+                if constexpr (KV) vout[i] = vin[i];
+            }
+        }
+        return;
+    }
+    if (mine && (lo < base || hi > end)) {  // non-monotone offsets: not inside the staged range
+        mine = false;
+        atomicAdd(bad, 1u);
+    }
+    const uint32_t len = end - base;
+    for (uint32_t i = threadIdx.x; i < len; i += kSegSmallBlock) {
+        sk[i] = kin[base + i] ^ flip;
+        if constexpr (KV) sv[i] = vin[base + i];
+    }
+    __syncthreads();
+    if (mine) {
+        // the segment into registers, padded with the largest key (padding stays
+        // last: the network only moves a key past a strictly greater one)
+        const uint32_t a = lo - base, m = hi - lo;
+        K r[L];
+        uint32_t q[KV ? L : 1];
+#pragma unroll
+        for (int i = 0; i < L; i++) {
+            r[i] = (uint32_t)i < m ? sk[a + i] : ~K(0);
+            if constexpr (KV) q[i] = (uint32_t)i < m ? sv[a + i] : 0u;
+        }
+        sort_regs(r, q);
 #pragma unroll
         for (int i = 0; i < L; i++)
             if ((uint32_t)i < m) {

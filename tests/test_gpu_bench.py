@@ -27,15 +27,19 @@ def test_bench_line_contract():
               "gpu_launches"):
         assert k in d, k
     assert d["n_gpus"] == 1 and d["steps"] == 5 and d["warmup"] == 3 and d["higher_is_better"] is True
-    n = 1 << 24  # cfg2, the default workload
-    assert d["config"]["workload"] == "cfg2"
+    n = 1 << 28  # cfg5 r=32, the default workload: 2^28 (key, value) pairs, above BASELINE's 2^26 gate
+    assert d["config"]["workload"] == "cfg5_r32" and d["config"]["kv"] is True
     assert d["value"] == pytest.approx(n / (d["ms_per_step"] * 1e-3) / 1e9, rel=1e-3)
+    hk = d["headline_keys"]  # second headline: keys-only GENERAL at 2^26
+    assert hk["workload"] == "cfg4a" and hk["n"] == 1 << 26 and hk["value"] > 0
+    assert hk["roofline"]["frac"] == pytest.approx(hk["roofline"]["achieved"] / hk["roofline"]["peak"], rel=1e-3)
     r = d["roofline"]
     assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] < 1
     assert r["frac"] == pytest.approx(r["achieved"] / r["peak"], rel=1e-3)
     e = d["e2e"]
-    assert e["value"] > 0 and e["h2d_bytes_per_step"] == 4 * n and e["d2h_bytes_per_step"] == 4 * n
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] == 8 * n and e["d2h_bytes_per_step"] == 8 * n
     c = d["cpu_baseline"]
-    assert c["kind"] == "oracle" and c["value"] > 0 and c["cores"] >= 1
+    assert c["kind"] == "oracle" and c["value"] > 0 and c["cores"] == 1
+    assert c["host"]["os_cpu_count"] >= 1 and "pinned" in c["sample"]
     assert d["gpu_launches"] > 0
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])

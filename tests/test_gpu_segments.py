@@ -186,6 +186,26 @@ def test_segments_longer_than_declared_are_refused():
     assert bad == 1 and np.array_equal(ko[:10], np.sort(keys[:10]))
 
 
+@pytest.mark.parametrize("inplace", [False, True])
+def test_small_path_one_long_segment_spares_its_neighbours(inplace):
+    """One over-long segment pushes a K9s CTA's range past its staging buffer: only that
+    segment is reported (and left unsorted); the CTA's 255 other segments are still sorted."""
+    lens = np.full(300, 20, dtype=np.int64)
+    lens[100] = 10000
+    lens[7] = 0
+    off = np.zeros(lens.size + 1, dtype=np.uint32)
+    off[1:] = np.cumsum(lens)
+    n = int(off[-1])
+    keys = make_keys("i32", n, 43)
+    vals = np.arange(n, dtype=np.uint32)
+    ko, vo, bad = run(keys, vals, off, 32, inplace=inplace)
+    assert bad == 1
+    ek, ev = expected(keys, vals, off, 32)
+    a, b = int(off[100]), int(off[101])
+    ek[a:b], ev[a:b] = keys[a:b], vals[a:b]  # the refused segment stays as it was
+    assert np.array_equal(ko, ek) and np.array_equal(vo, ev)
+
+
 def test_no_segments_and_errors():
     keys = to_dev(make_keys("i32", 10, 37))
     off = torch.zeros(1, dtype=torch.int32, device="cuda")
