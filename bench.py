@@ -460,15 +460,19 @@ def dominant_roofline(res, n, kv, kb, workload, peak, peak_kind):
                       "same K steps (the headline value is timed without them)"}
 
 
-def table_row(torch, ahs, cfg, k2, v2, steps, device, flush, peak, skip=True):
+def table_row(torch, ahs, cfg, k2, v2, steps, device, flush, peak, skip=True, count_single=False):
     """One per-strategy row: pipeline and sort throughput, fractions of the roofline.  With
     skip=False the NEXT-1 trivial-pass skipping is off: every nominal pass executes (the
     contract row of SURVEY §8(d)); with skip=True the row is the NEXT-1 row."""
-    prev = ahs.ahs_set_skip_trivial(1 if skip else 0)
+    prev = ahs.ahs_set_skip_trivial(-1)
+    prev_cs = ahs.ahs_set_count_kv_single(-1)
+    ahs.ahs_set_skip_trivial(1 if skip else 0)
+    ahs.ahs_set_count_kv_single(1 if count_single else 0)
     try:
         r2 = time_pipeline(torch, ahs, k2, v2, steps, 2, device, flush, profile=True)
     finally:
         ahs.ahs_set_skip_trivial(prev)
+        ahs.ahs_set_count_kv_single(prev_cs)
     p2 = r2["prof"]
     n2 = k2.size
     kv2 = v2 is not None
@@ -479,6 +483,7 @@ def table_row(torch, ahs, cfg, k2, v2, steps, device, flush, peak, skip=True):
     row = {
         "workload": cfg, "n": n2, "kv": kv2, "strategy": ahs.STRATEGY_NAMES[r2["s"]],
         "rule": ahs.RULE_NAMES[r2["r"]], "skip_trivial": skip, "passes": r2["passes"],
+        "count_kv_single": count_single,
         "passes_executed": r2["executed"],
         "pipeline_Gkeys_s": n2 * steps / (r2["total_ms"] * 1e-3) / 1e9,
         "sort_Gkeys_s": n2 / (sort_ms2 * 1e-3) / 1e9 if sort_ms2 > 0 else None,
@@ -593,6 +598,11 @@ def run_ours(args):
             if r2["executed"] < r2["passes"]:
                 row_c, _ = table_row(torch, ahs, cfg, k2, v2, args.table_steps, device, flush, peak, skip=False)
                 rows.append(row_c)
+            if v2 is not None and r2["s"] == 0 and 8 < r2["f"].bits <= 10:
+                # key-value COUNTING with 256 < k <= 1024: the opt-in single 10-bit scatter beside the default
+                row_s, _ = table_row(torch, ahs, cfg, k2, v2, args.table_steps, device, flush, peak,
+                                     count_single=True)
+                rows.append(row_s)
             del k2, v2
         out["strategies"] = rows
     # CPU oracle baseline (rank 0, N = 1 only)
@@ -649,7 +659,7 @@ def main():
     ap.add_argument("--workload", default="cfg5_r32", choices=sorted(synth.CONFIGS))
     ap.add_argument("--keys-workload", default="cfg4a", help="second (keys-only) headline block; '' to skip")
     ap.add_argument("--configs", default="cfg1,cfg2,cfg2kv,cfg3,cfg4a,cfg4b,cfg4c,cfg4d,cfg5_r8,cfg5_r16,cfg5_r20,"
-                                         "cfg5_r24,cfg5_r28,cfg5_r32,cfg6,cfg6kv",
+                                         "cfg5_r24,cfg5_r28,cfg5_r32,cfg6,cfg6kv,cfg7kv",
                     help="per-strategy table rows (single GPU only); '' to skip")
     ap.add_argument("--table-steps", type=int, default=5)
     ap.add_argument("--soak", type=float, default=2.0, help="untimed seconds of load before timing")

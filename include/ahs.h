@@ -318,6 +318,18 @@ AHS_API int ahs_lane_order_ok(void);
  * invalid, and the pass finished instead of trapping the context).
  * ahs_sort_host() performs the same check after its final synchronisation. */
 AHS_API int ahs_set_skip_trivial(int on);
+
+/* Key-value COUNTING with 256 < k <= 1024 (§III.F Listing 2, lines
+ * 187-214; k_counting = 1024, Table II): one stable scatter by the
+ * 10-bit digit key - min (16 n bytes moved: read and write of keys and values)
+ * instead of two 8-bit radix passes over key - min (32 n bytes).  Output is
+ * identical.  Default off (environment AHS_COUNT_KV_SINGLE=1 turns it on):
+ * on B200 the single pass measured slower, because 1024 digit runs per
+ * 4096-key tile fragment its write-out (profiles/r02_summary.md).  32-bit keys
+ * with 4-byte values and the ordered ranking only; otherwise the two passes
+ * run.  ahs_set_count_kv_single(0/1) sets it (any other value queries);
+ * returns the setting.  ahs_sort_passes() reports 1 for such inputs when on. */
+AHS_API int ahs_set_count_kv_single(int on);
 AHS_API int ahs_sort_executed_passes(const void *d_tmp, size_t tmp_bytes, uint64_t n, int has_vals,
                                      void *stream);
 

@@ -7,7 +7,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "lib", "libahs.so")
+# AHS_LIB: development A/B of two library builds (tools/); the default is the in-tree build
+_LIB_PATH = os.environ.get("AHS_LIB") or os.path.join(_HERE, "lib", "libahs.so")
 
 AHS_I32, AHS_U32, AHS_I64, AHS_U64 = 0, 1, 2, 3
 AHS_COUNTING, AHS_RADIX, AHS_GENERAL = 0, 1, 2
@@ -97,6 +98,7 @@ def lib():
             "ahs_launch_count": ([], C.c_uint64),
             "ahs_rank_mode": ([C.c_int], C.c_int),
             "ahs_set_skip_trivial": ([C.c_int], C.c_int),
+            "ahs_set_count_kv_single": ([C.c_int], C.c_int),
             "ahs_entropy_sorted": ([vp, u64, vp, sz, C.POINTER(C.c_double), vp], C.c_int),
             "ahs_sort_executed_passes": ([vp, sz, u64, C.c_int, vp], C.c_int),
             "ahs_lane_order_ok": ([], C.c_int),
@@ -177,6 +179,12 @@ def ahs_entropy_sorted(keys, ws: "Workspace", stream=None) -> float:
 def ahs_set_skip_trivial(on: int = -1) -> int:
     """NEXT-1 trivial-pass skipping: 1 on, 0 off, -1 query; returns the setting."""
     return lib().ahs_set_skip_trivial(on)
+
+
+def ahs_set_count_kv_single(on: int = -1) -> int:
+    """Key-value COUNTING with 256 < k <= 1024 as one 10-bit stable scatter (1) or two 8-bit passes
+    (0, default); -1 queries.  Returns the setting."""
+    return lib().ahs_set_count_kv_single(on)
 
 
 def ahs_sort_executed_passes(ws: "Workspace", stream=None) -> int:

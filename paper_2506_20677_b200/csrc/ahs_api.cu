@@ -44,6 +44,14 @@ struct DevInfo {
     const void *osl_fn = nullptr;
     size_t osl_smem = 0;
     int osl_tile = 0, osl_per_sm = 0;
+    // K6 v2 (onesweep2.cuh, hot-digit ranking) for RADIX over 32-bit keys: [0 keys, 1 pairs]
+    const void *os2_fn[2] = {};
+    size_t os2_smem[2] = {};
+    int os2_tile[2] = {}, os2_per_sm[2] = {}, os2_block[2] = {};
+    // K6 v2 10-bit pairs: key-value COUNTING with 256 < k <= 1024 in one pass (opt-in)
+    const void *os10_fn = nullptr;
+    size_t os10_smem = 0;
+    int os10_tile = 0, os10_per_sm = 0;
     bool lane_order_ok = false;              // self-test of the ordered ranking passed
     int ent_grid[2] = {0, 0};                // K8 grid per key width (32 / 64-bit): one resident wave
     int rank_mode = kRankMasked;
@@ -156,6 +164,32 @@ int device_info(int *sms, int *hist_clusters = nullptr, DevInfo **info = nullptr
                 good &= cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.osl_per_sm, d.osl_fn, kSortBlock,
                                                                       d.osl_smem) == cudaSuccess;
             good &= d.osl_per_sm > 0;
+            d.os2_fn[0] = (const void *)K6V2_KEYS;
+            d.os2_smem[0] = Os2Keys::kSmem;
+            d.os2_tile[0] = Os2Keys::kTile;
+            d.os2_block[0] = kSortBlock;
+            d.os2_fn[1] = (const void *)K6V2_PAIRS;
+            d.os2_smem[1] = Os2Pairs::kSmem;
+            d.os2_tile[1] = Os2Pairs::kTile;
+            d.os2_block[1] = kSortBlockPairsO;
+            d.os10_fn = (const void *)K6V2_PAIRS10;
+            d.os10_smem = Os2Pairs10::kSmem;
+            d.os10_tile = Os2Pairs10::kTile;
+            good &= cudaFuncSetAttribute(d.os10_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d.os10_smem) ==
+                    cudaSuccess;
+            if (good)
+                good &= cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.os10_per_sm, d.os10_fn, 256, d.os10_smem) ==
+                        cudaSuccess;
+            good &= d.os10_per_sm > 0;
+            for (int kv = 0; kv < 2; kv++) {
+                good &= cudaFuncSetAttribute(d.os2_fn[kv], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)d.os2_smem[kv]) == cudaSuccess;
+                if (good)
+                    good &= cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.os2_per_sm[kv], d.os2_fn[kv],
+                                                                          d.os2_block[kv], d.os2_smem[kv]) ==
+                            cudaSuccess;
+                good &= d.os2_per_sm[kv] > 0;
+            }
             for (int w = 0; w < 2; w++)
                 for (int kv = 0; kv < 3; kv++)
                     for (int m = 0; m < 2; m++) {
@@ -233,6 +267,17 @@ std::atomic<bool> g_skip_trivial{[] {
 // AHS_PDL=0 turns it off: plain stream serialization)
 std::atomic<bool> g_pdl{[] {
     const char *e = std::getenv("AHS_PDL");
+    return !(e && e[0] == '0');
+}()};
+// key-value COUNTING with 256 < k <= 1024: one 10-bit stable scatter instead of two 8-bit radix
+// passes (default off; AHS_COUNT_KV_SINGLE=1 or ahs_set_count_kv_single(1))
+std::atomic<bool> g_count_kv_single{[] {
+    const char *e = std::getenv("AHS_COUNT_KV_SINGLE");
+    return e && e[0] == '1';
+}()};
+// K6 v2 for RADIX passes (default on; AHS_K6V2=0 turns it off: K6 everywhere)
+std::atomic<bool> g_k6v2{[] {
+    const char *e = std::getenv("AHS_K6V2");
     return !(e && e[0] == '0');
 }()};
 std::atomic<bool> g_prof{false};
@@ -348,6 +393,11 @@ TmpLayout tmp_layout(uint64_t n, int has_vals, size_t key_bytes = 4, size_t val_
     L.status = o;
     const uint64_t tiles = (n + kMinTile - 1) / kMinTile;
     L.status_region_bytes = align_up((size_t)tiles * kBins * 4, 256);
+    if (has_vals && key_bytes == 4 && val_bytes == 4) {
+        // the single 10-bit COUNTING scatter (Os2Pairs10) uses both regions as one: 1024 statuses per tile
+        const uint64_t t10 = (n + Os2Pairs10::kTile - 1) / Os2Pairs10::kTile;
+        L.status_region_bytes = std::max(L.status_region_bytes, align_up((size_t)t10 * 1024 * 4 / 2 + 256, 256));
+    }
     o += 2 * L.status_region_bytes;
     L.keys = o;
     o += align_up(n * key_bytes, 256);
@@ -441,7 +491,13 @@ int ahs_sort_passes(const ahs_features_t *f, int32_t strategy, int has_vals)
     case AHS_COUNTING:
         if (f->shift > 0) return radix_passes(f->bits);
         if (!has_vals) return 0;
-        return f->bits <= 8 ? 1 : radix_passes(f->bits);
+        if (f->bits <= 8) return 1;
+        if (f->bits <= 10 && !dtype_wide((int32_t)f->dtype) && g_count_kv_single.load()) {
+            int sms = 0;
+            DevInfo *di = nullptr;
+            if (device_info(&sms, nullptr, &di) == AHS_OK && di->rank_mode == kRankOrdered) return 1;
+        }
+        return radix_passes(f->bits);
     default: return AHS_EINVAL;
     }
 }
@@ -470,6 +526,13 @@ int ahs_set_skip_trivial(int on)
 {
     if (on != 0 && on != 1) return g_skip_trivial.load() ? 1 : 0;
     g_skip_trivial.store(on == 1);
+    return on;
+}
+
+int ahs_set_count_kv_single(int on)
+{
+    if (on != 0 && on != 1) return g_count_kv_single.load() ? 1 : 0;
+    g_count_kv_single.store(on == 1);
     return on;
 }
 
@@ -837,7 +900,10 @@ int sort_impl(const K *kin, const V *d_vals_in, K *kout, V *d_vals_out, uint64_t
     uint32_t *tickets = (uint32_t *)(tmp + TL.ticket);
     uint32_t *status = (uint32_t *)(tmp + TL.status);
 
-    const bool count_kv = strategy == AHS_COUNTING && exact_hist && kv && feat->bits <= 8;
+    const bool count_kv8 = strategy == AHS_COUNTING && exact_hist && kv && feat->bits <= 8;
+    const bool count_kv10 = strategy == AHS_COUNTING && exact_hist && kv && feat->bits > 8 && feat->bits <= 10 &&
+                            W == 0 && VK == 1 && di->rank_mode == kRankOrdered && g_count_kv_single.load();
+    const bool count_kv = count_kv8 || count_kv10;  // one stable scatter by key - min (Listing 2)
     int passes;
     if (count_kv) passes = 1;
     else if (strategy == AHS_GENERAL) passes = kWide ? 8 : 4;  // full width, on key - min (R14)
@@ -846,14 +912,30 @@ int sort_impl(const K *kin, const V *d_vals_in, K *kout, V *d_vals_out, uint64_t
     // zero the control words and both status regions (one memset); passes
     // alternate between the regions, each clearing the previous pass's
     const int mode = di->rank_mode;
-    const bool large = W == 0 && VK == 0 && mode == kRankOrdered && n >= kLargeN;
-    const uint64_t tile = large ? (uint64_t)di->osl_tile : (uint64_t)di->os_tile[W][VK][mode];
+    // RADIX over 32-bit keys (ordered ranking): K6 v2 with the hot-digit ranking (low-entropy
+    // inputs have skewed digits); everything else: K6
+    const bool v2 = W == 0 && VK < 2 && mode == kRankOrdered && strategy == AHS_RADIX && !count_kv &&
+                    g_k6v2.load(std::memory_order_relaxed);
+    const bool large = !v2 && W == 0 && VK == 0 && mode == kRankOrdered && n >= kLargeN;
+    const uint64_t tile = v2 ? (uint64_t)di->os2_tile[VK]
+                        : large ? (uint64_t)di->osl_tile : (uint64_t)di->os_tile[W][VK][mode];
     const uint64_t tiles = (n + tile - 1) / tile;
-    const int per_sm = large ? di->osl_per_sm : di->os_per_sm[W][VK][mode];
+    const int per_sm = v2 ? di->os2_per_sm[VK] : large ? di->osl_per_sm : di->os_per_sm[W][VK][mode];
     const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)sms * per_sm);
-    const void *k6 = large ? di->osl_fn : di->os_fn[W][VK][mode];
-    const size_t k6_smem = large ? di->osl_smem : di->os_smem[W][VK][mode];
-    const size_t status_words_per_pass = (size_t)tiles * kBins;
+    const void *k6 = v2 ? di->os2_fn[VK] : large ? di->osl_fn : di->os_fn[W][VK][mode];
+    size_t k6_smem = v2 ? di->os2_smem[VK] : large ? di->osl_smem : di->os_smem[W][VK][mode];
+    unsigned k6_block = v2 ? (unsigned)di->os2_block[VK] : (unsigned)di->os_block[W][VK][mode];
+    unsigned grid_k6 = grid;
+    if (count_kv10) {
+        k6 = di->os10_fn;
+        k6_smem = di->os10_smem;
+        k6_block = 256;
+        const uint64_t t10 = (n + di->os10_tile - 1) / di->os10_tile;
+        grid_k6 = (unsigned)std::min<uint64_t>(t10, (uint64_t)sms * di->os10_per_sm);
+    }
+    // statuses of one pass; the 10-bit COUNTING scatter (1024 per tile) spans both regions
+    const size_t status_words_per_pass =
+        count_kv10 ? (size_t)((n + di->os10_tile - 1) / di->os10_tile) * 1024 : (size_t)tiles * kBins;
     const size_t zero_bytes = (TL.status - TL.ctrl) + status_words_per_pass * 4 * (passes > 1 ? 2 : 1);
     if (cudaMemsetAsync(tmp + TL.ctrl, 0, zero_bytes, s) != cudaSuccess) return AHS_ECUDA;
 
@@ -932,7 +1014,7 @@ int sort_impl(const K *kin, const V *d_vals_in, K *kout, V *d_vals_out, uint64_t
         const cudaError_t e = launch(kv ? (count_kv ? KID_COUNT_SCATTER_KV : KID_ONESWEEP_KV) : KID_ONESWEEP, s, [&] {
             cudaLaunchConfig_t cfg;
             cudaLaunchAttribute attr[1];
-            pdl_config(cfg, attr, dim3(grid), dim3(di->os_block[W][VK][mode]), k6_smem, s);
+            pdl_config(cfg, attr, dim3(grid_k6), dim3(k6_block), k6_smem, s);
             cudaLaunchKernelExC(&cfg, k6, args);
         });
         if (e != cudaSuccess) return AHS_ECUDA;

@@ -840,7 +840,9 @@ __global__ void __launch_bounds__(BLOCK)
     for (uint32_t w = 0; w < warp; w++) wofs += s_u[w];
     if (b < nb) scan[b] = off + wofs + incl - c;
     if (b == nb - 1u) scan[nb] = n;
-    if (b > nb && b <= 256u) scan[b] = n;  // K6 reads 257 bucket bases when it scatters COUNTING pairs
+    // K6 reads 257 bucket bases when it scatters COUNTING pairs with 8-bit digits, K6 v2 1024
+    // with 10-bit digits (onesweep2.cuh: digit counts base[d + 1] - base[d], d < 1023)
+    if (b > nb && b < 1024u) scan[b] = n;
 }
 
 }  // namespace ahs

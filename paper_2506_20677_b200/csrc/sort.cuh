@@ -19,6 +19,7 @@
 #include "common.cuh"
 #include "features.cuh"
 #include "onesweep.cuh"
+#include "onesweep2.cuh"
 
 namespace ahs {
 
@@ -66,13 +67,25 @@ using OsPairs64V64M = Onesweep<true, 256, 11, kRankMasked, uint64_t, uint64_t>;
 #define K6V_PAIRS_M k_onesweep<true, kSortBlock, 5, 2, kRankMasked, uint32_t, uint64_t>
 #define K6WV_PAIRS_O k_onesweep<true, kSortBlockPairsO, 7, 2, kRankOrdered, uint64_t, uint64_t>
 #define K6WV_PAIRS_M k_onesweep<true, 256, 11, 2, kRankMasked, uint64_t, uint64_t>
+// K6 v2 (onesweep2.cuh: hot-digit ranking) for RADIX passes over 32-bit keys (ordered ranking):
+// the FSM sends low-entropy inputs there, whose digits are skewed (cfg3's last pass: 64 % one
+// digit).  On uniform digits it is 1-4 % slower than K6, so GENERAL keeps K6.
+using Os2Keys = Onesweep2<false, kSortBlock, 18, 8>;
+using Os2Pairs = Onesweep2<true, kSortBlockPairsO, 16, 8>;
+#define K6V2_KEYS k_onesweep2<false, kSortBlock, 18, 2, 8>
+#define K6V2_PAIRS k_onesweep2<true, kSortBlockPairsO, 16, 2, 8>
+// key-value COUNTING with 256 < k <= 1024 as ONE stable 10-bit scatter (opt-in: ahs_set_count_kv_single;
+// the default runs two 8-bit passes, measured faster: profiles/r02_summary.md)
+using Os2Pairs10 = Onesweep2<true, 256, 16, 10>;
+#define K6V2_PAIRS10 k_onesweep2<true, 256, 16, 2, 10>
 constexpr int kMinTile = 2560;  // smallest K6 tile: sizes the look-back status regions
 static_assert(kMinTile <= OsKeysM::kTile && kMinTile <= OsPairsM::kTile && kMinTile <= OsKeysO::kTile &&
                   kMinTile <= OsKeysOL::kTile &&
                   kMinTile <= OsPairsO::kTile && kMinTile <= OsKeys64M::kTile &&
                   kMinTile <= OsPairs64M::kTile && kMinTile <= OsKeys64O::kTile && kMinTile <= OsPairs64O::kTile &&
                   kMinTile <= OsPairsV64O::kTile && kMinTile <= OsPairsV64M::kTile &&
-                  kMinTile <= OsPairs64V64O::kTile && kMinTile <= OsPairs64V64M::kTile,
+                  kMinTile <= OsPairs64V64O::kTile && kMinTile <= OsPairs64V64M::kTile &&
+                  kMinTile <= Os2Keys::kTile && kMinTile <= Os2Pairs::kTile && kMinTile <= Os2Pairs10::kTile,
               "kMinTile");
 
 // ------------------------------------------------------------------ K5 ----

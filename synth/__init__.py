@@ -170,6 +170,17 @@ for _r in CFG5_R:
     CONFIGS[f"cfg5_r{_r}"] = ("u32", 1 << 28, (lambda r: (lambda n: cfg5(r, n)))(_r))
 
 
+def cfg7(n: int = 1 << 28, seed: int = 7):
+    """Key-value COUNTING beyond 8-bit digits (not a BASELINE config): (uint32 key
+    uniform in [0, 1000), uint32 value = index), 2^28 pairs: k = 1000 <= k_counting (Table II), so
+    the FSM picks COUNTING, and the stable scatter needs a 10-bit digit."""
+    keys = _chunked(seed, n, lambda x: uniform_below(x, 1000).astype(np.uint32), np.uint32)
+    return keys, np.arange(n, dtype=np.uint32)
+
+
+CONFIGS["cfg7kv"] = ("u32", 1 << 28, lambda n: cfg7(n))
+
+
 def _cfg6(n: int, kv: bool):
     keys = kmers(6, n)  # NEXT-3: genomic-like 30-mers, k = 4^30 (PAPER.md P:120), uint64
     return keys, (np.arange(n, dtype=np.uint32) if kv else None)

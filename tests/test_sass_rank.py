@@ -21,6 +21,7 @@ RE_FUNC = re.compile(r"Function : (\S+)")
 RE_ATOMS = re.compile(r"(?:@!?U?P\w+\s+)?(ATOMS\.[A-Z0-9.]+)\s+(\w+),\s*\[([^\]]*)\],?\s*([^;]*);")
 RE_K6 = re.compile(r"_ZN3ahs10k_onesweepILb(\d)ELi(\d+)ELi(\d+)ELi(\d+)ELi(\d)E")
 RE_K9R = re.compile(r"_ZN3ahs11k_seg_radixI[jm]Lb(\d)ELi(\d+)ELi(\d+)ELb(\d)E")
+RE_K6V2 = re.compile(r"_ZN3ahs11k_onesweep2I")  # K6 v2 (onesweep2.cuh): ordered ranking only
 
 
 @pytest.fixture(scope="module")
@@ -57,6 +58,8 @@ def ordered_kernels(funcs):
         m = RE_K9R.search(f)
         if m and m.group(4) == "1":
             out[f] = insts
+        if RE_K6V2.search(f):
+            out[f] = insts
     return out
 
 
@@ -72,6 +75,7 @@ def test_ordered_rank_sites_match_the_selftest_form(sass):
     # every ordered instantiation the library ships: K6 32/64-bit keys, pairs, 64-bit values; K9r
     assert sum(1 for f in ordered if "k_onesweep" in f) >= 6
     assert sum(1 for f in ordered if "k_seg_radix" in f) >= 8
+    assert sum(1 for f in ordered if "k_onesweep2" in f) >= 2  # RADIX keys and pairs
     for f, insts in ordered.items():
         ret = returning(insts)
         assert ret, f"{f}: no returning shared atomic (rank site) found"

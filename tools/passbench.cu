@@ -85,7 +85,7 @@ static bool g_mid = false;      // env PB_MID=1: run as a middle pass of a chain
 template <bool KV>
 float run_kern(const Bufs &B, uint32_t n, uint32_t shift, int sms, int reps, bool check,
                const std::vector<uint32_t> &hk, const std::vector<uint32_t> &hbase, const void *kern, size_t smem,
-               int tile, int block, const char *name)
+               int tile, int block, const char *name, uint32_t bins = 256)
 {
     if (g_only >= 0 && g_idx++ != g_only) return 0.f;
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -100,7 +100,7 @@ float run_kern(const Bufs &B, uint32_t n, uint32_t shift, int sms, int reps, boo
     std::vector<float> ts;
     for (int r = 0; r < reps + 2; r++) {
         if (!g_noflush) k_flush<<<sms * 4, 512>>>(B.flush, B.flush_n);
-        CK(cudaMemsetAsync(B.status, 0, (size_t)tiles * 256 * 4));
+        CK(cudaMemsetAsync(B.status, 0, (size_t)tiles * bins * 4));
         CK(cudaMemsetAsync(B.ticket, 0, 4));
         CK(cudaEventRecord(a));
         PassArgs pa{};
@@ -172,7 +172,7 @@ float run_kern(const Bufs &B, uint32_t n, uint32_t shift, int sms, int reps, boo
         CK(cudaMemcpy(got.data(), B.ko, n * 4ull, cudaMemcpyDeviceToHost));
         if (KV) CK(cudaMemcpy(gotv.data(), B.vo, n * 4ull, cudaMemcpyDeviceToHost));
         for (uint32_t i = 0; i < n && ok; i++) {
-            const uint32_t p = pos[(hk[i] >> shift) & 255u]++;
+            const uint32_t p = pos[(hk[i] >> shift) & (bins - 1)]++;
             if (got[p] != hk[i] || (KV && gotv[p] != i)) {
                 printf("  MISMATCH at out %u (in %u): got %08x want %08x\n", p, i, got[p], hk[i]);
                 ok = false;
@@ -210,15 +210,17 @@ float run_p(const Bufs &B, uint32_t n, uint32_t shift, int sms, int reps, bool c
                         (const void *)k_onesweep_p<KV, NW, ITEMS, LBW, W>, C::kSmem, C::kTile, C::kBlock, nm);
 }
 
-template <bool KV, int BLOCK, int ITEMS>
+template <bool KV, int BLOCK, int ITEMS, int BITS = 8, int HOT = kHotDefault>
 float run2(const Bufs &B, uint32_t n, uint32_t shift, int sms, int reps, bool check,
            const std::vector<uint32_t> &hk, const std::vector<uint32_t> &hbase)
 {
-    using C = Onesweep2<KV, BLOCK, ITEMS>;
+    using C = Onesweep2<KV, BLOCK, ITEMS, BITS, uint32_t, uint32_t, HOT>;
     char nm[96];
-    snprintf(nm, sizeof nm, "v2<%s,B%d,I%d>", KV ? "kv" : "k", BLOCK, ITEMS);
-    return run_kern<KV>(B, n, shift, sms, reps, check, hk, hbase, (const void *)k_onesweep2<KV, BLOCK, ITEMS, (BLOCK == 256 ? 4 : 2)>,
-                        C::kSmem, C::kTile, BLOCK, nm);
+    snprintf(nm, sizeof nm, "v2<%s,B%d,I%d,b%d,hot%x>", KV ? "kv" : "k", BLOCK, ITEMS, BITS, HOT);
+    return run_kern<KV>(B, n, shift, sms, reps, check, hk, hbase,
+                        (const void *)k_onesweep2<KV, BLOCK, ITEMS, (BLOCK == 256 && BITS == 8 ? 4 : 2), BITS,
+                                                  uint32_t, uint32_t, HOT>,
+                        C::kSmem, C::kTile, BLOCK, nm, 1u << BITS);
 }
 
 template <bool KV>
@@ -273,8 +275,8 @@ int main(int argc, char **argv)
     CK(cudaMalloc(&B.v, n * 4ull));
     CK(cudaMalloc(&B.ko, n * 4ull));
     CK(cudaMalloc(&B.vo, n * 4ull));
-    CK(cudaMalloc(&B.bb, 256 * 4));
-    CK(cudaMalloc(&B.status, ((size_t)n / 1024 + 16) * 256 * 4));
+    CK(cudaMalloc(&B.bb, 2048 * 4));
+    CK(cudaMalloc(&B.status, ((size_t)n / 1024 + 16) * 2048 * 4));
     CK(cudaMalloc(&B.ticket, 64));
     B.flush_n = 64u << 20;  // 256 MiB
     CK(cudaMalloc(&B.flush, B.flush_n * 4));
@@ -298,6 +300,14 @@ int main(int argc, char **argv)
         shifts = {16u, 24u};
     }
     printf("n = %u, dist %d, %d SMs\n", n, dist, sms);
+    if (getenv("PB_SHIFTS")) {  // e.g. PB_SHIFTS=24 or 16,24
+        shifts.clear();
+        for (const char *q = getenv("PB_SHIFTS"); *q;) {
+            shifts.push_back((uint32_t)strtoul(q, (char **)&q, 10));
+            if (*q == ',') q++;
+        }
+    }
+    if (getenv("PB_SKIP8")) shifts.clear();
     for (uint32_t shift : shifts)
         if (g_only < 0 || shift == shifts[0]) {
         std::vector<uint32_t> hist(256, 0), base(256);
@@ -312,14 +322,39 @@ int main(int argc, char **argv)
         printf("digit shift %u (max digit share %.3f)\n", shift, (double)mx / n);
         g_idx = 0;
         run_cfg<false, 512, 18, 2, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
-        run2<false, 512, 18>(B, n, shift, sms, reps, true, hk, base);
-        run2<false, 512, 20>(B, n, shift, sms, reps, true, hk, base);
-        run2<false, 256, 16>(B, n, shift, sms, reps, true, hk, base);
-        run2<false, 256, 20>(B, n, shift, sms, reps, true, hk, base);
-        run2<false, 384, 16>(B, n, shift, sms, reps, true, hk, base);
+        run2<false, 512, 18, 8, 0>(B, n, shift, sms, reps, true, hk, base);
+        run2<false, 512, 18, 8, hotcfg(1, 3, false)>(B, n, shift, sms, reps, true, hk, base);
+        run2<false, 512, 18, 8, hotcfg(4, 3, false)>(B, n, shift, sms, reps, true, hk, base);
+        run2<false, 512, 18, 8, hotcfg(2, 4, false)>(B, n, shift, sms, reps, true, hk, base);
         run_cfg<true, 384, 16, 2, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
-        run2<true, 384, 16>(B, n, shift, sms, reps, true, hk, base);
-        run2<true, 256, 16>(B, n, shift, sms, reps, true, hk, base);
+        run2<true, 384, 16, 8, hotcfg(1, 3, false)>(B, n, shift, sms, reps, true, hk, base);
+        run2<true, 384, 16, 8, hotcfg(4, 3, false)>(B, n, shift, sms, reps, true, hk, base);
+    }
+    // wider digits (low BITS bits): KV counting with k <= 1024 (10 bits), the 11-bit experiment
+    if (getenv("PB_WIDE")) {
+        for (int bits : {10, 11}) {
+            const uint32_t bins = 1u << bits;
+            std::vector<uint32_t> hist(bins, 0), base(bins);
+            for (uint32_t i = 0; i < n; i++) hist[hk[i] & (bins - 1)]++;
+            uint32_t run = 0;
+            for (uint32_t d = 0; d < bins; d++) {
+                base[d] = run;
+                run += hist[d];
+            }
+            CK(cudaMemcpy(B.bb, base.data(), bins * 4, cudaMemcpyHostToDevice));
+            printf("digit bits %d, shift 0\n", bits);
+            g_idx = 0;
+            if (bits == 10) {
+                run2<false, 512, 16, 10>(B, n, 0, sms, reps, true, hk, base);
+                run2<true, 512, 8, 10>(B, n, 0, sms, reps, true, hk, base);
+                run2<true, 512, 10, 10>(B, n, 0, sms, reps, true, hk, base);
+                run2<true, 256, 16, 10>(B, n, 0, sms, reps, true, hk, base);
+            } else {
+                run2<false, 512, 16, 11>(B, n, 0, sms, reps, true, hk, base);
+                run2<false, 512, 12, 11>(B, n, 0, sms, reps, true, hk, base);
+                run2<false, 512, 24, 11>(B, n, 0, sms, reps, true, hk, base);
+            }
+        }
     }
     if (cub) {
         run_cub<false>(B, n, 0, 32, sms, reps);
