@@ -243,8 +243,8 @@ AHS_API int ahs_entropy_sorted_dtype(const void *d_keys, uint64_t n, int32_t dty
  * num_segments + 1 non-decreasing offsets <= n; segments need not start at 0),
  * each sorted ascending and stably, values travelling with their keys; keys
  * outside every segment are not touched.  max_segment: an upper bound on the
- * segment lengths, <= 2048 (ERANGE above); <= 32 runs one thread per segment
- * with Listing 1's insertion sort in shared memory, otherwise 32 .. 128
+ * segment lengths, <= 8192 (ERANGE above); <= 32 runs one thread per segment
+ * with Listing 1's insertion sort in shared memory, otherwise 32 .. 512
  * threads per segment (a stable LSD radix sort in shared memory, 8-bit digits,
  * digits all keys of the segment share skipped).  Out may alias in.
  * d_bad (device uint32, required) receives the number of segments found longer
@@ -330,6 +330,28 @@ AHS_API int ahs_set_skip_trivial(int on);
  * run.  ahs_set_count_kv_single(0/1) sets it (any other value queries);
  * returns the setting.  ahs_sort_passes() reports 1 for such inputs when on. */
 AHS_API int ahs_set_count_kv_single(int on);
+
+/* Bucket-local GENERAL plan (the paper's GENERAL branch, QuickSort in
+ * Listing 4, served by radix passes, R14).  For 32-bit keys whose
+ * feature bins (key - min) >> s are coarser than single values (s > 0), with
+ * 4-byte or no values and out of place: two stable LSD passes over the two bytes
+ * of the bin make every bin a contiguous bucket (its boundaries are the exclusive
+ * scan of the feature histogram), then K10 sorts each bucket in shared memory by
+ * its low s bits (the K9 segment sort, one CTA per bucket, digits a bucket shares
+ * skipped) -- three reads and writes of the keys instead of four.  The library
+ * picks K10's capacity from the mean bin size (up to 8192 keys); K5 falls back to
+ * the four full-width passes on the device when a bin is larger.  Default off
+ * (environment AHS_BUCKET_LOCAL=1 turns it on): on B200 the in-shared-memory
+ * bucket pass measured slower than the two digit passes it replaces (cfg4a sort
+ * 888 vs 801 us, cfg5 r=32 pairs 6.57 vs 4.99 ms; profiles/r02_summary.md).
+ * Output identical.
+ * ahs_set_bucket_local(0/1) sets it (any other value queries); returns the setting.
+ * ahs_sort_plan() reads the plan of the last ahs_sort on d_tmp (synchronizes):
+ * executed digit passes and whether the bucket-local pass ran.
+ * ahs_sort_executed_passes() counts the bucket-local pass as one pass. */
+AHS_API int ahs_set_bucket_local(int on);
+AHS_API int ahs_sort_plan(const void *d_tmp, size_t tmp_bytes, int *digit_passes, int *bucket_local,
+                          void *stream);
 AHS_API int ahs_sort_executed_passes(const void *d_tmp, size_t tmp_bytes, uint64_t n, int has_vals,
                                      void *stream);
 

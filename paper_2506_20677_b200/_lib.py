@@ -99,6 +99,8 @@ def lib():
             "ahs_rank_mode": ([C.c_int], C.c_int),
             "ahs_set_skip_trivial": ([C.c_int], C.c_int),
             "ahs_set_count_kv_single": ([C.c_int], C.c_int),
+            "ahs_set_bucket_local": ([C.c_int], C.c_int),
+            "ahs_sort_plan": ([C.c_void_p, C.c_size_t, C.POINTER(C.c_int), C.POINTER(C.c_int), C.c_void_p], C.c_int),
             "ahs_entropy_sorted": ([vp, u64, vp, sz, C.POINTER(C.c_double), vp], C.c_int),
             "ahs_sort_executed_passes": ([vp, sz, u64, C.c_int, vp], C.c_int),
             "ahs_lane_order_ok": ([], C.c_int),
@@ -185,6 +187,19 @@ def ahs_set_count_kv_single(on: int = -1) -> int:
     """Key-value COUNTING with 256 < k <= 1024 as one 10-bit stable scatter (1) or two 8-bit passes
     (0, default); -1 queries.  Returns the setting."""
     return lib().ahs_set_count_kv_single(on)
+
+
+def ahs_set_bucket_local(on: int = -1) -> int:
+    """The bucket-local GENERAL plan on (1, default) or off (0); -1 queries.  Returns the setting."""
+    return lib().ahs_set_bucket_local(on)
+
+
+def ahs_sort_plan(ws: "Workspace", stream=None) -> tuple[int, int]:
+    """(executed digit passes, bucket-local pass ran) of the last ahs_sort with this workspace."""
+    p, b = C.c_int(), C.c_int()
+    _check(lib().ahs_sort_plan(_dev_ptr(ws.tmp), ws.tmp_bytes, C.byref(p), C.byref(b), _stream(stream)),
+           "ahs_sort_plan")
+    return p.value, b.value
 
 
 def ahs_sort_executed_passes(ws: "Workspace", stream=None) -> int:

@@ -250,12 +250,13 @@ enum KernelId {
     KID_HIST_SCAN,
     KID_DIGIT_COUNT,
     KID_SEG_SORT,
+    KID_BUCKET_SORT,
     KID_COUNT
 };
 const char *kKernelNames[KID_COUNT] = {"feat_reduce", "feat_hist",   "feat_finalize",
                                        "radix_hist",  "onesweep",    "onesweep_kv",
                                        "count_fill",  "count_scatter_kv", "entropy_sorted",
-                                       "hist_scan",   "digit_count64", "seg_sort"};
+                                       "hist_scan",   "digit_count64", "seg_sort", "bucket_sort"};
 
 std::atomic<uint64_t> g_launches{0};
 // NEXT-1 trivial-pass skipping (default on; AHS_SKIP_TRIVIAL=0 or ahs_set_skip_trivial(0) turn it off)
@@ -273,6 +274,12 @@ std::atomic<bool> g_pdl{[] {
 // passes (default off; AHS_COUNT_KV_SINGLE=1 or ahs_set_count_kv_single(1))
 std::atomic<bool> g_count_kv_single{[] {
     const char *e = std::getenv("AHS_COUNT_KV_SINGLE");
+    return e && e[0] == '1';
+}()};
+// bucket-local GENERAL plan (sort.cuh; default off: measured slower than the four passes on B200,
+// profiles/r02_summary.md; AHS_BUCKET_LOCAL=1 or ahs_set_bucket_local(1) turn it on)
+std::atomic<bool> g_bucket_local{[] {
+    const char *e = std::getenv("AHS_BUCKET_LOCAL");
     return e && e[0] == '1';
 }()};
 // K6 v2 for RADIX passes (default on; AHS_K6V2=0 turns it off: K6 everywhere)
@@ -381,6 +388,8 @@ struct TmpLayout {
 };
 constexpr int kTicketPlan = 16;   // plan offset in the ticket block (words)
 constexpr int kTicketFault = 32;  // K6 look-back gave up (onesweep.cuh kLookbackSpinLimit): AHS_ECUDA
+constexpr int kTicketMaxBin = kMaxPasses + 1;  // K5: largest feature-bin count (bucket-local plan)
+constexpr int kTicketSegBad = 33;              // K10: buckets above the segment sort's capacity (never, by K5)
 TmpLayout tmp_layout(uint64_t n, int has_vals, size_t key_bytes = 4, size_t val_bytes = 4)
 {
     TmpLayout L;
@@ -536,29 +545,51 @@ int ahs_set_count_kv_single(int on)
     return on;
 }
 
-int ahs_sort_executed_passes(const void *d_tmp, size_t tmp_bytes, uint64_t n, int has_vals, void *stream)
+// the plan block of the last ahs_sort on d_tmp (synchronizes): executed digit passes, bucket-local
+// flag; AHS_ECUDA when a look-back gave up; -1 passes when that sort wrote no plan
+static int read_plan(const void *d_tmp, size_t tmp_bytes, int *passes, int *bl, void *stream)
 {
-    (void)n;
-    (void)has_vals;
     const TmpLayout TL = tmp_layout(0, 0);  // the ctrl block does not depend on n or the key width
     if (!d_tmp || tmp_bytes < TL.status) return AHS_EINVAL;
-    uint32_t w[kMaxPasses + 2];
+    uint32_t w[kPlanBL + 1];
+    uint32_t fault = 0;
     cudaStream_t s = (cudaStream_t)stream;
     if (cudaMemcpyAsync(w, (const char *)d_tmp + TL.ticket + kTicketPlan * 4, sizeof(w), cudaMemcpyDeviceToHost,
                         s) != cudaSuccess ||
-        cudaStreamSynchronize(s) != cudaSuccess) {
-        cudaGetLastError();
-        return AHS_ECUDA;
-    }
-    uint32_t fault = 0;
-    if (cudaMemcpyAsync(&fault, (const char *)d_tmp + TL.ticket + kTicketFault * 4, 4, cudaMemcpyDeviceToHost, s) !=
+        cudaMemcpyAsync(&fault, (const char *)d_tmp + TL.ticket + kTicketFault * 4, 4, cudaMemcpyDeviceToHost, s) !=
             cudaSuccess ||
         cudaStreamSynchronize(s) != cudaSuccess) {
         cudaGetLastError();
         return AHS_ECUDA;
     }
     if (fault) return AHS_ECUDA;
-    return w[kMaxPasses + 1] == kPlanMagic ? (int)w[kMaxPasses] : -1;
+    const bool has = w[kMaxPasses + 1] == kPlanMagic;
+    *passes = has ? (int)w[kMaxPasses] : -1;
+    *bl = has && w[kPlanBL] ? 1 : 0;
+    return AHS_OK;
+}
+
+int ahs_sort_executed_passes(const void *d_tmp, size_t tmp_bytes, uint64_t n, int has_vals, void *stream)
+{
+    (void)n;
+    (void)has_vals;
+    int p = -1, bl = 0;
+    const int rc = read_plan(d_tmp, tmp_bytes, &p, &bl, stream);
+    if (rc) return rc;
+    return p < 0 ? p : p + bl;  // the bucket-local pass reads and writes every key once, like a digit pass
+}
+
+int ahs_sort_plan(const void *d_tmp, size_t tmp_bytes, int *digit_passes, int *bucket_local, void *stream)
+{
+    if (!digit_passes || !bucket_local) return AHS_EINVAL;
+    return read_plan(d_tmp, tmp_bytes, digit_passes, bucket_local, stream);
+}
+
+int ahs_set_bucket_local(int on)
+{
+    if (on != 0 && on != 1) return g_bucket_local.load() ? 1 : 0;
+    g_bucket_local.store(on == 1);
+    return on;
 }
 
 int ahs_lane_order_ok(void)
@@ -825,6 +856,12 @@ int ahs_select(const ahs_features_t *f, const ahs_thresholds_t *th, int32_t *str
 
 namespace {
 // The digit passes of ahs_sort for key type K (uint32_t, or uint64_t: NEXT-3).
+// the K9 segment sort launcher (defined with ahs_sort_segments below), used by the bucket-local plan
+template <typename K, bool KV>
+cudaError_t seg_launch(const void *kin, const uint32_t *vin, void *kout, uint32_t *vout, uint64_t n,
+                       const uint32_t *offsets, uint32_t nseg, uint32_t max_segment, K flip, uint32_t *bad,
+                       bool ord, cudaStream_t s, const uint32_t *gate = nullptr);
+
 template <typename K, typename V>
 int sort_impl(const K *kin, const V *d_vals_in, K *kout, V *d_vals_out, uint64_t n, int32_t strategy,
               const ahs_features_t *feat, void *d_ws, size_t ws_bytes, void *d_tmp, size_t tmp_bytes,
@@ -956,6 +993,24 @@ int sort_impl(const K *kin, const V *d_vals_in, K *kout, V *d_vals_out, uint64_t
 
     if (!d_ws || ws_bytes < WL.total) return AHS_ENOSPACE;
     uint32_t *plan = tickets + kTicketPlan;
+    // bucket-local plan candidate (GENERAL over 32-bit keys with <= 32-bit values, buckets of the
+    // feature histogram coarser than single values): two passes over the bin digits + K10.  K5 takes
+    // it when the largest bin fits the K10 capacity chosen here from the mean bin size.
+    uint32_t bl_cap = 0;
+    const uint32_t *bl_offsets = nullptr;
+    if (strategy == AHS_GENERAL && W == 0 && VK <= 1 && !inplace && feat->shift > 0 && passes == 4 &&
+        g_bucket_local.load(std::memory_order_relaxed)) {
+        const double mean = (double)n / (double)feat->nbins;
+        for (uint32_t c : {256u, 512u, 1024u, 2048u, 4096u, 8192u})
+            if (1.25 * mean + 32.0 <= (double)c) {
+                bl_cap = c;
+                break;
+            }
+        if (bl_cap) {
+            bl_offsets = hist_scan(d_ws, feat, s);  // bucket boundaries: scan[b] .. scan[b + 1]
+            if (!bl_offsets) return AHS_ECUDA;
+        }
+    }
     const uint32_t *bases;
     if (count_kv) {
         bases = hist_scan(d_ws, feat, s);
@@ -982,7 +1037,7 @@ int sort_impl(const K *kin, const V *d_vals_in, K *kout, V *d_vals_out, uint64_t
             launch_k(k_radix_hist<kRHBlock, kWide ? 8 : 4>, dim3((unsigned)g5), dim3(kRHBlock), 0, s, n,
                      (uint32_t)umin, passes, fhist, feat->nbins, feat->shift, (const DevFeatures *)(wsc + WL.feat),
                      (const uint32_t *)(wsc + WL.byte0), (const uint32_t *)(wsc + WL.digit1), dhist, bucket,
-                     tickets + kMaxPasses, plan, skip ? 1 : 0);
+                     tickets + kMaxPasses, plan, skip ? 1 : 0, bl_cap, tickets + kTicketMaxBin);
         });
         if (e != cudaSuccess) return AHS_ECUDA;
         bases = bucket;
@@ -1018,6 +1073,23 @@ int sort_impl(const K *kin, const V *d_vals_in, K *kout, V *d_vals_out, uint64_t
             cudaLaunchKernelExC(&cfg, k6, args);
         });
         if (e != cudaSuccess) return AHS_ECUDA;
+    }
+    if (bl_cap) {
+        // K10: the bucket-local pass (K9's in-shared-memory stable radix sort, one CTA per bucket, in
+        // place on the output; digits all keys of a bucket share are skipped); returns at once when K5
+        // chose the classic plan
+        cudaError_t le = cudaSuccess;
+        const cudaError_t e = launch(KID_BUCKET_SORT, s, [&] {
+            const bool ord = di->rank_mode == kRankOrdered;
+            if (kv)
+                le = seg_launch<K, true>(kout, (const uint32_t *)d_vals_out, kout, (uint32_t *)d_vals_out, n,
+                                         bl_offsets, feat->nbins, bl_cap, flip, tickets + kTicketSegBad, ord, s,
+                                         plan + kPlanBL);
+            else
+                le = seg_launch<K, false>(kout, nullptr, kout, nullptr, n, bl_offsets, feat->nbins, bl_cap, flip,
+                                          tickets + kTicketSegBad, ord, s, plan + kPlanBL);
+        });
+        if (e != cudaSuccess || le != cudaSuccess) return AHS_ECUDA;
     }
     return AHS_OK;
 }
@@ -1240,20 +1312,20 @@ cudaError_t seg_small(const void *kin, const uint32_t *vin, void *kout, uint32_t
 template <typename K, bool KV, int GROUP, int CAP, bool ORD>
 cudaError_t seg_radix(const void *kin, const uint32_t *vin, void *kout, uint32_t *vout, uint64_t n,
                       const uint32_t *offsets, uint32_t nseg, uint32_t max_segment, K flip, uint32_t *bad,
-                      cudaStream_t s)
+                      cudaStream_t s, const uint32_t *gate = nullptr)
 {
     constexpr size_t smem = seg_radix_smem<K, KV, GROUP, CAP>();
     const cudaError_t ae = opt_in_smem((const void *)k_seg_radix<K, KV, GROUP, CAP, ORD>, smem);
     if (ae != cudaSuccess) return ae;
     return launch_k(k_seg_radix<K, KV, GROUP, CAP, ORD>, dim3(nseg), dim3(GROUP), smem,
-                    s, (const K *)kin, vin, (K *)kout, vout, offsets, nseg, n, flip, max_segment, bad);
+                    s, (const K *)kin, vin, (K *)kout, vout, offsets, nseg, n, flip, max_segment, bad, gate);
 }
 
 // register network length / CTA size from the declared maximum segment
 template <typename K, bool KV>
 cudaError_t seg_launch(const void *kin, const uint32_t *vin, void *kout, uint32_t *vout, uint64_t n,
                        const uint32_t *offsets, uint32_t nseg, uint32_t max_segment, K flip, uint32_t *bad,
-                       bool ord, cudaStream_t s)
+                       bool ord, cudaStream_t s, const uint32_t *gate)
 {
 #define AHS_SEG_ARGS kin, vin, kout, vout, n, offsets, nseg, max_segment, flip, bad, s
     if (max_segment <= 8) return seg_small<K, KV, 8>(AHS_SEG_ARGS);
@@ -1264,15 +1336,19 @@ cudaError_t seg_launch(const void *kin, const uint32_t *vin, void *kout, uint32_
     // K9r: threads per segment from the declared maximum (16 keys per thread, one
     // warp up to 512 keys); the ordered ranking when the device passed its self-test
     if (ord) {
-        if (max_segment <= 256) return seg_radix<K, KV, 32, 256, true>(AHS_SEG_ARGS);
-        if (max_segment <= 512) return seg_radix<K, KV, 32, 512, true>(AHS_SEG_ARGS);
-        if (max_segment <= 1024) return seg_radix<K, KV, 64, 1024, true>(AHS_SEG_ARGS);
-        return seg_radix<K, KV, 128, 2048, true>(AHS_SEG_ARGS);
+        if (max_segment <= 256) return seg_radix<K, KV, 32, 256, true>(AHS_SEG_ARGS, gate);
+        if (max_segment <= 512) return seg_radix<K, KV, 32, 512, true>(AHS_SEG_ARGS, gate);
+        if (max_segment <= 1024) return seg_radix<K, KV, 64, 1024, true>(AHS_SEG_ARGS, gate);
+        if (max_segment <= 2048) return seg_radix<K, KV, 128, 2048, true>(AHS_SEG_ARGS, gate);
+        if (max_segment <= 4096) return seg_radix<K, KV, 256, 4096, true>(AHS_SEG_ARGS, gate);
+        return seg_radix<K, KV, 512, 8192, true>(AHS_SEG_ARGS, gate);
     }
-    if (max_segment <= 256) return seg_radix<K, KV, 32, 256, false>(AHS_SEG_ARGS);
-    if (max_segment <= 512) return seg_radix<K, KV, 32, 512, false>(AHS_SEG_ARGS);
-    if (max_segment <= 1024) return seg_radix<K, KV, 64, 1024, false>(AHS_SEG_ARGS);
-    return seg_radix<K, KV, 128, 2048, false>(AHS_SEG_ARGS);
+    if (max_segment <= 256) return seg_radix<K, KV, 32, 256, false>(AHS_SEG_ARGS, gate);
+    if (max_segment <= 512) return seg_radix<K, KV, 32, 512, false>(AHS_SEG_ARGS, gate);
+    if (max_segment <= 1024) return seg_radix<K, KV, 64, 1024, false>(AHS_SEG_ARGS, gate);
+    if (max_segment <= 2048) return seg_radix<K, KV, 128, 2048, false>(AHS_SEG_ARGS, gate);
+    if (max_segment <= 4096) return seg_radix<K, KV, 256, 4096, false>(AHS_SEG_ARGS, gate);
+    return seg_radix<K, KV, 512, 8192, false>(AHS_SEG_ARGS, gate);
 #undef AHS_SEG_ARGS
 }
 }  // namespace

@@ -73,7 +73,8 @@ __device__ unsigned long long g_lb_stats[4];  // tiles, rounds, empty rounds, st
 
 __device__ __forceinline__ uint32_t digit8(uint32_t v, uint32_t shift)
 {
-    return __byte_perm(v, 0u, 0x4440u | (shift >> 3));
+    // any bit offset: the bucket-local GENERAL plan runs digits at the feature-bin shift
+    return (v >> shift) & 255u;
 }
 
 // 64-bit keys (NEXT-3): digit at bit `shift` (a multiple of 8, < 64)
@@ -124,6 +125,9 @@ struct Onesweep {
     static constexpr size_t kSmem = kOffAux + (size_t)(4 * kBins + 8) * 4;
 };
 
+// Device pass plan word (K5): kPassSkip, or (digit shift << 16) | (executed index << 8) | executed count.
+constexpr uint32_t plan_word(uint32_t shift, uint32_t e, uint32_t m) { return (shift << 16) | (e << 8) | m; }
+
 // One digit pass of a chain of `npasses` LSD passes.  Buffers: the chain reads
 // `keys_in` (first executed pass, input transform v = (key ^ flip) - sub) and
 // ping-pongs between `keys_tmp` and `keys_out` so that the last executed pass
@@ -170,13 +174,14 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(const PassArgsT<K, V> 
     // is cleared for the pass after this one (also when this pass is skipped)
     for (uint32_t i = blockIdx.x * BLOCK + threadIdx.x; i < a.clear_words; i += gridDim.x * BLOCK)
         a.status_clear[i] = 0u;
-    // ---- this pass's place in the chain
-    uint32_t e = a.pass, m = a.npasses;
+    // ---- this pass's place in the chain (and its digit's bit offset, from the plan when there is one)
+    uint32_t e = a.pass, m = a.npasses, shift = a.shift;
     if (a.plan) {
         const uint32_t w = a.plan[a.pass];
-        if (w == kPassSkip) return;  // constant digit: identity
-        e = w >> 8;
+        if (w == kPassSkip) return;  // constant digit (or a pass the plan does not use): identity
+        e = (w >> 8) & 255u;
         m = w & 255u;
+        shift = w >> 16;
     }
     const bool first = e == 0, last = e + 1 == m;
     const bool to_out = ((m - 1 - e) & 1u) == 0;        // destination parity: the last lands in out
@@ -185,7 +190,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(const PassArgsT<K, V> 
     const V *__restrict__ vals_in = first ? a.vals_in : (from_out ? a.vals_out : a.vals_tmp);
     K *__restrict__ keys_out = to_out ? a.keys_out : a.keys_tmp;
     V *__restrict__ vals_out = to_out ? a.vals_out : a.vals_tmp;
-    const uint32_t n = a.n, shift = a.shift;
+    const uint32_t n = a.n;
     const K in_flip = first ? a.flip : K(0), in_sub = first ? a.sub : K(0);
     const K out_flip = last ? a.flip : K(0), out_add = last ? a.sub : K(0);
     const uint32_t *__restrict__ bucket_base = a.bucket_base;

@@ -115,14 +115,14 @@ __device__ __forceinline__ void st_status(uint32_t *p, const uint32_t (&v)[DPT])
 template <bool KV, int BLOCK, int ITEMS, int BITS, bool TIN, bool TOUT, typename K, typename V, int HOTCFG>
 __device__ __forceinline__ void onesweep2_body(const PassArgsT<K, V> &a, const K *__restrict__ keys_in,
                                                const V *__restrict__ vals_in, K *__restrict__ keys_out,
-                                               V *__restrict__ vals_out)
+                                               V *__restrict__ vals_out, const uint32_t shift)
 {
     using C = Onesweep2<KV, BLOCK, ITEMS, BITS, K, V, HOTCFG>;
     constexpr int TILE = C::kTile, SEG = C::kSeg, NWARP = C::kWarps, BINS = C::kBins, DPT = C::kDPT,
                   NT = C::kNT, TW = C::kTabWords, NHOT = C::kHot;
     constexpr bool PACKED = C::kPacked;
     constexpr uint32_t KB = sizeof(K), VB = sizeof(V);
-    const uint32_t n = a.n, shift = a.shift;
+    const uint32_t n = a.n;
     const K flip = a.flip, subv = a.sub;
     const uint32_t *__restrict__ bucket_base = a.bucket_base;
     uint32_t *__restrict__ status = a.status;
@@ -145,12 +145,7 @@ __device__ __forceinline__ void onesweep2_body(const PassArgsT<K, V> &a, const K
     const uint32_t ntiles = (n + TILE - 1) / TILE;
     const uint32_t ltj = lanemask_lt();
     uint32_t *const cw = s_cnt + warp * TW;  // this warp's digit table
-    const uint32_t dsel = 0x4440u | (shift >> 3);
-
-    auto digit = [&](K v) -> uint32_t {
-        if constexpr (BITS == 8 && sizeof(K) == 4) return __byte_perm((uint32_t)v, 0u, dsel);
-        else return (uint32_t)(v >> shift) & (uint32_t)(BINS - 1);
-    };
+    auto digit = [&](K v) -> uint32_t { return (uint32_t)(v >> shift) & (uint32_t)(BINS - 1); };
     // per-warp table: 32-bit counters (8-bit digits) or two 16-bit counters per word
     auto t_inc = [&](uint32_t d) {
         if constexpr (PACKED) atomicAdd(&cw[d >> 1], 1u << ((d & 1u) << 4));
@@ -564,12 +559,13 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep2(const PassArgsT<K, V>
     pdl_begin();
     for (uint32_t i = blockIdx.x * BLOCK + threadIdx.x; i < a.clear_words; i += gridDim.x * BLOCK)
         a.status_clear[i] = 0u;
-    uint32_t e = a.pass, m = a.npasses;
+    uint32_t e = a.pass, m = a.npasses, shift = a.shift;
     if (a.plan) {
         const uint32_t w = a.plan[a.pass];
         if (w == kPassSkip) return;
-        e = w >> 8;
+        e = (w >> 8) & 255u;
         m = w & 255u;
+        shift = w >> 16;
     }
     const bool first = e == 0, last = e + 1 == m;
     const bool to_out = ((m - 1 - e) & 1u) == 0;
@@ -582,11 +578,11 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep2(const PassArgsT<K, V>
     const bool tin = first && (a.flip != K(0) || a.sub != K(0));
     const bool tout = last && (a.flip != K(0) || a.sub != K(0));
     if (tin) {
-        if (tout) onesweep2_body<KV, BLOCK, ITEMS, BITS, true, true, K, V, HOTCFG>(a, keys_in, vals_in, keys_out, vals_out);
-        else onesweep2_body<KV, BLOCK, ITEMS, BITS, true, false, K, V, HOTCFG>(a, keys_in, vals_in, keys_out, vals_out);
+        if (tout) onesweep2_body<KV, BLOCK, ITEMS, BITS, true, true, K, V, HOTCFG>(a, keys_in, vals_in, keys_out, vals_out, shift);
+        else onesweep2_body<KV, BLOCK, ITEMS, BITS, true, false, K, V, HOTCFG>(a, keys_in, vals_in, keys_out, vals_out, shift);
     } else {
-        if (tout) onesweep2_body<KV, BLOCK, ITEMS, BITS, false, true, K, V, HOTCFG>(a, keys_in, vals_in, keys_out, vals_out);
-        else onesweep2_body<KV, BLOCK, ITEMS, BITS, false, false, K, V, HOTCFG>(a, keys_in, vals_in, keys_out, vals_out);
+        if (tout) onesweep2_body<KV, BLOCK, ITEMS, BITS, false, true, K, V, HOTCFG>(a, keys_in, vals_in, keys_out, vals_out, shift);
+        else onesweep2_body<KV, BLOCK, ITEMS, BITS, false, false, K, V, HOTCFG>(a, keys_in, vals_in, keys_out, vals_out, shift);
     }
 }
 

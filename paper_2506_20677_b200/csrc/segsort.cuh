@@ -23,7 +23,7 @@ namespace ahs {
 
 constexpr int kSegSmallBlock = 256;
 constexpr int kSegSmallMax = 32;
-constexpr int kSegMedMax = 2048;
+constexpr int kSegMedMax = 8192;  // K9r capacity (512 threads); also the bucket-local GENERAL pass, K10
 
 template <typename K, bool KV>
 constexpr size_t seg_small_smem()
@@ -162,15 +162,17 @@ constexpr size_t seg_radix_smem()  // per segment group
 
 // a CTA of GROUP threads sorts one segment (one-warp groups use warp barriers;
 // packing several one-warp segments per CTA measured no faster)
+// gate (nullable): the launch does nothing unless *gate != 0 (the bucket-local plan word of K5)
 template <typename K, bool KV, int GROUP, int CAP, bool ORD>
 __global__ void __launch_bounds__(GROUP)
     k_seg_radix(const K *__restrict__ kin, const uint32_t *__restrict__ vin, K *__restrict__ kout,
                 uint32_t *__restrict__ vout, const uint32_t *__restrict__ offsets, uint32_t nseg, uint64_t n, K flip,
-                uint32_t maxlen, uint32_t *__restrict__ bad)
+                uint32_t maxlen, uint32_t *__restrict__ bad, const uint32_t *__restrict__ gate)
 {
     constexpr int NW = GROUP / 32;
     static_assert(CAP <= kSegMedMax && GROUP % 32 == 0 && CAP % 16 == 0, "segment capacity");
     pdl_begin();
+    if (gate && __ldcg(gate) == 0u) return;
     extern __shared__ __align__(16) uint8_t seg_smem[];  // seg_radix_smem<K, KV, GROUP, CAP>()
     K *const kbuf0 = reinterpret_cast<K *>(seg_smem);
     K *const kbuf1 = kbuf0 + CAP;

@@ -105,24 +105,36 @@ static_assert(kMinTile <= OsKeysM::kTile && kMinTile <= OsPairsM::kTile && kMinT
 // plan[kMaxPasses + 1] = kPlanMagic.
 constexpr int kMaxPasses = 8;                 // 64-bit keys
 constexpr uint32_t kPlanMagic = 0xa45c0de1u;  // plan[kMaxPasses + 1] once K5 has written a plan
+constexpr int kPlanBL = kMaxPasses + 2;       // plan[kPlanBL] = 1: bucket-local plan (K10 runs after the passes)
 constexpr int kRHBlock = 1024;
 constexpr int kRowCtas = 4;  // K5 CTAs per row set (K1 low bytes, K2 digit 1)
 
+// Bucket-local plan (GENERAL, 32-bit keys): two LSD passes over the two bytes of the
+// feature bin (key - min) >> s -- digits at bit offsets s and s + 8 -- sort the keys stably by their
+// bin, so every bin is a contiguous bucket (boundaries: the exclusive scan of the feature histogram);
+// then K10 sorts each bucket in shared memory by its low s bits (the K9 segment sort with the bucket
+// scan as offsets).  K5 chooses it when bl_cap > 0 and the largest bin holds <= bl_cap keys (the K10
+// variant's capacity), and the classic full-width passes otherwise; the host launches both plans'
+// kernels and the unused ones return at once (plan words kPassSkip, plan[kPlanBL] = 0).
 template <int BLOCK, int MAXP = 4>
 __global__ void __launch_bounds__(BLOCK, 1)
     k_radix_hist(uint64_t n, uint32_t sub, int passes, const uint32_t *__restrict__ fhist, uint32_t nb,
                  uint32_t fshift, const DevFeatures *__restrict__ dfeat, const uint32_t *__restrict__ byte0_rows,
                  const uint32_t *__restrict__ digit1_rows, uint32_t *__restrict__ dhist,
                  uint32_t *__restrict__ bucket_base, uint32_t *__restrict__ ticket, uint32_t *__restrict__ plan,
-                 int skip_trivial)
+                 int skip_trivial, uint32_t bl_cap, uint32_t *__restrict__ maxbin)
 {
     pdl_begin();
     static_assert(MAXP <= kMaxPasses && MAXP * 32 <= BLOCK, "one warp per pass in the final scan");
     __shared__ uint32_t s_dig[MAXP][256];
+    __shared__ uint32_t s_bl[2][256];  // the bucket-local plan's two bin digits
     __shared__ bool s_last;
     __shared__ uint32_t s_triv[MAXP];
+    __shared__ uint32_t s_blon;
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+    const bool bl = bl_cap != 0u && fshift > 0u;
     for (int i = threadIdx.x; i < MAXP * 256; i += BLOCK) (&s_dig[0][0])[i] = 0u;
+    for (int i = threadIdx.x; i < 2 * 256; i += BLOCK) (&s_bl[0][0])[i] = 0u;
     __syncthreads();
     // rows of K1 (digit 0): CTAs 0 .. kRowCtas-1; rows of K2 (digit 1): the next
     // kRowCtas (the grid has >= 2 kRowCtas); four threads per bin and CTA, each
@@ -142,6 +154,7 @@ __global__ void __launch_bounds__(BLOCK, 1)
         }
     }
     // digits inside the feature buckets: this CTA's slice of the bins
+    uint32_t mx_bin = 0;
     for (uint32_t b = blockIdx.x * BLOCK + threadIdx.x; b < nb; b += gridDim.x * BLOCK) {
         const uint32_t c = __ldg(&fhist[b]);
         if (!c) continue;
@@ -150,24 +163,43 @@ __global__ void __launch_bounds__(BLOCK, 1)
         for (int p = 0; p < MAXP; p++)
             if (p < passes && (uint32_t)(8 * p) >= fshift)
                 atomicAdd(&s_dig[p][(uint32_t)(base >> (8 * p)) & 255u], c);
+        if (bl) {
+            atomicAdd(&s_bl[0][b & 255u], c);
+            atomicAdd(&s_bl[1][(b >> 8) & 255u], c);
+            mx_bin = max(mx_bin, c);
+        }
+    }
+    if (bl) {
+        mx_bin = __reduce_max_sync(kFull, mx_bin);
+        if (lane == 0 && mx_bin) atomicMax(maxbin, mx_bin);
     }
     __syncthreads();
     for (int i = threadIdx.x; i < passes * 256; i += BLOCK) {
         const uint32_t v = (&s_dig[0][0])[i];
         if (v) atomicAdd(&dhist[i], v);
     }
+    if (bl)
+        for (int i = threadIdx.x; i < 2 * 256; i += BLOCK) {
+            const uint32_t v = (&s_bl[0][0])[i];
+            if (v) atomicAdd(&dhist[MAXP * 256 + i], v);
+        }
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    if ((int)warp < passes) {
-        // exclusive scan of dhist[warp][0..256): lane owns 8 consecutive digits
+    if (threadIdx.x == 0) s_blon = bl && __ldcg(maxbin) <= bl_cap ? 1u : 0u;
+    __syncthreads();
+    const bool blon = s_blon != 0u;
+    const int np = blon ? 2 : passes;  // digit histograms scanned: the bin digits or the classic ones
+    if ((int)warp < np) {
+        // exclusive scan of one digit histogram: lane owns 8 consecutive digits
+        const uint32_t *src = dhist + (blon ? MAXP * 256 : 0) + warp * 256;
         uint32_t c[8], sum = 0;
 #pragma unroll
         for (int j = 0; j < 8; j++) {
-            c[j] = __ldcg(&dhist[warp * 256 + lane * 8 + j]);
+            c[j] = __ldcg(&src[lane * 8 + j]);
             sum += c[j];
         }
         uint32_t incl = sum;
@@ -189,15 +221,17 @@ __global__ void __launch_bounds__(BLOCK, 1)
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        // device pass plan: executed passes renumbered 0 .. m-1
+        // device pass plan: executed passes renumbered 0 .. m-1, each with its digit's bit offset
         uint32_t m = 0;
-        for (int p = 0; p < passes; p++) m += s_triv[p] ? 0u : 1u;
+        for (int p = 0; p < np; p++) m += s_triv[p] ? 0u : 1u;
         uint32_t e = 0;
         for (int p = 0; p < passes; p++) {
-            plan[p] = s_triv[p] ? kPassSkip : ((e << 8) | m);
-            e += s_triv[p] ? 0u : 1u;
+            const bool run = p < np && !s_triv[p];
+            plan[p] = run ? plan_word(blon ? fshift + 8u * p : 8u * p, e, m) : kPassSkip;
+            e += run ? 1u : 0u;
         }
         plan[kMaxPasses] = m;
+        plan[kPlanBL] = blon ? 1u : 0u;
         plan[kMaxPasses + 1] = kPlanMagic;
     }
 }

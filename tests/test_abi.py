@@ -168,9 +168,9 @@ def test_new_entry_points_check_arguments():
         L.ahs_sort_tmp_bytes_ex(1 << 20, 0, 3) > L.ahs_sort_tmp_bytes_ex(1 << 20, 0, 1)
     # 64-bit keys must be 8-byte aligned
     assert L.ahs_features(C.c_void_p(4100), 10, ahs.AHS_U64, C.c_void_p(4096), 1 << 30, C.byref(f), None) == -1
-    # segment sort: above the 2048-key limit, bad dtype, missing counter
+    # segment sort: above the 8192-key limit, bad dtype, missing counter
     bad = C.c_void_p(4096)
-    assert L.ahs_sort_segments(C.c_void_p(4096), None, C.c_void_p(8192), None, 10, C.c_void_p(12288), 2, 4096,
+    assert L.ahs_sort_segments(C.c_void_p(4096), None, C.c_void_p(8192), None, 10, C.c_void_p(12288), 2, 8193,
                                0, bad, None) == -3
     assert L.ahs_sort_segments(C.c_void_p(4096), None, C.c_void_p(8192), None, 10, C.c_void_p(12288), 2, 32,
                                7, bad, None) == -1

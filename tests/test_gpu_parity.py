@@ -527,3 +527,40 @@ def test_concurrent_host_threads():
     for i, keys in enumerate(cases):
         ref = oracle.ahs(keys, np.arange(keys.size, dtype=np.uint32))
         assert np.array_equal(results[i][0], ref["keys"]) and np.array_equal(results[i][1], ref["vals"]), i
+
+
+# ------------------------------------------- bucket-local GENERAL plan (opt-in)
+
+@pytest.fixture
+def bucket_local():
+    prev = ahs.ahs_set_bucket_local(-1)
+    ahs.ahs_set_bucket_local(1)
+    yield
+    ahs.ahs_set_bucket_local(prev)
+
+
+@pytest.mark.parametrize("family", ["full32", "range3M", "desc", "alt_extremes"])
+def test_bucket_local_plan_parity(family, bucket_local):
+    """Two passes over the feature-bin digits + the in-shared-memory bucket pass (K10): keys and
+    values against the oracle, and the plan it reports (bucket-local exactly when the bins are
+    coarser than single values and the largest bin fits the K10 capacity)."""
+    for i, n in enumerate((5000, 65537, 250_001, 3_000_017)):
+        keys = FAMILIES[family](n, 900 + i)
+        vals = np.arange(n, dtype=np.uint32)
+        for v in (None, vals):
+            f, s, r = check_pipeline(keys, v)
+            if ahs.STRATEGY_NAMES[s] != "GENERAL":
+                continue
+            dk = to_dev(keys)
+            ws = ahs.Workspace(n, v is not None)
+            f2 = ahs.ahs_features(dk, ws)
+            ko = torch.empty_like(dk)
+            dv = to_dev(v) if v is not None else None
+            vo = torch.empty_like(dv) if dv is not None else None
+            ahs.ahs_sort(dk, dv, ko, vo, s, f2, ws)
+            passes, bl = ahs.ahs_sort_plan(ws)
+            if f2.shift == 0:
+                assert bl == 0
+            if bl:
+                assert 1 <= passes <= 2  # the two bin digits (a constant one is skipped)
+                assert ahs.ahs_sort_executed_passes(ws) == passes + 1
