@@ -393,6 +393,15 @@ __device__ __forceinline__ Partial64 KeyTraits<uint64_t>::reduce(const Partial64
 // Both modes first merge runs of equal bins: within a thread's 4 keys, and
 // across lanes whose 4 keys all fall into one bin (sorted / nearly sorted
 // input would otherwise serialise 32 lanes on one address).
+// Mode B word of bin b: the pair word b >> 1 with its low five bits XORed with bits 5-9 (a bijection
+// on the 32768 words).  Structured keys put their bins on a few banks otherwise: cfg3's 4096 values
+// 2^18 apart fall 16 bins apart, i.e. on words 8 apart, i.e. on 4 of the 32 banks.
+__device__ __forceinline__ uint32_t hist_word(uint32_t b)
+{
+    const uint32_t w = b >> 1;
+    return w ^ ((w >> 5) & 31u);
+}
+
 struct HistAdd {
     uint32_t *sh, *ovf;
     uint32_t copy_base;
@@ -403,14 +412,14 @@ struct HistAdd {
             atomicAdd(&sh[copy_base + b], c);
             return;
         }
-        fix(atomicAdd(&sh[b >> 1], c << ((b & 1u) << 4)), b, c);
+        fix(atomicAdd(&sh[hist_word(b)], c << ((b & 1u) << 4)), b, c);
     }
     __device__ __forceinline__ void fix(uint32_t old, uint32_t b, uint32_t c) const
     {
         const uint32_t sft = (b & 1u) << 4;
         const uint32_t h = (old >> sft) & 0xffffu;
         if (h < 0x8000u && h + c >= 0x8000u) {
-            atomicSub(&sh[b >> 1], 0x8000u << sft);
+            atomicSub(&sh[hist_word(b)], 0x8000u << sft);
             atomicAdd(&ovf[b], 0x8000u);
         }
     }
@@ -424,10 +433,10 @@ struct HistAdd {
             atomicAdd(&sh[copy_base + b3], 1u);
             return;
         }
-        const uint32_t o0 = atomicAdd(&sh[b0 >> 1], 1u << ((b0 & 1u) << 4));
-        const uint32_t o1 = atomicAdd(&sh[b1 >> 1], 1u << ((b1 & 1u) << 4));
-        const uint32_t o2 = atomicAdd(&sh[b2 >> 1], 1u << ((b2 & 1u) << 4));
-        const uint32_t o3 = atomicAdd(&sh[b3 >> 1], 1u << ((b3 & 1u) << 4));
+        const uint32_t o0 = atomicAdd(&sh[hist_word(b0)], 1u << ((b0 & 1u) << 4));
+        const uint32_t o1 = atomicAdd(&sh[hist_word(b1)], 1u << ((b1 & 1u) << 4));
+        const uint32_t o2 = atomicAdd(&sh[hist_word(b2)], 1u << ((b2 & 1u) << 4));
+        const uint32_t o3 = atomicAdd(&sh[hist_word(b3)], 1u << ((b3 & 1u) << 4));
         // a +1 crosses 0x8000 only from 0x7fff: one combined test, the rare fix-ups behind it
         const bool f0 = ((o0 >> ((b0 & 1u) << 4)) & 0xffffu) == 0x7fffu;
         const bool f1 = ((o1 >> ((b1 & 1u) << 4)) & 0xffffu) == 0x7fffu;
@@ -443,7 +452,7 @@ struct HistAdd {
     // move 0x8000 of bin b's packed counter into its overflow word
     __device__ __forceinline__ void carry(uint32_t b) const
     {
-        atomicSub(&sh[b >> 1], 0x8000u << ((b & 1u) << 4));
+        atomicSub(&sh[hist_word(b)], 0x8000u << ((b & 1u) << 4));
         atomicAdd(&ovf[b], 0x8000u);
     }
 };
@@ -522,7 +531,8 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(BLOCK, 1)
         R = kHistWords / rg.nb;
         if (R > BLOCK / 32) R = BLOCK / 32;
     }
-    const uint32_t words = packed ? (rg.nb + 1u) >> 1 : (cols ? rg.nb * BLOCK : R * rg.nb);
+    // packed: every word (hist_word's XOR can move a pair past (nb + 1) / 2)
+    const uint32_t words = packed ? kHistWords : (cols ? rg.nb * BLOCK : R * rg.nb);
     for (uint32_t i = threadIdx.x; i < words; i += BLOCK) sh[i] = 0u;
     // Digit 1 of v = key - min for the radix sort, counted here when the feature
     // buckets are coarser than 2^8 (shift > 8, always the packed mode) and the
@@ -644,7 +654,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(BLOCK, 1)
             uint32_t lo = 0, hi = 0;
 #pragma unroll
             for (int c = 0; c < CL; c++) {
-                const uint32_t v = peer[c][w];
+                const uint32_t v = peer[c][w ^ ((w >> 5) & 31u)];  // hist_word of bins 2w, 2w + 1
                 lo += v & 0xffffu;
                 hi += v >> 16;
             }
