@@ -253,10 +253,12 @@ def time_pipeline(torch, ahs, keys_np, vals_np, steps, warmup, device, flush, pr
     clocks = sampler.stop() if sampler else None
     passes = ahs.ahs_sort_passes(f, s, dv is not None)
     executed = ahs.ahs_sort_executed_passes(ws, stream) if passes > 0 else 0
+    digit_passes, bucket_local = ahs.ahs_sort_plan(ws, stream) if passes > 0 else (0, 0)
     if executed < 0:  # no device plan on this path (COUNTING): the nominal passes all run
-        executed = passes
+        executed = digit_passes = passes
     return dict(total_ms=total_ms, f=f, s=s, r=r, launches=launches, prof=prof, passes=passes,
-                executed=executed, clocks=clocks, step_ms=step_ms)
+                executed=executed, digit_passes=digit_passes, bucket_local=bucket_local, clocks=clocks,
+                step_ms=step_ms)
 
 
 def entropy_exact_report(torch, ahs, keys_np, vals_np, device, reps=5):
@@ -445,8 +447,9 @@ def dominant_roofline(res, n, kv, kb, workload, peak, peak_kind):
     if prof.get(kname, {}).get("launches", 0) == 0:
         kname = max(prof, key=lambda k: prof[k]["ms"])
     kl = prof[kname]["launches"]
-    if kname.startswith("onesweep") and res["executed"] < res["passes"]:
-        kl = kl * res["executed"] // res["passes"]  # NEXT-1 skipped launches return at once
+    if kname.startswith("onesweep") and res["digit_passes"] < res["passes"]:
+        # launches the plan skips return at once (NEXT-1; the bucket-local plan's unused passes)
+        kl = kl * res["digit_passes"] // res["passes"]
     kms = prof[kname]["ms"] / max(1, kl)
     per = PER_LAUNCH_BYTES.get(kname, 4) * n
     if kname.startswith("onesweep") and kb == 8:
@@ -466,13 +469,16 @@ def table_row(torch, ahs, cfg, k2, v2, steps, device, flush, peak, skip=True, co
     contract row of SURVEY §8(d)); with skip=True the row is the NEXT-1 row."""
     prev = ahs.ahs_set_skip_trivial(-1)
     prev_cs = ahs.ahs_set_count_kv_single(-1)
+    prev_bl = ahs.ahs_set_bucket_local(-1)
     ahs.ahs_set_skip_trivial(1 if skip else 0)
     ahs.ahs_set_count_kv_single(1 if count_single else 0)
+    ahs.ahs_set_bucket_local(1 if skip else 0)  # the contract row (skip off) runs the classic plan
     try:
         r2 = time_pipeline(torch, ahs, k2, v2, steps, 2, device, flush, profile=True)
     finally:
         ahs.ahs_set_skip_trivial(prev)
         ahs.ahs_set_count_kv_single(prev_cs)
+        ahs.ahs_set_bucket_local(prev_bl)
     p2 = r2["prof"]
     n2 = k2.size
     kv2 = v2 is not None
@@ -483,7 +489,8 @@ def table_row(torch, ahs, cfg, k2, v2, steps, device, flush, peak, skip=True, co
     row = {
         "workload": cfg, "n": n2, "kv": kv2, "strategy": ahs.STRATEGY_NAMES[r2["s"]],
         "rule": ahs.RULE_NAMES[r2["r"]], "skip_trivial": skip, "passes": r2["passes"],
-        "count_kv_single": count_single,
+        "count_kv_single": count_single, "bucket_local": bool(r2["bucket_local"]),
+        "digit_passes_executed": r2["digit_passes"],
         "passes_executed": r2["executed"],
         "pipeline_Gkeys_s": n2 * steps / (r2["total_ms"] * 1e-3) / 1e9,
         "sort_Gkeys_s": n2 / (sort_ms2 * 1e-3) / 1e9 if sort_ms2 > 0 else None,
@@ -538,7 +545,8 @@ def run_ours(args):
         "data": "synthetic (SplitMix64 recipe of SURVEY.md §8(d))",
         "config": {"workload": args.workload, "n": n, "key_dtype": dt, "kv": kv,
                    "strategy": ahs.STRATEGY_NAMES[s], "rule": ahs.RULE_NAMES[r], "passes": res["passes"],
-                   "passes_executed": res["executed"],
+                   "passes_executed": res["executed"], "digit_passes_executed": res["digit_passes"],
+                   "bucket_local": bool(res["bucket_local"]),
                    "l2": "flushed before every timed step (256 MiB write); the inputs are also larger than L2",
                    "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU"},
         "roofline": roof,
@@ -595,7 +603,7 @@ def run_ours(args):
             else:
                 row.update({"H16": r2["f"].entropy})
             rows.append(row)
-            if r2["executed"] < r2["passes"]:
+            if r2["executed"] < r2["passes"] or r2["bucket_local"]:
                 row_c, _ = table_row(torch, ahs, cfg, k2, v2, args.table_steps, device, flush, peak, skip=False)
                 rows.append(row_c)
             if v2 is not None and r2["s"] == 0 and 8 < r2["f"].bits <= 10:

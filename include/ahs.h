@@ -337,14 +337,15 @@ AHS_API int ahs_set_count_kv_single(int on);
  * 4-byte or no values and out of place: two stable LSD passes over the two bytes
  * of the bin make every bin a contiguous bucket (its boundaries are the exclusive
  * scan of the feature histogram), then K10 sorts each bucket in shared memory by
- * its low s bits (the K9 segment sort, one CTA per bucket, digits a bucket shares
- * skipped) -- three reads and writes of the keys instead of four.  The library
- * picks K10's capacity from the mean bin size (up to 8192 keys); K5 falls back to
- * the four full-width passes on the device when a bin is larger.  Default off
- * (environment AHS_BUCKET_LOCAL=1 turns it on): on B200 the in-shared-memory
- * bucket pass measured slower than the two digit passes it replaces (cfg4a sort
- * 888 vs 801 us, cfg5 r=32 pairs 6.57 vs 4.99 ms; profiles/r02_summary.md).
- * Output identical.
+ * its low s bits (K10, bucket.cuh: one CTA per bucket, digits a bucket shares
+ * skipped) -- three reads and writes of the keys instead of four.  Used where it
+ * pays on B200: keys wider than 24 bits (the classic plan runs four passes) and
+ * bins of >= 1536 keys on average (2^28 pairs over 32 bits: sort 5.01 -> 4.87 ms;
+ * with three classic passes or smaller bins the bucket pass is slower than the
+ * passes it replaces, profiles/r02_summary.md).  The library picks K10's
+ * capacity from the mean bin size (up to 8192 keys); K5 falls back to the four
+ * full-width passes on the device when a bin is larger.  Default on (environment
+ * AHS_BUCKET_LOCAL=0 turns it off).  Output identical.
  * ahs_set_bucket_local(0/1) sets it (any other value queries); returns the setting.
  * ahs_sort_plan() reads the plan of the last ahs_sort on d_tmp (synchronizes):
  * executed digit passes and whether the bucket-local pass ran.

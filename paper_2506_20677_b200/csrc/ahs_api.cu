@@ -21,6 +21,7 @@
 #include "entropy.cuh"
 #include "classifier.hpp"
 #include "segsort.cuh"
+#include "bucket.cuh"
 
 using namespace ahs;
 
@@ -276,11 +277,16 @@ std::atomic<bool> g_count_kv_single{[] {
     const char *e = std::getenv("AHS_COUNT_KV_SINGLE");
     return e && e[0] == '1';
 }()};
-// bucket-local GENERAL plan (sort.cuh; default off: measured slower than the four passes on B200,
-// profiles/r02_summary.md; AHS_BUCKET_LOCAL=1 or ahs_set_bucket_local(1) turn it on)
+// bucket-local GENERAL plan (sort.cuh; default on where it pays: bins of >= 1536 keys on average,
+// keys wider than 24 bits; AHS_BUCKET_LOCAL=0 or ahs_set_bucket_local(0) turn it off)
 std::atomic<bool> g_bucket_local{[] {
     const char *e = std::getenv("AHS_BUCKET_LOCAL");
-    return e && e[0] == '1';
+    return !(e && e[0] == '0');
+}()};
+// K10 for medium segments and the bucket pass (default on; AHS_K10=0: K9r everywhere)
+std::atomic<bool> g_k10{[] {
+    const char *e = std::getenv("AHS_K10");
+    return !(e && e[0] == '0');
 }()};
 // K6 v2 for RADIX passes (default on; AHS_K6V2=0 turns it off: K6 everywhere)
 std::atomic<bool> g_k6v2{[] {
@@ -880,12 +886,13 @@ int sort_impl(const K *kin, const V *d_vals_in, K *kout, V *d_vals_out, uint64_t
     const K umin = kWide ? (K)umin64_of(feat) : (K)umin_of(feat);
     const uint32_t n32 = (uint32_t)n;
 
-    // paths without digit passes still clear the look-back fault word of a reused d_tmp
-    // (the digit-pass path clears the whole control block below)
+    // paths without digit passes still clear the plan and look-back fault words of a reused d_tmp
+    // (ticket words kTicketPlan .. kTicketFault; the digit-pass path clears the whole control block)
     auto clear_fault = [&]() -> bool {
         const TmpLayout T0 = tmp_layout(0, 0);
         if (!d_tmp || tmp_bytes < T0.status) return true;
-        return cudaMemsetAsync((char *)d_tmp + T0.ticket + kTicketFault * 4, 0, 4, s) == cudaSuccess;
+        return cudaMemsetAsync((char *)d_tmp + T0.ticket + kTicketPlan * 4, 0, (kTicketFault - kTicketPlan + 1) * 4,
+                               s) == cudaSuccess;
     };
     // constant input: stable identity
     if (feat->k == 1) {
@@ -998,14 +1005,20 @@ int sort_impl(const K *kin, const V *d_vals_in, K *kout, V *d_vals_out, uint64_t
     // it when the largest bin fits the K10 capacity chosen here from the mean bin size.
     uint32_t bl_cap = 0;
     const uint32_t *bl_offsets = nullptr;
+    // (it pays only where the classic plan runs all four passes, bits > 24: there the bucket pass
+    // replaces two onesweep passes; with three the classic plan is faster, profiles/r02_summary.md)
     if (strategy == AHS_GENERAL && W == 0 && VK <= 1 && !inplace && feat->shift > 0 && passes == 4 &&
-        g_bucket_local.load(std::memory_order_relaxed)) {
+        feat->bits > 24 && g_bucket_local.load(std::memory_order_relaxed)) {
+        // capacity: the bin mean plus six standard deviations of a uniform fill; below ~1500 keys per
+        // bin the bucket pass is no faster than the two digit passes it replaces (profiles/r02_summary.md)
         const double mean = (double)n / (double)feat->nbins;
-        for (uint32_t c : {256u, 512u, 1024u, 2048u, 4096u, 8192u})
-            if (1.25 * mean + 32.0 <= (double)c) {
-                bl_cap = c;
-                break;
-            }
+        const double need = mean + 6.0 * std::sqrt(mean) + 32.0;
+        if (mean >= 1536.0)
+            for (uint32_t c : {2048u, 4096u, 4608u, 5120u, 6144u, 8192u})
+                if (need <= (double)c) {
+                    bl_cap = c;
+                    break;
+                }
         if (bl_cap) {
             bl_offsets = hist_scan(d_ws, feat, s);  // bucket boundaries: scan[b] .. scan[b + 1]
             if (!bl_offsets) return AHS_ECUDA;
@@ -1309,6 +1322,20 @@ cudaError_t seg_small(const void *kin, const uint32_t *vin, void *kout, uint32_t
                     vout, offsets, nseg, n, flip, max_segment, bad);
 }
 
+// K10 (bucket.cuh): one CTA of 256 threads per segment of <= 256 IPT keys, ordered ranking
+template <typename K, bool KV, int IPT>
+cudaError_t seg_bucket(const void *kin, const uint32_t *vin, void *kout, uint32_t *vout, uint64_t n,
+                       const uint32_t *offsets, uint32_t nseg, K flip, uint32_t *bad, cudaStream_t s,
+                       const uint32_t *gate)
+{
+    using BS = BucketSort<K, KV, IPT>;
+    constexpr int MINB = IPT >= 16 ? 2 : 4;
+    const cudaError_t ae = opt_in_smem((const void *)k_bucket_sort<K, KV, IPT, MINB>, BS::kSmem);
+    if (ae != cudaSuccess) return ae;
+    return launch_k(k_bucket_sort<K, KV, IPT, MINB>, dim3(nseg), dim3(kBucketBlock), BS::kSmem, s, (const K *)kin,
+                    vin, (K *)kout, vout, offsets, nseg, n, flip, bad, gate);
+}
+
 template <typename K, bool KV, int GROUP, int CAP, bool ORD>
 cudaError_t seg_radix(const void *kin, const uint32_t *vin, void *kout, uint32_t *vout, uint64_t n,
                       const uint32_t *offsets, uint32_t nseg, uint32_t max_segment, K flip, uint32_t *bad,
@@ -1335,6 +1362,18 @@ cudaError_t seg_launch(const void *kin, const uint32_t *vin, void *kout, uint32_
     if (max_segment <= (uint32_t)kSegSmallMax) return seg_small<K, KV, 32>(AHS_SEG_ARGS);
     // K9r: threads per segment from the declared maximum (16 keys per thread, one
     // warp up to 512 keys); the ordered ranking when the device passed its self-test
+    if (ord && g_k10.load(std::memory_order_relaxed) && max_segment > 1024) {
+        // K10: 256 threads per segment, keys in registers between the passes (faster than K9r above
+        // 1024 keys: 2048-pair segments 563 vs 678 us per 2^27 pairs; slower below, profiles/r02_summary.md)
+#define AHS_BK_ARGS kin, vin, kout, vout, n, offsets, nseg, flip, bad, s, gate
+        if (max_segment <= 2048) return seg_bucket<K, KV, 8>(AHS_BK_ARGS);
+        if (max_segment <= 4096) return seg_bucket<K, KV, 16>(AHS_BK_ARGS);
+        if (max_segment <= 4608) return seg_bucket<K, KV, 18>(AHS_BK_ARGS);
+        if (max_segment <= 5120) return seg_bucket<K, KV, 20>(AHS_BK_ARGS);
+        if (max_segment <= 6144) return seg_bucket<K, KV, 24>(AHS_BK_ARGS);
+        return seg_bucket<K, KV, 32>(AHS_BK_ARGS);
+#undef AHS_BK_ARGS
+    }
     if (ord) {
         if (max_segment <= 256) return seg_radix<K, KV, 32, 256, true>(AHS_SEG_ARGS, gate);
         if (max_segment <= 512) return seg_radix<K, KV, 32, 512, true>(AHS_SEG_ARGS, gate);

@@ -1,0 +1,176 @@
+// bucket.cuh — K10: stable in-shared-memory LSD radix sort of many independent
+// segments, one CTA of 256 threads per segment of up to 256 x IPT keys.  It serves
+// the medium segments of ahs_sort_segments (NEXT-4: the paper's small-n path,
+// Listing 1, batched) and the bucket pass of the bucket-local GENERAL
+// plan (after two LSD passes over the feature-bin digits every bin is
+// a contiguous bucket, and each bucket still needs sorting by its low bits).
+//
+// Per CTA (segment [lo, hi), len <= CAP = 256 IPT):
+//   load      the keys (ordered image key ^ flip) and values straight into
+//             registers: warp w owns the contiguous slice [w C, (w + 1) C), C = a
+//             multiple of 32 >= len / 8, lane l holds its items k at w C + 32 k + l
+//             (so register order (warp, item, lane) is index order);
+//   digits    the OR of key ^ first key over the segment: only the 8-bit digits in
+//             which some key differs get a pass (a stable pass over a constant digit
+//             is the identity);
+//   per pass  count (one shared atomic per key into the warp's 256-entry table) |
+//             barrier | the 256 scan threads turn the 8 warp tables into slots:
+//             digit start (block scan of the totals) + earlier warps' counts |
+//             barrier | rank (one shared atomic with return per key: the ordered
+//             ranking, the device's lane order being self-tested as for K6) and
+//             scatter into the segment buffer | barrier | reload the registers in
+//             (warp, item, lane) order.  Four shared operations per key, three
+//             barriers; one buffer (the keys live in registers across the scatter);
+//   store     from the registers, coalesced, output transform fused.
+// Stable: every pass ranks in index order.  kout may alias kin.  A segment longer
+// than CAP (or reaching past n) is counted in *bad and left as is.
+#pragma once
+
+#include "common.cuh"
+
+namespace ahs {
+
+constexpr int kBucketBlock = 256;
+
+template <typename K, bool KV, int IPT>
+struct BucketSort {
+    static constexpr int kCap = kBucketBlock * IPT;
+    static constexpr int kWarps = kBucketBlock / 32;
+    static constexpr size_t kSmem = (size_t)kCap * sizeof(K) + (KV ? (size_t)kCap * 4 : 0) +
+                                    (size_t)kWarps * 256 * 4 + 256 * 4 + 64;
+};
+
+template <typename K, bool KV, int IPT, int MINB>
+__global__ void __launch_bounds__(kBucketBlock, MINB)
+    k_bucket_sort(const K *__restrict__ kin, const uint32_t *__restrict__ vin, K *__restrict__ kout,
+                  uint32_t *__restrict__ vout, const uint32_t *__restrict__ offsets, uint32_t nseg, uint64_t n,
+                  K flip, uint32_t *__restrict__ bad, const uint32_t *__restrict__ gate)
+{
+    using C = BucketSort<K, KV, IPT>;
+    constexpr int NW = C::kWarps, CAP = C::kCap;
+    pdl_begin();
+    if (gate && __ldcg(gate) == 0u) return;
+    extern __shared__ __align__(16) uint8_t bk_smem[];
+    K *const kb = reinterpret_cast<K *>(bk_smem);
+    [[maybe_unused]] uint32_t *const vb = reinterpret_cast<uint32_t *>(bk_smem + (size_t)CAP * sizeof(K));
+    uint32_t *const tab = reinterpret_cast<uint32_t *>(bk_smem + (size_t)CAP * sizeof(K) +
+                                                       (KV ? (size_t)CAP * 4 : 0));  // [NW][256]
+    uint32_t *const s_wsum = tab + NW * 256;                                          // [8]
+    __shared__ uint32_t s_diff[2];
+
+    const uint32_t seg = blockIdx.x;
+    if (seg >= nseg) return;
+    const uint32_t lo = __ldg(&offsets[seg]), hi = __ldg(&offsets[seg + 1]);
+    const uint32_t t = threadIdx.x, lane = t & 31u, warp = t >> 5;
+    if (hi < lo || (uint64_t)hi > n || hi - lo > (uint32_t)CAP) {
+        if (t == 0) atomicAdd(bad, 1u);
+        return;
+    }
+    const uint32_t len = hi - lo;
+    if (len < 2) {
+        if (len == 1 && t == 0 && kout != kin) {
+            kout[lo] = kin[lo];
+            if constexpr (KV) vout[lo] = vin[lo];
+        }
+        return;
+    }
+    // warp slices: C keys each (a multiple of 32), the last ones possibly short or empty
+    const uint32_t Cw = ((len + NW - 1) / NW + 31u) & ~31u;
+    const uint32_t wb = min(len, warp * Cw), we = min(len, wb + Cw);
+    auto slot = [&](int k) { return wb + (uint32_t)k * 32u + lane; };
+    auto valid = [&](int k) { return slot(k) < we; };
+
+    if (t == 0) s_diff[0] = s_diff[1] = 0u;
+    for (int i = t; i < NW * 256; i += kBucketBlock) tab[i] = 0u;
+    __syncthreads();
+    const K first = kin[lo] ^ flip;
+    K x[IPT];
+    [[maybe_unused]] uint32_t y[KV ? IPT : 1];
+    K dacc = 0;
+#pragma unroll
+    for (int k = 0; k < IPT; k++) {
+        x[k] = valid(k) ? (K)(kin[lo + slot(k)] ^ flip) : first;
+        if constexpr (KV) y[k] = valid(k) ? vin[lo + slot(k)] : 0u;
+        dacc |= x[k] ^ first;
+    }
+    {
+        const uint32_t dlo = __reduce_or_sync(kFull, (uint32_t)dacc);
+        const uint32_t dhi = sizeof(K) == 8 ? __reduce_or_sync(kFull, (uint32_t)((uint64_t)dacc >> 32)) : 0u;
+        if (lane == 0) {
+            if (dlo) atomicOr(&s_diff[0], dlo);
+            if (dhi) atomicOr(&s_diff[1], dhi);
+        }
+    }
+    __syncthreads();
+    const uint64_t diff = ((uint64_t)s_diff[1] << 32) | s_diff[0];
+    uint32_t *const wt = tab + warp * 256;
+
+    for (int b = 0; b < (int)sizeof(K); b++) {
+        if (((diff >> (8 * b)) & 0xffu) == 0) continue;  // a digit the whole segment shares
+        const uint32_t sh = 8u * (uint32_t)b;
+        auto dig = [&](K v) { return (uint32_t)(v >> sh) & 0xffu; };
+        // ---- count (non-returning atomics: same-word lanes merge)
+#pragma unroll
+        for (int k = 0; k < IPT; k++)
+            if (valid(k)) atomicAdd(&wt[dig(x[k])], 1u);
+        __syncthreads();
+        // ---- slots: digit start (block scan of the totals) + earlier warps' counts
+        {
+            const uint32_t d = t;  // 256 scan threads = the block
+            uint32_t c[NW], tot = 0;
+#pragma unroll
+            for (int w = 0; w < NW; w++) {
+                c[w] = tab[w * 256 + d];
+                tot += c[w];
+            }
+            uint32_t incl = tot;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t v = __shfl_up_sync(kFull, incl, o);
+                if (lane >= (uint32_t)o) incl += v;
+            }
+            if (lane == 31) s_wsum[warp] = incl;
+            __syncthreads();
+            uint32_t run = incl - tot;
+#pragma unroll
+            for (int w = 0; w < NW; w++)
+                if (w < (int)warp) run += s_wsum[w];
+#pragma unroll
+            for (int w = 0; w < NW; w++) {
+                tab[w * 256 + d] = run;
+                run += c[w];
+            }
+        }
+        __syncthreads();
+        // ---- rank (lanes of one instruction served in lane order: self-tested) and scatter
+#pragma unroll
+        for (int k = 0; k < IPT; k++) {
+            if (valid(k)) {
+                const uint32_t pos = atomicAdd(&wt[dig(x[k])], 1u);
+                kb[pos] = x[k];
+                if constexpr (KV) vb[pos] = y[k];
+            }
+            __syncwarp();
+        }
+        __syncthreads();
+        // ---- reload in index order; clear this warp's table for the next pass
+#pragma unroll
+        for (int k = 0; k < IPT; k++) {
+            if (valid(k)) {
+                x[k] = kb[slot(k)];
+                if constexpr (KV) y[k] = vb[slot(k)];
+            }
+        }
+        for (int i = lane; i < 256; i += 32) wt[i] = 0u;
+        __syncthreads();
+    }
+#pragma unroll
+    for (int k = 0; k < IPT; k++) {
+        if (valid(k)) {
+            kout[lo + slot(k)] = x[k] ^ flip;
+            if constexpr (KV) vout[lo + slot(k)] = y[k];
+        }
+    }
+}
+
+}  // namespace ahs

@@ -564,3 +564,42 @@ def test_bucket_local_plan_parity(family, bucket_local):
             if bl:
                 assert 1 <= passes <= 2  # the two bin digits (a constant one is skipped)
                 assert ahs.ahs_sort_executed_passes(ws) == passes + 1
+
+
+@pytest.mark.parametrize("kv", [False, True])
+def test_bucket_local_plan_large(kv, bucket_local):
+    """2^27 keys over the full 32-bit range: bins of ~2048 keys, so the plan is bucket-local (two
+    bin-digit passes + K10 with 4096-key capacity).  Checked by the properties that define the
+    unique stable order plus oracle-computed samples, against the classic plan's output too."""
+    n = 1 << 27
+    keys = (synth.stream(71, n) >> np.uint64(32)).astype(np.uint32)
+    vals = np.arange(n, dtype=np.uint32) if kv else None
+    dk = to_dev(keys)
+    dv = to_dev(vals) if kv else None
+    ws = ahs.Workspace(n, kv)
+    f = ahs.ahs_features(dk, ws)
+    s, r = ahs.ahs_select(f)
+    assert ahs.STRATEGY_NAMES[s] == "GENERAL" and f.shift == 16
+    ko, vo = torch.empty_like(dk), (torch.empty_like(dv) if kv else None)
+    ahs.ahs_sort(dk, dv, ko, vo, s, f, ws)
+    assert ahs.ahs_sort_plan(ws) == (2, 1)
+    k1 = to_host(ko)
+    assert np.all(k1[1:] >= k1[:-1])
+    assert np.array_equal(np.bincount(k1 >> np.uint32(16), minlength=65536),
+                          np.bincount(keys >> np.uint32(16), minlength=65536))
+    idx = synth.uniform_below(synth.stream(72, 4096), n).astype(np.int64)
+    assert np.array_equal(k1[idx], np.sort(keys)[idx])
+    if kv:
+        v1 = to_host(vo)
+        assert np.array_equal(k1, keys[v1])
+        tie = k1[1:] == k1[:-1]
+        assert np.all(v1[1:][tie] > v1[:-1][tie])
+    # the classic plan gives the same bytes
+    prev = ahs.ahs_set_bucket_local(0)
+    try:
+        ko2, vo2 = torch.empty_like(dk), (torch.empty_like(dv) if kv else None)
+        ahs.ahs_sort(dk, dv, ko2, vo2, s, f, ws)
+        assert ahs.ahs_sort_plan(ws)[1] == 0
+        assert torch.equal(ko, ko2) and (not kv or torch.equal(vo, vo2))
+    finally:
+        ahs.ahs_set_bucket_local(prev)

@@ -17,7 +17,8 @@ import paper_2506_20677_b200 as ahs  # noqa: E402
 import synth  # noqa: E402
 
 
-def case(name, n, low_bits, seg, kv=False, reps=10):
+def case(name, n, low_bits, seg, kv=False, reps=10, cap=None):
+    cap = cap or seg
     nseg = n // seg
     x = synth.stream(11, n)
     low = (x >> np.uint64(40)).astype(np.uint32) & np.uint32((1 << low_bits) - 1)
@@ -31,14 +32,14 @@ def case(name, n, low_bits, seg, kv=False, reps=10):
     bad = torch.zeros(1, dtype=torch.int32, device="cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     for _ in range(3):
-        ahs.ahs_sort_segments(dk, dv, ko, vo, off, seg, bad)
+        ahs.ahs_sort_segments(dk, dv, ko, vo, off, cap, bad)
     torch.cuda.synchronize()
     ts = []
     for _ in range(reps):
         flush.zero_()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        ahs.ahs_sort_segments(dk, dv, ko, vo, off, seg, bad)
+        ahs.ahs_sort_segments(dk, dv, ko, vo, off, cap, bad)
         b.record()
         torch.cuda.synchronize()
         ts.append(a.elapsed_time(b))
@@ -46,12 +47,12 @@ def case(name, n, low_bits, seg, kv=False, reps=10):
     h = ko.view(torch.int32).cpu().numpy().view(np.uint32)
     ok = bool(np.all(h[1:] >= h[:-1])) and int(bad.item()) == 0
     byts = n * (8 + (8 if kv else 0))
-    print(f"{name}: n={n} segs={nseg}x{seg} low_bits={low_bits} kv={kv}: {ms * 1e3:.1f} us "
+    print(f"{name}: n={n} segs={nseg}x{seg} cap={cap} low_bits={low_bits} kv={kv}: {ms * 1e3:.1f} us "
           f"{n / ms / 1e6:.1f} Gkeys/s {byts / ms / 1e6:.0f} GB/s sorted={ok}")
 
 
 if __name__ == "__main__":
-    case("cfg4a-like", 1 << 26, 10, 1024)
-    case("cfg2-like", 1 << 24, 16, 256)
-    case("r24-like pairs, 2048", 1 << 27, 8, 2048, kv=True)
-    case("r32-like pairs, 2048", 1 << 27, 16, 2048, kv=True)
+    case("r32-like pairs, 4096 cap 4608", 1 << 28, 16, 4096, kv=True, cap=4608)
+    case("r32-like pairs, 4096 cap 5120", 1 << 28, 16, 4096, kv=True, cap=5120)
+    case("r24-like pairs, 4096 cap 4608", 1 << 28, 8, 4096, kv=True, cap=4608)
+    case("r32-like keys, 4096 cap 4608", 1 << 28, 16, 4096, kv=False, cap=4608)
