@@ -339,10 +339,9 @@ AHS_API int ahs_set_count_kv_single(int on);
  * scan of the feature histogram), then K10 sorts each bucket in shared memory by
  * its low s bits (K10, bucket.cuh: one CTA per bucket, digits a bucket shares
  * skipped) -- three reads and writes of the keys instead of four.  Used where it
- * pays on B200: keys wider than 24 bits (the classic plan runs four passes) and
- * bins of >= 1536 keys on average (2^28 pairs over 32 bits: sort 5.01 -> 4.87 ms;
- * with three classic passes or smaller bins the bucket pass is slower than the
- * passes it replaces, profiles/r02_summary.md).  The library picks K10's
+ * pays on B200: bins of >= 1536 keys on average (2^28 pairs, keys over 20..32
+ * bits: sort 3.77-5.04 -> 3.71-4.46 ms; with smaller bins the bucket pass is
+ * slower than the passes it replaces, profiles/r02_summary.md).  The library picks K10's
  * capacity from the mean bin size (up to 8192 keys); K5 falls back to the four
  * full-width passes on the device when a bin is larger.  Default on (environment
  * AHS_BUCKET_LOCAL=0 turns it off).  Output identical.

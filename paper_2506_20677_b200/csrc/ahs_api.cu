@@ -1005,10 +1005,8 @@ int sort_impl(const K *kin, const V *d_vals_in, K *kout, V *d_vals_out, uint64_t
     // it when the largest bin fits the K10 capacity chosen here from the mean bin size.
     uint32_t bl_cap = 0;
     const uint32_t *bl_offsets = nullptr;
-    // (it pays only where the classic plan runs all four passes, bits > 24: there the bucket pass
-    // replaces two onesweep passes; with three the classic plan is faster, profiles/r02_summary.md)
     if (strategy == AHS_GENERAL && W == 0 && VK <= 1 && !inplace && feat->shift > 0 && passes == 4 &&
-        feat->bits > 24 && g_bucket_local.load(std::memory_order_relaxed)) {
+        g_bucket_local.load(std::memory_order_relaxed)) {
         // capacity: the bin mean plus six standard deviations of a uniform fill; below ~1500 keys per
         // bin the bucket pass is no faster than the two digit passes it replaces (profiles/r02_summary.md)
         const double mean = (double)n / (double)feat->nbins;
@@ -1329,7 +1327,7 @@ cudaError_t seg_bucket(const void *kin, const uint32_t *vin, void *kout, uint32_
                        const uint32_t *gate)
 {
     using BS = BucketSort<K, KV, IPT>;
-    constexpr int MINB = IPT >= 16 ? 2 : 4;
+    constexpr int MINB = IPT >= 32 ? 2 : (IPT >= 16 ? 3 : 4);
     const cudaError_t ae = opt_in_smem((const void *)k_bucket_sort<K, KV, IPT, MINB>, BS::kSmem);
     if (ae != cudaSuccess) return ae;
     return launch_k(k_bucket_sort<K, KV, IPT, MINB>, dim3(nseg), dim3(kBucketBlock), BS::kSmem, s, (const K *)kin,

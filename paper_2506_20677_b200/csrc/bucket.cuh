@@ -36,6 +36,8 @@ template <typename K, bool KV, int IPT>
 struct BucketSort {
     static constexpr int kCap = kBucketBlock * IPT;
     static constexpr int kWarps = kBucketBlock / 32;
+    // 32-bit keys with values: one 64-bit slot per pair (one scatter store and one reload per pair)
+    static constexpr bool kPack = KV && sizeof(K) == 4;
     static constexpr size_t kSmem = (size_t)kCap * sizeof(K) + (KV ? (size_t)kCap * 4 : 0) +
                                     (size_t)kWarps * 256 * 4 + 256 * 4 + 64;
 };
@@ -53,6 +55,7 @@ __global__ void __launch_bounds__(kBucketBlock, MINB)
     extern __shared__ __align__(16) uint8_t bk_smem[];
     K *const kb = reinterpret_cast<K *>(bk_smem);
     [[maybe_unused]] uint32_t *const vb = reinterpret_cast<uint32_t *>(bk_smem + (size_t)CAP * sizeof(K));
+    [[maybe_unused]] uint64_t *const pb = reinterpret_cast<uint64_t *>(bk_smem);  // kPack: (value << 32) | key
     uint32_t *const tab = reinterpret_cast<uint32_t *>(bk_smem + (size_t)CAP * sizeof(K) +
                                                        (KV ? (size_t)CAP * 4 : 0));  // [NW][256]
     uint32_t *const s_wsum = tab + NW * 256;                                          // [8]
@@ -147,8 +150,12 @@ __global__ void __launch_bounds__(kBucketBlock, MINB)
         for (int k = 0; k < IPT; k++) {
             if (valid(k)) {
                 const uint32_t pos = atomicAdd(&wt[dig(x[k])], 1u);
-                kb[pos] = x[k];
-                if constexpr (KV) vb[pos] = y[k];
+                if constexpr (C::kPack) {
+                    pb[pos] = ((uint64_t)y[k] << 32) | (uint32_t)x[k];
+                } else {
+                    kb[pos] = x[k];
+                    if constexpr (KV) vb[pos] = y[k];
+                }
             }
             __syncwarp();
         }
@@ -157,8 +164,14 @@ __global__ void __launch_bounds__(kBucketBlock, MINB)
 #pragma unroll
         for (int k = 0; k < IPT; k++) {
             if (valid(k)) {
-                x[k] = kb[slot(k)];
-                if constexpr (KV) y[k] = vb[slot(k)];
+                if constexpr (C::kPack) {
+                    const uint64_t q = pb[slot(k)];
+                    x[k] = (K)(uint32_t)q;
+                    y[k] = (uint32_t)(q >> 32);
+                } else {
+                    x[k] = kb[slot(k)];
+                    if constexpr (KV) y[k] = vb[slot(k)];
+                }
             }
         }
         for (int i = lane; i < 256; i += 32) wt[i] = 0u;
