@@ -866,7 +866,7 @@ namespace {
 template <typename K, bool KV>
 cudaError_t seg_launch(const void *kin, const uint32_t *vin, void *kout, uint32_t *vout, uint64_t n,
                        const uint32_t *offsets, uint32_t nseg, uint32_t max_segment, K flip, uint32_t *bad,
-                       bool ord, cudaStream_t s, const uint32_t *gate = nullptr);
+                       bool ord, cudaStream_t s, const uint32_t *gate = nullptr, uint32_t group = 1);
 
 template <typename K, typename V>
 int sort_impl(const K *kin, const V *d_vals_in, K *kout, V *d_vals_out, uint64_t n, int32_t strategy,
@@ -1003,15 +1003,22 @@ int sort_impl(const K *kin, const V *d_vals_in, K *kout, V *d_vals_out, uint64_t
     // bucket-local plan candidate (GENERAL over 32-bit keys with <= 32-bit values, buckets of the
     // feature histogram coarser than single values): two passes over the bin digits + K10.  K5 takes
     // it when the largest bin fits the K10 capacity chosen here from the mean bin size.
-    uint32_t bl_cap = 0;
+    uint32_t bl_cap = 0, bl_group = 1;
     const uint32_t *bl_offsets = nullptr;
     if (strategy == AHS_GENERAL && W == 0 && VK <= 1 && !inplace && feat->shift > 0 && passes == 4 &&
         g_bucket_local.load(std::memory_order_relaxed)) {
-        // capacity: the bin mean plus six standard deviations of a uniform fill; below ~1500 keys per
-        // bin the bucket pass is no faster than the two digit passes it replaces (profiles/r02_summary.md)
+        // K10 sorts groups of G consecutive bins as one segment (the array is ordered by bin after the
+        // two bin-digit passes): G doubles while a group stays <= ~4096 keys and its bin bits stay inside
+        // the digits the low s bits already use (no extra sub-pass).  Capacity: the group mean plus six
+        // standard deviations of a uniform fill.  Below ~1500 keys per group the bucket pass is no
+        // faster than the two digit passes it replaces (profiles/r02_summary.md).
+        // (groups of several bins, G > 1, measured slower for cfg4a's 1024-key bins: the plan's two
+        // bin-digit passes over nearly sorted keys and the 4096-key groups cost more than the two
+        // classic passes, 892 vs 785 us; so G = 1 and bins of >= 1536 keys, profiles/r02_summary.md)
         const double mean = (double)n / (double)feat->nbins;
-        const double need = mean + 6.0 * std::sqrt(mean) + 32.0;
-        if (mean >= 1536.0)
+        const double gm = mean * bl_group;
+        const double need = gm + 6.0 * std::sqrt(gm) + 32.0;
+        if (gm >= 1536.0)
             for (uint32_t c : {2048u, 4096u, 4608u, 5120u, 6144u, 8192u})
                 if (need <= (double)c) {
                     bl_cap = c;
@@ -1048,7 +1055,7 @@ int sort_impl(const K *kin, const V *d_vals_in, K *kout, V *d_vals_out, uint64_t
             launch_k(k_radix_hist<kRHBlock, kWide ? 8 : 4>, dim3((unsigned)g5), dim3(kRHBlock), 0, s, n,
                      (uint32_t)umin, passes, fhist, feat->nbins, feat->shift, (const DevFeatures *)(wsc + WL.feat),
                      (const uint32_t *)(wsc + WL.byte0), (const uint32_t *)(wsc + WL.digit1), dhist, bucket,
-                     tickets + kMaxPasses, plan, skip ? 1 : 0, bl_cap, tickets + kTicketMaxBin);
+                     tickets + kMaxPasses, plan, skip ? 1 : 0, bl_cap, bl_group, tickets + kTicketMaxBin);
         });
         if (e != cudaSuccess) return AHS_ECUDA;
         bases = bucket;
@@ -1095,10 +1102,10 @@ int sort_impl(const K *kin, const V *d_vals_in, K *kout, V *d_vals_out, uint64_t
             if (kv)
                 le = seg_launch<K, true>(kout, (const uint32_t *)d_vals_out, kout, (uint32_t *)d_vals_out, n,
                                          bl_offsets, feat->nbins, bl_cap, flip, tickets + kTicketSegBad, ord, s,
-                                         plan + kPlanBL);
+                                         plan + kPlanBL, bl_group);
             else
                 le = seg_launch<K, false>(kout, nullptr, kout, nullptr, n, bl_offsets, feat->nbins, bl_cap, flip,
-                                          tickets + kTicketSegBad, ord, s, plan + kPlanBL);
+                                          tickets + kTicketSegBad, ord, s, plan + kPlanBL, bl_group);
         });
         if (e != cudaSuccess || le != cudaSuccess) return AHS_ECUDA;
     }
@@ -1324,14 +1331,15 @@ cudaError_t seg_small(const void *kin, const uint32_t *vin, void *kout, uint32_t
 template <typename K, bool KV, int IPT>
 cudaError_t seg_bucket(const void *kin, const uint32_t *vin, void *kout, uint32_t *vout, uint64_t n,
                        const uint32_t *offsets, uint32_t nseg, K flip, uint32_t *bad, cudaStream_t s,
-                       const uint32_t *gate)
+                       const uint32_t *gate, uint32_t group)
 {
     using BS = BucketSort<K, KV, IPT>;
     constexpr int MINB = IPT >= 32 ? 2 : (IPT >= 16 ? 3 : 4);
     const cudaError_t ae = opt_in_smem((const void *)k_bucket_sort<K, KV, IPT, MINB>, BS::kSmem);
     if (ae != cudaSuccess) return ae;
-    return launch_k(k_bucket_sort<K, KV, IPT, MINB>, dim3(nseg), dim3(kBucketBlock), BS::kSmem, s, (const K *)kin,
-                    vin, (K *)kout, vout, offsets, nseg, n, flip, bad, gate);
+    const unsigned grid = (unsigned)((nseg + group - 1) / group);
+    return launch_k(k_bucket_sort<K, KV, IPT, MINB>, dim3(grid), dim3(kBucketBlock), BS::kSmem, s, (const K *)kin,
+                    vin, (K *)kout, vout, offsets, nseg, n, flip, bad, gate, group);
 }
 
 template <typename K, bool KV, int GROUP, int CAP, bool ORD>
@@ -1350,7 +1358,7 @@ cudaError_t seg_radix(const void *kin, const uint32_t *vin, void *kout, uint32_t
 template <typename K, bool KV>
 cudaError_t seg_launch(const void *kin, const uint32_t *vin, void *kout, uint32_t *vout, uint64_t n,
                        const uint32_t *offsets, uint32_t nseg, uint32_t max_segment, K flip, uint32_t *bad,
-                       bool ord, cudaStream_t s, const uint32_t *gate)
+                       bool ord, cudaStream_t s, const uint32_t *gate, uint32_t group)
 {
 #define AHS_SEG_ARGS kin, vin, kout, vout, n, offsets, nseg, max_segment, flip, bad, s
     if (max_segment <= 8) return seg_small<K, KV, 8>(AHS_SEG_ARGS);
@@ -1360,10 +1368,10 @@ cudaError_t seg_launch(const void *kin, const uint32_t *vin, void *kout, uint32_
     if (max_segment <= (uint32_t)kSegSmallMax) return seg_small<K, KV, 32>(AHS_SEG_ARGS);
     // K9r: threads per segment from the declared maximum (16 keys per thread, one
     // warp up to 512 keys); the ordered ranking when the device passed its self-test
-    if (ord && g_k10.load(std::memory_order_relaxed) && max_segment > 1024) {
+    if (ord && (group > 1 || (g_k10.load(std::memory_order_relaxed) && max_segment > 1024))) {
         // K10: 256 threads per segment, keys in registers between the passes (faster than K9r above
         // 1024 keys: 2048-pair segments 563 vs 678 us per 2^27 pairs; slower below, profiles/r02_summary.md)
-#define AHS_BK_ARGS kin, vin, kout, vout, n, offsets, nseg, flip, bad, s, gate
+#define AHS_BK_ARGS kin, vin, kout, vout, n, offsets, nseg, flip, bad, s, gate, group
         if (max_segment <= 2048) return seg_bucket<K, KV, 8>(AHS_BK_ARGS);
         if (max_segment <= 4096) return seg_bucket<K, KV, 16>(AHS_BK_ARGS);
         if (max_segment <= 4608) return seg_bucket<K, KV, 18>(AHS_BK_ARGS);

@@ -42,11 +42,14 @@ struct BucketSort {
                                     (size_t)kWarps * 256 * 4 + 256 * 4 + 64;
 };
 
+// group: segment j is [offsets[j group], offsets[min((j + 1) group, nseg)]) -- several consecutive
+// buckets sorted as one (the bucket-local plan: the array is already ordered by bucket, so sorting
+// a run of buckets by the whole key keeps their order); nseg counts offsets - 1 entries.
 template <typename K, bool KV, int IPT, int MINB>
 __global__ void __launch_bounds__(kBucketBlock, MINB)
     k_bucket_sort(const K *__restrict__ kin, const uint32_t *__restrict__ vin, K *__restrict__ kout,
                   uint32_t *__restrict__ vout, const uint32_t *__restrict__ offsets, uint32_t nseg, uint64_t n,
-                  K flip, uint32_t *__restrict__ bad, const uint32_t *__restrict__ gate)
+                  K flip, uint32_t *__restrict__ bad, const uint32_t *__restrict__ gate, uint32_t group)
 {
     using C = BucketSort<K, KV, IPT>;
     constexpr int NW = C::kWarps, CAP = C::kCap;
@@ -61,9 +64,9 @@ __global__ void __launch_bounds__(kBucketBlock, MINB)
     uint32_t *const s_wsum = tab + NW * 256;                                          // [8]
     __shared__ uint32_t s_diff[2];
 
-    const uint32_t seg = blockIdx.x;
-    if (seg >= nseg) return;
-    const uint32_t lo = __ldg(&offsets[seg]), hi = __ldg(&offsets[seg + 1]);
+    const uint64_t s0 = (uint64_t)blockIdx.x * group;
+    if (s0 >= nseg) return;
+    const uint32_t lo = __ldg(&offsets[s0]), hi = __ldg(&offsets[min(s0 + group, (uint64_t)nseg)]);
     const uint32_t t = threadIdx.x, lane = t & 31u, warp = t >> 5;
     if (hi < lo || (uint64_t)hi > n || hi - lo > (uint32_t)CAP) {
         if (t == 0) atomicAdd(bad, 1u);

@@ -293,16 +293,9 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(const PassArgsT<K, V> 
                 if constexpr (KV) pv[it] = valid ? sv[idx] : V(0);
                 const uint32_t d = digit8(v[it], shift);
                 if (it == 0 && !wskew) wskew = __all_sync(kFull, d == __shfl_sync(kFull, d, 0));
-                if (wskew) {
-                    const uint32_t d0 = __shfl_sync(kFull, d, 0);
-                    if (__all_sync(kFull, !valid || d == d0)) {
-                        // one digit across the warp: same-address atomics would serialise
-                        const uint32_t vm = FULL ? kFull : __ballot_sync(kFull, valid);
-                        if (j == 0) cw[d0] += __popc(ORDERED ? vm : (vm >> (h * 16u)) & 0xffffu);
-                        __syncwarp();
-                        continue;
-                    }
-                }
+                // the count atomic returns nothing: the lanes of one instruction that hit the same
+                // word are merged by the hardware, so warp-uniform digits need no special path here
+                // (only the returning rank atomic below serialises them)
                 if (valid) atomicAdd(&cw[d], 1u);
             }
             __syncthreads();

@@ -269,21 +269,7 @@ __device__ __forceinline__ void onesweep2_body(const PassArgsT<K, V> &a, const K
 #pragma unroll
                 for (int i = 0; i < ITEMS; i++)
                     if (valid_at(i)) t_inc(digit(v[i]));
-            } else if (form == 1) {
-#pragma unroll
-                for (int i = 0; i < ITEMS; i++) {
-                    const bool valid = valid_at(i);
-                    const uint32_t d = digit(v[i]);
-                    const uint32_t d0 = __shfl_sync(kFull, d, 0);
-                    if (__all_sync(kFull, !valid || d == d0)) {
-                        const uint32_t vm = FULL ? kFull : __ballot_sync(kFull, valid);
-                        if (lane == 0) t_add(d0, __popc(vm));
-                        __syncwarp();
-                    } else if (valid) {
-                        t_inc(d);
-                    }
-                }
-            } else if constexpr (!C::kHotCount) {
+            } else if (form == 1 || !C::kHotCount) {
                 // same-address lanes of an atomic without return are merged: plain counts
 #pragma unroll
                 for (int i = 0; i < ITEMS; i++)

@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(BLOCK, 1)
                  uint32_t fshift, const DevFeatures *__restrict__ dfeat, const uint32_t *__restrict__ byte0_rows,
                  const uint32_t *__restrict__ digit1_rows, uint32_t *__restrict__ dhist,
                  uint32_t *__restrict__ bucket_base, uint32_t *__restrict__ ticket, uint32_t *__restrict__ plan,
-                 int skip_trivial, uint32_t bl_cap, uint32_t *__restrict__ maxbin)
+                 int skip_trivial, uint32_t bl_cap, uint32_t bl_group, uint32_t *__restrict__ maxbin)
 {
     pdl_begin();
     static_assert(MAXP <= kMaxPasses && MAXP * 32 <= BLOCK, "one warp per pass in the final scan");
@@ -166,9 +166,15 @@ __global__ void __launch_bounds__(BLOCK, 1)
         if (bl) {
             atomicAdd(&s_bl[0][b & 255u], c);
             atomicAdd(&s_bl[1][(b >> 8) & 255u], c);
-            mx_bin = max(mx_bin, c);
         }
     }
+    // the bucket pass sorts groups of bl_group consecutive bins: the largest group must fit bl_cap
+    if (bl)
+        for (uint32_t g = blockIdx.x * BLOCK + threadIdx.x; (uint64_t)g * bl_group < nb; g += gridDim.x * BLOCK) {
+            uint32_t c = 0;
+            for (uint32_t b = g * bl_group; b < min(nb, (g + 1) * bl_group); b++) c += __ldg(&fhist[b]);
+            mx_bin = max(mx_bin, c);
+        }
     if (bl) {
         mx_bin = __reduce_max_sync(kFull, mx_bin);
         if (lane == 0 && mx_bin) atomicMax(maxbin, mx_bin);
