@@ -1334,7 +1334,10 @@ cudaError_t seg_bucket(const void *kin, const uint32_t *vin, void *kout, uint32_
                        const uint32_t *gate, uint32_t group)
 {
     using BS = BucketSort<K, KV, IPT>;
-    constexpr int MINB = IPT >= 32 ? 2 : (IPT >= 16 ? 3 : 4);
+#ifndef AHS_K10_MINB16
+#define AHS_K10_MINB16 4  // 64 registers (12-32 B of spill), 4 CTAs per SM: cfg5_r32 bucket pass 1923 -> 1863 us
+#endif
+    constexpr int MINB = IPT >= 32 ? 2 : (IPT >= 20 ? 3 : (IPT >= 16 ? AHS_K10_MINB16 : 4));
     const cudaError_t ae = opt_in_smem((const void *)k_bucket_sort<K, KV, IPT, MINB>, BS::kSmem);
     if (ae != cudaSuccess) return ae;
     const unsigned grid = (unsigned)((nseg + group - 1) / group);
