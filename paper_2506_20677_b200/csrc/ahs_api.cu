@@ -283,6 +283,11 @@ std::atomic<bool> g_bucket_local{[] {
     const char *e = std::getenv("AHS_BUCKET_LOCAL");
     return !(e && e[0] == '0');
 }()};
+// bucket-local plan with groups of several small bins per K10 segment (AHS_BL_GROUP=1; experiment)
+std::atomic<bool> g_bl_group{[] {
+    const char *e = std::getenv("AHS_BL_GROUP");
+    return e && e[0] == '1';
+}()};
 // K10 for medium segments and the bucket pass (default on; AHS_K10=0: K9r everywhere)
 std::atomic<bool> g_k10{[] {
     const char *e = std::getenv("AHS_K10");
@@ -1012,10 +1017,11 @@ int sort_impl(const K *kin, const V *d_vals_in, K *kout, V *d_vals_out, uint64_t
         // the digits the low s bits already use (no extra sub-pass).  Capacity: the group mean plus six
         // standard deviations of a uniform fill.  Below ~1500 keys per group the bucket pass is no
         // faster than the two digit passes it replaces (profiles/r02_summary.md).
-        // (groups of several bins, G > 1, measured slower for cfg4a's 1024-key bins: the plan's two
-        // bin-digit passes over nearly sorted keys and the 4096-key groups cost more than the two
-        // classic passes, 892 vs 785 us; so G = 1 and bins of >= 1536 keys, profiles/r02_summary.md)
         const double mean = (double)n / (double)feat->nbins;
+        const uint32_t low_digits = (feat->shift + 7u) / 8u;
+        while (g_bl_group.load(std::memory_order_relaxed) && mean * 2.0 * bl_group <= 4096.0 &&
+               feat->shift + (uint32_t)__builtin_ctz(bl_group * 2u) <= 8u * low_digits)
+            bl_group *= 2u;
         const double gm = mean * bl_group;
         const double need = gm + 6.0 * std::sqrt(gm) + 32.0;
         if (gm >= 1536.0)

@@ -603,3 +603,26 @@ def test_bucket_local_plan_large(kv, bucket_local):
         assert torch.equal(ko, ko2) and (not kv or torch.equal(vo, vo2))
     finally:
         ahs.ahs_set_bucket_local(prev)
+
+
+def test_bucket_local_plan_falls_back_on_a_large_bin(bucket_local):
+    """A bin far above the bucket pass's capacity (a tenth of 2^27 keys share one value): K5 picks
+    the classic plan on the device, and the bucket pass launched after it returns at once."""
+    n = 1 << 27
+    x = synth.stream(73, n)
+    keys = (x >> np.uint64(32)).astype(np.uint32)
+    keys[(x & np.uint64(1023)) < np.uint64(102)] = np.uint32(0x9e3779b9)
+    vals = np.arange(n, dtype=np.uint32)
+    dk, dv = to_dev(keys), to_dev(vals)
+    ws = ahs.Workspace(n, True)
+    f = ahs.ahs_features(dk, ws)
+    s, r = ahs.ahs_select(f)
+    assert ahs.STRATEGY_NAMES[s] == "GENERAL" and f.shift == 16
+    ko, vo = torch.empty_like(dk), torch.empty_like(dv)
+    ahs.ahs_sort(dk, dv, ko, vo, s, f, ws)
+    assert ahs.ahs_sort_plan(ws) == (4, 0)
+    k1, v1 = to_host(ko), to_host(vo)
+    assert np.all(k1[1:] >= k1[:-1])
+    assert np.array_equal(k1, keys[v1])
+    tie = k1[1:] == k1[:-1]
+    assert np.all(v1[1:][tie] > v1[:-1][tie])
