@@ -134,6 +134,14 @@ typedef struct {
 AHS_API const char *ahs_version(void);
 AHS_API const char *ahs_status_string(int status);
 AHS_API void ahs_thresholds_default(ahs_thresholds_t *th);
+/* Table II's defaults (ahs_thresholds_default) with environment overrides named
+ * after SPEC's CLI flags: AHS_N_INSERTION, AHS_K_COUNTING, AHS_K_RADIX
+ * (unsigned decimal), AHS_ENTROPY_COEFF (decimal), AHS_ENTROPY_NORM ("buckets" /
+ * "range" or 0 / 1).  Unset or empty variables keep the default.  Returns AHS_OK,
+ * or AHS_EINVAL when a variable is malformed or the result fails ahs_select's
+ * threshold check (th then holds the defaults).  ahs_select(f, NULL, ...) does
+ * NOT read the environment; the Python binding's sort() does, through this. */
+AHS_API int ahs_thresholds_from_env(ahs_thresholds_t *th);
 
 /* Device workspace for ahs_features (histogram, scan, reduction partials).
  * Independent of n in this version (~600 KiB); pass n anyway. */

@@ -99,6 +99,7 @@ def lib():
             "ahs_rank_mode": ([C.c_int], C.c_int),
             "ahs_set_skip_trivial": ([C.c_int], C.c_int),
             "ahs_set_count_kv_single": ([C.c_int], C.c_int),
+            "ahs_thresholds_from_env": ([C.c_void_p], C.c_int),
             "ahs_set_bucket_local": ([C.c_int], C.c_int),
             "ahs_sort_plan": ([C.c_void_p, C.c_size_t, C.POINTER(C.c_int), C.POINTER(C.c_int), C.c_void_p], C.c_int),
             "ahs_entropy_sorted": ([vp, u64, vp, sz, C.POINTER(C.c_double), vp], C.c_int),
@@ -133,6 +134,14 @@ def ahs_thresholds_default(**overrides) -> Thresholds:
     lib().ahs_thresholds_default(C.byref(th))
     for k, v in overrides.items():
         setattr(th, k, v)
+    return th
+
+
+def ahs_thresholds_from_env() -> Thresholds:
+    """Table II defaults with the AHS_N_INSERTION / AHS_K_COUNTING / AHS_K_RADIX / AHS_ENTROPY_COEFF /
+    AHS_ENTROPY_NORM environment overrides; AhsError on a malformed or invalid value."""
+    th = Thresholds()
+    _check(lib().ahs_thresholds_from_env(C.byref(th)), "ahs_thresholds_from_env")
     return th
 
 
@@ -358,7 +367,7 @@ def sort(keys, vals=None, th: Thresholds | None = None, ws: Workspace | None = N
         ws = Workspace(n, vals is not None, keys.device, key_dtype=keys.dtype,
                        val_bytes=vals.element_size() if vals is not None else 4)
     feat = ahs_features(keys, ws, stream)
-    strategy, rule = ahs_select(feat, th)
+    strategy, rule = ahs_select(feat, th if th is not None else ahs_thresholds_from_env())
     if out is None:
         ko = torch.empty_like(keys)
         vo = torch.empty_like(vals) if vals is not None else None

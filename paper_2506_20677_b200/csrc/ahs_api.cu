@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cerrno>
 #include <atomic>
 #include <cmath>
 #include <chrono>
@@ -484,6 +485,42 @@ void ahs_thresholds_default(ahs_thresholds_t *th)
     th->entropy_coeff = 0.7;
     th->entropy_norm = AHS_NORM_BUCKETS;
     th->reserved = 0;
+}
+
+// SURVEY §5 Config/flags: environment overrides of the Table II thresholds, named after SPEC's CLI
+// flags.  Malformed or invalid values -> AHS_EINVAL (th keeps the defaults).
+int ahs_thresholds_from_env(ahs_thresholds_t *th)
+{
+    if (!th) return AHS_EINVAL;
+    ahs_thresholds_t t;
+    ahs_thresholds_default(&t);
+    auto u64 = [](const char *name, uint64_t *out) -> bool {
+        const char *e = std::getenv(name);
+        if (!e || !*e) return true;
+        char *end = nullptr;
+        errno = 0;
+        const unsigned long long v = std::strtoull(e, &end, 10);
+        if (errno || !end || *end || e[0] == '-') return false;
+        *out = (uint64_t)v;
+        return true;
+    };
+    bool ok = u64("AHS_N_INSERTION", &t.n_insertion) && u64("AHS_K_COUNTING", &t.k_counting) &&
+              u64("AHS_K_RADIX", &t.k_radix);
+    if (const char *e = std::getenv("AHS_ENTROPY_COEFF"); ok && e && *e) {
+        char *end = nullptr;
+        errno = 0;
+        t.entropy_coeff = std::strtod(e, &end);
+        ok = !errno && end && !*end;
+    }
+    if (const char *e = std::getenv("AHS_ENTROPY_NORM"); ok && e && *e) {
+        if (!std::strcmp(e, "buckets") || !std::strcmp(e, "0")) t.entropy_norm = AHS_NORM_BUCKETS;
+        else if (!std::strcmp(e, "range") || !std::strcmp(e, "1")) t.entropy_norm = AHS_NORM_RANGE;
+        else ok = false;
+    }
+    ahs_thresholds_default(th);
+    if (!ok || !thresholds_valid(&t)) return AHS_EINVAL;
+    *th = t;
+    return AHS_OK;
 }
 
 size_t ahs_workspace_bytes(uint64_t) { return ws_layout().total; }
