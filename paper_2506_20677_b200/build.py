@@ -14,7 +14,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libahs.so")
 SOURCES = [os.path.join(CSRC, "ahs_api.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("common.cuh", "features.cuh", "sort.cuh", "onesweep.cuh", "entropy.cuh", "classifier.hpp", "segsort.cuh")] + [
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("common.cuh", "features.cuh", "sort.cuh", "onesweep.cuh", "entropy.cuh", "classifier.hpp", "segsort.cuh", "onesweep2.cuh", "bucket.cuh")] + [
     os.path.join(ROOT, "include", "ahs.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 

@@ -908,7 +908,7 @@ namespace {
 template <typename K, bool KV>
 cudaError_t seg_launch(const void *kin, const uint32_t *vin, void *kout, uint32_t *vout, uint64_t n,
                        const uint32_t *offsets, uint32_t nseg, uint32_t max_segment, K flip, uint32_t *bad,
-                       bool ord, cudaStream_t s, const uint32_t *gate = nullptr, uint32_t group = 1);
+                       bool ord, cudaStream_t s, const uint32_t *gate = nullptr, uint32_t group = 1, K sub = 0);
 
 template <typename K, typename V>
 int sort_impl(const K *kin, const V *d_vals_in, K *kout, V *d_vals_out, uint64_t n, int32_t strategy,
@@ -1138,17 +1138,20 @@ int sort_impl(const K *kin, const V *d_vals_in, K *kout, V *d_vals_out, uint64_t
     if (bl_cap) {
         // K10: the bucket-local pass (K9's in-shared-memory stable radix sort, one CTA per bucket, in
         // place on the output; digits all keys of a bucket share are skipped); returns at once when K5
-        // chose the classic plan
+        // chose the classic plan.  It sorts v = key - min, as the digit passes do: a bucket is one
+        // feature bin, v >> shift = b, so exactly the low `shift` bits of v differ (ceil(shift / 8)
+        // sub-passes); on the key image itself a bin straddles a 2^16 boundary whenever min's low bits
+        // are not zero (cfg5 r = 32: ~63 % of the buckets took a third sub-pass)
         cudaError_t le = cudaSuccess;
         const cudaError_t e = launch(KID_BUCKET_SORT, s, [&] {
             const bool ord = di->rank_mode == kRankOrdered;
             if (kv)
                 le = seg_launch<K, true>(kout, (const uint32_t *)d_vals_out, kout, (uint32_t *)d_vals_out, n,
                                          bl_offsets, feat->nbins, bl_cap, flip, tickets + kTicketSegBad, ord, s,
-                                         plan + kPlanBL, bl_group);
+                                         plan + kPlanBL, bl_group, umin);
             else
                 le = seg_launch<K, false>(kout, nullptr, kout, nullptr, n, bl_offsets, feat->nbins, bl_cap, flip,
-                                          tickets + kTicketSegBad, ord, s, plan + kPlanBL, bl_group);
+                                          tickets + kTicketSegBad, ord, s, plan + kPlanBL, bl_group, umin);
         });
         if (e != cudaSuccess || le != cudaSuccess) return AHS_ECUDA;
     }
@@ -1373,7 +1376,7 @@ cudaError_t seg_small(const void *kin, const uint32_t *vin, void *kout, uint32_t
 // K10 (bucket.cuh): one CTA of 256 threads per segment of <= 256 IPT keys, ordered ranking
 template <typename K, bool KV, int IPT>
 cudaError_t seg_bucket(const void *kin, const uint32_t *vin, void *kout, uint32_t *vout, uint64_t n,
-                       const uint32_t *offsets, uint32_t nseg, K flip, uint32_t *bad, cudaStream_t s,
+                       const uint32_t *offsets, uint32_t nseg, K flip, K sub, uint32_t *bad, cudaStream_t s,
                        const uint32_t *gate, uint32_t group)
 {
     using BS = BucketSort<K, KV, IPT>;
@@ -1385,26 +1388,26 @@ cudaError_t seg_bucket(const void *kin, const uint32_t *vin, void *kout, uint32_
     if (ae != cudaSuccess) return ae;
     const unsigned grid = (unsigned)((nseg + group - 1) / group);
     return launch_k(k_bucket_sort<K, KV, IPT, MINB>, dim3(grid), dim3(kBucketBlock), BS::kSmem, s, (const K *)kin,
-                    vin, (K *)kout, vout, offsets, nseg, n, flip, bad, gate, group);
+                    vin, (K *)kout, vout, offsets, nseg, n, flip, sub, bad, gate, group);
 }
 
 template <typename K, bool KV, int GROUP, int CAP, bool ORD>
 cudaError_t seg_radix(const void *kin, const uint32_t *vin, void *kout, uint32_t *vout, uint64_t n,
                       const uint32_t *offsets, uint32_t nseg, uint32_t max_segment, K flip, uint32_t *bad,
-                      cudaStream_t s, const uint32_t *gate = nullptr)
+                      cudaStream_t s, const uint32_t *gate = nullptr, K sub = 0)
 {
     constexpr size_t smem = seg_radix_smem<K, KV, GROUP, CAP>();
     const cudaError_t ae = opt_in_smem((const void *)k_seg_radix<K, KV, GROUP, CAP, ORD>, smem);
     if (ae != cudaSuccess) return ae;
     return launch_k(k_seg_radix<K, KV, GROUP, CAP, ORD>, dim3(nseg), dim3(GROUP), smem,
-                    s, (const K *)kin, vin, (K *)kout, vout, offsets, nseg, n, flip, max_segment, bad, gate);
+                    s, (const K *)kin, vin, (K *)kout, vout, offsets, nseg, n, flip, sub, max_segment, bad, gate);
 }
 
 // register network length / CTA size from the declared maximum segment
 template <typename K, bool KV>
 cudaError_t seg_launch(const void *kin, const uint32_t *vin, void *kout, uint32_t *vout, uint64_t n,
                        const uint32_t *offsets, uint32_t nseg, uint32_t max_segment, K flip, uint32_t *bad,
-                       bool ord, cudaStream_t s, const uint32_t *gate, uint32_t group)
+                       bool ord, cudaStream_t s, const uint32_t *gate, uint32_t group, K sub)
 {
 #define AHS_SEG_ARGS kin, vin, kout, vout, n, offsets, nseg, max_segment, flip, bad, s
     if (max_segment <= 8) return seg_small<K, KV, 8>(AHS_SEG_ARGS);
@@ -1417,7 +1420,7 @@ cudaError_t seg_launch(const void *kin, const uint32_t *vin, void *kout, uint32_
     if (ord && (group > 1 || (g_k10.load(std::memory_order_relaxed) && max_segment > 1024))) {
         // K10: 256 threads per segment, keys in registers between the passes (faster than K9r above
         // 1024 keys: 2048-pair segments 563 vs 678 us per 2^27 pairs; slower below, profiles/r02_summary.md)
-#define AHS_BK_ARGS kin, vin, kout, vout, n, offsets, nseg, flip, bad, s, gate, group
+#define AHS_BK_ARGS kin, vin, kout, vout, n, offsets, nseg, flip, sub, bad, s, gate, group
         if (max_segment <= 2048) return seg_bucket<K, KV, 8>(AHS_BK_ARGS);
         if (max_segment <= 4096) return seg_bucket<K, KV, 16>(AHS_BK_ARGS);
         if (max_segment <= 4608) return seg_bucket<K, KV, 18>(AHS_BK_ARGS);
@@ -1427,19 +1430,19 @@ cudaError_t seg_launch(const void *kin, const uint32_t *vin, void *kout, uint32_
 #undef AHS_BK_ARGS
     }
     if (ord) {
-        if (max_segment <= 256) return seg_radix<K, KV, 32, 256, true>(AHS_SEG_ARGS, gate);
-        if (max_segment <= 512) return seg_radix<K, KV, 32, 512, true>(AHS_SEG_ARGS, gate);
-        if (max_segment <= 1024) return seg_radix<K, KV, 64, 1024, true>(AHS_SEG_ARGS, gate);
-        if (max_segment <= 2048) return seg_radix<K, KV, 128, 2048, true>(AHS_SEG_ARGS, gate);
-        if (max_segment <= 4096) return seg_radix<K, KV, 256, 4096, true>(AHS_SEG_ARGS, gate);
-        return seg_radix<K, KV, 512, 8192, true>(AHS_SEG_ARGS, gate);
+        if (max_segment <= 256) return seg_radix<K, KV, 32, 256, true>(AHS_SEG_ARGS, gate, sub);
+        if (max_segment <= 512) return seg_radix<K, KV, 32, 512, true>(AHS_SEG_ARGS, gate, sub);
+        if (max_segment <= 1024) return seg_radix<K, KV, 64, 1024, true>(AHS_SEG_ARGS, gate, sub);
+        if (max_segment <= 2048) return seg_radix<K, KV, 128, 2048, true>(AHS_SEG_ARGS, gate, sub);
+        if (max_segment <= 4096) return seg_radix<K, KV, 256, 4096, true>(AHS_SEG_ARGS, gate, sub);
+        return seg_radix<K, KV, 512, 8192, true>(AHS_SEG_ARGS, gate, sub);
     }
-    if (max_segment <= 256) return seg_radix<K, KV, 32, 256, false>(AHS_SEG_ARGS, gate);
-    if (max_segment <= 512) return seg_radix<K, KV, 32, 512, false>(AHS_SEG_ARGS, gate);
-    if (max_segment <= 1024) return seg_radix<K, KV, 64, 1024, false>(AHS_SEG_ARGS, gate);
-    if (max_segment <= 2048) return seg_radix<K, KV, 128, 2048, false>(AHS_SEG_ARGS, gate);
-    if (max_segment <= 4096) return seg_radix<K, KV, 256, 4096, false>(AHS_SEG_ARGS, gate);
-    return seg_radix<K, KV, 512, 8192, false>(AHS_SEG_ARGS, gate);
+    if (max_segment <= 256) return seg_radix<K, KV, 32, 256, false>(AHS_SEG_ARGS, gate, sub);
+    if (max_segment <= 512) return seg_radix<K, KV, 32, 512, false>(AHS_SEG_ARGS, gate, sub);
+    if (max_segment <= 1024) return seg_radix<K, KV, 64, 1024, false>(AHS_SEG_ARGS, gate, sub);
+    if (max_segment <= 2048) return seg_radix<K, KV, 128, 2048, false>(AHS_SEG_ARGS, gate, sub);
+    if (max_segment <= 4096) return seg_radix<K, KV, 256, 4096, false>(AHS_SEG_ARGS, gate, sub);
+    return seg_radix<K, KV, 512, 8192, false>(AHS_SEG_ARGS, gate, sub);
 #undef AHS_SEG_ARGS
 }
 }  // namespace

@@ -6,20 +6,22 @@
 // a contiguous bucket, and each bucket still needs sorting by its low bits).
 //
 // Per CTA (segment [lo, hi), len <= CAP = 256 IPT):
-//   load      the keys (ordered image key ^ flip) and values straight into
+//   load      the keys (v = (key ^ flip) - sub: the ordered image, range-reduced
+//             by the bucket-local plan's minimum, 0 for ahs_sort_segments) and values straight into
 //             registers: warp w owns the contiguous slice [w C, (w + 1) C), C = a
 //             multiple of 32 >= len / 8, lane l holds its items k at w C + 32 k + l
 //             (so register order (warp, item, lane) is index order);
 //   digits    the OR of key ^ first key over the segment: only the 8-bit digits in
 //             which some key differs get a pass (a stable pass over a constant digit
 //             is the identity);
-//   per pass  count (one shared atomic per key into the warp's 256-entry table) |
-//             barrier | the 256 scan threads turn the 8 warp tables into slots:
-//             digit start (block scan of the totals) + earlier warps' counts |
-//             barrier | rank (one shared atomic with return per key: the ordered
-//             ranking, the device's lane order being self-tested as for K6) and
-//             scatter into the segment buffer | barrier | reload the registers in
-//             (warp, item, lane) order.  Four shared operations per key, three
+//   per pass  count (one shared atomic per key into the warp's 256-entry table;
+//             for every pass after the first it is taken right after the previous
+//             pass's reload) | barrier | the 256 scan threads turn the 8 warp tables
+//             into slots: digit start (block scan of the totals) + earlier warps'
+//             counts | barrier | rank (one shared atomic with return per key: the
+//             ordered ranking, the device's lane order being self-tested as for K6)
+//             and scatter into the segment buffer | barrier | reload the registers
+//             in (warp, item, lane) order.  Four shared operations per key, three
 //             barriers; one buffer (the keys live in registers across the scatter);
 //   store     from the registers, coalesced, output transform fused.
 // Stable: every pass ranks in index order.  kout may alias kin.  A segment longer
@@ -49,7 +51,7 @@ template <typename K, bool KV, int IPT, int MINB>
 __global__ void __launch_bounds__(kBucketBlock, MINB)
     k_bucket_sort(const K *__restrict__ kin, const uint32_t *__restrict__ vin, K *__restrict__ kout,
                   uint32_t *__restrict__ vout, const uint32_t *__restrict__ offsets, uint32_t nseg, uint64_t n,
-                  K flip, uint32_t *__restrict__ bad, const uint32_t *__restrict__ gate, uint32_t group)
+                  K flip, K sub, uint32_t *__restrict__ bad, const uint32_t *__restrict__ gate, uint32_t group)
 {
     using C = BucketSort<K, KV, IPT>;
     constexpr int NW = C::kWarps, CAP = C::kCap;
@@ -89,13 +91,13 @@ __global__ void __launch_bounds__(kBucketBlock, MINB)
     if (t == 0) s_diff[0] = s_diff[1] = 0u;
     for (int i = t; i < NW * 256; i += kBucketBlock) tab[i] = 0u;
     __syncthreads();
-    const K first = kin[lo] ^ flip;
+    const K first = (K)((kin[lo] ^ flip) - sub);
     K x[IPT];
     [[maybe_unused]] uint32_t y[KV ? IPT : 1];
     K dacc = 0;
 #pragma unroll
     for (int k = 0; k < IPT; k++) {
-        x[k] = valid(k) ? (K)(kin[lo + slot(k)] ^ flip) : first;
+        x[k] = valid(k) ? (K)((kin[lo + slot(k)] ^ flip) - sub) : first;
         if constexpr (KV) y[k] = valid(k) ? vin[lo + slot(k)] : 0u;
         dacc |= x[k] ^ first;
     }
@@ -111,15 +113,21 @@ __global__ void __launch_bounds__(kBucketBlock, MINB)
     const uint64_t diff = ((uint64_t)s_diff[1] << 32) | s_diff[0];
     uint32_t *const wt = tab + warp * 256;
 
-    for (int b = 0; b < (int)sizeof(K); b++) {
-        if (((diff >> (8 * b)) & 0xffu) == 0) continue;  // a digit the whole segment shares
-        const uint32_t sh = 8u * (uint32_t)b;
-        auto dig = [&](K v) { return (uint32_t)(v >> sh) & 0xffu; };
-        // ---- count (non-returning atomics: same-word lanes merge)
+    // the digits some key of the segment differs in (a stable pass over a constant digit is the identity)
+    uint32_t act = 0;
+#pragma unroll
+    for (int b = 0; b < (int)sizeof(K); b++) act |= (((diff >> (8 * b)) & 0xffu) != 0 ? 1u : 0u) << b;
+    auto count = [&](uint32_t sh) {  // non-returning atomics: same-word lanes merge
 #pragma unroll
         for (int k = 0; k < IPT; k++)
-            if (valid(k)) atomicAdd(&wt[dig(x[k])], 1u);
-        __syncthreads();
+            if (valid(k)) atomicAdd(&wt[(uint32_t)(x[k] >> sh) & 0xffu], 1u);
+    };
+    if (act) count(8u * (uint32_t)(__ffs(act) - 1));
+    while (act) {
+        const uint32_t sh = 8u * (uint32_t)(__ffs(act) - 1);
+        act &= act - 1u;
+        auto dig = [&](K v) { return (uint32_t)(v >> sh) & 0xffu; };
+        __syncthreads();  // every warp's counts of this digit are in
         // ---- slots: digit start (block scan of the totals) + earlier warps' counts
         {
             const uint32_t d = t;  // 256 scan threads = the block
@@ -163,7 +171,8 @@ __global__ void __launch_bounds__(kBucketBlock, MINB)
             __syncwarp();
         }
         __syncthreads();
-        // ---- reload in index order; clear this warp's table for the next pass
+        // ---- reload in index order; this warp's table (only this warp touches it until the
+        // next barrier) is cleared and takes the counts of the next digit
 #pragma unroll
         for (int k = 0; k < IPT; k++) {
             if (valid(k)) {
@@ -177,13 +186,16 @@ __global__ void __launch_bounds__(kBucketBlock, MINB)
                 }
             }
         }
-        for (int i = lane; i < 256; i += 32) wt[i] = 0u;
-        __syncthreads();
+        if (act) {
+            for (int i = lane; i < 256; i += 32) wt[i] = 0u;
+            __syncwarp();
+            count(8u * (uint32_t)(__ffs(act) - 1));
+        }
     }
 #pragma unroll
     for (int k = 0; k < IPT; k++) {
         if (valid(k)) {
-            kout[lo + slot(k)] = x[k] ^ flip;
+            kout[lo + slot(k)] = (K)(x[k] + sub) ^ flip;
             if constexpr (KV) vout[lo + slot(k)] = y[k];
         }
     }

@@ -167,7 +167,7 @@ template <typename K, bool KV, int GROUP, int CAP, bool ORD>
 __global__ void __launch_bounds__(GROUP)
     k_seg_radix(const K *__restrict__ kin, const uint32_t *__restrict__ vin, K *__restrict__ kout,
                 uint32_t *__restrict__ vout, const uint32_t *__restrict__ offsets, uint32_t nseg, uint64_t n, K flip,
-                uint32_t maxlen, uint32_t *__restrict__ bad, const uint32_t *__restrict__ gate)
+                K sub, uint32_t maxlen, uint32_t *__restrict__ bad, const uint32_t *__restrict__ gate)
 {
     constexpr int NW = GROUP / 32;
     static_assert(CAP <= kSegMedMax && GROUP % 32 == 0 && CAP % 16 == 0, "segment capacity");
@@ -205,10 +205,10 @@ __global__ void __launch_bounds__(GROUP)
     // coalesced staging; the bits in which some key differs from the first
     if (t == 0) s_diff[0] = s_diff[1] = 0u;
     gsync();
-    const K first = kin[lo] ^ flip;
+    const K first = (K)((kin[lo] ^ flip) - sub);
     K dacc = 0;
     for (uint32_t i = t; i < len; i += GROUP) {
-        const K x = kin[lo + i] ^ flip;
+        const K x = (K)((kin[lo + i] ^ flip) - sub);
         kbuf0[i] = x;
         dacc |= x ^ first;
         if constexpr (KV) vbuf0[i] = vin[lo + i];
@@ -329,7 +329,7 @@ __global__ void __launch_bounds__(GROUP)
     const K *fk = cur ? kbuf1 : kbuf0;
     [[maybe_unused]] const uint32_t *fv = cur ? vbuf1 : vbuf0;
     for (uint32_t i = t; i < len; i += GROUP) {
-        kout[lo + i] = fk[i] ^ flip;
+        kout[lo + i] = (K)(fk[i] + sub) ^ flip;
         if constexpr (KV) vout[lo + i] = fv[i];
     }
 }
