@@ -289,6 +289,13 @@ std::atomic<bool> g_bl_group{[] {
     const char *e = std::getenv("AHS_BL_GROUP");
     return e && e[0] == '1';
 }()};
+// bucket-local plan: smallest mean keys per K10 segment it is chosen for (AHS_BL_MIN_KEYS; below it
+// the bucket pass is no faster than the two digit passes it replaces, profiles/r02_summary.md)
+const double g_bl_min_keys = [] {
+    const char *e = std::getenv("AHS_BL_MIN_KEYS");
+    const double v = e ? std::atof(e) : 0.0;
+    return v > 0.0 ? v : 1536.0;
+}();
 // K10 for medium segments and the bucket pass (default on; AHS_K10=0: K9r everywhere)
 std::atomic<bool> g_k10{[] {
     const char *e = std::getenv("AHS_K10");
@@ -1061,8 +1068,8 @@ int sort_impl(const K *kin, const V *d_vals_in, K *kout, V *d_vals_out, uint64_t
             bl_group *= 2u;
         const double gm = mean * bl_group;
         const double need = gm + 6.0 * std::sqrt(gm) + 32.0;
-        if (gm >= 1536.0)
-            for (uint32_t c : {2048u, 4096u, 4608u, 5120u, 6144u, 8192u})
+        if (gm >= g_bl_min_keys)
+            for (uint32_t c : {1536u, 2048u, 4096u, 4608u, 5120u, 6144u, 8192u})
                 if (need <= (double)c) {
                     bl_cap = c;
                     break;
@@ -1373,21 +1380,22 @@ cudaError_t seg_small(const void *kin, const uint32_t *vin, void *kout, uint32_t
                     vout, offsets, nseg, n, flip, max_segment, bad);
 }
 
-// K10 (bucket.cuh): one CTA of 256 threads per segment of <= 256 IPT keys, ordered ranking
-template <typename K, bool KV, int IPT>
+// K10 (bucket.cuh): one CTA of BLOCK threads per segment of <= BLOCK IPT keys, ordered ranking
+template <typename K, bool KV, int IPT, int BLOCK = 256>
 cudaError_t seg_bucket(const void *kin, const uint32_t *vin, void *kout, uint32_t *vout, uint64_t n,
                        const uint32_t *offsets, uint32_t nseg, K flip, K sub, uint32_t *bad, cudaStream_t s,
                        const uint32_t *gate, uint32_t group)
 {
-    using BS = BucketSort<K, KV, IPT>;
+    using BS = BucketSort<K, KV, IPT, BLOCK>;
 #ifndef AHS_K10_MINB16
 #define AHS_K10_MINB16 4  // 64 registers (12-32 B of spill), 4 CTAs per SM: cfg5_r32 bucket pass 1923 -> 1863 us
 #endif
-    constexpr int MINB = IPT >= 32 ? 2 : (IPT >= 20 ? 3 : (IPT >= 16 ? AHS_K10_MINB16 : 4));
-    const cudaError_t ae = opt_in_smem((const void *)k_bucket_sort<K, KV, IPT, MINB>, BS::kSmem);
+    // 256 threads: 64 registers at 4 CTAs per SM up to 18 keys per thread; 128 threads: 8 CTAs
+    constexpr int MINB = BLOCK == 128 ? 8 : (IPT >= 32 ? 2 : (IPT >= 20 ? 3 : (IPT >= 16 ? AHS_K10_MINB16 : 4)));
+    const cudaError_t ae = opt_in_smem((const void *)k_bucket_sort<K, KV, IPT, MINB, BLOCK>, BS::kSmem);
     if (ae != cudaSuccess) return ae;
     const unsigned grid = (unsigned)((nseg + group - 1) / group);
-    return launch_k(k_bucket_sort<K, KV, IPT, MINB>, dim3(grid), dim3(kBucketBlock), BS::kSmem, s, (const K *)kin,
+    return launch_k(k_bucket_sort<K, KV, IPT, MINB, BLOCK>, dim3(grid), dim3(BLOCK), BS::kSmem, s, (const K *)kin,
                     vin, (K *)kout, vout, offsets, nseg, n, flip, sub, bad, gate, group);
 }
 
@@ -1421,7 +1429,10 @@ cudaError_t seg_launch(const void *kin, const uint32_t *vin, void *kout, uint32_
         // K10: 256 threads per segment, keys in registers between the passes (faster than K9r above
         // 1024 keys: 2048-pair segments 563 vs 678 us per 2^27 pairs; slower below, profiles/r02_summary.md)
 #define AHS_BK_ARGS kin, vin, kout, vout, n, offsets, nseg, flip, sub, bad, s, gate, group
-        if (max_segment <= 2048) return seg_bucket<K, KV, 8>(AHS_BK_ARGS);
+        if (max_segment <= 1536) return seg_bucket<K, KV, 12, 128>(AHS_BK_ARGS);
+        // 128 threads up to 2048 keys (2^13 segments of 1000-2048 keys: 122.6 -> 102.1 us against
+        // 256 x 8, pairs 147.5 -> 135.1, uint64 270.2 -> 249.5; profiles/r02_summary.md)
+        if (max_segment <= 2048) return seg_bucket<K, KV, 16, 128>(AHS_BK_ARGS);
         if (max_segment <= 4096) return seg_bucket<K, KV, 16>(AHS_BK_ARGS);
         if (max_segment <= 4608) return seg_bucket<K, KV, 18>(AHS_BK_ARGS);
         if (max_segment <= 5120) return seg_bucket<K, KV, 20>(AHS_BK_ARGS);

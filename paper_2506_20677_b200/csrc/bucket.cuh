@@ -1,11 +1,11 @@
 // bucket.cuh — K10: stable in-shared-memory LSD radix sort of many independent
-// segments, one CTA of 256 threads per segment of up to 256 x IPT keys.  It serves
+// segments, one CTA of BLOCK (128 or 256) threads per segment of up to BLOCK x IPT keys.  It serves
 // the medium segments of ahs_sort_segments (NEXT-4: the paper's small-n path,
 // Listing 1, batched) and the bucket pass of the bucket-local GENERAL
 // plan (after two LSD passes over the feature-bin digits every bin is
 // a contiguous bucket, and each bucket still needs sorting by its low bits).
 //
-// Per CTA (segment [lo, hi), len <= CAP = 256 IPT):
+// Per CTA (segment [lo, hi), len <= CAP = BLOCK IPT):
 //   load      the keys (v = (key ^ flip) - sub: the ordered image, range-reduced
 //             by the bucket-local plan's minimum, 0 for ahs_sort_segments) and values straight into
 //             registers: warp w owns the contiguous slice [w C, (w + 1) C), C = a
@@ -32,12 +32,11 @@
 
 namespace ahs {
 
-constexpr int kBucketBlock = 256;
-
-template <typename K, bool KV, int IPT>
+template <typename K, bool KV, int IPT, int BLOCK = 256>
 struct BucketSort {
-    static constexpr int kCap = kBucketBlock * IPT;
-    static constexpr int kWarps = kBucketBlock / 32;
+    static_assert(BLOCK == 128 || BLOCK == 256, "128 or 256 threads per segment");
+    static constexpr int kCap = BLOCK * IPT;
+    static constexpr int kWarps = BLOCK / 32;
     // 32-bit keys with values: one 64-bit slot per pair (one scatter store and one reload per pair)
     static constexpr bool kPack = KV && sizeof(K) == 4;
     static constexpr size_t kSmem = (size_t)kCap * sizeof(K) + (KV ? (size_t)kCap * 4 : 0) +
@@ -47,13 +46,13 @@ struct BucketSort {
 // group: segment j is [offsets[j group], offsets[min((j + 1) group, nseg)]) -- several consecutive
 // buckets sorted as one (the bucket-local plan: the array is already ordered by bucket, so sorting
 // a run of buckets by the whole key keeps their order); nseg counts offsets - 1 entries.
-template <typename K, bool KV, int IPT, int MINB>
-__global__ void __launch_bounds__(kBucketBlock, MINB)
+template <typename K, bool KV, int IPT, int MINB, int BLOCK>
+__global__ void __launch_bounds__(BLOCK, MINB)
     k_bucket_sort(const K *__restrict__ kin, const uint32_t *__restrict__ vin, K *__restrict__ kout,
                   uint32_t *__restrict__ vout, const uint32_t *__restrict__ offsets, uint32_t nseg, uint64_t n,
                   K flip, K sub, uint32_t *__restrict__ bad, const uint32_t *__restrict__ gate, uint32_t group)
 {
-    using C = BucketSort<K, KV, IPT>;
+    using C = BucketSort<K, KV, IPT, BLOCK>;
     constexpr int NW = C::kWarps, CAP = C::kCap;
     pdl_begin();
     if (gate && __ldcg(gate) == 0u) return;
@@ -89,7 +88,7 @@ __global__ void __launch_bounds__(kBucketBlock, MINB)
     auto valid = [&](int k) { return slot(k) < we; };
 
     if (t == 0) s_diff[0] = s_diff[1] = 0u;
-    for (int i = t; i < NW * 256; i += kBucketBlock) tab[i] = 0u;
+    for (int i = t; i < NW * 256; i += BLOCK) tab[i] = 0u;
     __syncthreads();
     const K first = (K)((kin[lo] ^ flip) - sub);
     K x[IPT];
@@ -128,15 +127,18 @@ __global__ void __launch_bounds__(kBucketBlock, MINB)
         act &= act - 1u;
         auto dig = [&](K v) { return (uint32_t)(v >> sh) & 0xffu; };
         __syncthreads();  // every warp's counts of this digit are in
-        // ---- slots: digit start (block scan of the totals) + earlier warps' counts
+        // ---- slots: digit start (block scan of the totals) + earlier warps' counts; thread t
+        // owns digits t DPT .. t DPT + DPT - 1
         {
-            const uint32_t d = t;  // 256 scan threads = the block
-            uint32_t c[NW], tot = 0;
+            constexpr int DPT = 256 / BLOCK;
+            uint32_t c[DPT][NW], tot = 0;
 #pragma unroll
-            for (int w = 0; w < NW; w++) {
-                c[w] = tab[w * 256 + d];
-                tot += c[w];
-            }
+            for (int j = 0; j < DPT; j++)
+#pragma unroll
+                for (int w = 0; w < NW; w++) {
+                    c[j][w] = tab[w * 256 + t * DPT + j];
+                    tot += c[j][w];
+                }
             uint32_t incl = tot;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -150,10 +152,12 @@ __global__ void __launch_bounds__(kBucketBlock, MINB)
             for (int w = 0; w < NW; w++)
                 if (w < (int)warp) run += s_wsum[w];
 #pragma unroll
-            for (int w = 0; w < NW; w++) {
-                tab[w * 256 + d] = run;
-                run += c[w];
-            }
+            for (int j = 0; j < DPT; j++)
+#pragma unroll
+                for (int w = 0; w < NW; w++) {
+                    tab[w * 256 + t * DPT + j] = run;
+                    run += c[j][w];
+                }
         }
         __syncthreads();
         // ---- rank (lanes of one instruction served in lane order: self-tested) and scatter

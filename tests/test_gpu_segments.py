@@ -110,7 +110,7 @@ def rank(request):
 
 
 @pytest.mark.parametrize("dt", list(DT))
-@pytest.mark.parametrize("max_len", [33, 100, 512, 1000, 2048, 4096, 8192])
+@pytest.mark.parametrize("max_len", [33, 100, 512, 1000, 1536, 2048, 4096, 8192])
 def test_medium_segments(dt, max_len, rank):
     nseg = 300 if max_len <= 100 else 40
     off = make_offsets(nseg, max_len, 17 + max_len)
@@ -127,7 +127,7 @@ def test_medium_segments(dt, max_len, rank):
 
 
 @pytest.mark.parametrize("pattern", ["byte2", "bytes0_7", "top_bit", "all_equal", "two_values"])
-@pytest.mark.parametrize("max_len", [256, 2048, 8192])
+@pytest.mark.parametrize("max_len", [256, 1536, 2048, 8192])
 def test_medium_digit_patterns(pattern, max_len, rank):
     """keys that differ only in some bytes: the radix path skips the shared digits"""
     nseg = 60

@@ -17,12 +17,15 @@ import synth  # noqa: E402
 def run(cfg, reps=10):
     keys, vals, dt = synth.make(cfg)
     n = keys.size
-    dk = torch.from_numpy(keys.view(np.int32)).cuda()
+    wide = keys.dtype.itemsize == 8
+    dk = torch.from_numpy(keys.view(np.int64 if wide else np.int32)).cuda()
     if keys.dtype == np.uint32:
         dk = dk.view(torch.uint32)
+    elif keys.dtype == np.uint64:
+        dk = dk.view(torch.uint64)
     dv = torch.from_numpy(vals.view(np.int32)).cuda().view(torch.uint32) if vals is not None else None
     ko, vo = torch.empty_like(dk), (torch.empty_like(dv) if dv is not None else None)
-    ws = ahs.Workspace(n, dv is not None)
+    ws = ahs.Workspace(n, dv is not None, key_dtype=keys.dtype if wide else None)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     for _ in range(2):
         f = ahs.ahs_features(dk, ws)
@@ -47,7 +50,7 @@ def run(cfg, reps=10):
             if not k.startswith("feat"):
                 sort_ms += v["ms"] / reps
     passes = ahs.ahs_sort_passes(f, s, dv is not None)
-    kvb = 16 if dv is not None else 8
+    kvb = (2 * keys.dtype.itemsize) + (8 if dv is not None else 0)
     out["sort_us"] = round(sort_ms * 1e3, 1)
     out["sort_Gkeys"] = round(n / (sort_ms * 1e-3) / 1e9, 1)
     if passes:
@@ -55,7 +58,7 @@ def run(cfg, reps=10):
             if k in out:
                 out[k + "_GBps"] = round(kvb * n / (out[k] * 1e-6) / 1e9)
     # correctness spot check
-    h = ko.view(torch.int32).cpu().numpy().view(keys.dtype)
+    h = ko.view(torch.int64 if wide else torch.int32).cpu().numpy().view(keys.dtype)
     out["sorted_ok"] = bool(np.array_equal(h, np.sort(keys, kind="stable")))
     return out
 
