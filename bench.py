@@ -583,7 +583,7 @@ def run_ours(args):
             r["frac_of_peak"] = r["GBps"] / peak
     # end to end through the C ABI with host buffers
     if not args.no_e2e:
-        e_steps = max(3, args.steps // 2)
+        e_steps = max(3, args.steps)  # the same K steps as the device-timed region
         e_ms, bi, bo = time_e2e(torch, ahs, keys, vals, e_steps, 2, device)
         e_max = dist_max(pg, e_ms, device)
         out["e2e"] = {"value": round(ws * n * e_steps / (e_max * 1e-3) / 1e9, 4), "unit": "Gkeys/s",

@@ -1105,7 +1105,9 @@ int sort_impl(const K *kin, const V *d_vals_in, K *kout, V *d_vals_out, uint64_t
             launch_k(k_radix_hist<kRHBlock, kWide ? 8 : 4>, dim3((unsigned)g5), dim3(kRHBlock), 0, s, n,
                      (uint32_t)umin, passes, fhist, feat->nbins, feat->shift, (const DevFeatures *)(wsc + WL.feat),
                      (const uint32_t *)(wsc + WL.byte0), (const uint32_t *)(wsc + WL.digit1), dhist, bucket,
-                     tickets + kMaxPasses, plan, skip ? 1 : 0, bl_cap, bl_group, tickets + kTicketMaxBin);
+                     tickets + kMaxPasses, plan, skip ? 1 : 0, bl_cap, bl_group, tickets + kTicketMaxBin,
+                     kWide ? nullptr
+                           : reinterpret_cast<const uint32_t *>(((const FinalCtrl *)(wsc + WL.fctrl))->reduced));
         });
         if (e != cudaSuccess) return AHS_ECUDA;
         bases = bucket;

@@ -16,7 +16,9 @@ constexpr uint32_t kFull = 0xffffffffu;
 struct Partial {
     uint32_t mn, mx;   // ordered space
     uint64_t desc;
+    uint32_t an, orv;  // AND and OR of the ordered images: bits every key shares (K5's digit placement)
 };
+static_assert(sizeof(Partial) == 24, "Partial: mn, mx, desc, an, orv");
 
 // Device-side feature record, written by K3 into ws and into the host's
 // mapped buffer (seq last).  umin/umax: ordered images (32-bit keys zero-extended).

@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(BLOCK)
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     const VecSplit sp = vec_split(keys, n);
     const uint4 *body = reinterpret_cast<const uint4 *>(keys + sp.head);
-    uint32_t mn = 0xffffffffu, mx = 0u, desc = 0u;
+    uint32_t mn = 0xffffffffu, mx = 0u, desc = 0u, an = 0xffffffffu, orv = 0u;
     stream_chunks<kReduceStages, kReduceChunk>(
         body, sp.nvec, smem_raw, bars, [&](const uint4 *c, uint32_t nv, uint64_t v0) {
             for (uint32_t j = threadIdx.x; j < nv; j += BLOCK) {
@@ -125,6 +125,8 @@ __global__ void __launch_bounds__(BLOCK)
                 }
                 mn = min(mn, min(min(a0, a1), min(a2, a3)));
                 mx = max(mx, max(max(a0, a1), max(a2, a3)));
+                an &= a0 & a1 & a2 & a3;
+                orv |= a0 | a1 | a2 | a3;
                 atomicAdd(&s_b0[((a0 & 255u) << 5) | lane], 1u);
                 atomicAdd(&s_b0[((a1 & 255u) << 5) | lane], 1u);
                 atomicAdd(&s_b0[((a2 & 255u) << 5) | lane], 1u);
@@ -141,6 +143,8 @@ __global__ void __launch_bounds__(BLOCK)
             const uint32_t a = keys[i] ^ flip;
             mn = min(mn, a);
             mx = max(mx, a);
+            an &= a;
+            orv |= a;
             atomicAdd(&s_b0[((a & 255u) << 5) | lane], 1u);
             if (i + 1 < n) desc += (uint32_t)(a > (keys[i + 1] ^ flip));
         }
@@ -148,22 +152,28 @@ __global__ void __launch_bounds__(BLOCK)
 
     __syncthreads();
     b0_fold<BLOCK>(s_b0, byte0_rows + (size_t)blockIdx.x * 256);
-    __shared__ uint32_t s_mn[BLOCK / 32], s_mx[BLOCK / 32], s_d[BLOCK / 32];
+    __shared__ uint32_t s_mn[BLOCK / 32], s_mx[BLOCK / 32], s_d[BLOCK / 32], s_an[BLOCK / 32], s_or[BLOCK / 32];
     mn = __reduce_min_sync(kFull, mn);
     mx = __reduce_max_sync(kFull, mx);
     desc = __reduce_add_sync(kFull, desc);
+    an = __reduce_and_sync(kFull, an);
+    orv = __reduce_or_sync(kFull, orv);
     if (lane == 0) {
         s_mn[warp] = mn;
         s_mx[warp] = mx;
         s_d[warp] = desc;
+        s_an[warp] = an;
+        s_or[warp] = orv;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        Partial p{0xffffffffu, 0u, 0ull};
+        Partial p{0xffffffffu, 0u, 0ull, 0xffffffffu, 0u};
         for (int w = 0; w < BLOCK / 32; w++) {
             p.mn = min(p.mn, s_mn[w]);
             p.mx = max(p.mx, s_mx[w]);
             p.desc += s_d[w];
+            p.an &= s_an[w];
+            p.orv |= s_or[w];
         }
         partials[blockIdx.x] = p;
     }
@@ -328,19 +338,23 @@ struct KeyTraits<uint64_t> {
 template <int BLOCK>
 __device__ __forceinline__ Partial reduce_partials(const Partial *__restrict__ partials, int nparts)
 {
-    __shared__ uint32_t r_mn[BLOCK / 32], r_mx[BLOCK / 32];
+    __shared__ uint32_t r_mn[BLOCK / 32], r_mx[BLOCK / 32], r_an[BLOCK / 32], r_or[BLOCK / 32];
     __shared__ unsigned long long r_d[BLOCK / 32];
     __shared__ Partial r_out;
-    uint32_t mn = 0xffffffffu, mx = 0u;
+    uint32_t mn = 0xffffffffu, mx = 0u, an = 0xffffffffu, orv = 0u;
     unsigned long long d = 0ull;
     for (int i = threadIdx.x; i < nparts; i += BLOCK) {
         const uint32_t *pw = reinterpret_cast<const uint32_t *>(partials + i);
         mn = min(mn, __ldcg(pw));
         mx = max(mx, __ldcg(pw + 1));
         d += __ldcg(reinterpret_cast<const unsigned long long *>(pw + 2));
+        an &= __ldcg(pw + 4);
+        orv |= __ldcg(pw + 5);
     }
     mn = __reduce_min_sync(kFull, mn);
     mx = __reduce_max_sync(kFull, mx);
+    an = __reduce_and_sync(kFull, an);
+    orv = __reduce_or_sync(kFull, orv);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) d += __shfl_down_sync(kFull, d, o);
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
@@ -348,14 +362,18 @@ __device__ __forceinline__ Partial reduce_partials(const Partial *__restrict__ p
         r_mn[warp] = mn;
         r_mx[warp] = mx;
         r_d[warp] = d;
+        r_an[warp] = an;
+        r_or[warp] = orv;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        Partial p{0xffffffffu, 0u, 0ull};
+        Partial p{0xffffffffu, 0u, 0ull, 0xffffffffu, 0u};
         for (int w = 0; w < BLOCK / 32; w++) {
             p.mn = min(p.mn, r_mn[w]);
             p.mx = max(p.mx, r_mx[w]);
             p.desc += r_d[w];
+            p.an &= r_an[w];
+            p.orv |= r_or[w];
         }
         r_out = p;
     }

@@ -122,7 +122,8 @@ __global__ void __launch_bounds__(BLOCK, 1)
                  uint32_t fshift, const DevFeatures *__restrict__ dfeat, const uint32_t *__restrict__ byte0_rows,
                  const uint32_t *__restrict__ digit1_rows, uint32_t *__restrict__ dhist,
                  uint32_t *__restrict__ bucket_base, uint32_t *__restrict__ ticket, uint32_t *__restrict__ plan,
-                 int skip_trivial, uint32_t bl_cap, uint32_t bl_group, uint32_t *__restrict__ maxbin)
+                 int skip_trivial, uint32_t bl_cap, uint32_t bl_group, uint32_t *__restrict__ maxbin,
+                 const uint32_t *__restrict__ red)
 {
     pdl_begin();
     static_assert(MAXP <= kMaxPasses && MAXP * 32 <= BLOCK, "one warp per pass in the final scan");
@@ -133,6 +134,20 @@ __global__ void __launch_bounds__(BLOCK, 1)
     __shared__ uint32_t s_blon;
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
     const bool bl = bl_cap != 0u && fshift > 0u;
+    // Digit placement (NEXT-1): the keys' ordered images all share their bits below lo (K1's AND / OR,
+    // red = the reduced K1 record: words 4, 5), so v = key - min has lo zero low bits.  When lo is
+    // not a multiple of 8 and the feature bins resolve every bit from lo up (lo >= fshift), the passes
+    // take the digits at bit offsets lo, lo + 8, ... of v instead of 0, 8, ...: the same or fewer
+    // passes, and dense digits (cfg3's values 2^18 apart: byte-aligned digits take every 4th value,
+    // i.e. 8 of the 32 shared-memory banks; profiles/r02_summary.md).  Digits past the top bit are
+    // constant (skipped), so this needs trivial-pass skipping.
+    uint32_t lo = 0;
+    if (red && !bl && skip_trivial) {
+        const uint32_t varying = __ldcg(red + 4) ^ __ldcg(red + 5);
+        const uint32_t l = varying ? (uint32_t)(__ffs(varying) - 1) : 0u;
+        if ((l & 7u) != 0u && l >= fshift) lo = l;
+    }
+    auto off = [&](int p) { return lo + 8u * (uint32_t)p; };  // lo = 0: the byte-aligned digits
     for (int i = threadIdx.x; i < MAXP * 256; i += BLOCK) (&s_dig[0][0])[i] = 0u;
     for (int i = threadIdx.x; i < 2 * 256; i += BLOCK) (&s_bl[0][0])[i] = 0u;
     __syncthreads();
@@ -141,7 +156,7 @@ __global__ void __launch_bounds__(BLOCK, 1)
     // summing every (4 kRowCtas)-th row: few dependent L2 round trips
     if (blockIdx.x < 2 * kRowCtas) {
         const bool d1 = blockIdx.x >= kRowCtas;
-        if (d1 ? fshift > 8u : fshift > 0u) {
+        if (lo == 0u && (d1 ? fshift > 8u : fshift > 0u)) {
             constexpr uint32_t PARTS = BLOCK / 256;
             const uint32_t t = threadIdx.x & 255u;
             const uint32_t part = (blockIdx.x % kRowCtas) * PARTS + (threadIdx.x >> 8);
@@ -161,8 +176,7 @@ __global__ void __launch_bounds__(BLOCK, 1)
         const uint64_t base = (uint64_t)b << fshift;
 #pragma unroll
         for (int p = 0; p < MAXP; p++)
-            if (p < passes && (uint32_t)(8 * p) >= fshift)
-                atomicAdd(&s_dig[p][(uint32_t)(base >> (8 * p)) & 255u], c);
+            if (p < passes && off(p) >= fshift) atomicAdd(&s_dig[p][(uint32_t)(base >> off(p)) & 255u], c);
         if (bl) {
             atomicAdd(&s_bl[0][b & 255u], c);
             atomicAdd(&s_bl[1][(b >> 8) & 255u], c);
@@ -233,7 +247,7 @@ __global__ void __launch_bounds__(BLOCK, 1)
         uint32_t e = 0;
         for (int p = 0; p < passes; p++) {
             const bool run = p < np && !s_triv[p];
-            plan[p] = run ? plan_word(blon ? fshift + 8u * p : 8u * p, e, m) : kPassSkip;
+            plan[p] = run ? plan_word(blon ? fshift + 8u * p : off(p), e, m) : kPassSkip;
             e += run ? 1u : 0u;
         }
         plan[kMaxPasses] = m;

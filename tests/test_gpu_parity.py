@@ -186,6 +186,14 @@ TRIVIAL_CASES = {
     "general_20bit": (lambda n: synth.uniform_range(7, n, -(2 ** 19), 2 ** 19 - 1), 2, 3),
     # full 32-bit: nothing to skip
     "general_32bit": (lambda n: synth.uniform_range(8, n, -(2 ** 31), 2 ** 31 - 1), 2, 4),
+    # digit placement (K5): key - min = j * 2^12, j < 2^16, feature shift 12: every key shares its
+    # low 12 bits, so the digits sit at bits 12 and 20 (bit 28 on: constant) -> 2 passes, where
+    # byte-aligned digits would need 3 (bits 8-15, 16-23, 24-27)
+    "general_shift12": (lambda n: (synth.uniform_range(9, n, 0, 65535).astype(np.int64) * 4096 - 777)
+                        .astype(np.int32), 2, 2),
+    # RADIX over j * 2^20 + c, j < 1024 (10 varying bits at 20..29): digits at 20 and 28
+    "radix_shift20": (lambda n: (synth.uniform_range(10, n, 0, 1023).astype(np.int64) * (1 << 20) - (1 << 29) + 5)
+                      .astype(np.int32), None, 2),
 }
 
 
