@@ -1002,8 +1002,8 @@ int sort_impl(const K *kin, const V *d_vals_in, K *kout, V *d_vals_out, uint64_t
     else if (strategy == AHS_GENERAL) passes = kWide ? 8 : 4;  // full width, on key - min (R14)
     else passes = radix_passes(feat->bits);                     // RADIX, or COUNTING without the histogram
 
-    // zero the control words and both status regions (one memset); passes
-    // alternate between the regions, each clearing the previous pass's
+    // passes alternate between two status regions; the host zeroes the control words and the first
+    // pass's region (one memset), and each pass clears the other region at its end for the next
     const int mode = di->rank_mode;
     // RADIX over 32-bit keys (ordered ranking): K6 v2 with the hot-digit ranking (low-entropy
     // inputs have skewed digits); everything else: K6
@@ -1029,7 +1029,9 @@ int sort_impl(const K *kin, const V *d_vals_in, K *kout, V *d_vals_out, uint64_t
     // statuses of one pass; the 10-bit COUNTING scatter (1024 per tile) spans both regions
     const size_t status_words_per_pass =
         count_kv10 ? (size_t)((n + di->os10_tile - 1) / di->os10_tile) * 1024 : (size_t)tiles * kBins;
-    const size_t zero_bytes = (TL.status - TL.ctrl) + status_words_per_pass * 4 * (passes > 1 ? 2 : 1);
+    // the control words and the first pass's status region; each pass clears the other region for
+    // the next one at its end (pass 0: region 1, still dirty)
+    const size_t zero_bytes = (TL.status - TL.ctrl) + status_words_per_pass * 4;
     if (cudaMemsetAsync(tmp + TL.ctrl, 0, zero_bytes, s) != cudaSuccess) return AHS_ECUDA;
 
     // in place with an odd pass count: stream the input to tmp first.  In place,
@@ -1132,8 +1134,8 @@ int sort_impl(const K *kin, const V *d_vals_in, K *kout, V *d_vals_out, uint64_t
         pa.status = status + (size_t)(p & 1) * status_words_per_pass;
         pa.ticket = tickets + p;
         pa.plan = count_kv ? nullptr : plan;  // K5's plan (no skipping when not enabled)
-        pa.status_clear = p > 0 ? status + (size_t)((p - 1) & 1) * status_words_per_pass : nullptr;
-        pa.clear_words = p > 0 && p + 1 < passes ? (uint32_t)status_words_per_pass : 0u;
+        pa.status_clear = p + 1 < passes ? status + (size_t)((p + 1) & 1) * status_words_per_pass : nullptr;
+        pa.clear_words = p + 1 < passes ? (uint32_t)status_words_per_pass : 0u;
         pa.fault = tickets + kTicketFault;
         void *args[] = {&pa};
         const cudaError_t e = launch(kv ? (count_kv ? KID_COUNT_SCATTER_KV : KID_ONESWEEP_KV) : KID_ONESWEEP, s, [&] {

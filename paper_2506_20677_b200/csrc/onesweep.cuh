@@ -150,7 +150,7 @@ struct PassArgsT {
     const uint32_t *bucket_base;  // this pass's 256 digit bases
     uint32_t *status, *ticket;    // this pass's look-back statuses and tile ticket (zeroed)
     const uint32_t *plan;         // nullptr: no skipping
-    uint32_t *status_clear;       // the previous pass's status region: zeroed here for the next pass
+    uint32_t *status_clear;       // the other status region: zeroed at the end of this pass for the next
     uint32_t clear_words;         //   (passes alternate between two regions; 0: nothing to clear)
     uint32_t *fault;              // set to 1 when a look-back gives up (nullptr: __trap instead)
 };
@@ -170,15 +170,23 @@ template <bool KV, int BLOCK, int ITEMS, int MINB, int RANK = kRankMasked, typen
 __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(const PassArgsT<K, V> a)
 {
     pdl_begin();
-    // the previous pass is complete (pdl_begin): its status region is free and
-    // is cleared for the pass after this one (also when this pass is skipped)
-    for (uint32_t i = blockIdx.x * BLOCK + threadIdx.x; i < a.clear_words; i += gridDim.x * BLOCK)
-        a.status_clear[i] = 0u;
+    // the previous pass is complete (pdl_begin): its status region is free and is cleared for the
+    // pass after this one -- by each CTA once its tiles are done (the tail of the pass), or at once
+    // when this pass is skipped
+    auto clear_other = [&] {
+        // (a next pass that the plan skips uses no statuses: its own launch clears for the one after)
+        if (a.plan && a.plan[a.pass + 1] == kPassSkip) return;
+        for (uint32_t i = blockIdx.x * BLOCK + threadIdx.x; i < a.clear_words; i += gridDim.x * BLOCK)
+            a.status_clear[i] = 0u;
+    };
     // ---- this pass's place in the chain (and its digit's bit offset, from the plan when there is one)
     uint32_t e = a.pass, m = a.npasses, shift = a.shift;
     if (a.plan) {
         const uint32_t w = a.plan[a.pass];
-        if (w == kPassSkip) return;  // constant digit (or a pass the plan does not use): identity
+        if (w == kPassSkip) {  // constant digit (or a pass the plan does not use): identity
+            clear_other();
+            return;
+        }
         e = (w >> 8) & 255u;
         m = w & 255u;
         shift = w >> 16;
@@ -513,6 +521,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(const PassArgsT<K, V> 
         __syncthreads();
         PHASE_MARK(6);
     }
+    clear_other();
 }
 
 // Self-test of the hardware property kRankOrdered relies on: the lanes of one

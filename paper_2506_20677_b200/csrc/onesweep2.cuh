@@ -543,12 +543,20 @@ template <bool KV, int BLOCK, int ITEMS, int MINB, int BITS = 8, typename K = ui
 __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep2(const PassArgsT<K, V> a)
 {
     pdl_begin();
-    for (uint32_t i = blockIdx.x * BLOCK + threadIdx.x; i < a.clear_words; i += gridDim.x * BLOCK)
-        a.status_clear[i] = 0u;
+    // the other status region is cleared for the next pass at the end (as K6 does)
+    auto clear_other = [&] {
+        // (a next pass that the plan skips uses no statuses: its own launch clears for the one after)
+        if (a.plan && a.plan[a.pass + 1] == kPassSkip) return;
+        for (uint32_t i = blockIdx.x * BLOCK + threadIdx.x; i < a.clear_words; i += gridDim.x * BLOCK)
+            a.status_clear[i] = 0u;
+    };
     uint32_t e = a.pass, m = a.npasses, shift = a.shift;
     if (a.plan) {
         const uint32_t w = a.plan[a.pass];
-        if (w == kPassSkip) return;
+        if (w == kPassSkip) {
+            clear_other();
+            return;
+        }
         e = (w >> 8) & 255u;
         m = w & 255u;
         shift = w >> 16;
@@ -570,6 +578,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep2(const PassArgsT<K, V>
         if (tout) onesweep2_body<KV, BLOCK, ITEMS, BITS, false, true, K, V, HOTCFG>(a, keys_in, vals_in, keys_out, vals_out, shift);
         else onesweep2_body<KV, BLOCK, ITEMS, BITS, false, false, K, V, HOTCFG>(a, keys_in, vals_in, keys_out, vals_out, shift);
     }
+    clear_other();
 }
 
 }  // namespace ahs
