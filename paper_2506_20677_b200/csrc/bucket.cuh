@@ -116,6 +116,97 @@ __global__ void __launch_bounds__(BLOCK, MINB)
     uint32_t act = 0;
 #pragma unroll
     for (int b = 0; b < (int)sizeof(K); b++) act |= (((diff >> (8 * b)) & 0xffu) != 0 ? 1u : 0u) << b;
+    // slots: digit start (block scan of the totals) + earlier warps' counts; thread t owns digits
+    // t DPT .. t DPT + DPT - 1
+    auto scan_tables = [&] {
+        constexpr int DPT = 256 / BLOCK;
+        uint32_t c[DPT][NW], tot = 0;
+#pragma unroll
+        for (int j = 0; j < DPT; j++)
+#pragma unroll
+            for (int w = 0; w < NW; w++) {
+                c[j][w] = tab[w * 256 + t * DPT + j];
+                tot += c[j][w];
+            }
+        uint32_t incl = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(kFull, incl, o);
+            if (lane >= (uint32_t)o) incl += v;
+        }
+        if (lane == 31) s_wsum[warp] = incl;
+        __syncthreads();
+        uint32_t run = incl - tot;
+#pragma unroll
+        for (int w = 0; w < NW; w++)
+            if (w < (int)warp) run += s_wsum[w];
+#pragma unroll
+        for (int j = 0; j < DPT; j++)
+#pragma unroll
+            for (int w = 0; w < NW; w++) {
+                tab[w * 256 + t * DPT + j] = run;
+                run += c[j][w];
+            }
+    };
+
+    if constexpr (C::kPack) {
+        if ((diff >> 16) == 0u) {
+            // Narrow segment (every key shares bits 16.. of v with the first; the bucket-local plan's
+            // buckets when the feature shift is <= 16): one 32-bit slot per pair, (v & 0xffff) << 16 |
+            // local index, sorted by its top half, the values parked in shared memory at their local
+            // index and gathered once at the end -- the 64-bit slot scatter and reload of every pair
+            // and sub-pass become 32-bit ones
+            uint32_t *const ws = reinterpret_cast<uint32_t *>(bk_smem);  // [CAP] slots
+            uint32_t *const vs = ws + CAP;                                 // [CAP] values by local index
+            uint32_t w[IPT];
+#pragma unroll
+            for (int k = 0; k < IPT; k++) {
+                if (valid(k)) vs[slot(k)] = y[k];
+                w[k] = (((uint32_t)x[k] & 0xffffu) << 16) | slot(k);
+            }
+            auto wcount = [&](uint32_t sh) {
+#pragma unroll
+                for (int k = 0; k < IPT; k++)
+                    if (valid(k)) atomicAdd(&wt[(w[k] >> sh) & 0xffu], 1u);
+            };
+            uint32_t wact = act & 3u;  // digits 0 and 1 of v: bits 16-23 and 24-31 of the slot
+            if (wact) wcount(16u + 8u * (uint32_t)(__ffs(wact) - 1));
+            while (wact) {
+                const uint32_t sh = 16u + 8u * (uint32_t)(__ffs(wact) - 1);
+                wact &= wact - 1u;
+                __syncthreads();  // every warp's counts of this digit are in
+                scan_tables();
+                __syncthreads();
+#pragma unroll
+                for (int k = 0; k < IPT; k++) {
+                    if (valid(k)) {
+                        const uint32_t pos = atomicAdd(&wt[(w[k] >> sh) & 0xffu], 1u);
+                        ws[pos] = w[k];
+                    }
+                    __syncwarp();
+                }
+                __syncthreads();
+#pragma unroll
+                for (int k = 0; k < IPT; k++)
+                    if (valid(k)) w[k] = ws[slot(k)];
+                if (wact) {
+                    for (int i = lane; i < 256; i += 32) wt[i] = 0u;
+                    __syncwarp();
+                    wcount(16u + 8u * (uint32_t)(__ffs(wact) - 1));
+                }
+            }
+            __syncthreads();  // the parked values are visible (also when no digit varies)
+            const uint32_t hi = (uint32_t)first & 0xffff0000u;
+#pragma unroll
+            for (int k = 0; k < IPT; k++) {
+                if (valid(k)) {
+                    kout[lo + slot(k)] = (K)((hi | (w[k] >> 16)) + sub) ^ flip;
+                    vout[lo + slot(k)] = vs[w[k] & 0xffffu];
+                }
+            }
+            return;
+        }
+    }
     auto count = [&](uint32_t sh) {  // non-returning atomics: same-word lanes merge
 #pragma unroll
         for (int k = 0; k < IPT; k++)
@@ -127,38 +218,7 @@ __global__ void __launch_bounds__(BLOCK, MINB)
         act &= act - 1u;
         auto dig = [&](K v) { return (uint32_t)(v >> sh) & 0xffu; };
         __syncthreads();  // every warp's counts of this digit are in
-        // ---- slots: digit start (block scan of the totals) + earlier warps' counts; thread t
-        // owns digits t DPT .. t DPT + DPT - 1
-        {
-            constexpr int DPT = 256 / BLOCK;
-            uint32_t c[DPT][NW], tot = 0;
-#pragma unroll
-            for (int j = 0; j < DPT; j++)
-#pragma unroll
-                for (int w = 0; w < NW; w++) {
-                    c[j][w] = tab[w * 256 + t * DPT + j];
-                    tot += c[j][w];
-                }
-            uint32_t incl = tot;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t v = __shfl_up_sync(kFull, incl, o);
-                if (lane >= (uint32_t)o) incl += v;
-            }
-            if (lane == 31) s_wsum[warp] = incl;
-            __syncthreads();
-            uint32_t run = incl - tot;
-#pragma unroll
-            for (int w = 0; w < NW; w++)
-                if (w < (int)warp) run += s_wsum[w];
-#pragma unroll
-            for (int j = 0; j < DPT; j++)
-#pragma unroll
-                for (int w = 0; w < NW; w++) {
-                    tab[w * 256 + t * DPT + j] = run;
-                    run += c[j][w];
-                }
-        }
+        scan_tables();
         __syncthreads();
         // ---- rank (lanes of one instruction served in lane order: self-tested) and scatter
 #pragma unroll
