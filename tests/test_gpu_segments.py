@@ -241,3 +241,31 @@ def test_bench_size_properties(lo, hi, nseg, rank):
     assert np.array_equal(keys[vi], ko)  # the values gather the output
     eq = inner & (ko[1:] == ko[:-1])
     assert (vi[1:][eq] > vi[:-1][eq]).all()  # stable
+
+
+@pytest.mark.parametrize("dt", ["i32", "u32"])
+@pytest.mark.parametrize("max_len", [1536, 2048, 4096, 8192])
+@pytest.mark.parametrize("spread", ["low16", "low16_dups", "crosses16"])
+def test_narrow_segments(dt, max_len, spread):
+    """K10's narrow path: 32-bit keys with values whose segment keys agree above bit 16 sort as
+    (low 16 bits, local index) slots with the values gathered at the end; a segment whose keys
+    cross a 2^16 boundary (bit 16 differs) takes the 64-bit slot path.  Keys and values against
+    the oracle's stable order per segment."""
+    nseg = 24
+    off = make_offsets(nseg, max_len, 41 + max_len)
+    n = int(off[-1])
+    x = synth.stream(43 + max_len, n)
+    seg = np.repeat(np.arange(nseg), np.diff(off.astype(np.int64)))
+    base = (synth.stream(47, nseg) & np.uint64(0x7fff0000)).astype(np.int64)[seg]
+    if spread == "low16":
+        k = base + (x & np.uint64(0xffff)).astype(np.int64)
+    elif spread == "low16_dups":  # few distinct low bits: long runs of equal keys
+        k = base + (x & np.uint64(0x0f0f)).astype(np.int64)
+    else:  # keys around a 2^16 boundary of the segment's base
+        k = base + 0x8000 + (x & np.uint64(0xffff)).astype(np.int64)
+    keys = (k - 0x40000000).astype(np.int32) if dt == "i32" else k.astype(np.uint32)
+    vals = np.arange(n, dtype=np.uint32)
+    ko, vo, bad = run(keys, vals, off, max_len)
+    ek, ev = expected(keys, vals, off, max_len)
+    assert bad == 0
+    assert np.array_equal(ko, ek) and np.array_equal(vo, ev)

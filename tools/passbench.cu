@@ -322,6 +322,13 @@ int main(int argc, char **argv)
         printf("digit shift %u (max digit share %.3f)\n", shift, (double)mx / n);
         g_idx = 0;
         run_cfg<false, 512, 18, 2, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
+        if (getenv("PB_SHAPES")) {  // keys-only launch shapes: tile vs CTAs per SM
+            run_cfg<false, 256, 18, 4, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
+            run_cfg<false, 256, 24, 3, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
+            run_cfg<false, 384, 16, 3, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
+            run_cfg<false, 512, 24, 2, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
+            run_cfg<false, 512, 12, 3, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
+        }
         run2<false, 512, 18, 8, 0>(B, n, shift, sms, reps, true, hk, base);
         run2<false, 512, 18, 8, hotcfg(1, 3, false)>(B, n, shift, sms, reps, true, hk, base);
         run2<false, 512, 18, 8, hotcfg(4, 3, false)>(B, n, shift, sms, reps, true, hk, base);
