@@ -1429,10 +1429,13 @@ cudaError_t seg_launch(const void *kin, const uint32_t *vin, void *kout, uint32_
     if (max_segment <= (uint32_t)kSegSmallMax) return seg_small<K, KV, 32>(AHS_SEG_ARGS);
     // K9r: threads per segment from the declared maximum (16 keys per thread, one
     // warp up to 512 keys); the ordered ranking when the device passed its self-test
-    if (ord && (group > 1 || (g_k10.load(std::memory_order_relaxed) && max_segment > 1024))) {
-        // K10: 256 threads per segment, keys in registers between the passes (faster than K9r above
-        // 1024 keys: 2048-pair segments 563 vs 678 us per 2^27 pairs; slower below, profiles/r02_summary.md)
+    if (ord && (group > 1 || (g_k10.load(std::memory_order_relaxed) && max_segment > 512))) {
+        // K10: 128 or 256 threads per segment, keys in registers between the passes (faster than K9r
+        // above 512 keys; slower below, profiles/r02_summary.md)
 #define AHS_BK_ARGS kin, vin, kout, vout, n, offsets, nseg, flip, sub, bad, s, gate, group
+        // 128 x 8 from 513 keys (2^14 segments of 600-1024 keys: 137.2 -> 118.8 us against K9r, pairs
+        // 192.5 -> 145.4, uint64 325.6 -> 268.3); K9r below (300-512 keys: K10 131.1 -> 153.6 us)
+        if (max_segment <= 1024) return seg_bucket<K, KV, 8, 128>(AHS_BK_ARGS);
         if (max_segment <= 1536) return seg_bucket<K, KV, 12, 128>(AHS_BK_ARGS);
         // 128 threads up to 2048 keys (2^13 segments of 1000-2048 keys: 122.6 -> 102.1 us against
         // 256 x 8, pairs 147.5 -> 135.1, uint64 270.2 -> 249.5; profiles/r02_summary.md)

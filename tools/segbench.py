@@ -61,3 +61,6 @@ bench("radix 1000-2048 u64", 1 << 13, 1000, 2048, 2048, False, np.uint64)
 bench("radix 33-256", 1 << 16, 33, 256, 256, False)
 bench("radix 300-512", 1 << 15, 300, 512, 512, False)
 bench("radix 600-1024 kv", 1 << 14, 600, 1024, 1024, True)
+bench("radix 600-1024", 1 << 14, 600, 1024, 1024, False)
+bench("radix 600-1024 u64", 1 << 14, 600, 1024, 1024, False, np.uint64)
+bench("radix 300-512 kv", 1 << 15, 300, 512, 512, True)
