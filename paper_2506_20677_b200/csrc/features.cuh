@@ -497,11 +497,10 @@ __device__ __forceinline__ void hist_vec(const Add &add, uint4 x, bool act, uint
         const uint32_t e = stop ? (uint32_t)(__ffs(stop) - 1) : 32u;
         add(b0, 4u * (e - lane));
     } else if (act && !single) {
-        uint32_t cur = b0, c = 1;
-        if (b1 == cur) c++; else { add(cur, c); cur = b1; c = 1; }
-        if (b2 == cur) c++; else { add(cur, c); cur = b2; c = 1; }
-        if (b3 == cur) c++; else { add(cur, c); cur = b3; c = 1; }
-        add(cur, c);
+        // a vector that straddles bins (or holds an outlier of a nearly sorted run): its four
+        // atomics back to back (merging its equal neighbours here cost more instructions than it
+        // saved: up to four dependent atomic-and-check sequences, serialised across the lanes)
+        add.add4(b0, b1, b2, b3);
     }
 }
 
