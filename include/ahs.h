@@ -315,8 +315,13 @@ AHS_API int ahs_lane_order_ok(void);
  * permutation.  With skipping on (default; environment AHS_SKIP_TRIVIAL=0
  * turns it off), K5 writes a device-side pass plan into d_tmp and such passes
  * return at once; the remaining passes keep the buffer parity so the result
- * still lands in keys_out.  Not used in place (keys_out == keys_in), where the
- * parity must be known on the host.  Output is identical either way.
+ * still lands in keys_out.  With skipping on, when every key shares its bits
+ * below a bit lo that is not a multiple of 8 and the feature bins resolve the
+ * bits from lo up, the digits are placed at lo, lo + 8, ... instead of 0, 8, ...
+ * (Eq. 4, fixes the digit count, not the digit positions;
+ * DESIGN.md R20): the same or fewer passes over denser digits.  Not used in place
+ * (keys_out == keys_in), where the parity must be known on the host.  Output is
+ * identical either way.
  * ahs_set_skip_trivial(0/1) sets it (any other value queries); returns the
  * setting.  ahs_sort_executed_passes() reads the plan of the last ahs_sort on
  * that d_tmp (synchronizes `stream`): the number of executed digit passes, or
@@ -346,13 +351,16 @@ AHS_API int ahs_set_count_kv_single(int on);
  * of the bin make every bin a contiguous bucket (its boundaries are the exclusive
  * scan of the feature histogram), then K10 sorts each bucket in shared memory by
  * its low s bits (K10, bucket.cuh: one CTA per bucket, digits a bucket shares
- * skipped) -- three reads and writes of the keys instead of four.  Used where it
- * pays on B200: bins of >= 1536 keys on average (2^28 pairs, keys over 20..32
- * bits: sort 3.77-5.04 -> 3.71-4.46 ms; with smaller bins the bucket pass is
- * slower than the passes it replaces, profiles/r02_summary.md).  The library picks K10's
- * capacity from the mean bin size (up to 8192 keys); K5 falls back to the four
- * full-width passes on the device when a bin is larger.  Default on (environment
- * AHS_BUCKET_LOCAL=0 turns it off).  Output identical.
+ * skipped; it sorts key - min, and for pairs whose bucket keys differ only in
+ * their low 16 bits it sorts 32-bit (key bits, index) slots and gathers the
+ * values once) -- three reads and writes of the keys instead of four.  Used where
+ * it pays on B200: bins of >= 1536 keys on average (environment AHS_BL_MIN_KEYS
+ * changes the bound; 2^28 pairs, keys over 20..32 bits: sort 3.72-4.96 ms ->
+ * 3.57-3.90 ms; with smaller bins the bucket pass is slower than the passes it
+ * replaces, profiles/r02_summary.md).  The library picks K10's capacity from the
+ * mean bin size (up to 8192 keys); K5 falls back to the four full-width passes on
+ * the device when a bin is larger.  Default on (environment AHS_BUCKET_LOCAL=0
+ * turns it off).  Output identical.
  * ahs_set_bucket_local(0/1) sets it (any other value queries); returns the setting.
  * ahs_sort_plan() reads the plan of the last ahs_sort on d_tmp (synchronizes):
  * executed digit passes and whether the bucket-local pass ran.
