@@ -334,6 +334,12 @@ int main(int argc, char **argv)
         run2<false, 512, 18, 8, hotcfg(4, 3, false)>(B, n, shift, sms, reps, true, hk, base);
         run2<false, 512, 18, 8, hotcfg(2, 4, false)>(B, n, shift, sms, reps, true, hk, base);
         run_cfg<true, 384, 16, 2, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
+        if (getenv("PB_SHAPES")) {  // key-value launch shapes
+            run_cfg<true, 256, 15, 3, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
+            run_cfg<true, 256, 20, 2, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
+            run_cfg<true, 512, 12, 2, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
+            run_cfg<true, 384, 10, 3, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
+        }
         run2<true, 384, 16, 8, hotcfg(1, 3, false)>(B, n, shift, sms, reps, true, hk, base);
         run2<true, 384, 16, 8, hotcfg(4, 3, false)>(B, n, shift, sms, reps, true, hk, base);
     }
