@@ -209,7 +209,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase)
 // on the chunk's mbarrier, call consume(chunk_smem, nv, v0) and meet at a
 // barrier before the buffer is refilled.  Memory-level parallelism is
 // STAGES * CHUNK bytes per CTA independent of register pressure.
-template <int STAGES, int CHUNK, typename F>
+// REV: the chunks are visited last to first (chunk nchunks - 1 - (b + i * G)), so a
+// pass that follows a forward pass over the same keys starts on the chunks that
+// pass read last, which are still in L2, and leaves the first chunks in L2 for
+// the sort's first digit pass.
+template <int STAGES, int CHUNK, bool REV = false, typename F>
 __device__ __forceinline__ void stream_chunks(const uint4 *__restrict__ body, uint64_t nvec, uint8_t *buf,
                                               uint64_t *bars, F &&consume)
 {
@@ -222,8 +226,12 @@ __device__ __forceinline__ void stream_chunks(const uint4 *__restrict__ body, ui
         mbar_fence_init();
     }
     __syncthreads();
+    auto chunk = [&](uint32_t i) -> uint64_t {
+        const uint32_t c = blockIdx.x + i * gridDim.x;
+        return REV ? nchunks - 1u - c : c;
+    };
     auto issue = [&](uint32_t i, uint32_t s) {
-        const uint64_t v0 = (uint64_t)(blockIdx.x + i * gridDim.x) * VPC;
+        const uint64_t v0 = chunk(i) * VPC;
         const uint64_t nv = min((uint64_t)VPC, nvec - v0);
         const uint64_t ncopy = min(nv + 1, nvec - v0);  // + successor vector when it exists
         mbar_expect_tx(&bars[s], (uint32_t)(ncopy * 16));
@@ -234,7 +242,7 @@ __device__ __forceinline__ void stream_chunks(const uint4 *__restrict__ body, ui
     uint32_t s = 0, phase = 0;
     for (uint32_t i = 0; i < mine; i++) {
         mbar_wait(&bars[s], phase);
-        const uint64_t v0 = (uint64_t)(blockIdx.x + i * gridDim.x) * VPC;
+        const uint64_t v0 = chunk(i) * VPC;
         const uint32_t nv = (uint32_t)min((uint64_t)VPC, nvec - v0);
         consume(reinterpret_cast<const uint4 *>(buf + s * STRIDE), nv, v0);
         __syncthreads();

@@ -567,7 +567,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(BLOCK, 1)
     const uint4 *body = reinterpret_cast<const uint4 *>(keys + sp.head);
     uint8_t *stage = reinterpret_cast<uint8_t *>(sh) + kHistBins;
     auto run = [&](const auto &add) {
-        stream_chunks<kHistStages, kHistChunk>(body, sp.nvec, stage, bars,
+        stream_chunks<kHistStages, kHistChunk, true>(body, sp.nvec, stage, bars,
                                                [&](const uint4 *c, uint32_t nv, uint64_t) {
             if constexpr (sizeof(K) == 4) {
             for (uint32_t j0 = 0; j0 < nv; j0 += BLOCK) {  // block-uniform trip count

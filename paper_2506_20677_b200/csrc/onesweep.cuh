@@ -88,6 +88,17 @@ __device__ __forceinline__ uint32_t digit8(uint64_t v, uint32_t shift)
 // apart land in different banks (an ascending input puts exactly 32 keys per
 // digit into an 8192-key tile: its scatter would otherwise hit one bank).
 __device__ __forceinline__ uint32_t swz(uint32_t i) { return i ^ ((i >> 5) & 31u); }
+// The same for 64-bit slots (16 per 128-byte bank row): 16 consecutive slots (one
+// half-warp phase of a 64-bit access) stay conflict-free.
+__device__ __forceinline__ uint32_t swz64(uint32_t i) { return i ^ ((i >> 4) & 15u); }
+
+// Key-value passes over 32-bit keys and values (ordered ranking) reorder each pair as
+// one packed 64-bit slot (value << 32 | key): one scatter store and one write-out load
+// per pair instead of two.  A tile buffer then holds its keys and values side by side
+// ([b][keys TILE | values TILE]) so that the packed slots reuse its 8 * TILE bytes.
+#ifndef AHS_K6_PACK
+#define AHS_K6_PACK 1
+#endif
 
 // RANK: kRankMasked  16-lane sub-warps, {lane mask | slot} words: atomic add,
 //                    read-back, mask clear (makes no assumption about the order
@@ -220,6 +231,12 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(const PassArgsT<K, V> 
     __shared__ __align__(8) uint64_t s_bar[2];
     __shared__ uint32_t s_ticket[2];
 
+    constexpr bool PK = AHS_K6_PACK && KV && ORDERED && sizeof(K) == 4 && sizeof(V) == 4;
+    // tile buffer b: keys and values (PK: side by side, [b][keys | values])
+    auto kbuf = [&](uint32_t b) -> K * { return PK ? s_kb + b * 2 * TILE : s_kb + b * TILE; };
+    auto vbuf = [&](uint32_t b) -> V * {
+        return PK ? reinterpret_cast<V *>(s_kb) + b * 2 * TILE + TILE : s_vb + b * TILE;
+    };
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint32_t h = ORDERED ? 0u : lane >> 4, j = ORDERED ? lane : lane & 15u;
     const uint32_t sub = ORDERED ? warp : warp * 2u + h;
@@ -230,8 +247,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(const PassArgsT<K, V> 
     auto issue = [&](uint32_t t, uint32_t b) {  // thread 0
         const uint32_t kbytes = (uint32_t)(TILE * sizeof(K)), vbytes = (uint32_t)(TILE * sizeof(V));
         mbar_expect_tx(&s_bar[b], kbytes + (KV ? vbytes : 0u));
-        tma_load_1d(s_kb + b * TILE, keys_in + (size_t)t * TILE, kbytes, &s_bar[b]);
-        if constexpr (KV) tma_load_1d(s_vb + b * TILE, vals_in + (size_t)t * TILE, vbytes, &s_bar[b]);
+        tma_load_1d(kbuf(b), keys_in + (size_t)t * TILE, kbytes, &s_bar[b]);
+        if constexpr (KV) tma_load_1d(vbuf(b), vals_in + (size_t)t * TILE, vbytes, &s_bar[b]);
     };
 
     // skewed digit distribution (a digit holds > 1/16 of the keys): enable the
@@ -267,8 +284,9 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(const PassArgsT<K, V> 
         const uint32_t tile_base = tile * (uint32_t)TILE;
         const uint32_t tile_n = min((uint32_t)TILE, n - tile_base);
         const bool full = tile_n == (uint32_t)TILE;
-        K *sk = s_kb + b * TILE;
-        V *sv = s_vb + b * TILE;
+        K *sk = kbuf(b);
+        V *sv = vbuf(b);
+        [[maybe_unused]] uint64_t *s_slot = reinterpret_cast<uint64_t *>(sk);  // PK: packed pairs
         if (tma_ok && full) {
             mbar_wait(&s_bar[b], (phase >> b) & 1u);
             PHASE_MARK(0);
@@ -390,8 +408,12 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(const PassArgsT<K, V> 
                     }
                 }
                 if (valid) {
-                    sk[swz(pos)] = v[it];
-                    if constexpr (KV) sv[swz(pos)] = pv[it];
+                    if constexpr (PK) {
+                        s_slot[swz64(pos)] = (uint64_t)pv[it] << 32 | v[it];
+                    } else {
+                        sk[swz(pos)] = v[it];
+                        if constexpr (KV) sv[swz(pos)] = pv[it];
+                    }
                 }
                 __syncwarp();
             }
@@ -499,7 +521,17 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(const PassArgsT<K, V> 
             }
 
             // ------------------------------------------------------- write out
-            if constexpr (FULL) {
+            if constexpr (PK) {
+                const uint32_t lim = FULL ? (uint32_t)TILE : tile_n;
+    #pragma unroll 4
+                for (uint32_t i = tid; i < lim; i += BLOCK) {
+                    const uint64_t x = s_slot[swz64(i)];
+                    const K xk = (K)(uint32_t)x;
+                    const uint32_t o = s_gofs[digit8(xk, shift)] + i;
+                    keys_out[o] = (xk + out_add) ^ out_flip;
+                    vals_out[o] = (V)(uint32_t)(x >> 32);
+                }
+            } else if constexpr (FULL) {
     #pragma unroll 5
                 for (int i = tid; i < TILE; i += BLOCK) {
                     const K x = sk[swz(i)];

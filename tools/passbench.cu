@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "onesweep_p.cuh"
+#include "onesweep_b.cuh"
 #include "../paper_2506_20677_b200/csrc/onesweep2.cuh"
 
 using namespace ahs;
@@ -210,6 +211,17 @@ float run_p(const Bufs &B, uint32_t n, uint32_t shift, int sms, int reps, bool c
                         (const void *)k_onesweep_p<KV, NW, ITEMS, LBW, W>, C::kSmem, C::kTile, C::kBlock, nm);
 }
 
+template <bool KV, int BLOCK, int ITEMS, int MINB>
+float run_b(const Bufs &B, uint32_t n, uint32_t shift, int sms, int reps, bool check,
+            const std::vector<uint32_t> &hk, const std::vector<uint32_t> &hbase)
+{
+    using C = OnesweepB<KV, BLOCK, ITEMS>;
+    char nm[96];
+    snprintf(nm, sizeof nm, "bulk<%s,B%d,I%d,minb%d>", KV ? "kv" : "k", BLOCK, ITEMS, MINB);
+    return run_kern<KV>(B, n, shift, sms, reps, check, hk, hbase,
+                        (const void *)k_onesweep_b<KV, BLOCK, ITEMS, MINB>, C::kSmem, C::kTile, BLOCK, nm);
+}
+
 template <bool KV, int BLOCK, int ITEMS, int BITS = 8, int HOT = kHotDefault>
 float run2(const Bufs &B, uint32_t n, uint32_t shift, int sms, int reps, bool check,
            const std::vector<uint32_t> &hk, const std::vector<uint32_t> &hbase)
@@ -322,6 +334,16 @@ int main(int argc, char **argv)
         printf("digit shift %u (max digit share %.3f)\n", shift, (double)mx / n);
         g_idx = 0;
         run_cfg<false, 512, 18, 2, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
+        if (getenv("PB_BULK")) {  // K6b: TMA bulk-store write-out per digit run
+            run_b<false, 512, 18, 2>(B, n, shift, sms, reps, true, hk, base);
+            run_b<false, 512, 16, 2>(B, n, shift, sms, reps, true, hk, base);
+            run_b<false, 384, 16, 3>(B, n, shift, sms, reps, true, hk, base);
+            run_cfg<true, 384, 16, 2, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
+            run_b<true, 384, 12, 2>(B, n, shift, sms, reps, true, hk, base);
+            run_b<true, 256, 20, 2>(B, n, shift, sms, reps, true, hk, base);
+            run_b<true, 256, 18, 2>(B, n, shift, sms, reps, true, hk, base);
+            continue;
+        }
         if (getenv("PB_SHAPES")) {  // keys-only launch shapes: tile vs CTAs per SM
             run_cfg<false, 256, 18, 4, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
             run_cfg<false, 256, 24, 3, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
