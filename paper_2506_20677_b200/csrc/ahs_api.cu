@@ -144,7 +144,7 @@ int device_info(int *sms, int *hist_clusters = nullptr, DevInfo **info = nullptr
             set_k6(0, 0, kRankMasked, (const void *)K6_KEYS_M, OsKeysM::kSmem, OsKeysM::kTile, kSortBlock);
             set_k6(0, 1, kRankMasked, (const void *)K6_PAIRS_M, OsPairsM::kSmem, OsPairsM::kTile, kSortBlock);
             set_k6(0, 0, kRankOrdered, (const void *)K6_KEYS_O, OsKeysO::kSmem, OsKeysO::kTile, kSortBlock);
-            set_k6(0, 1, kRankOrdered, (const void *)K6_PAIRS_O, OsPairsO::kSmem, OsPairsO::kTile, kSortBlockPairsO);
+            set_k6(0, 1, kRankOrdered, (const void *)K6_PAIRS_O, OsPairsO::kSmem, OsPairsO::kTile, kSortBlockPairs32O);
             set_k6(1, 0, kRankMasked, (const void *)K6W_KEYS_M, OsKeys64M::kSmem, OsKeys64M::kTile, kSortBlock);
             set_k6(1, 1, kRankMasked, (const void *)K6W_PAIRS_M, OsPairs64M::kSmem, OsPairs64M::kTile, kSortBlock);
             set_k6(1, 0, kRankOrdered, (const void *)K6W_KEYS_O, OsKeys64O::kSmem, OsKeys64O::kTile,
@@ -163,7 +163,7 @@ int device_info(int *sms, int *hist_clusters = nullptr, DevInfo **info = nullptr
             good &= cudaFuncSetAttribute(d.osl_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d.osl_smem) ==
                     cudaSuccess;
             if (good)
-                good &= cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.osl_per_sm, d.osl_fn, kSortBlock,
+                good &= cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.osl_per_sm, d.osl_fn, kSortBlockOL,
                                                                       d.osl_smem) == cudaSuccess;
             good &= d.osl_per_sm > 0;
             d.os2_fn[0] = (const void *)K6V2_KEYS;
@@ -1017,7 +1017,8 @@ int sort_impl(const K *kin, const V *d_vals_in, K *kout, V *d_vals_out, uint64_t
     const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)sms * per_sm);
     const void *k6 = v2 ? di->os2_fn[VK] : large ? di->osl_fn : di->os_fn[W][VK][mode];
     size_t k6_smem = v2 ? di->os2_smem[VK] : large ? di->osl_smem : di->os_smem[W][VK][mode];
-    unsigned k6_block = v2 ? (unsigned)di->os2_block[VK] : (unsigned)di->os_block[W][VK][mode];
+    unsigned k6_block = v2 ? (unsigned)di->os2_block[VK]
+                      : large ? (unsigned)kSortBlockOL : (unsigned)di->os_block[W][VK][mode];
     unsigned grid_k6 = grid;
     if (count_kv10) {
         k6 = di->os10_fn;

@@ -28,23 +28,28 @@ namespace ahs {
 //   masked ranking (no assumption on atomic lane order): keys 512 x 15 (tile
 //     7680, 2 CTAs/SM), pairs 512 x 9 (tile 4608, 2 CTAs/SM);
 //   ordered ranking (after the lane-order self-test): keys 512 x 16 (tile
-//     8192, 2 CTAs/SM), pairs 384 x 16 (tile 6144, 2 CTAs/SM, 112 KB of shared
-//     memory each: 13 % faster than 384 x 12 at 2^26, 10 % at 2^24).
+//     8192, 2 CTAs/SM), pairs 256 x 25 (tile 6400, 2 CTAs/SM, 110 KB of shared
+//     memory each; with the packed 64-bit reorder slots 3-5 % faster than
+//     384 x 16 at 2^26 / 2^28: profiles/r02_k6_shapes3.txt).
 constexpr int kSortBlock = 512;
-constexpr int kSortBlockPairsO = 384;
+constexpr int kSortBlockPairsO = 384;  // 64-bit keys / values (ordered)
+constexpr int kSortBlockPairs32O = 256;
 using OsKeysM = Onesweep<false, kSortBlock, 15, kRankMasked>;
 using OsPairsM = Onesweep<true, kSortBlock, 9, kRankMasked>;
 using OsKeysO = Onesweep<false, kSortBlock, 16, kRankOrdered>;
-using OsPairsO = Onesweep<true, kSortBlockPairsO, 16, kRankOrdered>;
+using OsPairsO = Onesweep<true, kSortBlockPairs32O, 25, kRankOrdered>;
 #define K6_KEYS_M k_onesweep<false, kSortBlock, 15, 2, kRankMasked>
 #define K6_PAIRS_M k_onesweep<true, kSortBlock, 9, 2, kRankMasked>
 #define K6_KEYS_O k_onesweep<false, kSortBlock, 16, 2, kRankOrdered>
-#define K6_PAIRS_O k_onesweep<true, kSortBlockPairsO, 16, 2, kRankOrdered>
+#define K6_PAIRS_O k_onesweep<true, kSortBlockPairs32O, 25, 2, kRankOrdered>
 // keys-only ordered passes over n >= kLargeN: 512 x 18 (tile 9216; 24 B of register spill at the
-// 64-register cap) is 2.6 % faster per pass at 2^26, 0.6 % slower at 2^24 (profiles/r01_ab_items18.txt)
+// 64-register cap) is 2.6 % faster per pass at 2^26, 0.6 % slower at 2^24 (profiles/r01_ab_items18.txt).
+// (384 x 24, same tile: 1-2 % faster on uniform digits in tools/passbench.cu, 1 % slower on cfg4a's
+// passes in the pipeline: profiles/r02_k6_shapes3.txt, r02_qb_shapes.txt.)
 constexpr uint64_t kLargeN = 1ull << 25;
-using OsKeysOL = Onesweep<false, kSortBlock, 18, kRankOrdered>;
-#define K6_KEYS_OL k_onesweep<false, kSortBlock, 18, 2, kRankOrdered>
+constexpr int kSortBlockOL = 512;
+using OsKeysOL = Onesweep<false, kSortBlockOL, 18, kRankOrdered>;
+#define K6_KEYS_OL k_onesweep<false, kSortBlockOL, 18, 2, kRankOrdered>
 // 64-bit keys (NEXT-3), 2 CTAs/SM each: ordered keys 384 x 14 (tile 5376, 102 KB
 // of shared memory; 11 % faster than 512 x 9 at cfg6), ordered pairs 384 x 10
 // (3840, 108 KB; 11 % faster than 384 x 8), masked keys 512 x 9 (4608, 111 KB),

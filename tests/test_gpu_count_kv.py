@@ -25,9 +25,9 @@ def kv_mode(request):
 
 
 # k = max - min + 1 in (256, 1024]: 9- and 10-bit digits, signed and unsigned, ragged sizes
-# around the 4096-pair tile of the single pass and the 6144-pair tile of the radix passes
+# around the 4096-pair tile of the single pass and the 6400-pair tile of the radix passes
 CASES = [(257, "i32"), (300, "u32"), (1000, "i32"), (1024, "u32"), (513, "i32")]
-SIZES = [1, 2, 33, 4095, 4096, 4097, 6143, 6145, 3 * 4096 + 17, 250_001, 1_000_003]
+SIZES = [1, 2, 33, 4095, 4096, 4097, 6399, 6400, 6401, 3 * 4096 + 17, 250_001, 1_000_003]
 
 
 @pytest.mark.parametrize("k,dt", CASES)

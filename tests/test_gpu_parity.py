@@ -3,8 +3,9 @@
 Bar: features n/min/max/k/bits/shift/nbins/descents bit-exact, |dH| <= 1e-9
 (BASELINE.json north_star), strategy + rule identical, keys and values
 bit-exact (the unique stable order).  Sizes span several tiles (onesweep
-tiles: 8192 keys / 7680 pairs with the ordered ranking, 7680 / 4608 with the
-masked ranking, which has its own parity test) with ragged tails, and sizes
+tiles: 8192 keys (9216 from n = 2^25 on) / 6400 pairs with the ordered ranking,
+7680 / 4608 with the masked ranking, which has its own parity test) with ragged
+tails, and sizes
 where every persistent CTA walks several tiles; full BASELINE.json configs at
 the end.
 """
@@ -110,7 +111,8 @@ def check_forced(keys, vals, strategy, **kw):
 # --------------------------------------------------------------- T4 small
 
 SIZES = [1, 2, 3, 4, 5, 7, 8, 15, 16, 17, 21, 33, 1000, 4607, 4608, 4609, 7679, 7680, 7681,
-         8191, 8192, 8193, 3 * 7680 + 77, 3 * 8192 + 77, 5 * 4608 + 13, 65537, 250_001]
+         8191, 8192, 8193, 6399, 6400, 6401, 3 * 7680 + 77, 3 * 8192 + 77, 3 * 6400 + 77, 5 * 4608 + 13,
+         65537, 250_001]
 
 FAMILIES = {
     "u1000": lambda n, s: synth.uniform_range(s, n, 0, 999),
@@ -141,6 +143,14 @@ def test_pipeline_many_tiles_per_cta(family):
     keys = FAMILIES[family](n, 7)
     check_pipeline(keys)
     check_pipeline(keys, np.arange(n, dtype=np.uint32))
+
+
+@pytest.mark.parametrize("n", [3641 * 9216, 3641 * 9216 + 1, 2 ** 25 + 77])
+def test_large_keys_tile_boundaries(n):
+    # keys-only ordered passes over n >= 2^25 run the 512 x 18 shape (tile 9216): an exact
+    # multiple of the tile, one key past it, and a ragged tail
+    keys = FAMILIES["full32"](n, 11)
+    check_pipeline(keys)
 
 
 @pytest.fixture

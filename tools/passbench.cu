@@ -356,6 +356,19 @@ int main(int argc, char **argv)
         run2<false, 512, 18, 8, hotcfg(4, 3, false)>(B, n, shift, sms, reps, true, hk, base);
         run2<false, 512, 18, 8, hotcfg(2, 4, false)>(B, n, shift, sms, reps, true, hk, base);
         run_cfg<true, 384, 16, 2, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
+        if (getenv("PB_SHAPES3")) {  // keys-only: 256 threads, 2 CTAs per SM, large tiles
+            run_cfg<false, 256, 32, 2, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
+            run_cfg<false, 256, 36, 2, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
+            run_cfg<false, 256, 40, 2, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
+            run_cfg<false, 256, 44, 2, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
+            run_cfg<false, 384, 24, 2, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
+        }
+        if (getenv("PB_SHAPES2")) {  // key-value launch shapes with packed slots (72 registers)
+            run_cfg<true, 512, 11, 2, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
+            run_cfg<true, 256, 24, 2, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
+            run_cfg<true, 256, 25, 2, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
+            run_cfg<true, 384, 15, 2, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
+        }
         if (getenv("PB_SHAPES")) {  // key-value launch shapes
             run_cfg<true, 256, 15, 3, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
             run_cfg<true, 256, 20, 2, kRankOrdered>(B, n, shift, sms, reps, true, hk, base);
