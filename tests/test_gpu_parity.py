@@ -153,6 +153,24 @@ def test_large_keys_tile_boundaries(n):
     check_pipeline(keys)
 
 
+@pytest.mark.parametrize("bits,kind", [(25, "uniform"), (26, "uniform"), (28, "uniform"), (26, "nearly_sorted"),
+                                       (29, "uniform")])
+def test_narrow_top_digit_last_pass(bits, kind):
+    # large keys-only sorts whose last pass has a top digit of 1-5 bits (few distinct digits per warp:
+    # the returning rank atomic serves same-word lanes in turn), ragged last tile
+    n = 2 ** 25 + 77
+    if kind == "uniform":
+        keys = synth.uniform_range(21 + bits, n, 0, 2 ** bits - 1).astype(np.int32)
+    else:
+        keys = np.arange(n, dtype=np.int64) % (2 ** bits)
+        rng = np.random.default_rng(bits)
+        i = rng.integers(0, n, n // 100)
+        j = rng.integers(0, n, n // 100)
+        keys[i], keys[j] = keys[j], keys[i]
+        keys = keys.astype(np.int32)
+    check_pipeline(keys)
+
+
 @pytest.fixture
 def masked_rank():
     """Run a test with the masked (order-agnostic) onesweep ranking, then restore."""
