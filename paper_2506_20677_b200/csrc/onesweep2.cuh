@@ -58,7 +58,7 @@ struct Onesweep2 {
     static constexpr bool kHotOn = (HOTCFG & 15) != 0;
     static constexpr int kHotShift = (HOTCFG >> 4) & 15;               // share > 2^-kHotShift
     static constexpr bool kHotCount = (HOTCFG & 256) != 0;
-    static_assert(BITS == 8 || BITS == 10 || BITS == 11, "8-, 10- or 11-bit digits");
+    static_assert(BITS >= 8 && BITS <= 11, "8- to 11-bit digits (9: tools/passbench.cu only)");
     static_assert(BLOCK % 128 == 0 && BLOCK >= 256 && BLOCK <= 512, "256, 384 or 512 threads");
     static_assert(kBins <= BLOCK || kBins % BLOCK == 0, "scan threads own whole digit groups");
     static_assert(!kPacked || kDPT % 2 == 0, "packed tables: a scan thread owns whole words");

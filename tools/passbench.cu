@@ -380,7 +380,7 @@ int main(int argc, char **argv)
     }
     // wider digits (low BITS bits): KV counting with k <= 1024 (10 bits), the 11-bit experiment
     if (getenv("PB_WIDE")) {
-        for (int bits : {10, 11}) {
+        for (int bits : {9, 10, 11}) {
             const uint32_t bins = 1u << bits;
             std::vector<uint32_t> hist(bins, 0), base(bins);
             for (uint32_t i = 0; i < n; i++) hist[hk[i] & (bins - 1)]++;
@@ -392,7 +392,12 @@ int main(int argc, char **argv)
             CK(cudaMemcpy(B.bb, base.data(), bins * 4, cudaMemcpyHostToDevice));
             printf("digit bits %d, shift 0\n", bits);
             g_idx = 0;
-            if (bits == 10) {
+            if (bits == 9) {
+                run2<false, 256, 36, 9>(B, n, 0, sms, reps, true, hk, base);
+                run2<false, 256, 32, 9>(B, n, 0, sms, reps, true, hk, base);
+                run2<false, 256, 24, 9>(B, n, 0, sms, reps, true, hk, base);
+                run2<false, 256, 18, 9>(B, n, 0, sms, reps, true, hk, base);
+            } else if (bits == 10) {
                 run2<false, 512, 16, 10>(B, n, 0, sms, reps, true, hk, base);
                 run2<true, 512, 8, 10>(B, n, 0, sms, reps, true, hk, base);
                 run2<true, 512, 10, 10>(B, n, 0, sms, reps, true, hk, base);
