@@ -196,11 +196,11 @@ __global__ void __launch_bounds__(BLOCK, MINB)
                 }
             }
             __syncthreads();  // the parked values are visible (also when no digit varies)
-            const uint32_t hi = (uint32_t)first & 0xffff0000u;
+            const uint32_t top = (uint32_t)first & 0xffff0000u;  // the bits of v every key shares
 #pragma unroll
             for (int k = 0; k < IPT; k++) {
                 if (valid(k)) {
-                    kout[lo + slot(k)] = (K)((hi | (w[k] >> 16)) + sub) ^ flip;
+                    kout[lo + slot(k)] = (K)((top | (w[k] >> 16)) + sub) ^ flip;
                     vout[lo + slot(k)] = vs[w[k] & 0xffffu];
                 }
             }
