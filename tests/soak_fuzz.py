@@ -2,6 +2,7 @@
 the tests it calls the oracle; not collected by pytest).
 
     python tests/soak_fuzz.py FIRST LAST [SECONDS]     (env AHS_BL_MIN_KEYS etc. pass through)
+    SOAK_LOG2=22,25 python tests/soak_fuzz.py ...      (n log-uniform in [2^22, 2^25] instead of [2, 2^22])
 
 Prints one line per failing seed and a summary; exit code 1 when any seed failed.
 """
@@ -23,7 +24,11 @@ bad, done = [], 0
 for seed in range(first, last):
     if time.time() - t0 > budget:
         break
-    keys, vals, desc = draw_case(seed)
+    n_big = None
+    if os.environ.get("SOAK_LOG2"):
+        a, b = (float(v) for v in os.environ["SOAK_LOG2"].split(","))
+        n_big = int(2 ** (a + (b - a) * ((seed * 2654435761) % 1000) / 1000.0))
+    keys, vals, desc = draw_case(seed, n_big)
     try:
         check_pipeline(keys, vals)
     except Exception as e:  # noqa: BLE001

@@ -20,11 +20,13 @@ torch = pytest.importorskip("torch")
 import paper_2506_20677_b200 as ahs  # noqa: E402
 
 
-def draw_case(seed: int):
+def draw_case(seed: int, n_override=None):
     r = synth.stream(1000 + seed, 16)
     u = [int(x) for x in r]
     n = int(2 ** (1 + (u[0] % 2100) / 100.0))  # log-uniform in [2, 2^22]
     n = min(n, 1 << 22)
+    if n_override is not None:  # tests/soak_fuzz.py: larger sizes
+        n = int(n_override)
     fam = u[1] % 6
     dt = np.int32 if u[2] & 1 else np.uint32
     kv = bool(u[2] & 2)
