@@ -169,7 +169,7 @@ int device_info(int *sms, int *hist_clusters = nullptr, DevInfo **info = nullptr
             d.os2_fn[0] = (const void *)K6V2_KEYS;
             d.os2_smem[0] = Os2Keys::kSmem;
             d.os2_tile[0] = Os2Keys::kTile;
-            d.os2_block[0] = kSortBlock;
+            d.os2_block[0] = 512;
             d.os2_fn[1] = (const void *)K6V2_PAIRS;
             d.os2_smem[1] = Os2Pairs::kSmem;
             d.os2_tile[1] = Os2Pairs::kTile;

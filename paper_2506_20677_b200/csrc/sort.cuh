@@ -42,25 +42,25 @@ using OsPairsO = Onesweep<true, kSortBlockPairs32O, 25, kRankOrdered>;
 #define K6_PAIRS_M k_onesweep<true, kSortBlock, 9, 2, kRankMasked>
 #define K6_KEYS_O k_onesweep<false, kSortBlock, 16, 2, kRankOrdered>
 #define K6_PAIRS_O k_onesweep<true, kSortBlockPairs32O, 25, 2, kRankOrdered>
-// keys-only ordered passes over n >= kLargeN: 512 x 18 (tile 9216; 24 B of register spill at the
-// 64-register cap) is 2.6 % faster per pass at 2^26, 0.6 % slower at 2^24 (profiles/r01_ab_items18.txt).
-// (384 x 24, same tile: 1-2 % faster on uniform digits in tools/passbench.cu, 1 % slower on cfg4a's
-// passes in the pipeline: profiles/r02_k6_shapes3.txt, r02_qb_shapes.txt.)
+// keys-only ordered passes over n >= kLargeN: 512 x 21 (tile 10752; 56 B of register spill at the
+// 64-register cap).  In the pipeline at 2^26 (tools/quickbench.py, profiles/r02_summary.md) 512 x 18 /
+// 20 / 21 / 22 sort cfg4a in 779 / 749 / 743 / 738 us and cfg4b in 765 / 724 / 730 / 746 us: fewer tiles
+// mean fewer scans, look-backs and barriers per key.  (384 x 24: 1 % slower than 512 x 18 on cfg4a.)
 constexpr uint64_t kLargeN = 1ull << 25;
 constexpr int kSortBlockOL = 512;
-using OsKeysOL = Onesweep<false, kSortBlockOL, 18, kRankOrdered>;
-#define K6_KEYS_OL k_onesweep<false, kSortBlockOL, 18, 2, kRankOrdered>
-// 64-bit keys (NEXT-3), 2 CTAs/SM each: ordered keys 384 x 14 (tile 5376, 102 KB
-// of shared memory; 11 % faster than 512 x 9 at cfg6), ordered pairs 384 x 10
-// (3840, 108 KB; 11 % faster than 384 x 8), masked keys 512 x 9 (4608, 111 KB),
-// masked pairs 512 x 5 (2560).
+using OsKeysOL = Onesweep<false, kSortBlockOL, 21, kRankOrdered>;
+#define K6_KEYS_OL k_onesweep<false, kSortBlockOL, 21, 2, kRankOrdered>
+// 64-bit keys (NEXT-3), 2 CTAs/SM each: ordered keys 384 x 16 (tile 6144, 110 KB
+// of shared memory; cfg6 pass 315 -> 300 us against 384 x 14), ordered pairs 384 x 10
+// (3840, 108 KB; 11 % faster than 384 x 8; 384 x 11 drops to one CTA per SM: 467 -> 594 us),
+// masked keys 512 x 9 (4608, 111 KB), masked pairs 512 x 5 (2560).
 using OsKeys64M = Onesweep<false, kSortBlock, 9, kRankMasked, uint64_t>;
 using OsPairs64M = Onesweep<true, kSortBlock, 5, kRankMasked, uint64_t>;
-using OsKeys64O = Onesweep<false, kSortBlockPairsO, 14, kRankOrdered, uint64_t>;
+using OsKeys64O = Onesweep<false, kSortBlockPairsO, 16, kRankOrdered, uint64_t>;
 using OsPairs64O = Onesweep<true, kSortBlockPairsO, 10, kRankOrdered, uint64_t>;
 #define K6W_KEYS_M k_onesweep<false, kSortBlock, 9, 2, kRankMasked, uint64_t>
 #define K6W_PAIRS_M k_onesweep<true, kSortBlock, 5, 2, kRankMasked, uint64_t>
-#define K6W_KEYS_O k_onesweep<false, kSortBlockPairsO, 14, 2, kRankOrdered, uint64_t>
+#define K6W_KEYS_O k_onesweep<false, kSortBlockPairsO, 16, 2, kRankOrdered, uint64_t>
 #define K6W_PAIRS_O k_onesweep<true, kSortBlockPairsO, 10, 2, kRankOrdered, uint64_t>
 // 64-bit values (NEXT-3 payloads), 2 CTAs/SM: 32-bit keys ordered 384 x 10 (3840), masked 512 x 5
 // (2560); 64-bit keys ordered 384 x 7 (2688), masked 256 x 11 (2816).
@@ -74,10 +74,11 @@ using OsPairs64V64M = Onesweep<true, 256, 11, kRankMasked, uint64_t, uint64_t>;
 #define K6WV_PAIRS_M k_onesweep<true, 256, 11, 2, kRankMasked, uint64_t, uint64_t>
 // K6 v2 (onesweep2.cuh: hot-digit ranking) for RADIX passes over 32-bit keys (ordered ranking):
 // the FSM sends low-entropy inputs there, whose digits are skewed (cfg3's last pass: 64 % one
-// digit).  On uniform digits it is 1-4 % slower than K6, so GENERAL keeps K6.
-using Os2Keys = Onesweep2<false, kSortBlock, 18, 8>;
+// digit).  On uniform digits it is 1-4 % slower than K6, so GENERAL keeps K6.  Keys: 512 x 22 (tile
+// 11264, no spills): cfg3 sort 477 (512 x 18) -> 455 (x 20) -> 443 us (x 22); 384 x 28: 451 us.
+using Os2Keys = Onesweep2<false, 512, 22, 8>;
 using Os2Pairs = Onesweep2<true, kSortBlockPairsO, 16, 8>;
-#define K6V2_KEYS k_onesweep2<false, kSortBlock, 18, 2, 8>
+#define K6V2_KEYS k_onesweep2<false, 512, 22, 2, 8>
 #define K6V2_PAIRS k_onesweep2<true, kSortBlockPairsO, 16, 2, 8>
 // key-value COUNTING with 256 < k <= 1024 as ONE stable 10-bit scatter (opt-in: ahs_set_count_kv_single;
 // the default runs two 8-bit passes, measured faster: profiles/r02_summary.md)

@@ -4,7 +4,7 @@ through the C ABI against the CPU oracle (tests/test_oracle64.py pins it).
 Bar as for 32-bit keys: features bit-exact (min, max, k saturated at 2^64 - 1
 with its flag, bits, shift, nbins, descents, flags), |dH| <= 1e-9, strategy +
 rule identical, keys and values bit-exact (the unique stable order).  Sizes
-span several 64-bit K6 tiles (4608 keys, 3072 pairs ordered; 4608 / 2560
+span several 64-bit K6 tiles (6144 keys, 3840 pairs ordered; 4608 / 2560
 masked) with ragged tails; families reach every digit source of K5 for 64-bit
 keys (feature histogram, K1 / K2 rows, and K5b's key read for digits 2-5).
 """
@@ -105,7 +105,8 @@ FAMILIES = {
                                        np.where(synth.uniform_range64(49, n, 0, 1, np.int64) == 0, I64_MAX, -1)
                                        ).astype(np.int64),
 }
-SIZES = [1, 2, 3, 17, 21, 1000, 2559, 2560, 2561, 3071, 3072, 3073, 4607, 4608, 4609, 9217, 100_003]
+SIZES = [1, 2, 3, 17, 21, 1000, 2559, 2560, 2561, 3071, 3072, 3073, 3839, 3840, 3841, 4607, 4608, 4609, 5376, 6143, 6144,
+         6145, 9217, 12289, 100_003]
 
 
 @pytest.mark.parametrize("family", list(FAMILIES))
