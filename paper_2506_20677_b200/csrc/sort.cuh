@@ -46,7 +46,9 @@ using OsPairsO = Onesweep<true, kSortBlockPairs32O, 25, kRankOrdered>;
 // 64-register cap).  In the pipeline at 2^26 (tools/quickbench.py, profiles/r02_summary.md) 512 x 18 /
 // 20 / 21 / 22 sort cfg4a in 779 / 749 / 743 / 738 us and cfg4b in 765 / 724 / 730 / 746 us: fewer tiles
 // mean fewer scans, look-backs and barriers per key.  (384 x 24: 1 % slower than 512 x 18 on cfg4a.)
-constexpr uint64_t kLargeN = 1ull << 25;
+// At 2^24 (cfg2) 512 x 16 / 18 / 20 / 22 sort in 259 / 250 / 247 / 242 us, so the shape serves n >= 2^24;
+// below, 512 x 16 keeps more tiles than resident CTAs.
+constexpr uint64_t kLargeN = 1ull << 24;
 constexpr int kSortBlockOL = 512;
 using OsKeysOL = Onesweep<false, kSortBlockOL, 21, kRankOrdered>;
 #define K6_KEYS_OL k_onesweep<false, kSortBlockOL, 21, 2, kRankOrdered>

@@ -3,7 +3,7 @@
 Bar: features n/min/max/k/bits/shift/nbins/descents bit-exact, |dH| <= 1e-9
 (BASELINE.json north_star), strategy + rule identical, keys and values
 bit-exact (the unique stable order).  Sizes span several tiles (onesweep
-tiles: 8192 keys (10752 from n = 2^25 on; RADIX: 11264) / 6400 pairs with the ordered ranking,
+tiles: 8192 keys (10752 from n = 2^24 on; RADIX: 11264) / 6400 pairs with the ordered ranking,
 7680 / 4608 with the masked ranking, which has its own parity test) with ragged
 tails, and sizes
 where every persistent CTA walks several tiles; full BASELINE.json configs at
@@ -145,10 +145,11 @@ def test_pipeline_many_tiles_per_cta(family):
     check_pipeline(keys, np.arange(n, dtype=np.uint32))
 
 
-@pytest.mark.parametrize("n", [3121 * 10752, 3121 * 10752 + 1, 3641 * 9216, 2 ** 25 + 77])
+@pytest.mark.parametrize("n", [2 ** 24 - 1, 2 ** 24, 1561 * 10752, 1561 * 10752 + 1, 3121 * 10752, 3641 * 9216, 2 ** 25 + 77])
 def test_large_keys_tile_boundaries(n):
-    # keys-only ordered passes over n >= 2^25 run the 512 x 21 shape (tile 10752): an exact
-    # multiple of the tile, one key past it, a multiple of the former 9216 tile, and a ragged tail
+    # keys-only ordered passes over n >= 2^24 run the 512 x 21 shape (tile 10752): the switch-over size
+    # and the one below it, exact multiples of the tile, one key past, a multiple of the former 9216
+    # tile, and a ragged tail
     keys = FAMILIES["full32"](n, 11)
     check_pipeline(keys)
 
